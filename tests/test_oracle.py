@@ -1,0 +1,78 @@
+"""Pin the CPU restatement (oracle/curvetop_oracle.py) to the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by the reference compiled unmodified
+(oracle/_ref/refdriver, oracle/make_golden.py).  If these pass, the restatement is a
+faithful oracle for the GPU path's parity tests.
+"""
+
+import pytest
+
+import curvetop_oracle as O
+from golden_io import dec_arg, dec_bipoly, dec_sqf, dec_upoly, load
+from paper_1103_4697_b200 import curves
+
+
+def _run(op, args):
+    if op == "resultant_y":
+        return O.resultant(args[0], args[1], "y")
+    if op == "resultant_x":
+        return O.resultant(args[0], args[1], "x")
+    if op == "resultant_fy":
+        return O.resultant(args[0], O.derive_y(args[0]), "y")
+    if op == "yun":
+        return O.yun_squarefree(args[0])
+    if op == "gcd":
+        return O.gcd_univariate(args[0], args[1])
+    if op == "sqfp":
+        return O.square_free_part(args[0])
+    raise ValueError(op)
+
+
+def _check_row(row):
+    args = [dec_arg(a) if a else ({} if row["op"].startswith("resultant") else []) for a in row["args"]]
+    if "error" in row:
+        with pytest.raises(O.PreconditionError):
+            _run(row["op"], args)
+        return
+    got = _run(row["op"], args)
+    if row["op"] == "yun":
+        assert got == dec_sqf(row["result"])
+    else:
+        assert got == dec_upoly(row["result"])
+
+
+@pytest.mark.parametrize("name", ["worked.jsonl", "resultant_random.jsonl", "univariate_random.jsonl"])
+def test_restatement_matches_reference(name):
+    rows = load(name)
+    assert rows, name
+    for row in rows:
+        _check_row(row)
+
+
+def test_restatement_on_reference_test_elim_inputs():
+    rows = load("elim_cases.jsonl")
+    assert len(rows) > 300
+    for r in rows:
+        c = r["case"]
+        if c.startswith(("sylvester", "common", "generic")):
+            assert O.resultant(dec_bipoly(r["p"]), dec_bipoly(r["q"])) == dec_upoly(r["result"])
+            if c.startswith("sylvester"):
+                assert r["sylvester_agrees"]
+        elif c.startswith("yun"):
+            got = O.yun_squarefree(dec_upoly(r["u"]))
+            assert got == dec_sqf(r["result"])
+            assert O.reconstruct(*got) == dec_upoly(r["u"])
+        elif c.startswith("gcd"):
+            assert O.gcd_univariate(dec_upoly(r["a"]), dec_upoly(r["b"])) == dec_upoly(r["result"])
+
+
+def test_restatement_on_small_configs():
+    for r in load("configs_small.jsonl"):
+        kind, a, b, s = r["curve"]
+        if kind == "dense" and a > 10:
+            continue  # covered on the GPU path; keeps the CPU suite fast
+        f = curves.make(kind, a, b, s)
+        R = O.resultant(f, O.derive_y(f))
+        assert R == dec_upoly(r["result"])
+        if "yun" in r and a <= 8:
+            assert O.yun_squarefree(R) == dec_sqf(r["yun"])
