@@ -1,0 +1,158 @@
+/* ctg.h -- C ABI of the B200 multi-modular elimination library (libctg.so).
+ *
+ * This is the drop-in boundary for the reference's elimination hot path
+ * (namespace curvetop, /root/reference/proj):
+ *
+ *   ctg_resultant         replaces  curvetop::resultant(p, q, Var)
+ *                                   proj/include/curvetop/elim.hpp:30-31, proj/src/elim.cpp:95-136
+ *   ctg_yun_squarefree    replaces  curvetop::yun_squarefree(p)
+ *                                   elim.hpp:34, elim.cpp:138-165
+ *   ctg_gcd_univariate    replaces  curvetop::gcd_univariate(p, q)
+ *                                   upoly.hpp:92, elim.cpp:80-93
+ *   ctg_square_free_part  replaces  curvetop::square_free_part(p)
+ *                                   elim.hpp:45, elim.cpp:204-210
+ *
+ * The C++ TU paper_1103_4697_b200/cxx/curvetop_elim_gpu.cpp defines those
+ * curvetop:: symbols with the reference's exact signatures on top of this ABI
+ * (see INTEGRATION.md), mapping status codes to the reference's exceptions:
+ * CTG_PRECONDITION -> curvetop::PreconditionError, everything else -> curvetop::Error.
+ *
+ * Big integers cross the ABI in sign-magnitude form: one int8 sign (-1, 0, +1)
+ * per coefficient and little-endian uint32 magnitude limbs in CSR layout
+ * (limb_off has n+1 entries; coefficient i owns limbs[limb_off[i] .. limb_off[i+1])).
+ * All input pointers are caller-owned host memory; outputs are library-allocated
+ * host buffers released with the matching ctg_*_free.  There is no CPU fallback:
+ * when no usable CUDA device is present, every compute entry point returns CTG_CUDA.
+ */
+#ifndef CTG_H
+#define CTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTG_ABI_VERSION 1
+
+typedef enum {
+  CTG_OK = 0,
+  CTG_PRECONDITION = 1, /* reference PreconditionError (e.g. both inputs zero)        */
+  CTG_INVALID = 2,      /* malformed arguments (null pointers, bad CSR, bad range)     */
+  CTG_UNSUPPORTED = 3,  /* size beyond the library's limits (message says which)       */
+  CTG_INTERNAL = 4,     /* a self-check failed (bound exceeded, certificate failed)    */
+  CTG_CUDA = 5,         /* CUDA runtime error or no device                             */
+} ctg_status;
+
+/* Sparse bivariate polynomial sum c_t x^dx[t] y^dy[t] (exponents >= 0; repeated
+ * exponent pairs are summed, zero terms ignored -- bipoly.cpp:7-15). */
+typedef struct {
+  int32_t n_terms;
+  const int32_t* dx;
+  const int32_t* dy;
+  const int8_t* sign;
+  const uint32_t* limb_off; /* n_terms + 1 */
+  const uint32_t* limbs;
+} ctg_bipoly;
+
+/* Dense univariate polynomial, coefficients low -> high; n_coeffs = 0 is the zero polynomial.
+ * Trailing zero coefficients are allowed on input (they are trimmed, upoly.hpp:83-85). */
+typedef struct {
+  int32_t n_coeffs;
+  const int8_t* sign;
+  const uint32_t* limb_off; /* n_coeffs + 1 */
+  const uint32_t* limbs;
+} ctg_upoly;
+
+/* Library-allocated univariate result (trimmed: the last coefficient is nonzero). */
+typedef struct {
+  int32_t n_coeffs;
+  int8_t* sign;
+  uint32_t* limb_off;
+  uint32_t* limbs;
+} ctg_upoly_buf;
+
+/* Square-free factorization: value = unit * prod factors[i]^mult[i] (elim.hpp:13-22). */
+typedef struct {
+  int8_t unit_sign;
+  int32_t unit_nlimbs;
+  uint32_t* unit_limbs;
+  int32_t n_factors;
+  int32_t* mult;          /* strictly increasing */
+  ctg_upoly_buf* factors; /* primitive, positive leading coefficient, square-free */
+} ctg_sqf_buf;
+
+typedef struct {
+  int32_t device;   /* CUDA device ordinal; -1 = current device */
+  int32_t verify;   /* 1 (default) = run the on-device self-checks; 0 = skip the optional ones */
+  int32_t reserved[6];
+} ctg_opts;
+
+/* Timings of the last call on this thread (milliseconds; host wall clock around each phase). */
+typedef struct {
+  double total_ms, setup_ms, h2d_ms, device_ms, d2h_ms, decode_ms;
+  int64_t h2d_bytes, d2h_bytes;
+  int32_t n_primes, n_points, n_coeffs, out_limbs, kernel_launches, flagged_units;
+} ctg_call_stats;
+
+/* ---- entry points (the drop-in surface) ---- */
+ctg_status ctg_resultant(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                         ctg_upoly_buf* out, const ctg_opts* opts);
+ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_opts* opts);
+ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_buf* out,
+                              const ctg_opts* opts);
+ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ctg_opts* opts);
+
+void ctg_upoly_free(ctg_upoly_buf* buf);
+void ctg_sqf_free(ctg_sqf_buf* buf);
+const char* ctg_last_error(void); /* thread-local message of the last failing call */
+int32_t ctg_abi_version(void);
+int32_t ctg_device_count(void);
+void ctg_last_call_stats(ctg_call_stats* out);
+
+/* ---- staged resultant (prime sharding across GPUs; device-resident benchmarking) ----
+ * A plan fixes the primes, the evaluation points and the CRT constants for one
+ * resultant on the device that is current when it is created.  Prime k of the
+ * plan owns row k of the residue matrix (pitch = n_points words, values R mod p_k
+ * coefficients 0..n_coeffs-1 after ctg_plan_residues).  Any subset of rows can be
+ * computed on any GPU (one plan per GPU), exchanged (e.g. NCCL all-gather), and
+ * ctg_plan_crt reconstructs any coefficient range from the full matrix. */
+typedef struct ctg_plan ctg_plan;
+
+typedef struct {
+  int32_t n_primes;    /* rows of the residue matrix                              */
+  int32_t n_points;    /* evaluation points per prime (= row pitch, NTT size)      */
+  int32_t n_coeffs;    /* degree bound + 1 of the result                           */
+  int32_t out_limbs;   /* uint32 limbs per reconstructed coefficient               */
+  int32_t deg_p, deg_q;/* formal degrees in the eliminated variable                */
+  int32_t derivative;  /* 1 if q == dp/dy was detected (shared evaluation)         */
+  int32_t trivial;     /* 1 if the result is fixed by a convention (no GPU work)    */
+  double bound_bits;   /* log2 of the Hadamard coefficient bound                    */
+  double work_mulmods; /* algorithmic mulmods of the mod-p resultant stage */
+} ctg_plan_info;
+
+ctg_status ctg_plan_create(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                           const ctg_opts* opts, ctg_plan** plan);
+ctg_status ctg_plan_get_info(const ctg_plan* plan, ctg_plan_info* info);
+/* Upload the inputs (H2D) -- part of an end-to-end call, separate for device-only timing. */
+ctg_status ctg_plan_upload(ctg_plan* plan, void* stream);
+/* Rows [k0, k1) of the residue matrix into d_rows (device, (k1-k0) x n_points words). */
+ctg_status ctg_plan_residues(ctg_plan* plan, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream);
+/* Coefficients [j0, j1) from the full residue matrix d_all (device, n_primes x n_points):
+ * d_out gets (j1-j0) x (out_limbs + 1) words: word 0 = sign (as int32), then magnitude limbs. */
+ctg_status ctg_plan_crt(ctg_plan* plan, const uint32_t* d_all, int32_t j0, int32_t j1, uint32_t* d_out,
+                        void* stream);
+/* Decode a host copy of the full CRT output (n_coeffs x (out_limbs + 1) words) into a result. */
+ctg_status ctg_plan_decode(ctg_plan* plan, const uint32_t* h_crt, ctg_upoly_buf* out);
+/* Device error flags accumulated by the plan's kernels (0 = clean); synchronizes the stream. */
+ctg_status ctg_plan_check(ctg_plan* plan, void* stream);
+/* Number of kernel launches issued by the plan since creation. */
+int32_t ctg_plan_launches(const ctg_plan* plan);
+void ctg_plan_destroy(ctg_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTG_H */

@@ -265,7 +265,7 @@ def digest(coeffs_hex: list) -> str:
     return hashlib.sha256(",".join(coeffs_hex).encode()).hexdigest()
 
 
-def configs_big(cache_dir: str) -> list[dict]:
+def configs_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
     rows = []
     for (kind, a, b, s) in [("dense", 20, 64, 1), ("sheared", 3, 0, 1), ("dense", 16, 1024, 1),
                             ("dense", 30, 128, 1)]:
@@ -273,6 +273,9 @@ def configs_big(cache_dir: str) -> list[dict]:
         cached = os.path.join(cache_dir, f"out_{name}.txt")
         if os.path.exists(cached) and os.path.getsize(cached) > 0:
             r = json.loads(open(cached).read().splitlines()[0])
+        elif cached_only:
+            print(f"skip {name}: no cached reference output")
+            continue
         else:
             f = curves.make(kind, a, b, s)
             r = run_batch([("resultant_fy", [f])])[0]
@@ -293,6 +296,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--cache", default="/tmp/gold")
+    ap.add_argument("--cached-only", action="store_true", help="--big: use only cached reference outputs")
     args = ap.parse_args()
     elim = subprocess.run([DRIVER, "elim_cases"], capture_output=True, text=True, check=True).stdout
     write("elim_cases.jsonl", [json.loads(l) for l in elim.splitlines() if l.strip()])
@@ -301,7 +305,7 @@ def main() -> None:
     write("univariate_random.jsonl", univariate_random())
     write("configs_small.jsonl", configs_small())
     if args.big:
-        write("configs_big.jsonl", configs_big(args.cache))
+        write("configs_big.jsonl", configs_big(args.cache, args.cached_only))
 
 
 if __name__ == "__main__":

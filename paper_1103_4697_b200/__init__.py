@@ -1,0 +1,361 @@
+"""paper_1103_4697_b200 -- B200-native multi-modular elimination for curvetop.
+
+Python mirror of the reference's elimination API (namespace ``curvetop``,
+/root/reference/proj/include/curvetop/elim.hpp) over the C ABI of
+``libctg.so`` (include/ctg.h).  Same names, argument meaning and error
+behaviour as the reference:
+
+=============================  ==========================================  =========================
+this module                    reference                                   C ABI
+=============================  ==========================================  =========================
+``resultant(p, q, var)``       ``curvetop::resultant`` elim.cpp:95-136     ``ctg_resultant``
+``yun_squarefree(p)``          ``curvetop::yun_squarefree`` elim.cpp:138   ``ctg_yun_squarefree``
+``gcd_univariate(p, q)``       ``curvetop::gcd_univariate`` elim.cpp:80    ``ctg_gcd_univariate``
+``square_free_part(p)``        ``curvetop::square_free_part`` elim.cpp:204 ``ctg_square_free_part``
+=============================  ==========================================  =========================
+
+Polynomials: bivariate = ``{(deg_x, deg_y): int}``, univariate = list of ints
+(low -> high).  ``PreconditionError`` / ``Error`` mirror the reference's
+exception types (numeric.hpp:15-30).  Every computation runs on the GPU;
+without a CUDA device (or without the built library) the calls raise -- there
+is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libctg.so")
+
+
+class Error(RuntimeError):
+    """curvetop::Error (numeric.hpp:15-18)."""
+
+
+class PreconditionError(Error):
+    """curvetop::PreconditionError (numeric.hpp:20-24)."""
+
+
+class CudaError(Error):
+    """A CUDA failure or no device: libctg has no CPU fallback."""
+
+
+CTG_OK, CTG_PRECONDITION, CTG_INVALID, CTG_UNSUPPORTED, CTG_INTERNAL, CTG_CUDA = range(6)
+
+_i32p = C.POINTER(C.c_int32)
+_i8p = C.POINTER(C.c_int8)
+_u32p = C.POINTER(C.c_uint32)
+
+
+class _Bipoly(C.Structure):
+    _fields_ = [("n_terms", C.c_int32), ("dx", _i32p), ("dy", _i32p), ("sign", _i8p), ("limb_off", _u32p),
+                ("limbs", _u32p)]
+
+
+class _Upoly(C.Structure):
+    _fields_ = [("n_coeffs", C.c_int32), ("sign", _i8p), ("limb_off", _u32p), ("limbs", _u32p)]
+
+
+class _UpolyBuf(C.Structure):
+    _fields_ = [("n_coeffs", C.c_int32), ("sign", _i8p), ("limb_off", _u32p), ("limbs", _u32p)]
+
+
+class _SqfBuf(C.Structure):
+    _fields_ = [("unit_sign", C.c_int8), ("unit_nlimbs", C.c_int32), ("unit_limbs", _u32p), ("n_factors", C.c_int32),
+                ("mult", _i32p), ("factors", C.POINTER(_UpolyBuf))]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("verify", C.c_int32), ("reserved", C.c_int32 * 6)]
+
+
+class CallStats(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("setup_ms", C.c_double), ("h2d_ms", C.c_double), ("device_ms", C.c_double),
+                ("d2h_ms", C.c_double), ("decode_ms", C.c_double), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64), ("n_primes", C.c_int32), ("n_points", C.c_int32),
+                ("n_coeffs", C.c_int32), ("out_limbs", C.c_int32), ("kernel_launches", C.c_int32),
+                ("flagged_units", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("n_primes", C.c_int32), ("n_points", C.c_int32), ("n_coeffs", C.c_int32), ("out_limbs", C.c_int32),
+                ("deg_p", C.c_int32), ("deg_q", C.c_int32), ("derivative", C.c_int32), ("trivial", C.c_int32),
+                ("bound_bits", C.c_double), ("work_mulmods", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# Every symbol include/ctg.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "ctg_resultant", "ctg_yun_squarefree", "ctg_gcd_univariate", "ctg_square_free_part", "ctg_upoly_free",
+    "ctg_sqf_free", "ctg_last_error", "ctg_abi_version", "ctg_device_count", "ctg_last_call_stats",
+    "ctg_plan_create", "ctg_plan_get_info", "ctg_plan_upload", "ctg_plan_residues", "ctg_plan_crt",
+    "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libctg.so (built by ``paper_1103_4697_b200.build``); raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1103_4697_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.ctg_resultant.argtypes = [C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.c_int32, C.POINTER(_UpolyBuf),
+                                    C.POINTER(_Opts)]
+        L.ctg_yun_squarefree.argtypes = [C.POINTER(_Upoly), C.POINTER(_SqfBuf), C.POINTER(_Opts)]
+        L.ctg_gcd_univariate.argtypes = [C.POINTER(_Upoly), C.POINTER(_Upoly), C.POINTER(_UpolyBuf),
+                                         C.POINTER(_Opts)]
+        L.ctg_square_free_part.argtypes = [C.POINTER(_Upoly), C.POINTER(_UpolyBuf), C.POINTER(_Opts)]
+        L.ctg_upoly_free.argtypes = [C.POINTER(_UpolyBuf)]
+        L.ctg_sqf_free.argtypes = [C.POINTER(_SqfBuf)]
+        L.ctg_last_error.restype = C.c_char_p
+        L.ctg_last_call_stats.argtypes = [C.POINTER(CallStats)]
+        L.ctg_plan_create.argtypes = [C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.c_int32, C.POINTER(_Opts),
+                                      C.POINTER(C.c_void_p)]
+        L.ctg_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
+        L.ctg_plan_upload.argtypes = [C.c_void_p, C.c_void_p]
+        L.ctg_plan_residues.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_plan_crt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_plan_decode.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_UpolyBuf)]
+        L.ctg_plan_check.argtypes = [C.c_void_p, C.c_void_p]
+        L.ctg_plan_launches.argtypes = [C.c_void_p]
+        L.ctg_plan_destroy.argtypes = [C.c_void_p]
+        _lib = L
+        return L
+
+
+def _raise(status: int, what: str):
+    msg = lib().ctg_last_error().decode(errors="replace") or what
+    if status == CTG_PRECONDITION:
+        raise PreconditionError(msg)
+    if status == CTG_CUDA:
+        raise CudaError(msg)
+    raise Error(msg)
+
+
+def _check(status: int, what: str):
+    if status != CTG_OK:
+        _raise(status, what)
+
+
+# ----------------------------------------------------------------------------
+# Marshaling: Python ints <-> sign + little-endian u32 limbs (CSR)
+# ----------------------------------------------------------------------------
+
+def _encode_ints(values):
+    n = len(values)
+    sign = np.zeros(n, dtype=np.int8)
+    off = np.zeros(n + 1, dtype=np.uint32)
+    chunks = []
+    pos = 0
+    for i, v in enumerate(values):
+        if v:
+            mag = -v if v < 0 else v
+            sign[i] = -1 if v < 0 else 1
+            nl = (mag.bit_length() + 31) >> 5
+            chunks.append(mag.to_bytes(nl * 4, "little"))
+            pos += nl
+        off[i + 1] = pos
+    limbs = np.frombuffer(b"".join(chunks), dtype=np.uint32) if chunks else np.zeros(1, dtype=np.uint32)
+    return sign, off, np.ascontiguousarray(limbs)
+
+
+class HostBipoly:
+    """Caller-owned host buffers of one bivariate operand (kept alive with the struct)."""
+
+    def __init__(self, f: dict):
+        items = sorted((k, v) for k, v in f.items() if v)
+        self.dx = np.array([k[0] for k, _ in items], dtype=np.int32)
+        self.dy = np.array([k[1] for k, _ in items], dtype=np.int32)
+        self.sign, self.off, self.limbs = _encode_ints([v for _, v in items])
+        self.struct = _Bipoly(len(items), self.dx.ctypes.data_as(_i32p), self.dy.ctypes.data_as(_i32p),
+                              self.sign.ctypes.data_as(_i8p), self.off.ctypes.data_as(_u32p),
+                              self.limbs.ctypes.data_as(_u32p))
+        self.nbytes = self.dx.nbytes + self.dy.nbytes + self.sign.nbytes + self.off.nbytes + self.limbs.nbytes
+
+
+class HostUpoly:
+    def __init__(self, p):
+        self.sign, self.off, self.limbs = _encode_ints(list(p))
+        self.struct = _Upoly(len(p), self.sign.ctypes.data_as(_i8p), self.off.ctypes.data_as(_u32p),
+                             self.limbs.ctypes.data_as(_u32p))
+
+
+def _decode_buf(buf: _UpolyBuf) -> list:
+    n = buf.n_coeffs
+    if n == 0:
+        return []
+    off = np.ctypeslib.as_array(buf.limb_off, shape=(n + 1,))
+    total = int(off[n])
+    sign = np.ctypeslib.as_array(buf.sign, shape=(n,))
+    raw = bytes(np.ctypeslib.as_array(buf.limbs, shape=(max(total, 1),)).tobytes()) if total else b""
+    out = []
+    for i in range(n):
+        a, b = int(off[i]) * 4, int(off[i + 1]) * 4
+        v = int.from_bytes(raw[a:b], "little")
+        out.append(-v if sign[i] < 0 else v)
+    return out
+
+
+def _opts(device):
+    o = _Opts()
+    o.device = -1 if device is None else int(device)
+    o.verify = 1
+    return o
+
+
+def last_call_stats() -> dict:
+    s = CallStats()
+    lib().ctg_last_call_stats(C.byref(s))
+    return s.as_dict()
+
+
+def device_count() -> int:
+    return int(lib().ctg_device_count())
+
+
+# ----------------------------------------------------------------------------
+# The reference-facing API
+# ----------------------------------------------------------------------------
+
+def resultant_host(p: HostBipoly, q: HostBipoly, var: str = "y", device=None) -> list:
+    """ctg_resultant on pre-marshaled host operands (the e2e benchmark path)."""
+    out = _UpolyBuf()
+    o = _opts(device)
+    _check(lib().ctg_resultant(C.byref(p.struct), C.byref(q.struct), 1 if var in ("x", "X") else 0, C.byref(out),
+                               C.byref(o)), "resultant")
+    try:
+        return _decode_buf(out)
+    finally:
+        lib().ctg_upoly_free(C.byref(out))
+
+
+def resultant(p: dict, q: dict, var: str = "y", device=None) -> list:
+    """res(p, q) eliminating ``var`` -- curvetop::resultant (elim.hpp:30-31).
+
+    Conventions (elim.hpp:24-29): both zero -> PreconditionError; one zero -> [];
+    both of degree 0 in var -> [1]; degree-0 operand q -> q^deg(p).
+    """
+    return resultant_host(HostBipoly(p), HostBipoly(q), var, device)
+
+
+def yun_squarefree(p: list, device=None):
+    """curvetop::yun_squarefree (elim.hpp:34): returns (unit, [(factor, multiplicity), ...])."""
+    hp = HostUpoly(p)
+    out = _SqfBuf()
+    o = _opts(device)
+    _check(lib().ctg_yun_squarefree(C.byref(hp.struct), C.byref(out), C.byref(o)), "yun_squarefree")
+    try:
+        unit = 0
+        if out.unit_nlimbs:
+            limbs = np.ctypeslib.as_array(out.unit_limbs, shape=(out.unit_nlimbs,))
+            unit = int.from_bytes(limbs.tobytes(), "little")
+        unit = -unit if out.unit_sign < 0 else unit
+        factors = []
+        for i in range(out.n_factors):
+            factors.append((_decode_buf(out.factors[i]), int(out.mult[i])))
+        return unit, factors
+    finally:
+        lib().ctg_sqf_free(C.byref(out))
+
+
+def gcd_univariate(p: list, q: list, device=None) -> list:
+    """curvetop::gcd_univariate (upoly.hpp:92): primitive gcd with positive leading coefficient."""
+    hp, hq = HostUpoly(p), HostUpoly(q)
+    out = _UpolyBuf()
+    o = _opts(device)
+    _check(lib().ctg_gcd_univariate(C.byref(hp.struct), C.byref(hq.struct), C.byref(out), C.byref(o)),
+           "gcd_univariate")
+    try:
+        return _decode_buf(out)
+    finally:
+        lib().ctg_upoly_free(C.byref(out))
+
+
+def square_free_part(p: list, device=None) -> list:
+    """curvetop::square_free_part (elim.hpp:45)."""
+    hp = HostUpoly(p)
+    out = _UpolyBuf()
+    o = _opts(device)
+    _check(lib().ctg_square_free_part(C.byref(hp.struct), C.byref(out), C.byref(o)), "square_free_part")
+    try:
+        return _decode_buf(out)
+    finally:
+        lib().ctg_upoly_free(C.byref(out))
+
+
+# ----------------------------------------------------------------------------
+# Staged plans (device-resident timing, prime sharding across GPUs)
+# ----------------------------------------------------------------------------
+
+class Plan:
+    """A ``ctg_plan``: fixed primes / points / CRT constants for one resultant.
+
+    Device buffers are provided by the caller as raw pointers (e.g. torch tensors'
+    ``data_ptr()``); streams as raw ``cudaStream_t`` handles (``stream.cuda_stream``).
+    """
+
+    def __init__(self, p: dict, q: dict, var: str = "y", device=None):
+        self._hp, self._hq = HostBipoly(p), HostBipoly(q)
+        self._h = C.c_void_p()
+        o = _opts(device)
+        _check(lib().ctg_plan_create(C.byref(self._hp.struct), C.byref(self._hq.struct),
+                                     1 if var in ("x", "X") else 0, C.byref(o), C.byref(self._h)), "plan_create")
+        info = PlanInfo()
+        _check(lib().ctg_plan_get_info(self._h, C.byref(info)), "plan_info")
+        self.info = info.as_dict()
+
+    def upload(self, stream=0):
+        _check(lib().ctg_plan_upload(self._h, C.c_void_p(stream)), "plan_upload")
+
+    def residues(self, k0, k1, rows_ptr, stream=0):
+        _check(lib().ctg_plan_residues(self._h, k0, k1, C.c_void_p(rows_ptr), C.c_void_p(stream)), "plan_residues")
+
+    def crt(self, all_ptr, j0, j1, out_ptr, stream=0):
+        _check(lib().ctg_plan_crt(self._h, C.c_void_p(all_ptr), j0, j1, C.c_void_p(out_ptr), C.c_void_p(stream)),
+               "plan_crt")
+
+    def check(self, stream=0):
+        _check(lib().ctg_plan_check(self._h, C.c_void_p(stream)), "plan_check")
+
+    def decode(self, host_words: np.ndarray) -> list:
+        host_words = np.ascontiguousarray(host_words, dtype=np.uint32)
+        out = _UpolyBuf()
+        _check(lib().ctg_plan_decode(self._h, C.c_void_p(host_words.ctypes.data), C.byref(out)), "plan_decode")
+        try:
+            return _decode_buf(out)
+        finally:
+            lib().ctg_upoly_free(C.byref(out))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().ctg_plan_launches(self._h))
+
+    def close(self):
+        if self._h:
+            lib().ctg_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

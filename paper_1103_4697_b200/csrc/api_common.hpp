@@ -1,0 +1,99 @@
+// Shared host plumbing of the C ABI: error mapping, device contexts (stream,
+// scratch, pinned staging), call statistics and result buffers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ctg.h"
+
+namespace ctg {
+
+struct ApiError {
+  ctg_status code;
+  std::string msg;
+  ApiError(ctg_status c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+#define CTG_CUDA_CHECK(expr)                                                                        \
+  do {                                                                                              \
+    cudaError_t ctg_err_ = (expr);                                                                  \
+    if (ctg_err_ != cudaSuccess)                                                                    \
+      throw ::ctg::ApiError(CTG_CUDA, std::string("CUDA error: ") + cudaGetErrorString(ctg_err_) + \
+                                          " at " + __FILE__ + ":" + std::to_string(__LINE__));      \
+  } while (0)
+
+void set_last_error(const std::string& msg);
+ctg_call_stats& stats_tls();
+
+template <class F>
+ctg_status guarded(F&& f) {
+  try {
+    f();
+    set_last_error("");
+    return CTG_OK;
+  } catch (const ApiError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return CTG_INTERNAL;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return CTG_INTERNAL;
+  }
+}
+
+// Resolves opts->device (or the current device); throws CTG_CUDA without a device.
+int select_device(const ctg_opts* opts);
+
+// Sets the requested device for the scope of a call and restores the previous one.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const ctg_opts* opts);
+  ~DeviceGuard();
+};
+struct PlanDeviceGuard {
+  int prev = -1;
+  explicit PlanDeviceGuard(int device);
+  ~PlanDeviceGuard();
+};
+
+// Per-device context: one non-blocking stream, grow-only device scratch and pinned staging.
+struct Ctx {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> scratch;
+  std::vector<size_t> scratch_bytes;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  uint32_t* scratch_u32(int slot, size_t words);
+  uint32_t* pinned_u32(size_t words);
+};
+Ctx& context(int device);
+cudaStream_t resolve_stream(int device, void* stream);
+
+struct CallTimer {
+  using clk = std::chrono::steady_clock;
+  clk::time_point t0, t_last;
+  CallTimer();
+  double lap();
+  void mark_setup();
+  void mark_h2d();
+  void mark_device();
+  void finish();
+};
+
+// Decoded coefficient (sign-magnitude), used to fill library-owned result buffers.
+struct UCoeff {
+  int8_t sign = 0;
+  std::vector<uint32_t> limbs;
+};
+// Trims trailing zero coefficients and allocates/fills a ctg_upoly_buf.
+void fill_upoly(const std::vector<UCoeff>& coeffs, ctg_upoly_buf* out);
+
+}  // namespace ctg

@@ -1,0 +1,87 @@
+// Internal declarations shared by the host API (api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ctg.h"
+#include "hostmath.hpp"
+#include "modarith.cuh"
+
+namespace ctg {
+
+// Per-prime constants, one 32-byte record per row of the residue matrix.
+struct PrimeConst {
+  uint32_t p, pneg, r2, one;  // Montgomery constants (modarith.cuh)
+  uint32_t omega;             // primitive N-th root of unity, Montgomery form
+  uint32_t omega_inv;         // its inverse, Montgomery form
+  uint32_t scale;             // N^{-1} mod p, PLAIN (mmul(x_mont, scale) -> plain x*scale)
+  uint32_t crt_c;             // ((M / p)^{-1} mod p) in Montgomery form
+};
+
+constexpr int kFastMaxDeg = 40;     // fast mod-p resultant templates: deg_y p in [2, kFastMaxDeg], deg_y q = deg_y p - 1
+constexpr int kGeneralMaxDeg = 128; // general (formal-degree) kernel limit
+constexpr uint32_t kMaxNtt = 1u << 14;
+constexpr uint32_t kSentinel = 0xffffffffu;
+
+// Device error bits (plan counters[1]).
+enum : uint32_t {
+  kErrFlagOverflow = 1u,   // more degenerate units than the fallback list holds
+  kErrNttTail = 2u,        // interpolated coefficient beyond the degree bound is nonzero
+  kErrCrtRound = 4u,       // fixed-point CRT estimate not near an integer (bound violated)
+  kErrSentinel = 8u,       // an evaluation unit was never resolved
+};
+
+struct CrtTables;  // cached per (device, N, P)
+
+// Slot directory: y-degree j of a polynomial owns slots [off, off + len) of the
+// residue table; slot off + t holds the coefficient of x^t.
+struct SlotDir {
+  std::vector<int32_t> off, len;
+};
+
+struct ResParams {
+  const uint32_t* tab;      // [P][S] Montgomery residues of the slots
+  int S;
+  const PrimeConst* pc;     // [P]
+  int k0;                   // global index of the first prime of this launch
+  uint32_t* rows;           // output rows (k - k0) * pitch
+  int pitch;
+  int N;                    // evaluation points per prime
+  int n, m;                 // formal degrees in y (n >= m)
+  int deriv;                // q == dp/dy: q_j(x) = (j+1) p_{j+1}(x)
+  const int32_t* dir;       // device slot directory: off_p[n+1], len_p[n+1], off_q[m+1], len_q[m+1]
+  uint32_t* flag_list;      // degenerate units (fast path) -> general kernel
+  uint32_t* counters;       // [0] flagged count, [1] error bits
+  uint32_t flag_cap;
+};
+
+struct CrtParams {
+  const uint32_t* rows;  // full residue matrix [P][pitch], plain residues
+  int pitch, P;
+  int j0, J;             // coefficient range
+  const PrimeConst* pc;
+  const double* minv;    // 1/p_k
+  const uint32_t* Mk16;  // [P][L16] 16-bit digits of M / p_k
+  const uint32_t* M16;   // [L16] 16-bit digits of M
+  int L16;
+  uint32_t* Y;           // scratch [P][J]
+  int64_t* tq;           // scratch [J]
+  uint64_t* cols;        // scratch [J][L16]
+  uint32_t* out;         // [J][out_limbs + 1]
+  int out_limbs;
+  uint32_t* counters;
+};
+
+// Kernel launchers (kernels_res.cu).  Each returns the number of launches issued.
+int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0,
+                  int nk, uint32_t* d_tab, cudaStream_t st);
+int launch_modres(const ResParams& rp, int nk, bool fast, cudaStream_t st);
+int launch_interp(uint32_t* rows, int pitch, int nk, const PrimeConst* d_pc, int k0, int N, int r, int a, int D,
+                  int negate, uint32_t* counters, cudaStream_t st);
+int launch_crt(const CrtParams& cp, cudaStream_t st);
+
+}  // namespace ctg
