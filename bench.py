@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py -- res(f, f_y) on B200: mod-p resultants/s and wall ms, vs the reference CPU path.
+
+Metric (BASELINE.json): "res(f,f_y) wall ms + mod-p resultants/s at 1/2/4/8 B200 vs host-CPU ref".
+  value  = mod-p resultants per second over the whole job, inputs resident in HBM
+           (units = P * D per curve: primes x result coefficients);
+  e2e    = the same metric through the reference-facing C ABI (ctg_resultant) with HOST
+           buffers: H2D of the coefficient limbs, all kernels, D2H of the exact result.
+Workload (config.workload): BASELINE.json configs[1], random dense f of total degree 20 with
+64-bit coefficients (synthetic, the §8(d) generator), a batch of curves per step.  The headline
+d=30/128-bit curve is measured once more on its own (key "headline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N     (prime sharding + NCCL)
+  python bench.py --impl reference ...      (the reference CPU implementation, oracle/_ref, all host cores)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "res(f,f_y) wall ms + mod-p resultants/s at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "mod-p resultants/s"
+WORKLOADS = {
+    # name: (kind, a, b, description, units per curve = P * D as planned by libctg)
+    "d20_b64": ("dense", 20, 64, "random dense f, total degree 20, 64-bit coefficients (BASELINE configs[1])",
+                90 * 381),
+    "d30_b128": ("dense", 30, 128, "random dense f, total degree 30, 128-bit coefficients (BASELINE configs[2])",
+                 259 * 871),
+    "d10_b10": ("dense", 10, 10, "random dense f, total degree 10, 10-bit coefficients (BASELINE configs[0])",
+                11 * 91),
+    "d16_b1024": ("dense", 16, 1024, "random dense f, total degree 16, 1024-bit coefficients (BASELINE configs[4])",
+                  1031 * 241),
+}
+REFDRIVER = os.path.join(REPO, "oracle", "_ref", "refdriver")
+CACHED_REF_SECONDS = {"d30_b128": 1662.0, "d16_b1024": 268.0, "d20_b64": 27.2, "d10_b10": 0.020}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="d20_b64", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=32, help="curves per step (seeds 1..B)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-headline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation (oracle/_ref), all host cores
+# ----------------------------------------------------------------------------
+def run_refdriver(kind, a, b, seed, reps=1, yun=False, timeout=None):
+    cmd = [REFDRIVER, "time_res", kind, str(a), str(b), str(seed), str(reps)] + (["yun"] if yun else [])
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    kind, a, b, desc, units = WORKLOADS[args.workload]
+    if not os.path.exists(REFDRIVER):
+        print(json.dumps({"impl": "reference", "unavailable": f"{REFDRIVER} not built (make -C oracle)"}))
+        return 0
+    cores = os.cpu_count() or 1
+    # warm-up: a tiny reference call per step (the CPU has nothing to warm beyond page-in)
+    for _ in range(args.warmup):
+        run_refdriver("dense", 6, 10, 1)
+    walls = []
+    for step in range(args.steps):
+        t0 = time.perf_counter()
+        procs = [subprocess.Popen([REFDRIVER, "time_res", kind, str(a), str(b), str(1 + (step * cores + c) % 64), "1"],
+                                  stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for c in range(cores)]
+        for p in procs:
+            p.wait()
+        walls.append(time.perf_counter() - t0)
+    total = sum(walls)
+    value = args.steps * cores * units / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32 (GMP mpz)",
+        "data": "synthetic", "config": {"workload": desc, "curves_per_step": cores, "seeds": "1..64 cycling",
+                                        "units_per_curve": units},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{cores} curves per step (one per core, independent processes), "
+                                   f"curvetop::resultant(f, f_y, Y) from oracle/_ref/refdriver"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def main_ours(args):
+    import torch
+
+    import paper_1103_4697_b200 as P
+    from paper_1103_4697_b200 import curves
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    kind, a, b, desc, units = WORKLOADS[args.workload]
+    B = args.batch
+
+    # synthetic curves (seeds 1..B) and plans
+    fs = [curves.make(kind, a, b, s) for s in range(1, B + 1)]
+    plans = [P.Plan(f, curves.derive_y(f)) for f in fs]
+    info = plans[0].info
+    Pn, N, D, LM = info["n_primes"], info["n_points"], info["n_coeffs"], info["out_limbs"]
+    assert all(p.info["n_primes"] == Pn and p.info["n_points"] == N for p in plans)
+    assert Pn * D == units, (Pn, D, units)
+    W = LM + 1
+    G = world
+    Pb = (Pn + G - 1) // G
+    k0, k1 = min(rank * Pb, Pn), min((rank + 1) * Pb, Pn)
+    Jb = (D + G - 1) // G
+    j0, j1 = min(rank * Jb, D), min((rank + 1) * Jb, D)
+    for p in plans:
+        p.upload(sh)
+
+    send = torch.zeros((B, Pb, N), dtype=torch.int32, device=dev)
+    full = torch.zeros((G, B, Pb, N), dtype=torch.int32, device=dev) if G > 1 else None
+    out = torch.zeros((B, Jb, W), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def rows_ptr(bi):
+        return send[bi].data_ptr()
+
+    def all_ptr(bi):
+        return (full[0, bi] if G > 1 else send[bi]).data_ptr()
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    stage_ms = [0.0] * 5
+
+    def step(timed=False):
+        if timed:
+            evs[0].record(stream)
+        for s_ in (1, 2, 3):
+            for bi, p in enumerate(plans):
+                p.stage(s_, k0, k1, rows_ptr(bi), sh)
+            if timed:
+                evs[s_].record(stream)
+        if G > 1:
+            dist.all_gather_into_tensor(full, send)
+        if timed:
+            evs[4].record(stream)
+        for bi, p in enumerate(plans):
+            if G > 1:
+                p.crt_sharded(full[:, bi].data_ptr(), Pb, B * Pb * N, j0, j1, out[bi].data_ptr(), sh)
+            else:
+                p.crt(all_ptr(bi), j0, j1, out[bi].data_ptr(), sh)
+        if timed:
+            evs[5].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    for p in plans:
+        p.check(sh)
+    launches0 = sum(p.launches for p in plans)
+
+    # correctness spot check of the device-resident path (curve 0) against the one-shot C-ABI call
+    if G == 1:
+        host = out[0, :D].cpu().numpy().view("uint32")
+        assert plans[0].decode(host) == P.resultant(fs[0], curves.derive_y(fs[0])), "staged != one-shot"
+
+    total_ms = 0.0
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush between timed iterations (outside the events)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            step(timed=True)
+            torch.cuda.synchronize()
+            total_ms += evs[0].elapsed_time(evs[5])
+            for i in range(5):
+                stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
+    gpu_launches = sum(p.launches for p in plans) - launches0
+    t_max = total_ms
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    ms_per_step = t_max / args.steps
+    value = B * units / (ms_per_step * 1e-3)
+
+    # --- e2e through the C ABI with host buffers --------------------------------------
+    hps = [(P.HostBipoly(f), P.HostBipoly(curves.derive_y(f))) for f in fs]
+    e2e_ms, h2d, d2h = None, 0, 0
+    if G == 1:
+        for _ in range(max(1, args.warmup)):
+            for hp, hq in hps:
+                P.resultant_raw(hp, hq)
+        walls = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            h2d = d2h = 0
+            for hp, hq in hps:
+                P.resultant_raw(hp, hq)
+                st = P.last_call_stats()
+                h2d += st["h2d_bytes"]
+                d2h += st["d2h_bytes"]
+            walls.append(time.perf_counter() - t0)
+        e2e_ms = 1e3 * sum(walls) / len(walls)
+    else:
+        e2e_ms, h2d, d2h = e2e_sharded(args, plans, fs, P, curves, torch, dist, send, full, out, Pb, k0, k1, j0, j1,
+                                       D, W, sh, rank)
+    e2e_value = B * units / (e2e_ms * 1e-3)
+
+    # --- roofline of the dominant kernel (stage 2: eval + mod-p resultant) -------------
+    peaks = P.microbench_int(dev)
+    n = info["deg_p"]
+    k3_ms_per_launch = stage_ms[1] / (args.steps * B)
+    units_launch = (k1 - k0) * N
+    imad_launch = 4.0 * units_launch * (n * n + n - 2)
+    achieved = imad_launch / (k3_ms_per_launch * 1e-3) / 1e12
+    peak = peaks["imad_per_s"] / 1e12
+    roofline = {"bound": "int32-imad", "achieved": achieved, "peak": peak, "unit": "TIMAD/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": f"k_modres_fast<{n}> (+ k_modres_general on flagged units)",
+                "algorithmic": f"4 IMAD x (n^2+n-2) mulmods x {units_launch} units per launch, n={n}",
+                "peak_source": "measured live: ctg_microbench_int (8 IMAD chains/thread, all SMs)",
+                "imad_wide_peak_T": peaks["imad_wide_per_s"] / 1e12,
+                "mmul2_peak_G": peaks["mmul2_per_s"] / 1e9,
+                "stage_ms_per_curve": {nm: v / (args.steps * B) for nm, v in
+                                       zip(("reduce", "modres", "interp", "exchange", "crt"), stage_ms)}}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32 (31-bit modular, Montgomery)", "data": "synthetic",
+        "config": {"workload": desc, "curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N,
+                   "coeffs": D, "units_per_curve": units, "parallelism": f"prime-shard{G}" if G > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps",
+                   "res_ms_per_curve": ms_per_step / B},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "res_ms_per_curve": e2e_ms / B, "path": "ctg_resultant (C ABI), host CSR limbs in/out"},
+        "gpu_launches": int(gpu_launches // max(1, args.steps)) * args.steps,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and G == 1 and not args.no_headline:
+        line["headline"] = headline(P, curves)
+    if rank == 0 and G == 1:
+        line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_sharded(args, plans, fs, P, curves, torch, dist, send, full, out, Pb, k0, k1, j0, j1, D, W, sh, rank):
+    """Multi-GPU end-to-end: every rank uploads the inputs, computes its prime rows, all-gathers,
+    reconstructs its coefficient block; rank 0 gathers the exact limbs and decodes on the host."""
+    B = len(plans)
+    G = dist.get_world_size()
+    gathered = torch.zeros((G,) + tuple(out.shape), dtype=torch.int32, device=out.device)
+    walls = []
+    h2d = d2h = 0
+    for it in range(args.warmup + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for bi, p in enumerate(plans):
+            p.upload(sh)
+            p.residues(k0, k1, send[bi].data_ptr(), sh)
+        dist.all_gather_into_tensor(full, send)
+        for bi, p in enumerate(plans):
+            p.crt_sharded(full[:, bi].data_ptr(), Pb, B * Pb * send.shape[2], j0, j1, out[bi].data_ptr(), sh)
+        dist.all_gather_into_tensor(gathered, out)
+        if rank == 0:
+            host = gathered.cpu().numpy().view("uint32")
+            for bi, p in enumerate(plans):
+                words = host[:, bi].reshape(-1, W)[:D]
+                p.decode(words)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            walls.append(time.perf_counter() - t0)
+    h2d = sum(p.h2d_bytes for p in plans) * G
+    d2h = int(gathered.numel() * 4)
+    t = torch.tensor([1e3 * sum(walls) / len(walls)], dtype=torch.float64, device=out.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), h2d, d2h
+
+
+def headline(P, curves):
+    """The north-star config: one d=30 / 128-bit curve through ctg_resultant (host buffers)."""
+    f = curves.make("dense", 30, 128, 1)
+    hp, hq = P.HostBipoly(f), P.HostBipoly(curves.derive_y(f))
+    for _ in range(3):
+        P.resultant_raw(hp, hq)
+    ts, dev = [], []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        P.resultant_raw(hp, hq)
+        ts.append(1e3 * (time.perf_counter() - t0))
+        dev.append(P.last_call_stats()["device_ms"])
+    ms = statistics.median(ts)
+    ref_s = CACHED_REF_SECONDS["d30_b128"]
+    return {"workload": "dense d=30, 128-bit, seed 1 (BASELINE configs[2])", "e2e_ms_median": ms,
+            "device_phase_ms_median": statistics.median(dev),
+            "reference_cpu_s": ref_s, "reference_cpu_source": "SURVEY.md §6.2 (reference, 1 core, not re-run: 28 min)",
+            "speedup_vs_reference_1gpu": ref_s * 1e3 / ms}
+
+
+def cpu_baseline(workload):
+    kind, a, b, desc, units = WORKLOADS[workload]
+    if not os.path.exists(REFDRIVER):
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": "oracle/_ref/refdriver not built", "note": "run make -C oracle"}
+    try:
+        r = run_refdriver(kind, a, b, 1, timeout=300)
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+    secs = r["res_seconds_best"]
+    return {"value": units / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"1 curve {kind}({a},{b},seed=1): curvetop::resultant(f, f_y, Y), 1 thread, {secs:.2f} s",
+            "seconds_per_curve": secs}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -130,6 +130,7 @@ typedef struct {
   int32_t trivial;     /* 1 if the result is fixed by a convention (no GPU work)    */
   double bound_bits;   /* log2 of the Hadamard coefficient bound                    */
   double work_mulmods; /* algorithmic mulmods of the mod-p resultant stage */
+  int64_t h2d_bytes;   /* bytes ctg_plan_upload copies host -> device                */
 } ctg_plan_info;
 
 ctg_status ctg_plan_create(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
@@ -139,10 +140,17 @@ ctg_status ctg_plan_get_info(const ctg_plan* plan, ctg_plan_info* info);
 ctg_status ctg_plan_upload(ctg_plan* plan, void* stream);
 /* Rows [k0, k1) of the residue matrix into d_rows (device, (k1-k0) x n_points words). */
 ctg_status ctg_plan_residues(ctg_plan* plan, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream);
+/* One stage of ctg_plan_residues (for per-kernel timing): 1 = reduce (K1),
+ * 2 = evaluate + mod-p resultant (K2/K3 + the exact fallback), 3 = interpolate (K4). */
+ctg_status ctg_plan_stage(ctg_plan* plan, int32_t stage, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream);
 /* Coefficients [j0, j1) from the full residue matrix d_all (device, n_primes x n_points):
  * d_out gets (j1-j0) x (out_limbs + 1) words: word 0 = sign (as int32), then magnitude limbs. */
 ctg_status ctg_plan_crt(ctg_plan* plan, const uint32_t* d_all, int32_t j0, int32_t j1, uint32_t* d_out,
                         void* stream);
+/* Same, with the residue matrix spread over rank blocks (e.g. the output of an NCCL
+ * all-gather): row k lives at d_all + (k / row_block) * block_stride + (k % row_block) * n_points. */
+ctg_status ctg_plan_crt_sharded(ctg_plan* plan, const uint32_t* d_all, int32_t row_block, int64_t block_stride,
+                                int32_t j0, int32_t j1, uint32_t* d_out, void* stream);
 /* Decode a host copy of the full CRT output (n_coeffs x (out_limbs + 1) words) into a result. */
 ctg_status ctg_plan_decode(ctg_plan* plan, const uint32_t* h_crt, ctg_upoly_buf* out);
 /* Device error flags accumulated by the plan's kernels (0 = clean); synchronizes the stream. */
@@ -150,6 +158,11 @@ ctg_status ctg_plan_check(ctg_plan* plan, void* stream);
 /* Number of kernel launches issued by the plan since creation. */
 int32_t ctg_plan_launches(const ctg_plan* plan);
 void ctg_plan_destroy(ctg_plan* plan);
+
+/* Integer-pipe peak microbenchmarks on `device` (-1 = current): 32-bit IMAD
+ * (a*b+c) and IMAD.WIDE (u32*u32+u64) results per second over all SMs, and
+ * Montgomery two-product reductions (modarith.cuh mmul2) per second. */
+ctg_status ctg_microbench_int(int32_t device, double* imad_per_s, double* imad_wide_per_s, double* mmul2_per_s);
 
 #ifdef __cplusplus
 }

@@ -88,7 +88,7 @@ class CallStats(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("n_primes", C.c_int32), ("n_points", C.c_int32), ("n_coeffs", C.c_int32), ("out_limbs", C.c_int32),
                 ("deg_p", C.c_int32), ("deg_q", C.c_int32), ("derivative", C.c_int32), ("trivial", C.c_int32),
-                ("bound_bits", C.c_double), ("work_mulmods", C.c_double)]
+                ("bound_bits", C.c_double), ("work_mulmods", C.c_double), ("h2d_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -99,7 +99,8 @@ EXPORTS = (
     "ctg_resultant", "ctg_yun_squarefree", "ctg_gcd_univariate", "ctg_square_free_part", "ctg_upoly_free",
     "ctg_sqf_free", "ctg_last_error", "ctg_abi_version", "ctg_device_count", "ctg_last_call_stats",
     "ctg_plan_create", "ctg_plan_get_info", "ctg_plan_upload", "ctg_plan_residues", "ctg_plan_crt",
-    "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy",
+    "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy", "ctg_plan_stage",
+    "ctg_microbench_int", "ctg_plan_crt_sharded",
 )
 
 _lib = None
@@ -133,7 +134,12 @@ def lib():
         L.ctg_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
         L.ctg_plan_upload.argtypes = [C.c_void_p, C.c_void_p]
         L.ctg_plan_residues.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_plan_stage.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_microbench_int.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]
         L.ctg_plan_crt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_plan_crt_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                           C.c_void_p, C.c_void_p]
         L.ctg_plan_decode.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_UpolyBuf)]
         L.ctg_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.ctg_plan_launches.argtypes = [C.c_void_p]
@@ -228,6 +234,14 @@ def last_call_stats() -> dict:
     return s.as_dict()
 
 
+def microbench_int(device=None) -> dict:
+    """Measured integer-pipe peaks (results/s): IMAD, IMAD.WIDE, Montgomery two-product reductions."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().ctg_microbench_int(-1 if device is None else int(device), C.byref(a), C.byref(b), C.byref(c)),
+           "microbench")
+    return {"imad_per_s": a.value, "imad_wide_per_s": b.value, "mmul2_per_s": c.value}
+
+
 def device_count() -> int:
     return int(lib().ctg_device_count())
 
@@ -246,6 +260,18 @@ def resultant_host(p: HostBipoly, q: HostBipoly, var: str = "y", device=None) ->
         return _decode_buf(out)
     finally:
         lib().ctg_upoly_free(C.byref(out))
+
+
+def resultant_raw(p: HostBipoly, q: HostBipoly, var: str = "y", device=None) -> int:
+    """ctg_resultant into a library buffer that is freed again (no Python-int decoding):
+    the C-ABI call a C/C++ caller makes.  Returns the number of result coefficients."""
+    out = _UpolyBuf()
+    o = _opts(device)
+    _check(lib().ctg_resultant(C.byref(p.struct), C.byref(q.struct), 1 if var in ("x", "X") else 0, C.byref(out),
+                               C.byref(o)), "resultant")
+    n = out.n_coeffs
+    lib().ctg_upoly_free(C.byref(out))
+    return n
 
 
 def resultant(p: dict, q: dict, var: str = "y", device=None) -> list:
@@ -329,9 +355,20 @@ class Plan:
     def residues(self, k0, k1, rows_ptr, stream=0):
         _check(lib().ctg_plan_residues(self._h, k0, k1, C.c_void_p(rows_ptr), C.c_void_p(stream)), "plan_residues")
 
+    def stage(self, stage, k0, k1, rows_ptr, stream=0):
+        _check(lib().ctg_plan_stage(self._h, stage, k0, k1, C.c_void_p(rows_ptr), C.c_void_p(stream)), "plan_stage")
+
     def crt(self, all_ptr, j0, j1, out_ptr, stream=0):
         _check(lib().ctg_plan_crt(self._h, C.c_void_p(all_ptr), j0, j1, C.c_void_p(out_ptr), C.c_void_p(stream)),
                "plan_crt")
+
+    def crt_sharded(self, all_ptr, row_block, block_stride, j0, j1, out_ptr, stream=0):
+        _check(lib().ctg_plan_crt_sharded(self._h, C.c_void_p(all_ptr), row_block, block_stride, j0, j1,
+                                          C.c_void_p(out_ptr), C.c_void_p(stream)), "plan_crt_sharded")
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(self.info["h2d_bytes"])
 
     def check(self, stream=0):
         _check(lib().ctg_plan_check(self._h, C.c_void_p(stream)), "plan_check")

@@ -324,13 +324,25 @@ int64_t plan_h2d_bytes(const ctg_plan* pl) {
   return static_cast<int64_t>(sizeof(uint32_t) * pl->h_limbs.size() + pl->h_sign.size() + 4 * pl->dir.size());
 }
 
-void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, cudaStream_t st) {
+void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, cudaStream_t st) {
   if (pl->trivial) return;
   if (!pl->uploaded) throw ApiError(CTG_INVALID, "plan: inputs not uploaded");
   if (k0 < 0 || k1 > pl->P || k0 > k1) throw ApiError(CTG_INVALID, "plan: prime range out of bounds");
+  if (stage < 1 || stage > 3) throw ApiError(CTG_INVALID, "plan: stage must be 1, 2 or 3");
   const int nk = k1 - k0;
   if (nk == 0) return;
-  pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, k0, nk, pl->d_tab, st);
+  if (stage == 1) {
+    pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, k0, nk, pl->d_tab, st);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
+  if (stage == 3) {
+    pl->launches += launch_interp(d_rows, static_cast<int>(pl->N), nk, pl->tabs->d_pc, k0, static_cast<int>(pl->N),
+                                  static_cast<int>(pl->r), static_cast<int>(pl->a), static_cast<int>(pl->D),
+                                  pl->negate, pl->d_counters, st);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t), st));
   ResParams rp{};
   rp.tab = pl->d_tab;
@@ -348,13 +360,15 @@ void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, cudaStream_t 
   rp.counters = pl->d_counters;
   rp.flag_cap = pl->flag_cap;
   pl->launches += launch_modres(rp, nk, true, st);
-  pl->launches += launch_interp(d_rows, static_cast<int>(pl->N), nk, pl->tabs->d_pc, k0, static_cast<int>(pl->N),
-                                static_cast<int>(pl->r), static_cast<int>(pl->a), static_cast<int>(pl->D),
-                                pl->negate, pl->d_counters, st);
   CTG_CUDA_CHECK(cudaGetLastError());
 }
 
-void plan_crt(ctg_plan* pl, const uint32_t* d_all, int j0, int j1, uint32_t* d_out, cudaStream_t st) {
+void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, cudaStream_t st) {
+  for (int stage = 1; stage <= 3; ++stage) plan_stage(pl, stage, k0, k1, d_rows, st);
+}
+
+void plan_crt(ctg_plan* pl, const uint32_t* d_all, int j0, int j1, uint32_t* d_out, cudaStream_t st,
+              int row_block = 0, long long block_stride = 0) {
   if (pl->trivial) return;
   if (j0 < 0 || j1 > static_cast<int>(pl->D) || j0 > j1) throw ApiError(CTG_INVALID, "plan: coefficient range out of bounds");
   const int J = j1 - j0;
@@ -372,6 +386,8 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, int j0, int j1, uint32_t* d_o
   cp.rows = d_all;
   cp.pitch = static_cast<int>(pl->N);
   cp.P = pl->P;
+  cp.row_block = row_block > 0 ? row_block : pl->P;
+  cp.block_stride = row_block > 0 ? block_stride : 0;
   cp.j0 = j0;
   cp.J = J;
   cp.pc = pl->tabs->d_pc;
@@ -446,6 +462,7 @@ ctg_status ctg_plan_get_info(const ctg_plan* pl, ctg_plan_info* info) {
     info->bound_bits = pl->bound_bits;
     const double n = pl->n;
     info->work_mulmods = static_cast<double>(pl->P) * pl->D * (n * n + n - 2);
+    info->h2d_bytes = plan_h2d_bytes(pl);
   });
 }
 
@@ -465,11 +482,29 @@ ctg_status ctg_plan_residues(ctg_plan* pl, int32_t k0, int32_t k1, uint32_t* d_r
   });
 }
 
+ctg_status ctg_plan_stage(ctg_plan* pl, int32_t stage, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream) {
+  return guarded([&] {
+    if (!pl) throw ApiError(CTG_INVALID, "plan: null");
+    PlanDeviceGuard g(pl->device);
+    plan_stage(pl, stage, k0, k1, d_rows, resolve_stream(pl->device, stream));
+  });
+}
+
 ctg_status ctg_plan_crt(ctg_plan* pl, const uint32_t* d_all, int32_t j0, int32_t j1, uint32_t* d_out, void* stream) {
   return guarded([&] {
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");
     PlanDeviceGuard g(pl->device);
     plan_crt(pl, d_all, j0, j1, d_out, resolve_stream(pl->device, stream));
+  });
+}
+
+ctg_status ctg_plan_crt_sharded(ctg_plan* pl, const uint32_t* d_all, int32_t row_block, int64_t block_stride,
+                                int32_t j0, int32_t j1, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    if (!pl) throw ApiError(CTG_INVALID, "plan: null");
+    if (row_block <= 0 || block_stride < 0) throw ApiError(CTG_INVALID, "plan: bad row_block / block_stride");
+    PlanDeviceGuard g(pl->device);
+    plan_crt(pl, d_all, j0, j1, d_out, resolve_stream(pl->device, stream), row_block, block_stride);
   });
 }
 

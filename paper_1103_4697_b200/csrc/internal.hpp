@@ -60,8 +60,11 @@ struct ResParams {
 };
 
 struct CrtParams {
-  const uint32_t* rows;  // full residue matrix [P][pitch], plain residues
+  const uint32_t* rows;  // full residue matrix, plain residues; row k at
+                         // rows + (k / row_block) * block_stride + (k % row_block) * pitch
   int pitch, P;
+  int row_block;
+  long long block_stride;
   int j0, J;             // coefficient range
   const PrimeConst* pc;
   const double* minv;    // 1/p_k

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(256) k_crt_prep(CrtParams C) {
     for (int k = ty; k < C.P; k += 8) {
       const PrimeConst& pcv = C.pc[k];
       const Mod M = load_mod(pcv);
-      const uint32_t v = C.rows[static_cast<size_t>(k) * C.pitch + C.j0 + jl];
+      const uint32_t v = C.rows[static_cast<long long>(k / C.row_block) * C.block_stride +
+                                static_cast<long long>(k % C.row_block) * C.pitch + C.j0 + jl];
       const uint32_t y = mmul(v, pcv.crt_c, M);
       C.Y[static_cast<size_t>(k) * C.J + jl] = y;
       u += static_cast<double>(y) * C.minv[k];
