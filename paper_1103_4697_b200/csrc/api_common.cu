@@ -93,6 +93,12 @@ Ctx& context(int device) {
     cudaGetDevice(&prev);
     CTG_CUDA_CHECK(cudaSetDevice(device));
     CTG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // Keep stream-ordered allocations cached in the pool between calls.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     cudaSetDevice(prev);
   }
   return *c;

@@ -25,27 +25,7 @@
 
 namespace ctg {
 
-// ---------------------------------------------------------------------------
-// Cached per-(device, N, P) prime tables and CRT constants.
-// ---------------------------------------------------------------------------
-struct CrtTables {
-  int device = -1;
-  uint32_t N = 0;
-  int P = 0;
-  int LM = 0, L16 = 0;
-  std::vector<uint32_t> primes;
-  PrimeConst* d_pc = nullptr;
-  double* d_minv = nullptr;
-  uint32_t* d_Mk16 = nullptr;
-  uint32_t* d_M16 = nullptr;
-  ~CrtTables() {
-    cudaFree(d_pc);
-    cudaFree(d_minv);
-    cudaFree(d_Mk16);
-    cudaFree(d_M16);
-  }
-};
-
+// Cached per-(device, N, P) prime tables for the resultant path.
 static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, int P, const std::vector<uint32_t>& primes) {
   static std::mutex mu;
   static std::map<std::tuple<int, uint32_t, int>, std::shared_ptr<CrtTables>> cache;
@@ -53,57 +33,7 @@ static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, int P, cons
   auto key = std::make_tuple(device, N, P);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-
-  auto T = std::make_shared<CrtTables>();
-  T->device = device;
-  T->N = N;
-  T->P = P;
-  T->primes = primes;
-  // M = prod p_k
-  Big Mb{1u};
-  for (uint32_t p : primes) Mb = big_mul_u32(Mb, p);
-  T->LM = static_cast<int>(Mb.size());
-  T->L16 = 2 * T->LM;
-  std::vector<PrimeConst> pc(P);
-  std::vector<double> minv(P);
-  std::vector<uint32_t> Mk16(static_cast<size_t>(P) * T->L16, 0u), M16(T->L16, 0u);
-  for (int l = 0; l < T->LM; ++l) {
-    M16[2 * l] = Mb[l] & 0xffffu;
-    M16[2 * l + 1] = Mb[l] >> 16;
-  }
-  for (int k = 0; k < P; ++k) {
-    const uint32_t p = primes[k];
-    Mod M = make_mod(p);
-    PrimeConst& c = pc[k];
-    c.p = M.p;
-    c.pneg = M.pneg;
-    c.r2 = M.r2;
-    c.one = M.one;
-    const uint32_t g = primitive_root(p);
-    const uint32_t w = pow_mod_u32(g, (p - 1) / N, p);
-    const uint32_t wi = inv_mod_u32(w, p);
-    c.omega = static_cast<uint32_t>((static_cast<uint64_t>(w) << 32) % p);
-    c.omega_inv = static_cast<uint32_t>((static_cast<uint64_t>(wi) << 32) % p);
-    c.scale = inv_mod_u32(N % p, p);
-    uint32_t rem = 0;
-    Big Mk = big_div_u32(Mb, p, &rem);
-    const uint32_t mk_mod = big_mod_u32(Mk.data(), static_cast<int>(Mk.size()), p);
-    const uint32_t ck = inv_mod_u32(mk_mod, p);
-    c.crt_c = static_cast<uint32_t>((static_cast<uint64_t>(ck) << 32) % p);
-    minv[k] = 1.0 / static_cast<double>(p);
-    for (size_t l = 0; l < Mk.size(); ++l) {
-      Mk16[static_cast<size_t>(k) * T->L16 + 2 * l] = Mk[l] & 0xffffu;
-      Mk16[static_cast<size_t>(k) * T->L16 + 2 * l + 1] = Mk[l] >> 16;
-    }
-  }
-  CTG_CUDA_CHECK(cudaMalloc(&T->d_pc, sizeof(PrimeConst) * P));
-  CTG_CUDA_CHECK(cudaMalloc(&T->d_minv, sizeof(double) * P));
-  CTG_CUDA_CHECK(cudaMalloc(&T->d_Mk16, sizeof(uint32_t) * Mk16.size()));
-  CTG_CUDA_CHECK(cudaMalloc(&T->d_M16, sizeof(uint32_t) * M16.size()));
-  CTG_CUDA_CHECK(cudaMemcpy(T->d_pc, pc.data(), sizeof(PrimeConst) * P, cudaMemcpyHostToDevice));
-  CTG_CUDA_CHECK(cudaMemcpy(T->d_minv, minv.data(), sizeof(double) * P, cudaMemcpyHostToDevice));
-  CTG_CUDA_CHECK(cudaMemcpy(T->d_Mk16, Mk16.data(), sizeof(uint32_t) * Mk16.size(), cudaMemcpyHostToDevice));
-  CTG_CUDA_CHECK(cudaMemcpy(T->d_M16, M16.data(), sizeof(uint32_t) * M16.size(), cudaMemcpyHostToDevice));
+  auto T = build_tables(device, primes, N);
   cache[key] = T;
   return T;
 }

@@ -1,14 +1,545 @@
-// Univariate entry points (Yun / gcd / square-free part): implemented in the next milestone.
+// C ABI of the modular univariate path: gcd_univariate, yun_squarefree, square_free_part.
+//
+//   ctg_gcd_univariate    replaces curvetop::gcd_univariate  (/root/reference/proj/src/elim.cpp:80-93)
+//   ctg_yun_squarefree    replaces curvetop::yun_squarefree  (elim.cpp:138-165)
+//   ctg_square_free_part  replaces curvetop::square_free_part (elim.cpp:204-210)
+//
+// Method: images modulo many 31-bit primes on the GPU
+// (K1 reduce, K6 per-prime gcd / Yun), lucky-prime selection by degree pattern,
+// CRT of leading-coefficient-scaled images (K5), then an exactness certificate:
+//   gcd:  g U = e A and g W = e B hold modulo every CRT prime by construction; the
+//         norm bounds ||g||_1 ||U||_1 < M/2 and |e| ||A||_inf < M/2 make them exact
+//         over Z, so g | A, g | B, and deg g = min mod-p degree >= deg gcd(A, B).
+//   Yun:  P = prod r_m^m modulo every CRT prime iff prod lc(r_m)^m = lc(P) (checked
+//         exactly); with sum_m m log||r_m||_1 < log(M/2) the identity is exact.  The r_m
+//         are square-free and pairwise coprime modulo a prime not dividing their leading
+//         coefficients, hence over Q, so this is THE primitive square-free decomposition
+//         the reference returns (it is unique).
+// Host work is limited to marshaling, contents (integer gcds of coefficients) and
+// the certificate arithmetic on leading coefficients; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
 #include "api_common.hpp"
+#include "internal.hpp"
+#include "uni_internal.hpp"
+
+namespace ctg {
+namespace {
+
+using ZPoly = std::vector<SBig>;  // low -> high, trimmed
+
+ZPoly parse_upoly(const ctg_upoly* p) {
+  ZPoly out;
+  if (!p || p->n_coeffs == 0) return out;
+  if (p->n_coeffs < 0 || !p->sign || !p->limb_off || (!p->limbs && p->limb_off[p->n_coeffs] > 0))
+    throw ApiError(CTG_INVALID, "upoly: null pointer or negative coefficient count");
+  out.resize(p->n_coeffs);
+  for (int i = 0; i < p->n_coeffs; ++i) {
+    const uint32_t b = p->limb_off[i], e = p->limb_off[i + 1];
+    if (e < b) throw ApiError(CTG_INVALID, "upoly: limb_off not monotone");
+    const int s = p->sign[i];
+    if (s < -1 || s > 1) throw ApiError(CTG_INVALID, "upoly: sign must be -1, 0 or +1");
+    sbig_add_inplace(out[i], s, p->limbs + b, static_cast<int>(e - b));
+  }
+  while (!out.empty() && out.back().sign == 0) out.pop_back();
+  return out;
+}
+
+int zdeg(const ZPoly& p) { return static_cast<int>(p.size()) - 1; }
+
+// Positive gcd of all coefficients, stopping at 1 (upoly.cpp:59-66).
+Big zcontent(const ZPoly& p) {
+  Big g;
+  for (const auto& c : p) {
+    if (c.sign == 0) continue;
+    g = g.empty() ? c.mag : big_gcd(g, c.mag);
+    if (big_is_one(g)) break;
+  }
+  return g;
+}
+
+// p / (s * c) for the content c and s = sign(lc p): primitive with positive leading coefficient.
+ZPoly zprimitive_positive(const ZPoly& p, Big* content = nullptr, int* lcsign = nullptr) {
+  if (p.empty()) return p;
+  Big c = zcontent(p);
+  const int s = p.back().sign;
+  if (content) *content = c;
+  if (lcsign) *lcsign = s;
+  ZPoly q(p.size());
+  const bool unit = big_is_one(c);
+  for (size_t i = 0; i < p.size(); ++i) {
+    if (p[i].sign == 0) continue;
+    q[i].sign = p[i].sign * s;
+    q[i].mag = unit ? p[i].mag : big_divexact(p[i].mag, c);
+  }
+  return q;
+}
+
+double zlog2_l2(const ZPoly& p) {
+  std::vector<double> sq;
+  for (const auto& c : p)
+    if (c.sign) sq.push_back(2 * big_log2(c.mag));
+  return 0.5 * log2_sum_upper(sq);
+}
+double zlog2_l1(const ZPoly& p) {
+  std::vector<double> v;
+  for (const auto& c : p)
+    if (c.sign) v.push_back(big_log2(c.mag));
+  return log2_sum_upper(v);
+}
+double zlog2_linf(const ZPoly& p) {
+  double m = -INFINITY;
+  for (const auto& c : p)
+    if (c.sign) m = std::max(m, big_log2(c.mag));
+  return m;
+}
+
+std::vector<UCoeff> to_ucoeffs(const ZPoly& p) {
+  std::vector<UCoeff> out(p.size());
+  for (size_t i = 0; i < p.size(); ++i) {
+    out[i].sign = static_cast<int8_t>(p[i].sign);
+    out[i].limbs = p[i].mag;
+  }
+  return out;
+}
+
+// Device scratch owned by one call (stream-ordered allocations from the default pool).
+struct DevArena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit DevArena(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    CTG_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(T), st));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~DevArena() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+struct Launches {
+  int n = 0;
+};
+
+// Residues of a primitive polynomial modulo every prime of `tabs` (K1): [P][n+1] Montgomery.
+uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
+  const int S = static_cast<int>(p.size());
+  int Lw = 1;
+  for (const auto& c : p) Lw = std::max<int>(Lw, static_cast<int>(c.mag.size()));
+  std::vector<uint32_t> limbs(static_cast<size_t>(Lw) * S, 0u);
+  std::vector<int8_t> sign(S, 0);
+  for (int s = 0; s < S; ++s) {
+    sign[s] = static_cast<int8_t>(p[s].sign);
+    for (size_t l = 0; l < p[s].mag.size(); ++l) limbs[l * S + s] = p[s].mag[l];
+  }
+  uint32_t* d_limbs = ar.alloc<uint32_t>(limbs.size());
+  int8_t* d_sign = ar.alloc<int8_t>(S);
+  uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_limbs, limbs.data(), 4 * limbs.size(), cudaMemcpyHostToDevice, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_sign, sign.data(), S, cudaMemcpyHostToDevice, ar.st));
+  L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, 0, tabs.P, d_tab, ar.st);
+  auto& st = stats_tls();
+  st.h2d_bytes += static_cast<int64_t>(4 * limbs.size() + S);
+  return d_tab;
+}
+
+// Gather rows `lucky` of d_src (plain residues, pitch src_pitch), scale segment s of row r
+// by scale[r][s] (plain), CRT the first `cols` columns over the lucky primes.
+ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::vector<int>& lucky,
+               const std::vector<uint32_t>& primes, int cols, const std::vector<int32_t>& seg_end,
+               const std::vector<uint32_t>& scale_plain, int device, double* log2M, Launches& L) {
+  std::vector<uint32_t> lp;
+  for (int k : lucky) lp.push_back(primes[k]);
+  auto T = build_tables(device, lp, 1);
+  const int R = static_cast<int>(lp.size());
+  const int nseg = static_cast<int>(seg_end.size());
+  std::vector<uint32_t> scale_m(static_cast<size_t>(R) * nseg);
+  for (int r = 0; r < R; ++r)
+    for (int s = 0; s < nseg; ++s)
+      scale_m[static_cast<size_t>(r) * nseg + s] =
+          static_cast<uint32_t>((static_cast<uint64_t>(scale_plain[static_cast<size_t>(r) * nseg + s] % lp[r]) << 32) %
+                                lp[r]);
+  int32_t* d_idx = ar.alloc<int32_t>(R);
+  int32_t* d_seg = ar.alloc<int32_t>(nseg);
+  uint32_t* d_scale = ar.alloc<uint32_t>(scale_m.size());
+  uint32_t* d_rows = ar.alloc<uint32_t>(static_cast<size_t>(R) * cols);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_idx, lucky.data(), 4 * R, cudaMemcpyHostToDevice, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_seg, seg_end.data(), 4 * nseg, cudaMemcpyHostToDevice, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_scale, scale_m.data(), 4 * scale_m.size(), cudaMemcpyHostToDevice, ar.st));
+  L.n += launch_gather_scale(d_src, src_pitch, d_idx, R, cols, d_seg, nseg, d_scale, T->d_pc, d_rows, ar.st);
+  const int W = T->LM + 1;
+  uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(cols) * W);
+  uint32_t* d_Y = ar.alloc<uint32_t>(static_cast<size_t>(R) * cols);
+  int64_t* d_tq = ar.alloc<int64_t>(cols);
+  uint64_t* d_cols = ar.alloc<uint64_t>(static_cast<size_t>(T->L16) * cols);
+  uint32_t* d_cnt = ar.alloc<uint32_t>(4);
+  CTG_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 16, ar.st));
+  CrtParams cp{};
+  cp.rows = d_rows;
+  cp.pitch = cols;
+  cp.P = R;
+  cp.row_block = R;
+  cp.block_stride = 0;
+  cp.j0 = 0;
+  cp.J = cols;
+  cp.pc = T->d_pc;
+  cp.minv = T->d_minv;
+  cp.Mk16 = T->d_Mk16;
+  cp.M16 = T->d_M16;
+  cp.L16 = T->L16;
+  cp.Y = d_Y;
+  cp.tq = d_tq;
+  cp.cols = d_cols;
+  cp.out = d_out;
+  cp.out_limbs = T->LM;
+  cp.counters = d_cnt;
+  L.n += launch_crt(cp, ar.st);
+  CTG_CUDA_CHECK(cudaGetLastError());
+  std::vector<uint32_t> h(static_cast<size_t>(cols) * W + 4);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_out, 4 * static_cast<size_t>(cols) * W, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(h.data() + static_cast<size_t>(cols) * W, d_cnt, 16, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+  stats_tls().d2h_bytes += static_cast<int64_t>(4 * h.size());
+  if (h[static_cast<size_t>(cols) * W + 1]) throw ApiError(CTG_INTERNAL, "CRT self-check failed (bound exceeded)");
+  ZPoly out(cols);
+  for (int j = 0; j < cols; ++j) {
+    const uint32_t* rec = h.data() + static_cast<size_t>(j) * W;
+    int n = W - 1;
+    while (n > 0 && rec[n] == 0) --n;
+    out[j].sign = static_cast<int32_t>(rec[0]);
+    out[j].mag.assign(rec + 1, rec + 1 + n);
+    if (out[j].mag.empty()) out[j].sign = 0;
+  }
+  *log2M = T->log2M;
+  return out;
+}
+
+ZPoly slice(const ZPoly& p, int a, int b) {
+  ZPoly r(p.begin() + a, p.begin() + b);
+  while (!r.empty() && r.back().sign == 0) r.pop_back();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Yun over Z via per-prime Yun (K6) + CRT (K5) + certificate.
+// ---------------------------------------------------------------------------
+struct YunResult {
+  std::vector<std::pair<ZPoly, int>> factors;
+  ZPoly sqfp;
+};
+
+struct YunImages {
+  std::vector<uint32_t> primes;
+  std::vector<int32_t> deg;  // [P][n+1]
+  uint32_t* d_fac = nullptr;
+  uint32_t* d_sqf = nullptr;
+};
+
+YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& primes, int device, Launches& L) {
+  const int n = zdeg(P);
+  auto T = build_tables(device, primes, 1);
+  uint32_t* d_tab = reduce_poly(ar, P, *T, L);
+  const int nk = static_cast<int>(primes.size());
+  YunImages im;
+  im.primes = primes;
+  int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * (n + 1));
+  im.d_fac = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (2 * n + 2));
+  im.d_sqf = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (n + 1));
+  L.n += launch_modyun(d_tab, n, T->d_pc, nk, d_deg, im.d_fac, im.d_sqf, ar.st);
+  CTG_CUDA_CHECK(cudaGetLastError());
+  im.deg.resize(static_cast<size_t>(nk) * (n + 1));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(im.deg.data(), d_deg, 4 * im.deg.size(), cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+  stats_tls().d2h_bytes += static_cast<int64_t>(4 * im.deg.size());
+  return im;
+}
+
+YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t st, Launches& L) {
+  const int n = zdeg(P);
+  if (n > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "yun: degree exceeds 6000");
+  DevArena ar(st);
+  YunResult res;
+  // Probe: a square-free P is certified by one prime p with p !| lc(P) and deg gcd(P, P') = 0 mod p.
+  {
+    std::vector<uint32_t> probe = select_primes(1, 3 * 30.0);
+    YunImages im = run_modyun(ar, P, probe, device, L);
+    for (size_t k = 0; k < probe.size(); ++k) {
+      const int32_t* d = im.deg.data() + k * (n + 1);
+      if (d[0] == 0 && d[1] == n) {
+        res.factors.push_back({P, 1});
+        res.sqfp = P;
+        return res;
+      }
+    }
+  }
+  const Big& lcP = P.back().mag;
+  const double need = big_log2(lcP) + n + zlog2_l2(P) + 2 + 40;
+  double extra = 62;
+  for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
+    std::vector<uint32_t> primes = select_primes(1, need + extra);
+    const int nk = static_cast<int>(primes.size());
+    YunImages im = run_modyun(ar, P, primes, device, L);
+    // lucky pattern: maximal square-free-part degree, then the most frequent pattern
+    std::map<std::vector<int32_t>, std::vector<int>> by_pattern;
+    int best_sd = -1;
+    for (int k = 0; k < nk; ++k) {
+      const int32_t* d = im.deg.data() + static_cast<size_t>(k) * (n + 1);
+      if (d[0] != 0) continue;
+      int sd = 0;
+      for (int m = 1; m <= n; ++m) sd += d[m];
+      if (sd > best_sd) {
+        best_sd = sd;
+        by_pattern.clear();
+      }
+      if (sd == best_sd) by_pattern[std::vector<int32_t>(d + 1, d + n + 1)].push_back(k);
+    }
+    if (by_pattern.empty()) continue;
+    auto best = by_pattern.begin();
+    for (auto it = by_pattern.begin(); it != by_pattern.end(); ++it)
+      if (it->second.size() > best->second.size()) best = it;
+    const std::vector<int32_t>& pat = best->first;
+    const std::vector<int>& lucky = best->second;
+    double bits = 0;
+    for (int k : lucky) bits += std::log2(static_cast<double>(primes[k]));
+    if (bits < need) continue;
+    // CRT of lc(P) * monic factor images, concatenated in increasing multiplicity.
+    std::vector<std::pair<int, int>> fm;  // (multiplicity, degree)
+    int cols = 0;
+    for (int m = 1; m <= n; ++m)
+      if (pat[m - 1] > 0) {
+        fm.push_back({m, pat[m - 1]});
+        cols += pat[m - 1] + 1;
+      }
+    std::vector<uint32_t> scale;
+    for (int k : lucky) scale.push_back(big_mod(lcP, primes[k]));
+    double log2M = 0;
+    ZPoly H = crt_rows(ar, im.d_fac, 2 * n + 2, lucky, primes, cols, {cols}, scale, device, &log2M, L);
+    // r_m = pp(H_m); certificate
+    int off = 0, degsum = 0;
+    Big lcprod{1u};
+    double normsum = 0;
+    for (auto [m, dm] : fm) {
+      ZPoly Hm = slice(H, off, off + dm + 1);
+      off += dm + 1;
+      if (zdeg(Hm) != dm) throw ApiError(CTG_INTERNAL, "yun: factor degree mismatch after CRT");
+      ZPoly rm = zprimitive_positive(Hm);
+      degsum += m * dm;
+      for (int e = 0; e < m; ++e) lcprod = big_mul(lcprod, rm.back().mag);
+      normsum += m * zlog2_l1(rm);
+      res.factors.push_back({std::move(rm), m});
+    }
+    const bool ok = degsum == n && big_cmp(lcprod, lcP) == 0 && normsum + 1 < log2M - 1 &&
+                    zlog2_linf(P) + 1 < log2M - 1;
+    if (!ok) throw ApiError(CTG_INTERNAL, "yun: exactness certificate failed");
+    if (want_sqfp) {
+      // sqfp = prod r_m: CRT of L * v_p with L = prod lc(r_m) (v_p = monic square-free part mod p).
+      Big Lc{1u};
+      double l1 = 0;
+      int ds = 0;
+      for (auto& f : res.factors) {
+        Lc = big_mul(Lc, f.first.back().mag);
+        l1 += zlog2_l1(f.first);
+        ds += zdeg(f.first);
+      }
+      std::vector<uint32_t> sc;
+      for (int k : lucky) sc.push_back(big_mod(Lc, primes[k]));
+      double log2M2 = 0;
+      ZPoly S = crt_rows(ar, im.d_sqf, n + 1, lucky, primes, ds + 1, {ds + 1}, sc, device, &log2M2, L);
+      if (zdeg(S) != ds || big_cmp(S.back().mag, Lc) != 0 || S.back().sign != 1 || !(l1 + 1 < log2M2 - 1))
+        throw ApiError(CTG_INTERNAL, "square_free_part: exactness certificate failed");
+      res.sqfp = std::move(S);
+    }
+    return res;
+  }
+  throw ApiError(CTG_INTERNAL, "yun: could not find enough lucky primes");
+}
+
+// ---------------------------------------------------------------------------
+// gcd over Z via per-prime gcd + cofactors (K6) + CRT (K5) + certificate.
+// ---------------------------------------------------------------------------
+ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, Launches& L) {
+  const int na = zdeg(A), nb = zdeg(B);
+  if (std::max(na, nb) > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "gcd: degree exceeds 6000");
+  DevArena ar(st);
+  const Big gamma = big_gcd(A.back().mag, B.back().mag);
+  const double lg = big_log2(gamma), la = zlog2_l2(A), lb = zlog2_l2(B);
+  const double need = std::max({lg + std::min(na, nb) + std::min(la, lb), lg + na + la, lg + nb + lb}) + 2 + 40;
+  double extra = 62;
+  for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
+    std::vector<uint32_t> primes = select_primes(1, need + extra);
+    const int nk = static_cast<int>(primes.size());
+    auto T = build_tables(device, primes, 1);
+    uint32_t* tA = reduce_poly(ar, A, *T, L);
+    uint32_t* tB = reduce_poly(ar, B, *T, L);
+    const int pitch = na + nb + 3;
+    int32_t* d_deg = ar.alloc<int32_t>(nk);
+    uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(nk) * pitch);
+    L.n += launch_modgcd(tA, na, tB, nb, T->d_pc, nk, d_deg, d_out, pitch, ar.st);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    std::vector<int32_t> deg(nk);
+    CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * nk, cudaMemcpyDeviceToHost, ar.st));
+    CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+    int dmin = INT32_MAX;
+    for (int d : deg)
+      if (d >= 0) dmin = std::min(dmin, d);
+    if (dmin == INT32_MAX) continue;
+    if (dmin == 0) return ZPoly{SBig{1, Big{1u}}};  // coprime modulo a prime not dividing lc(A) lc(B)
+    std::vector<int> lucky;
+    double bits = 0;
+    for (int k = 0; k < nk; ++k)
+      if (deg[k] == dmin) {
+        lucky.push_back(k);
+        bits += std::log2(static_cast<double>(primes[k]));
+      }
+    if (bits < need) continue;
+    const int cg = dmin + 1, cu = na - dmin + 1, cw = nb - dmin + 1;
+    std::vector<uint32_t> scale;
+    for (int k : lucky) {
+      scale.push_back(big_mod(gamma, primes[k]));
+      scale.push_back(1u);
+    }
+    double log2M = 0;
+    ZPoly all = crt_rows(ar, d_out, pitch, lucky, primes, cg + cu + cw, {cg, cg + cu + cw}, scale, device, &log2M, L);
+    ZPoly G = slice(all, 0, cg), U = slice(all, cg, cg + cu), Wc = slice(all, cg + cu, cg + cu + cw);
+    if (zdeg(G) != dmin) throw ApiError(CTG_INTERNAL, "gcd: degree mismatch after CRT");
+    Big c;
+    int s = 0;
+    ZPoly g = zprimitive_positive(G, &c, &s);
+    // e = gamma / (s c) must be an integer; then g U = e A and g W = e B modulo M.
+    Big e;
+    try {
+      e = big_divexact(gamma, c);
+    } catch (const std::exception&) {
+      throw ApiError(CTG_INTERNAL, "gcd: exactness certificate failed (content)");
+    }
+    const double lg1 = zlog2_l1(g);
+    const bool ok = lg1 + zlog2_l1(U) + 1 < log2M - 1 && lg1 + zlog2_l1(Wc) + 1 < log2M - 1 &&
+                    big_log2(e) + zlog2_linf(A) + 1 < log2M - 1 && big_log2(e) + zlog2_linf(B) + 1 < log2M - 1;
+    if (!ok) throw ApiError(CTG_INTERNAL, "gcd: exactness certificate failed (norm bound)");
+    return g;
+  }
+  throw ApiError(CTG_INTERNAL, "gcd: could not find enough lucky primes");
+}
+
+void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly, int>>& factors, ctg_sqf_buf* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->unit_sign = static_cast<int8_t>(unit.empty() ? 0 : unit_sign);
+  out->unit_nlimbs = static_cast<int32_t>(unit.size());
+  out->unit_limbs = static_cast<uint32_t*>(std::malloc(4 * std::max<size_t>(1, unit.size())));
+  std::memcpy(out->unit_limbs, unit.data(), 4 * unit.size());
+  out->n_factors = static_cast<int32_t>(factors.size());
+  out->mult = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(1, factors.size())));
+  out->factors = static_cast<ctg_upoly_buf*>(std::calloc(std::max<size_t>(1, factors.size()), sizeof(ctg_upoly_buf)));
+  if (!out->unit_limbs || !out->mult || !out->factors) throw std::bad_alloc();
+  for (size_t i = 0; i < factors.size(); ++i) {
+    out->mult[i] = factors[i].second;
+    fill_upoly(to_ucoeffs(factors[i].first), &out->factors[i]);
+  }
+}
+
+}  // namespace
+}  // namespace ctg
+
+using namespace ctg;
 
 extern "C" {
-ctg_status ctg_yun_squarefree(const ctg_upoly*, ctg_sqf_buf*, const ctg_opts*) {
-  return ctg::guarded([] { throw ctg::ApiError(CTG_UNSUPPORTED, "yun_squarefree: not built yet"); });
+
+ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_opts* opts) {
+  return guarded([&] {
+    if (!out) throw ApiError(CTG_INVALID, "yun_squarefree: null output");
+    CallTimer timer;
+    ZPoly a = parse_upoly(p);
+    if (a.empty()) throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial");  // elim.cpp:139
+    Big content;
+    int s = 0;
+    ZPoly P = zprimitive_positive(a, &content, &s);  // elim.cpp:141-144: unit = sign(lc) * content
+    timer.mark_setup();
+    if (zdeg(P) == 0) {  // elim.cpp:145
+      fill_sqf(content, s, {}, out);
+      timer.finish();
+      return;
+    }
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    Launches L;
+    YunResult r = yun_modular(P, false, dev, ctx.stream, L);
+    timer.mark_device();
+    stats_tls().kernel_launches = L.n;
+    fill_sqf(content, s, r.factors, out);
+    timer.finish();
+  });
 }
-ctg_status ctg_gcd_univariate(const ctg_upoly*, const ctg_upoly*, ctg_upoly_buf*, const ctg_opts*) {
-  return ctg::guarded([] { throw ctg::ApiError(CTG_UNSUPPORTED, "gcd_univariate: not built yet"); });
+
+ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ctg_opts* opts) {
+  return guarded([&] {
+    if (!out) throw ApiError(CTG_INVALID, "square_free_part: null output");
+    CallTimer timer;
+    ZPoly a = parse_upoly(p);
+    if (a.empty()) throw ApiError(CTG_PRECONDITION, "square_free_part: zero polynomial");  // elim.cpp:205
+    ZPoly P = zprimitive_positive(a);
+    timer.mark_setup();
+    if (zdeg(P) == 0) {  // elim.cpp:207
+      fill_upoly(to_ucoeffs(P), out);
+      timer.finish();
+      return;
+    }
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    Launches L;
+    YunResult r = yun_modular(P, true, dev, ctx.stream, L);
+    timer.mark_device();
+    stats_tls().kernel_launches = L.n;
+    fill_upoly(to_ucoeffs(r.sqfp), out);
+    timer.finish();
+  });
 }
-ctg_status ctg_square_free_part(const ctg_upoly*, ctg_upoly_buf*, const ctg_opts*) {
-  return ctg::guarded([] { throw ctg::ApiError(CTG_UNSUPPORTED, "square_free_part: not built yet"); });
+
+ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_buf* out, const ctg_opts* opts) {
+  return guarded([&] {
+    if (!out) throw ApiError(CTG_INVALID, "gcd_univariate: null output");
+    CallTimer timer;
+    ZPoly a = parse_upoly(p), b = parse_upoly(q);
+    // elim.cpp:81-85
+    if (a.empty() && b.empty()) throw ApiError(CTG_PRECONDITION, "gcd_univariate: both inputs zero");
+    if (a.empty() || b.empty()) {
+      fill_upoly(to_ucoeffs(zprimitive_positive(a.empty() ? b : a)), out);
+      timer.finish();
+      return;
+    }
+    ZPoly A = zprimitive_positive(a), B = zprimitive_positive(b);
+    timer.mark_setup();
+    if (zdeg(A) == 0 || zdeg(B) == 0) {
+      fill_upoly(to_ucoeffs(ZPoly{SBig{1, Big{1u}}}), out);
+      timer.finish();
+      return;
+    }
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    Launches L;
+    ZPoly r = gcd_modular(A, B, dev, ctx.stream, L);
+    timer.mark_device();
+    stats_tls().kernel_launches = L.n;
+    fill_upoly(to_ucoeffs(r), out);
+    timer.finish();
+  });
 }
-}
+
+}  // extern "C"

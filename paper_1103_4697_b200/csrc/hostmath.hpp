@@ -42,6 +42,16 @@ double log2_upper(const uint32_t* limbs, int n);
 // log2(sum 2^x_i), rounded up; -inf for an empty list.
 double log2_sum_upper(const std::vector<double>& xs);
 
+Big big_mul(const Big& a, const Big& b);
+// gcd of magnitudes (binary gcd on 64-bit words).
+Big big_gcd(const Big& a, const Big& b);
+// a / b for an exact divisor b != 0 (throws if the remainder is nonzero).
+Big big_divexact(const Big& a, const Big& b);
+// a mod p for a u32 modulus.
+inline uint32_t big_mod(const Big& a, uint32_t p) { return big_mod_u32(a.data(), static_cast<int>(a.size()), p); }
+inline bool big_is_one(const Big& a) { return a.size() == 1 && a[0] == 1; }
+double big_log2(const Big& a);  // upper bound, -inf for zero
+
 // Signed big integer (sign-magnitude) for summing repeated input terms.
 struct SBig {
   int sign = 0;  // -1, 0, +1

@@ -35,7 +35,22 @@ enum : uint32_t {
   kErrSentinel = 8u,       // an evaluation unit was never resolved
 };
 
-struct CrtTables;  // cached per (device, N, P)
+struct CrtTables {
+  int device = -1;
+  uint32_t N = 0;
+  int P = 0;
+  int LM = 0, L16 = 0;
+  std::vector<uint32_t> primes;
+  PrimeConst* d_pc = nullptr;
+  double* d_minv = nullptr;
+  uint32_t* d_Mk16 = nullptr;
+  uint32_t* d_M16 = nullptr;
+  std::vector<PrimeConst> h_pc;
+  double log2M = 0;
+  ~CrtTables();
+};
+// Builds the tables for `primes` (in order) on `device`; N = NTT size (1 if unused).
+std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N);
 
 // Slot directory: y-degree j of a polynomial owns slots [off, off + len) of the
 // residue table; slot off + t holds the coefficient of x^t.

@@ -1,0 +1,281 @@
+// K6: per-prime univariate gcd / Yun square-free decomposition (one CTA per prime,
+// polynomials staged in shared memory), and the gather/scale kernel that builds
+// the CRT residue matrix of the lucky primes (K7 then reuses the K5 CRT kernels).
+//
+// Replaces the reference's primitive PRS gcd (/root/reference/proj/src/elim.cpp:80-93)
+// and Yun's loop (elim.cpp:138-165): over F_p there is no coefficient growth, so
+// the Euclidean remainder sequence runs division-free in place; each pass is one
+// vector update of the remainder (threads stride the coefficients) and one barrier.
+#include <cuda_runtime.h>
+
+#include "internal.hpp"
+#include "uni_internal.hpp"
+
+namespace ctg {
+namespace {
+
+__device__ __forceinline__ Mod load_mod_u(const PrimeConst& c) { return Mod{c.p, c.pneg, c.r2, c.one}; }
+
+__device__ __forceinline__ int blk_trim(const uint32_t* X, int d) {
+  while (d >= 0 && X[d] == 0u) --d;
+  return d;
+}
+
+__device__ __forceinline__ void swp(uint32_t*& a, uint32_t*& b) {
+  uint32_t* t = a;
+  a = b;
+  b = t;
+}
+
+// Monic gcd of X (degree dx) and Y (degree dy), destroying both; the result ends
+// up in X (pointers are swapped as the remainder sequence proceeds).  Degrees are
+// exact (top coefficient nonzero) or -1.  Returns the gcd's degree (-1 if both zero).
+// Caller must have synchronised after writing X and Y.
+__device__ int blk_gcd(uint32_t*& X, int dx, uint32_t*& Y, int dy, const Mod& M) {
+  const int tid = threadIdx.x, bs = blockDim.x;
+  if (dx < dy) {
+    swp(X, Y);
+    const int t = dx;
+    dx = dy;
+    dy = t;
+  }
+  while (dy >= 0) {
+    while (dx >= dy) {
+      // X <- c X - t y^(dx-dy) Y   (c = lc Y, t = lc X): the top coefficient cancels.
+      const uint32_t c = Y[dy], t = mneg(X[dx], M.p);
+      const int sh = dx - dy;
+      for (int i = tid; i < dx; i += bs) {
+        const uint32_t v = X[i];
+        X[i] = (i >= sh) ? mmul2(c, v, t, Y[i - sh], M) : mmul(c, v, M);
+      }
+      __syncthreads();
+      dx = blk_trim(X, dx - 1);
+    }
+    swp(X, Y);
+    const int t = dx;
+    dx = dy;
+    dy = t;
+  }
+  if (dx >= 0) {
+    const uint32_t inv = minv(X[dx], M);
+    __syncthreads();
+    for (int i = tid; i < dx; i += bs) X[i] = mmul(X[i], inv, M);
+    if (tid == 0) X[dx] = M.one;
+    __syncthreads();
+  }
+  return dx;
+}
+
+// Q = X / D for a monic divisor D (degree dd <= dx); X is destroyed.  Returns deg Q.
+__device__ int blk_divexact_monic(uint32_t* X, int dx, const uint32_t* D, int dd, uint32_t* Q, const Mod& M) {
+  const int tid = threadIdx.x, bs = blockDim.x;
+  if (dd == 0) {
+    for (int i = tid; i <= dx; i += bs) Q[i] = X[i];
+    __syncthreads();
+    return dx;
+  }
+  for (int i = dx; i >= dd; --i) {
+    const uint32_t q = X[i];
+    const uint32_t nq = mneg(q, M.p);
+    for (int j = tid; j < dd; j += bs) X[i - dd + j] = mmul2(M.one, X[i - dd + j], nq, D[j], M);
+    if (tid == 0) Q[i - dd] = q;
+    __syncthreads();
+  }
+  return dx - dd;
+}
+
+__device__ void blk_copy(uint32_t* dst, const uint32_t* src, int d) {
+  for (int i = threadIdx.x; i <= d; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+}
+
+// Z = d/dx V  (degree dv - 1), Montgomery form.
+__device__ void blk_derivative(uint32_t* Z, const uint32_t* V, int dv, const Mod& M) {
+  for (int i = threadIdx.x; i < dv; i += blockDim.x)
+    Z[i] = mmul(V[i + 1], mmul(static_cast<uint32_t>(i + 1), M.r2, M), M);
+  __syncthreads();
+}
+
+// Scale to monic in place (lc nonzero).
+__device__ void blk_monic(uint32_t* X, int d, const Mod& M) {
+  const uint32_t inv = minv(X[d], M);
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) X[i] = mmul(X[i], inv, M);
+  if (threadIdx.x == 0) X[d] = M.one;
+  __syncthreads();
+}
+
+__device__ void blk_store_plain(uint32_t* dst, const uint32_t* X, int d, const Mod& M) {
+  for (int i = threadIdx.x; i <= d; i += blockDim.x) dst[i] = from_mont(X[i], M);
+}
+
+// ---------------------------------------------------------------------------
+// Yun modulo p (elim.cpp:138-165 over F_p, p > deg P):
+//   g = gcd(P, P'), v = P/g, w = P'/g;  repeat: z = w - v', h = gcd(v, z),
+//   emit h (multiplicity k), v = v/h, w = z/h, k++  until deg v = 0.
+// Outputs (plain residues): deg[k][m] = degree of the multiplicity-m factor (m >= 1),
+// deg[k][0] = status (0 ok, 1 lc(P) = 0 mod p); the monic factors concatenated in
+// increasing m (deg + 1 words each) at fac[k][...]; the monic square-free part at sqf[k][...].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_modyun(const uint32_t* __restrict__ tab, int n, const PrimeConst* __restrict__ pc,
+                                                int32_t* deg, uint32_t* fac, uint32_t* sqf) {
+  extern __shared__ uint32_t sm[];
+  const int kl = blockIdx.x;
+  const Mod M = load_mod_u(pc[kl]);
+  const int cap = n + 2;
+  uint32_t* buf[8];
+  for (int b = 0; b < 8; ++b) buf[b] = sm + b * cap;
+  int32_t* dk = deg + static_cast<size_t>(kl) * (n + 1);
+  uint32_t* fk = fac + static_cast<size_t>(kl) * (2 * n + 2);
+  uint32_t* sk = sqf + static_cast<size_t>(kl) * (n + 1);
+  const uint32_t* row = tab + static_cast<size_t>(kl) * (n + 1);
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+    buf[0][i] = row[i];
+    dk[i] = 0;
+  }
+  __syncthreads();
+  if (buf[0][n] == 0u) {
+    if (threadIdx.x == 0) dk[0] = 1;
+    return;
+  }
+  uint32_t *A0 = buf[0], *A1 = buf[1], *X = buf[2], *Y = buf[3], *V = buf[4], *W = buf[5], *F1 = buf[6],
+           *F2 = buf[7];
+  blk_derivative(A1, A0, n, M);  // deg n-1 exactly (p > n, lc != 0)
+  blk_copy(X, A0, n);
+  blk_copy(Y, A1, n - 1);
+  const int dg = blk_gcd(X, n, Y, n - 1, M);  // monic gcd in X
+  if (dg == 0) {
+    blk_monic(A0, n, M);
+    blk_store_plain(fk, A0, n, M);
+    blk_store_plain(sk, A0, n, M);
+    if (threadIdx.x == 0) dk[1] = n;
+    return;
+  }
+  int dv = blk_divexact_monic(A0, n, X, dg, V, M);      // v = P / g
+  int dw = blk_divexact_monic(A1, n - 1, X, dg, W, M);  // w = P' / g
+  {
+    blk_copy(F1, V, dv);
+    blk_monic(F1, dv, M);
+    blk_store_plain(sk, F1, dv, M);
+  }
+  int off = 0;
+  for (int k = 1; dv > 0 && k <= n; ++k) {
+    // z = w - v'   (in place in W)
+    for (int i = threadIdx.x; i <= dw || i < dv; i += blockDim.x) {
+      const uint32_t wi = (i <= dw) ? W[i] : 0u;
+      const uint32_t di = (i < dv) ? mmul(V[i + 1], mmul(static_cast<uint32_t>(i + 1), M.r2, M), M) : 0u;
+      W[i] = msub(wi, di, M.p);
+    }
+    __syncthreads();
+    const int dz = blk_trim(W, dw > dv - 1 ? dw : dv - 1);
+    int dh;
+    uint32_t* H;
+    if (dz < 0) {
+      blk_copy(X, V, dv);
+      blk_monic(X, dv, M);
+      H = X;
+      dh = dv;
+    } else {
+      blk_copy(X, V, dv);
+      blk_copy(Y, W, dz);
+      dh = blk_gcd(X, dv, Y, dz, M);
+      H = X;
+    }
+    if (dh > 0) {
+      blk_store_plain(fk + off, H, dh, M);
+      off += dh + 1;
+      if (threadIdx.x == 0) dk[k] = dh;
+    }
+    dv = blk_divexact_monic(V, dv, H, dh, F1, M);
+    swp(V, F1);
+    if (dz >= 0) {
+      dw = blk_divexact_monic(W, dz, H, dh, F2, M);
+      swp(W, F2);
+    } else {
+      dw = -1;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gcd modulo p with cofactors: g = monic gcd(A, B), u = A / g, w = B / g.
+// Row layout (plain residues): g (dg+1) | u (na-dg+1) | w (nb-dg+1).  deg[k] = dg,
+// or -2 if lc(A) or lc(B) vanishes mod p.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_modgcd(const uint32_t* __restrict__ tabA, int na,
+                                                const uint32_t* __restrict__ tabB, int nb,
+                                                const PrimeConst* __restrict__ pc, int32_t* deg, uint32_t* out,
+                                                int pitch) {
+  extern __shared__ uint32_t sm[];
+  const int kl = blockIdx.x;
+  const Mod M = load_mod_u(pc[kl]);
+  const int cap = (na > nb ? na : nb) + 2;
+  uint32_t *A = sm, *B = sm + cap, *X = sm + 2 * cap, *Y = sm + 3 * cap, *Q = sm + 4 * cap;
+  const uint32_t* ra = tabA + static_cast<size_t>(kl) * (na + 1);
+  const uint32_t* rb = tabB + static_cast<size_t>(kl) * (nb + 1);
+  for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
+  for (int i = threadIdx.x; i <= nb; i += blockDim.x) B[i] = Y[i] = rb[i];
+  __syncthreads();
+  if (A[na] == 0u || B[nb] == 0u) {
+    if (threadIdx.x == 0) deg[kl] = -2;
+    return;
+  }
+  const int dg = blk_gcd(X, na, Y, nb, M);
+  uint32_t* o = out + static_cast<size_t>(kl) * pitch;
+  blk_store_plain(o, X, dg, M);
+  const int du = blk_divexact_monic(A, na, X, dg, Q, M);
+  blk_store_plain(o + dg + 1, Q, du, M);
+  __syncthreads();
+  const int dw = blk_divexact_monic(B, nb, X, dg, Q, M);
+  blk_store_plain(o + dg + 1 + du + 1, Q, dw, M);
+  if (threadIdx.x == 0) deg[kl] = dg;
+}
+
+// dst[r][c] = src[idx[r]][c] * scale[r][seg(c)]  (plain residues; scale in Montgomery form),
+// seg(c) = number of segment boundaries <= c.
+__global__ void k_gather_scale(const uint32_t* __restrict__ src, int src_pitch, const int32_t* __restrict__ idx,
+                               int rows, int cols, const int32_t* __restrict__ seg_end, int nseg,
+                               const uint32_t* __restrict__ scale, const PrimeConst* __restrict__ pc_dst,
+                               uint32_t* __restrict__ dst) {
+  const int r = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows || c >= cols) return;
+  int s = 0;
+  while (s + 1 < nseg && c >= seg_end[s]) ++s;
+  const Mod M = load_mod_u(pc_dst[r]);
+  const uint32_t v = src[static_cast<size_t>(idx[r]) * src_pitch + c];
+  dst[static_cast<size_t>(r) * cols + c] = mmul(v, scale[static_cast<size_t>(r) * nseg + s], M);
+}
+
+}  // namespace
+
+size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
+size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4; }
+
+int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
+                  uint32_t* sqf, cudaStream_t st) {
+  const size_t smem = modyun_smem(n);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_modyun, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_modyun<<<nk, 256, smem, st>>>(tab, n, pc, deg, fac, sqf);
+  return 1;
+}
+
+int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, const PrimeConst* pc, int nk,
+                  int32_t* deg, uint32_t* out, int pitch, cudaStream_t st) {
+  const size_t smem = modgcd_smem(na, nb);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_modgcd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_modgcd<<<nk, 256, smem, st>>>(tabA, na, tabB, nb, pc, deg, out, pitch);
+  return 1;
+}
+
+int launch_gather_scale(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, int cols,
+                        const int32_t* seg_end, int nseg, const uint32_t* scale, const PrimeConst* pc_dst,
+                        uint32_t* dst, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return 0;
+  dim3 grid((cols + 127) / 128, rows);
+  k_gather_scale<<<grid, 128, 0, st>>>(src, src_pitch, idx, rows, cols, seg_end, nseg, scale, pc_dst, dst);
+  return 1;
+}
+
+}  // namespace ctg

@@ -1,0 +1,99 @@
+"""GPU parity of yun_squarefree / gcd_univariate / square_free_part against the reference.
+
+Expected values: tests/golden/ (reference compiled unmodified, oracle/make_golden.py),
+including the exact random inputs of proj/tests/test_elim.cpp (seeds 23, 24).
+"""
+
+import hashlib
+
+import pytest
+
+import paper_1103_4697_b200 as P
+from golden_io import dec_sqf, dec_upoly, load
+from paper_1103_4697_b200 import curves
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(op, args):
+    if op == "yun":
+        return P.yun_squarefree(args[0])
+    if op == "gcd":
+        return P.gcd_univariate(args[0], args[1])
+    if op == "sqfp":
+        return P.square_free_part(args[0])
+    raise ValueError(op)
+
+
+@pytest.mark.parametrize("name", ["worked.jsonl", "univariate_random.jsonl"])
+def test_fixture_univariate(name):
+    rows = [r for r in load(name) if r["op"] in ("yun", "gcd", "sqfp")]
+    assert rows
+    for r in rows:
+        args = [dec_upoly(a) for a in r["args"]]
+        if "error" in r:
+            with pytest.raises(P.PreconditionError):
+                _run(r["op"], args)
+            continue
+        got = _run(r["op"], args)
+        want = dec_sqf(r["result"]) if r["op"] == "yun" else dec_upoly(r["result"])
+        assert got == want, r
+
+
+def test_reference_test_elim_yun_and_gcd_cases():
+    rows = load("elim_cases.jsonl")
+    n = 0
+    for r in rows:
+        if r["case"].startswith("yun"):
+            assert P.yun_squarefree(dec_upoly(r["u"])) == dec_sqf(r["result"])
+            n += 1
+        elif r["case"].startswith("gcd"):
+            assert P.gcd_univariate(dec_upoly(r["a"]), dec_upoly(r["b"])) == dec_upoly(r["result"])
+            n += 1
+    assert n == 133  # 70 yun products (seed 23) + 63 gcd cases (seed 24) survive the reference's rejection
+
+
+def test_yun_of_config_resultants():
+    for r in load("configs_small.jsonl"):
+        if "yun" not in r:
+            continue
+        R = dec_upoly(r["result"])
+        assert P.yun_squarefree(R) == dec_sqf(r["yun"]), r["curve"]
+
+
+def _digest(coeffs):
+    return hashlib.sha256(",".join(format(c, "x") for c in coeffs).encode()).hexdigest()
+
+
+def test_yun_sheared_k3_digest():
+    rows = [r for r in load("configs_big.jsonl") if r["curve"][0] == "sheared"]
+    if not rows:
+        pytest.skip("no sheared fixture")
+    row = rows[0]
+    f = curves.make(*row["curve"])
+    R = P.resultant(f, curves.derive_y(f))
+    unit, factors = P.yun_squarefree(R)
+    assert format(unit, "x") == row["yun_unit"]
+    got = [{"mult": m, "deg": len(p) - 1, "sha256": _digest(p)} for p, m in factors]
+    assert got == row["yun"]
+
+
+def test_square_free_part_matches_yun_product():
+    f = curves.sheared(2, 1)
+    R = P.resultant(f, curves.derive_y(f))
+    unit, factors = P.yun_squarefree(R)
+    prod = [1]
+    for p, _ in factors:
+        out = [0] * (len(prod) + len(p) - 1)
+        for i, a in enumerate(prod):
+            for j, b in enumerate(p):
+                out[i + j] += a * b
+        prod = out
+    assert P.square_free_part(R) == prod
+
+
+def test_gcd_conventions():
+    with pytest.raises(P.PreconditionError):
+        P.gcd_univariate([], [])
+    assert P.gcd_univariate([], [6, -4]) == [-3, 2]
+    assert P.gcd_univariate([12], [18]) == [1]
