@@ -1,0 +1,244 @@
+// Drop-in replacement for the reference's elimination TU (/root/reference/proj/src/elim.cpp).
+//
+// Defines every symbol elim.cpp defines, with the reference's exact signatures
+// (proj/include/curvetop/elim.hpp:13-45, upoly.hpp:92), on top of the C ABI of
+// libctg.so (include/ctg.h).  A curvetop build swaps elim.cpp for this file and
+// links libctg.so; callers (lift.cpp, bisolve.cpp, pipeline.cpp, realroots.cpp,
+// connect.cpp, bipoly.cpp and the tests) are unchanged.  See INTEGRATION.md.
+//
+//   resultant         -> ctg_resultant         (GPU: multi-modular, elim.cpp:95-136)
+//   yun_squarefree    -> ctg_yun_squarefree    (GPU: modular Yun + certificate, elim.cpp:138-165)
+//   gcd_univariate    -> ctg_gcd_univariate    (GPU: modular gcd + certificate, elim.cpp:80-93)
+//   square_free_part  -> ctg_square_free_part  (GPU, elim.cpp:204-210)
+//   SquareFreeFactorization::reconstruct, multiplicity_at: same semantics as elim.cpp:74-78,
+//     167-176 (products / sign tests on the host, gcds on the GPU)
+//   gcd_bivariate: the reference's PRS over Z[x][y] (elim.cpp:178-202) with its univariate
+//     contents on the GPU -- the bivariate GPU gcd is a "next" row.
+//
+// Status codes map to the reference's exceptions: CTG_PRECONDITION -> PreconditionError,
+// anything else -> Error (there is no CPU fallback: a CUDA failure throws).
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctg.h"
+#include "curvetop/elim.hpp"
+#include "curvetop/realroots.hpp"
+
+namespace curvetop {
+namespace {
+
+[[noreturn]] void raise(ctg_status st, const char* what) {
+  std::string msg = ctg_last_error();
+  if (msg.empty()) msg = what;
+  if (st == CTG_PRECONDITION) throw PreconditionError(msg);
+  throw Error(msg);
+}
+
+void check(ctg_status st, const char* what) {
+  if (st != CTG_OK) raise(st, what);
+}
+
+// mpz -> sign + little-endian u32 limbs (CSR).
+struct Limbs {
+  std::vector<int8_t> sign;
+  std::vector<uint32_t> off{0};
+  std::vector<uint32_t> limbs;
+  void push(const BigInt& v) {
+    const int s = sgn(v);
+    sign.push_back(static_cast<int8_t>(s));
+    if (s != 0) {
+      size_t count = 0;
+      const size_t words = (mpz_sizeinbase(v.get_mpz_t(), 2) + 31) / 32;
+      const size_t base = limbs.size();
+      limbs.resize(base + words);
+      mpz_export(limbs.data() + base, &count, -1, 4, 0, 0, v.get_mpz_t());
+      limbs.resize(base + count);
+    }
+    off.push_back(static_cast<uint32_t>(limbs.size()));
+  }
+};
+
+struct BiMarshal {
+  std::vector<int32_t> dx, dy;
+  Limbs L;
+  ctg_bipoly view{};
+  explicit BiMarshal(const BivariatePolynomial& f) {
+    for (const auto& [e, c] : f.terms()) {
+      dx.push_back(e.first);
+      dy.push_back(e.second);
+      L.push(c);
+    }
+    view.n_terms = static_cast<int32_t>(dx.size());
+    view.dx = dx.data();
+    view.dy = dy.data();
+    view.sign = L.sign.data();
+    view.limb_off = L.off.data();
+    view.limbs = L.limbs.data();
+  }
+};
+
+struct UniMarshal {
+  Limbs L;
+  ctg_upoly view{};
+  explicit UniMarshal(const UnivariatePolynomial& p) {
+    for (const auto& c : p.coeffs()) L.push(c);
+    view.n_coeffs = static_cast<int32_t>(p.coeffs().size());
+    view.sign = L.sign.data();
+    view.limb_off = L.off.data();
+    view.limbs = L.limbs.data();
+  }
+};
+
+BigInt from_limbs(int sign, const uint32_t* limbs, size_t n) {
+  BigInt v;
+  if (n) mpz_import(v.get_mpz_t(), n, -1, 4, 0, 0, limbs);
+  return sign < 0 ? BigInt(-v) : v;
+}
+
+UnivariatePolynomial take(ctg_upoly_buf& b) {
+  std::vector<BigInt> c(static_cast<size_t>(b.n_coeffs));
+  for (int i = 0; i < b.n_coeffs; ++i)
+    c[i] = from_limbs(b.sign[i], b.limbs + b.limb_off[i], b.limb_off[i + 1] - b.limb_off[i]);
+  ctg_upoly_free(&b);
+  return UnivariatePolynomial(std::move(c));
+}
+
+// ---- Z[x][y] helpers for gcd_bivariate (same results as elim.cpp:17-70) ----
+using ZxY = std::vector<UnivariatePolynomial>;  // y-coefficients in Z[x]
+
+int top_y(const ZxY& a) {
+  int d = static_cast<int>(a.size()) - 1;
+  while (d >= 0 && a[static_cast<size_t>(d)].is_zero()) --d;
+  return d;
+}
+
+// Full content in Z[x] (primitive gcd of the y-coefficients times their integer gcd).
+UnivariatePolynomial content_zx(const ZxY& a) {
+  UnivariatePolynomial g;
+  BigInt ig(0);
+  for (const auto& c : a) {
+    if (c.is_zero()) continue;
+    g = g.is_zero() ? c : gcd_univariate(g, c);  // GPU
+    const BigInt cc = c.content();
+    mpz_gcd(ig.get_mpz_t(), ig.get_mpz_t(), cc.get_mpz_t());
+  }
+  return g.is_zero() ? g : g.primitive_positive() * ig;
+}
+
+ZxY divide_zx(ZxY a, const UnivariatePolynomial& s) {
+  for (auto& c : a)
+    if (!c.is_zero()) c = c.divexact(s);
+  return a;
+}
+
+// lc_y(D)^(deg A - deg D + 1) * A  mod D  in Z[x][y].
+ZxY prem_y(ZxY A, const ZxY& D) {
+  const int dd = top_y(D);
+  if (dd < 0) throw Error("yv_prem: zero divisor");
+  int da = top_y(A);
+  if (da < dd) return A;
+  A.resize(static_cast<size_t>(da) + 1);
+  const UnivariatePolynomial& lead = D[static_cast<size_t>(dd)];
+  for (; da >= dd; --da) {
+    const UnivariatePolynomial t = std::move(A[static_cast<size_t>(da)]);
+    A[static_cast<size_t>(da)] = UnivariatePolynomial();
+    for (int j = 0; j < da; ++j) A[static_cast<size_t>(j)] = A[static_cast<size_t>(j)] * lead;
+    if (t.is_zero()) continue;
+    for (int j = 0; j < dd; ++j) {
+      auto& slot = A[static_cast<size_t>(da - dd + j)];
+      slot = slot - t * D[static_cast<size_t>(j)];
+    }
+  }
+  A.resize(static_cast<size_t>(dd));
+  A.resize(static_cast<size_t>(top_y(A) + 1));
+  return A;
+}
+
+UnivariatePolynomial power(const UnivariatePolynomial& p, int k) {
+  UnivariatePolynomial r = UnivariatePolynomial::constant(1);
+  while (k-- > 0) r = r * p;
+  return r;
+}
+
+}  // namespace
+
+UnivariatePolynomial SquareFreeFactorization::reconstruct() const {
+  UnivariatePolynomial r = UnivariatePolynomial::constant(unit);
+  for (const auto& f : factors) r = r * power(f.poly, f.multiplicity);
+  return r;
+}
+
+UnivariatePolynomial gcd_univariate(const UnivariatePolynomial& p, const UnivariatePolynomial& q) {
+  UniMarshal a(p), b(q);
+  ctg_upoly_buf out{};
+  check(ctg_gcd_univariate(&a.view, &b.view, &out, nullptr), "gcd_univariate");
+  return take(out);
+}
+
+UnivariatePolynomial resultant(const BivariatePolynomial& p, const BivariatePolynomial& q, Var eliminated) {
+  BiMarshal a(p), b(q);
+  ctg_upoly_buf out{};
+  check(ctg_resultant(&a.view, &b.view, eliminated == Var::X ? 1 : 0, &out, nullptr), "resultant");
+  return take(out);
+}
+
+SquareFreeFactorization yun_squarefree(const UnivariatePolynomial& p) {
+  UniMarshal a(p);
+  ctg_sqf_buf out{};
+  check(ctg_yun_squarefree(&a.view, &out, nullptr), "yun_squarefree");
+  SquareFreeFactorization sf;
+  sf.unit = from_limbs(out.unit_sign, out.unit_limbs, static_cast<size_t>(out.unit_nlimbs));
+  for (int i = 0; i < out.n_factors; ++i) {
+    ctg_upoly_buf& b = out.factors[i];
+    std::vector<BigInt> c(static_cast<size_t>(b.n_coeffs));
+    for (int j = 0; j < b.n_coeffs; ++j)
+      c[j] = from_limbs(b.sign[j], b.limbs + b.limb_off[j], b.limb_off[j + 1] - b.limb_off[j]);
+    sf.factors.push_back({UnivariatePolynomial(std::move(c)), out.mult[i]});
+  }
+  ctg_sqf_free(&out);
+  return sf;
+}
+
+UnivariatePolynomial square_free_part(const UnivariatePolynomial& p) {
+  UniMarshal a(p);
+  ctg_upoly_buf out{};
+  check(ctg_square_free_part(&a.view, &out, nullptr), "square_free_part");
+  return take(out);
+}
+
+int multiplicity_at(const SquareFreeFactorization& sf, const AlgebraicNumber& a) {
+  for (const auto& f : sf.factors) {
+    UnivariatePolynomial g = gcd_univariate(f.poly, a.poly());
+    if (g.degree() < 1) continue;
+    const int slo = g.sign_at(a.interval().lo().to_rational());
+    const int shi = g.sign_at(a.interval().hi().to_rational());
+    if (slo * shi < 0) return f.multiplicity;
+  }
+  return 0;
+}
+
+BivariatePolynomial gcd_bivariate(const BivariatePolynomial& f, const BivariatePolynomial& g) {
+  if (f.is_zero() && g.is_zero()) throw PreconditionError("gcd_bivariate: both inputs zero");
+  if (f.is_zero()) return g;
+  if (g.is_zero()) return f;
+  // Primitive PRS in y over Z[x] on the x-primitive parts; the x-content gcd is
+  // multiplied back and the leading (y, then x) coefficient made positive.
+  const UnivariatePolynomial cf = content_y(f), cg = content_y(g);
+  ZxY u = divexact_univariate_x(f, cf).y_coeffs();
+  ZxY v = divexact_univariate_x(g, cg).y_coeffs();
+  if (top_y(u) < top_y(v)) std::swap(u, v);
+  while (top_y(v) >= 0) {
+    ZxY r = prem_y(std::move(u), v);
+    const UnivariatePolynomial c = content_zx(r);
+    u = std::move(v);
+    v = c.is_zero() ? ZxY{} : divide_zx(std::move(r), c);
+  }
+  BivariatePolynomial h = BivariatePolynomial::from_y_coeffs(divide_zx(u, content_zx(u))) *
+                          BivariatePolynomial::from_univariate(gcd_univariate(cf, cg), Var::X);
+  if (h.y_coeffs()[static_cast<size_t>(h.degree_y())].leading() < 0) h = -h;
+  return h;
+}
+
+}  // namespace curvetop
