@@ -4,13 +4,14 @@
 Metric (BASELINE.json): "res(f,f_y) wall ms + mod-p resultants/s at 1/2/4/8 B200 vs host-CPU ref".
   value  = mod-p resultants per second over the whole job, inputs resident in HBM
            (units = P * D per curve: primes x result coefficients, SURVEY.md §8(d));
-  e2e    = the same metric through the reference-facing C ABI (ctg_resultant) with HOST
+  e2e    = the same metric through the reference-facing C ABI (ctg_resultant_batch) with HOST
            buffers: H2D of the coefficient limbs, all kernels, D2H of the exact result.
 Workload (config.workload): BASELINE.json configs[1], random dense f of total degree 20 with
-64-bit coefficients (synthetic, the §8(d) generator), a batch of curves per step.  The headline
-d=30/128-bit curve is measured once more on its own (key "headline").
+64-bit coefficients (synthetic, the §8(d) generator), a batch of curves per step processed by
+one batched plan (every kernel launch covers all curves).  The headline d=30/128-bit curve is
+measured once more on its own (key "headline").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--workload d20_b64|d30_b128|...]
   python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N     (prime sharding + NCCL)
   python bench.py --impl reference ...      (the reference CPU implementation, oracle/_ref, all host cores)
 """
@@ -32,7 +33,7 @@ sys.path.insert(0, REPO)
 METRIC = "res(f,f_y) wall ms + mod-p resultants/s at 1/2/4/8 B200 vs host-CPU ref"
 UNIT = "mod-p resultants/s"
 WORKLOADS = {
-    # name: (kind, a, b, description, units per curve = P * D as planned by libctg)
+    # name: (kind, a, b, description, nominal units per curve = P * D for seed 1)
     "d20_b64": ("dense", 20, 64, "random dense f, total degree 20, 64-bit coefficients (BASELINE configs[1])",
                 90 * 381),
     "d30_b128": ("dense", 30, 128, "random dense f, total degree 30, 128-bit coefficients (BASELINE configs[2])",
@@ -43,7 +44,7 @@ WORKLOADS = {
                   1031 * 241),
 }
 REFDRIVER = os.path.join(REPO, "oracle", "_ref", "refdriver")
-CACHED_REF_SECONDS = {"d30_b128": 1662.0, "d16_b1024": 268.0, "d20_b64": 27.2, "d10_b10": 0.020}
+CACHED_REF_SECONDS = {"d30_b128": 1700.4, "d16_b1024": 291.7, "d20_b64": 27.7, "d10_b10": 0.022}  # this container
 
 
 def parse_args():
@@ -53,7 +54,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="d20_b64", choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=32, help="curves per step (seeds 1..B)")
+    ap.add_argument("--batch", type=int, default=64, help="curves per step (seeds 1..B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-headline", action="store_true")
     return ap.parse_args()
@@ -183,72 +184,71 @@ def main_ours(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    stream = torch.cuda.current_stream()
+    # One explicit (non-default) stream for everything: our kernels, torch fills, NCCL and
+    # the timing events.  (Handle 0 would mean "the library's own stream" to libctg.)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
-    kind, a, b, desc, units = WORKLOADS[args.workload]
+    assert sh != 0
+    kind, a, b, desc, _ = WORKLOADS[args.workload]
     B = args.batch
 
-    # synthetic curves (seeds 1..B) and plans
+    # synthetic curves (seeds 1..B), one batched plan: every launch covers all B curves
     fs = [curves.make(kind, a, b, s) for s in range(1, B + 1)]
-    plans = [P.Plan(f, curves.derive_y(f)) for f in fs]
-    info = plans[0].info
-    Pn, N, D, LM = info["n_primes"], info["n_points"], info["n_coeffs"], info["out_limbs"]
-    assert all(p.info["n_primes"] == Pn and p.info["n_points"] == N for p in plans)
-    assert Pn * D == units, (Pn, D, units)
-    W = LM + 1
+    pairs = [(f, curves.derive_y(f)) for f in fs]
+    plan = P.Plan(pairs)
+    info = plan.info
+    Pn, N, D = info["n_primes"], info["n_points"], info["n_coeffs"]
+    W = info["out_limbs"] + 1
+    units_step = B * Pn * D  # mod-p resultants per step (P * D per curve)
     G = world
-    Pb = (Pn + G - 1) // G
+    Pb = (Pn + G - 1) // G   # rows per rank block (uniform for the all-gather)
     k0, k1 = min(rank * Pb, Pn), min((rank + 1) * Pb, Pn)
     Jb = (D + G - 1) // G
     j0, j1 = min(rank * Jb, D), min((rank + 1) * Jb, D)
-    for p in plans:
-        p.upload(sh)
+    plan.upload(sh)
 
     send = torch.zeros((B, Pb, N), dtype=torch.int32, device=dev)
     full = torch.zeros((G, B, Pb, N), dtype=torch.int32, device=dev) if G > 1 else None
-    out = torch.zeros((B, Jb, W), dtype=torch.int32, device=dev)
+    out = torch.zeros((B * Jb * W,), dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-
-    def rows_ptr(bi):
-        return send[bi].data_ptr()
-
-    def all_ptr(bi):
-        return (full[0, bi] if G > 1 else send[bi]).data_ptr()
 
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     stage_ms = [0.0] * 5
+
+    def crt():
+        if G > 1:
+            plan.crt_batch(full.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N, row_block=Pb,
+                           block_stride=B * Pb * N)
+        else:
+            plan.crt_batch(send.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N)
 
     def step(timed=False):
         if timed:
             evs[0].record(stream)
         for s_ in (1, 2, 3):
-            for bi, p in enumerate(plans):
-                p.stage(s_, k0, k1, rows_ptr(bi), sh)
+            plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
             if timed:
                 evs[s_].record(stream)
         if G > 1:
             dist.all_gather_into_tensor(full, send)
         if timed:
             evs[4].record(stream)
-        for bi, p in enumerate(plans):
-            if G > 1:
-                p.crt_sharded(full[:, bi].data_ptr(), Pb, B * Pb * N, j0, j1, out[bi].data_ptr(), sh)
-            else:
-                p.crt(all_ptr(bi), j0, j1, out[bi].data_ptr(), sh)
+        crt()
         if timed:
             evs[5].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    for p in plans:
-        p.check(sh)
-    launches0 = sum(p.launches for p in plans)
+    plan.check(sh)
+    launches0 = plan.launches
 
-    # correctness spot check of the device-resident path (curve 0) against the one-shot C-ABI call
+    # correctness spot check of the device-resident batch (curves 0 and B-1) against the one-shot call
     if G == 1:
-        host = out[0, :D].cpu().numpy().view("uint32")
-        assert plans[0].decode(host) == P.resultant(fs[0], curves.derive_y(fs[0])), "staged != one-shot"
+        host = out.cpu().numpy().view("uint32").reshape(B, D, W)
+        for bi in {0, B - 1}:
+            assert plan.decode(host[bi]) == P.resultant(*pairs[bi]), f"batched != one-shot (curve {bi})"
 
     total_ms = 0.0
     with ClockSampler(dev) as clk:
@@ -262,74 +262,74 @@ def main_ours(args):
             total_ms += evs[0].elapsed_time(evs[5])
             for i in range(5):
                 stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
-    gpu_launches = sum(p.launches for p in plans) - launches0
+    gpu_launches = plan.launches - launches0
     t_max = total_ms
     if dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
     ms_per_step = t_max / args.steps
-    value = B * units / (ms_per_step * 1e-3)
+    value = units_step / (ms_per_step * 1e-3)
 
     # --- e2e through the C ABI with host buffers --------------------------------------
-    hps = [(P.HostBipoly(f), P.HostBipoly(curves.derive_y(f))) for f in fs]
     e2e_ms, h2d, d2h = None, 0, 0
+    e2e_phases = None
     if G == 1:
+        hb = P.HostBatch(pairs)
         for _ in range(max(1, args.warmup)):
-            for hp, hq in hps:
-                P.resultant_raw(hp, hq)
+            P.resultant_batch_raw(hb)
         walls = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            h2d = d2h = 0
-            for hp, hq in hps:
-                P.resultant_raw(hp, hq)
-                st = P.last_call_stats()
-                h2d += st["h2d_bytes"]
-                d2h += st["d2h_bytes"]
+            P.resultant_batch_raw(hb)
             walls.append(time.perf_counter() - t0)
+            st = P.last_call_stats()
+            h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
         e2e_ms = 1e3 * sum(walls) / len(walls)
+        e2e_phases = {k: st[k] for k in ("setup_ms", "device_ms", "decode_ms", "total_ms")}
     else:
-        e2e_ms, h2d, d2h = e2e_sharded(args, plans, fs, P, curves, torch, dist, send, full, out, Pb, k0, k1, j0, j1,
-                                       D, W, sh, rank)
-    e2e_value = B * units / (e2e_ms * 1e-3)
+        e2e_ms, h2d, d2h = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh,
+                                       rank)
+    e2e_value = units_step / (e2e_ms * 1e-3)
 
-    # --- roofline of the dominant kernel (stage 2: eval + mod-p resultant) -------------
+    # --- roofline of the dominant kernel (stage 2: K2 eval + K3 mod-p resultant) ---------
     peaks = P.microbench_int(dev)
     n = info["deg_p"]
-    k3_ms_per_launch = stage_ms[1] / (args.steps * B)
-    units_launch = (k1 - k0) * N
+    k3_ms_per_launch = stage_ms[1] / args.steps  # one batched launch set per step
+    units_launch = B * (k1 - k0) * N
     imad_launch = 4.0 * units_launch * (n * n + n - 2)
     achieved = imad_launch / (k3_ms_per_launch * 1e-3) / 1e12
     peak = peaks["imad_per_s"] / 1e12
     roofline = {"bound": "int32-imad", "achieved": achieved, "peak": peak, "unit": "TIMAD/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": f"k_modres_fast<{n}> (+ k_modres_general on flagged units)",
-                "algorithmic": f"4 IMAD x (n^2+n-2) mulmods x {units_launch} units per launch, n={n}",
+                "kernel": f"stage 2 = k_eval_ntt (K2) + k_modres_fast<{n}> (K3) + k_modres_general (flagged units)",
+                "algorithmic": f"4 IMAD x (n^2+n-2) mulmods x {units_launch} units per launch, n={n} (SURVEY §8d)",
                 "peak_source": "measured live: ctg_microbench_int (8 IMAD chains/thread, all SMs)",
                 "imad_wide_peak_T": peaks["imad_wide_per_s"] / 1e12,
                 "mmul2_peak_G": peaks["mmul2_per_s"] / 1e9,
-                "stage_ms_per_curve": {nm: v / (args.steps * B) for nm, v in
-                                       zip(("reduce", "modres", "interp", "exchange", "crt"), stage_ms)}}
+                "stage_ms_per_step": {nm: v / args.steps for nm, v in
+                                      zip(("reduce", "modres", "interp", "exchange", "crt"), stage_ms)}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u32 (31-bit modular, Montgomery)", "data": "synthetic",
         "config": {"workload": desc, "curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N,
-                   "coeffs": D, "units_per_curve": units, "parallelism": f"prime-shard{G}" if G > 1 else "single",
+                   "coeffs": D, "units_per_step": units_step,
+                   "parallelism": f"prime-shard{G}" if G > 1 else "single",
                    "l2": "flushed (256 MB write) between timed steps",
                    "res_ms_per_curve": ms_per_step / B},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "res_ms_per_curve": e2e_ms / B, "path": "ctg_resultant (C ABI), host CSR limbs in/out"},
-        "gpu_launches": int(gpu_launches // max(1, args.steps)) * args.steps,
+                "res_ms_per_curve": e2e_ms / B, "path": "ctg_resultant_batch (C ABI), host CSR limbs in/out",
+                "phases_ms_last_call": e2e_phases},
+        "gpu_launches": int(gpu_launches),
         "roofline": roofline,
         "clocks": clk.summary(),
     }
     if rank == 0 and G == 1 and not args.no_headline:
         line["headline"] = headline(P, curves)
     if rank == 0 and G == 1:
-        line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+        line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args.workload, Pn * D)
     if rank == 0:
         print(json.dumps(line))
     if dist:
@@ -338,34 +338,39 @@ def main_ours(args):
     return 0
 
 
-def e2e_sharded(args, plans, fs, P, curves, torch, dist, send, full, out, Pb, k0, k1, j0, j1, D, W, sh, rank):
+def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh, rank):
     """Multi-GPU end-to-end: every rank uploads the inputs, computes its prime rows, all-gathers,
     reconstructs its coefficient block; rank 0 gathers the exact limbs and decodes on the host."""
-    B = len(plans)
+    B = plan.info["batch"]
     G = dist.get_world_size()
     gathered = torch.zeros((G,) + tuple(out.shape), dtype=torch.int32, device=out.device)
     walls = []
-    h2d = d2h = 0
     for it in range(args.warmup + args.steps):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for bi, p in enumerate(plans):
-            p.upload(sh)
-            p.residues(k0, k1, send[bi].data_ptr(), sh)
+        plan.upload(sh)
+        for s_ in (1, 2, 3):
+            plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
         dist.all_gather_into_tensor(full, send)
-        for bi, p in enumerate(plans):
-            p.crt_sharded(full[:, bi].data_ptr(), Pb, B * Pb * send.shape[2], j0, j1, out[bi].data_ptr(), sh)
+        plan.crt_batch(full.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N, row_block=Pb,
+                       block_stride=B * Pb * N)
         dist.all_gather_into_tensor(gathered, out)
         if rank == 0:
+            import numpy as np
+
             host = gathered.cpu().numpy().view("uint32")
-            for bi, p in enumerate(plans):
-                words = host[:, bi].reshape(-1, W)[:D]
-                p.decode(words)
+            blocks = []
+            for r in range(G):
+                Jr = max(0, min((r + 1) * Jb, D) - min(r * Jb, D))
+                blocks.append(host[r, :B * Jr * W].reshape(B, Jr, W))
+            full_host = np.concatenate(blocks, axis=1)
+            for bi in range(B):
+                plan.decode(full_host[bi])
         torch.cuda.synchronize()
         if it >= args.warmup:
             walls.append(time.perf_counter() - t0)
-    h2d = sum(p.h2d_bytes for p in plans) * G
+    h2d = plan.h2d_bytes * G
     d2h = int(gathered.numel() * 4)
     t = torch.tensor([1e3 * sum(walls) / len(walls)], dtype=torch.float64, device=out.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -388,12 +393,13 @@ def headline(P, curves):
     ref_s = CACHED_REF_SECONDS["d30_b128"]
     return {"workload": "dense d=30, 128-bit, seed 1 (BASELINE configs[2])", "e2e_ms_median": ms,
             "device_phase_ms_median": statistics.median(dev),
-            "reference_cpu_s": ref_s, "reference_cpu_source": "SURVEY.md §6.2 (reference, 1 core, not re-run: 28 min)",
+            "reference_cpu_s": ref_s,
+            "reference_cpu_source": "oracle/_ref/refdriver, 1 core of the build container (not re-run: 28 min)",
             "speedup_vs_reference_1gpu": ref_s * 1e3 / ms}
 
 
-def cpu_baseline(workload):
-    kind, a, b, desc, units = WORKLOADS[workload]
+def cpu_baseline(workload, units_per_curve):
+    kind, a, b, desc, _ = WORKLOADS[workload]
     if not os.path.exists(REFDRIVER):
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                 "sample": "oracle/_ref/refdriver not built", "note": "run make -C oracle"}
@@ -402,7 +408,7 @@ def cpu_baseline(workload):
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
     secs = r["res_seconds_best"]
-    return {"value": units / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+    return {"value": units_per_curve / secs, "unit": UNIT, "cores": 1, "kind": "reference",
             "sample": f"1 curve {kind}({a},{b},seed=1): curvetop::resultant(f, f_y, Y), 1 thread, {secs:.2f} s",
             "seconds_per_curve": secs}
 

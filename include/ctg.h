@@ -131,6 +131,7 @@ typedef struct {
   double bound_bits;   /* log2 of the Hadamard coefficient bound                    */
   double work_mulmods; /* algorithmic mulmods of the mod-p resultant stage */
   int64_t h2d_bytes;   /* bytes ctg_plan_upload copies host -> device                */
+  int32_t batch;       /* number of problems (curves) in the plan                     */
 } ctg_plan_info;
 
 ctg_status ctg_plan_create(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
@@ -158,6 +159,24 @@ ctg_status ctg_plan_check(ctg_plan* plan, void* stream);
 /* Number of kernel launches issued by the plan since creation. */
 int32_t ctg_plan_launches(const ctg_plan* plan);
 void ctg_plan_destroy(ctg_plan* plan);
+
+/* ---- batches: B same-shape problems per plan / call (one set of kernel launches) ----
+ * ctg_resultant_batch takes arrays p[0..batch), q[0..batch) and fills out[0..batch); inputs
+ * of different shapes are grouped internally.  A batch plan requires every member to have
+ * the same degrees in the eliminated variable (and the same q == dp/dy relation); its
+ * primes cover the largest coefficient bound of the batch.  Device layouts: residue rows of
+ * curve b at d_rows + b * curve_stride (curve_stride = 0: dense, (k1-k0) * n_points); CRT
+ * output of curve b at d_out + b * (j1-j0) * (out_limbs + 1). */
+ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                               ctg_upoly_buf* out, const ctg_opts* opts);
+ctg_status ctg_plan_create_batch(int32_t batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                                 const ctg_opts* opts, ctg_plan** plan);
+ctg_status ctg_plan_stage_batch(ctg_plan* plan, int32_t stage, int32_t k0, int32_t k1, uint32_t* d_rows,
+                                int64_t curve_stride, void* stream);
+/* Residues of curve b, prime k at d_all + b * curve_stride + (k / row_block) * block_stride
+ * + (k % row_block) * n_points (curve_stride 0: n_primes * n_points; row_block 0: n_primes). */
+ctg_status ctg_plan_crt_batch(ctg_plan* plan, const uint32_t* d_all, int64_t curve_stride, int32_t row_block,
+                              int64_t block_stride, int32_t j0, int32_t j1, uint32_t* d_out, void* stream);
 
 /* Integer-pipe peak microbenchmarks on `device` (-1 = current): 32-bit IMAD
  * (a*b+c) and IMAD.WIDE (u32*u32+u64) results per second over all SMs, and

@@ -88,7 +88,8 @@ class CallStats(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("n_primes", C.c_int32), ("n_points", C.c_int32), ("n_coeffs", C.c_int32), ("out_limbs", C.c_int32),
                 ("deg_p", C.c_int32), ("deg_q", C.c_int32), ("derivative", C.c_int32), ("trivial", C.c_int32),
-                ("bound_bits", C.c_double), ("work_mulmods", C.c_double), ("h2d_bytes", C.c_int64)]
+                ("bound_bits", C.c_double), ("work_mulmods", C.c_double), ("h2d_bytes", C.c_int64),
+                ("batch", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -100,7 +101,8 @@ EXPORTS = (
     "ctg_sqf_free", "ctg_last_error", "ctg_abi_version", "ctg_device_count", "ctg_last_call_stats",
     "ctg_plan_create", "ctg_plan_get_info", "ctg_plan_upload", "ctg_plan_residues", "ctg_plan_crt",
     "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy", "ctg_plan_stage",
-    "ctg_microbench_int", "ctg_plan_crt_sharded",
+    "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
+    "ctg_plan_stage_batch", "ctg_plan_crt_batch",
 )
 
 _lib = None
@@ -140,6 +142,14 @@ def lib():
         L.ctg_plan_crt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         L.ctg_plan_crt_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                            C.c_void_p, C.c_void_p]
+        L.ctg_resultant_batch.argtypes = [C.c_int32, C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.c_int32,
+                                          C.POINTER(_UpolyBuf), C.POINTER(_Opts)]
+        L.ctg_plan_create_batch.argtypes = [C.c_int32, C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.c_int32,
+                                            C.POINTER(_Opts), C.POINTER(C.c_void_p)]
+        L.ctg_plan_stage_batch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                           C.c_void_p]
+        L.ctg_plan_crt_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int32,
+                                         C.c_int32, C.c_void_p, C.c_void_p]
         L.ctg_plan_decode.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_UpolyBuf)]
         L.ctg_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.ctg_plan_launches.argtypes = [C.c_void_p]
@@ -274,6 +284,47 @@ def resultant_raw(p: HostBipoly, q: HostBipoly, var: str = "y", device=None) -> 
     return n
 
 
+class HostBatch:
+    """Caller-owned host operands of a batch of resultants (arrays of ctg_bipoly)."""
+
+    def __init__(self, pairs):
+        self.ops = [(HostBipoly(p), HostBipoly(q)) for p, q in pairs]
+        n = len(self.ops)
+        self.p = (_Bipoly * max(1, n))(*[a.struct for a, _ in self.ops])
+        self.q = (_Bipoly * max(1, n))(*[b.struct for _, b in self.ops])
+        self.n = n
+        self.nbytes = sum(a.nbytes + b.nbytes for a, b in self.ops)
+
+
+def resultant_batch_raw(hb: HostBatch, var: str = "y", device=None) -> int:
+    """ctg_resultant_batch into library buffers that are freed again (the C/C++ caller's call)."""
+    outs = (_UpolyBuf * max(1, hb.n))()
+    o = _opts(device)
+    _check(lib().ctg_resultant_batch(hb.n, hb.p, hb.q, 1 if var in ("x", "X") else 0, outs, C.byref(o)),
+           "resultant_batch")
+    total = 0
+    for i in range(hb.n):
+        total += outs[i].n_coeffs
+        lib().ctg_upoly_free(C.byref(outs[i]))
+    return total
+
+
+def resultant_batch(pairs, var: str = "y", device=None) -> list:
+    """[res(p, q) for (p, q) in pairs] with one batched GPU pipeline per input shape."""
+    hb = HostBatch(pairs)
+    outs = (_UpolyBuf * max(1, hb.n))()
+    o = _opts(device)
+    _check(lib().ctg_resultant_batch(hb.n, hb.p, hb.q, 1 if var in ("x", "X") else 0, outs, C.byref(o)),
+           "resultant_batch")
+    res = []
+    for i in range(hb.n):
+        try:
+            res.append(_decode_buf(outs[i]))
+        finally:
+            lib().ctg_upoly_free(C.byref(outs[i]))
+    return res
+
+
 def resultant(p: dict, q: dict, var: str = "y", device=None) -> list:
     """res(p, q) eliminating ``var`` -- curvetop::resultant (elim.hpp:30-31).
 
@@ -339,12 +390,18 @@ class Plan:
     ``data_ptr()``); streams as raw ``cudaStream_t`` handles (``stream.cuda_stream``).
     """
 
-    def __init__(self, p: dict, q: dict, var: str = "y", device=None):
-        self._hp, self._hq = HostBipoly(p), HostBipoly(q)
+    def __init__(self, p: dict, q: dict = None, var: str = "y", device=None):
+        """Plan(p, q) for one resultant, or Plan(pairs) for a batch of same-shape resultants."""
         self._h = C.c_void_p()
         o = _opts(device)
-        _check(lib().ctg_plan_create(C.byref(self._hp.struct), C.byref(self._hq.struct),
-                                     1 if var in ("x", "X") else 0, C.byref(o), C.byref(self._h)), "plan_create")
+        elim = 1 if var in ("x", "X") else 0
+        if q is None:
+            self._hb = HostBatch(p)
+            _check(lib().ctg_plan_create_batch(self._hb.n, self._hb.p, self._hb.q, elim, C.byref(o),
+                                               C.byref(self._h)), "plan_create_batch")
+        else:
+            self._hb = HostBatch([(p, q)])
+            _check(lib().ctg_plan_create(self._hb.p, self._hb.q, elim, C.byref(o), C.byref(self._h)), "plan_create")
         info = PlanInfo()
         _check(lib().ctg_plan_get_info(self._h, C.byref(info)), "plan_info")
         self.info = info.as_dict()
@@ -355,8 +412,13 @@ class Plan:
     def residues(self, k0, k1, rows_ptr, stream=0):
         _check(lib().ctg_plan_residues(self._h, k0, k1, C.c_void_p(rows_ptr), C.c_void_p(stream)), "plan_residues")
 
-    def stage(self, stage, k0, k1, rows_ptr, stream=0):
-        _check(lib().ctg_plan_stage(self._h, stage, k0, k1, C.c_void_p(rows_ptr), C.c_void_p(stream)), "plan_stage")
+    def stage(self, stage, k0, k1, rows_ptr, stream=0, curve_stride=0):
+        _check(lib().ctg_plan_stage_batch(self._h, stage, k0, k1, C.c_void_p(rows_ptr), curve_stride,
+                                          C.c_void_p(stream)), "plan_stage")
+
+    def crt_batch(self, all_ptr, j0, j1, out_ptr, stream=0, curve_stride=0, row_block=0, block_stride=0):
+        _check(lib().ctg_plan_crt_batch(self._h, C.c_void_p(all_ptr), curve_stride, row_block, block_stride, j0, j1,
+                                        C.c_void_p(out_ptr), C.c_void_p(stream)), "plan_crt_batch")
 
     def crt(self, all_ptr, j0, j1, out_ptr, stream=0):
         _check(lib().ctg_plan_crt(self._h, C.c_void_p(all_ptr), j0, j1, C.c_void_p(out_ptr), C.c_void_p(stream)),

@@ -6,6 +6,10 @@
 // zero inputs, degree-0 operands) fall out of the formal-degree Sylvester
 // resultant computed on the device; only "both zero" (PreconditionError) and
 // "one zero" (zero polynomial) are decided on the host without computation.
+//
+// A plan holds a BATCH of B >= 1 same-shape problems (same formal degrees, same
+// derivative relation): one slot layout (the union of the supports), one prime set
+// (enough for the largest bound), one set of kernel launches with blockIdx.z = curve.
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -77,136 +81,46 @@ static bool is_y_derivative(const TermMap& p, const TermMap& q) {
   return cnt == q.size();
 }
 
-}  // namespace ctg
-
-using namespace ctg;
-
-struct ctg_plan {
-  int device = 0;
-  bool trivial = false;
-  int trivial_kind = 0;  // 0: zero polynomial
-  int n = 0, m = 0, deriv = 0, negate = 0;
-  uint32_t D = 0, N = 0, r = 1, a = 0;
-  int P = 0, S = 0, L = 1;
-  double bound_bits = 0;
-  std::vector<int32_t> dir;
-  std::vector<uint32_t> h_limbs;  // [L][S]
-  std::vector<int8_t> h_sign;     // [S]
-  std::shared_ptr<CrtTables> tabs;
-  // device state
-  uint32_t* d_limbs = nullptr;
-  int8_t* d_sign = nullptr;
-  int32_t* d_dir = nullptr;
-  uint32_t* d_tab = nullptr;
-  uint32_t* d_flags = nullptr;
-  uint32_t* d_counters = nullptr;
-  uint32_t flag_cap = 1u << 16;
-  uint32_t* d_Y = nullptr;
-  int64_t* d_tq = nullptr;
-  uint64_t* d_cols = nullptr;
-  int crt_cap = 0;
-  int launches = 0;
-  bool uploaded = false;
-  ~ctg_plan() {
-    cudaFree(d_limbs);
-    cudaFree(d_sign);
-    cudaFree(d_dir);
-    cudaFree(d_tab);
-    cudaFree(d_flags);
-    cudaFree(d_counters);
-    cudaFree(d_Y);
-    cudaFree(d_tq);
-    cudaFree(d_cols);
-  }
-  int out_limbs() const { return tabs ? tabs->LM : 0; }
+// One parsed problem, normalised so that deg_y p >= deg_y q.
+struct Problem {
+  TermMap p, q;
+  int n = -1, m = -1, deriv = 0, negate = 0;
+  bool trivial = false;  // one input zero -> zero polynomial
+  int64_t degb = 0;      // degree bound of the result
+  double bound_bits = 0; // log2 Hadamard bound
 };
 
-namespace ctg {
-
-static void build_slots(const TermMap& t, int deg, int& S, std::vector<int32_t>& off, std::vector<int32_t>& len,
-                        std::vector<std::pair<int, const SBig*>>& slot_vals) {
-  off.assign(deg + 1, 0);
-  len.assign(deg + 1, 0);
-  std::vector<int> X(deg + 1, -1);
-  for (const auto& [e, c] : t) X[e.first] = std::max(X[e.first], e.second);
-  for (int j = 0; j <= deg; ++j) {
-    off[j] = S;
-    len[j] = X[j] + 1;
-    S += len[j];
-  }
-  slot_vals.resize(S, {0, nullptr});
-  for (const auto& [e, c] : t) slot_vals[off[e.first] + e.second] = {1, &c};
-}
-
-ctg_plan* plan_build(const ctg_bipoly* pin, const ctg_bipoly* qin, int32_t eliminate_x, const ctg_opts* opts) {
-  std::unique_ptr<ctg_plan> pl(new ctg_plan());
-  TermMap p = parse_bipoly(pin, eliminate_x != 0), q = parse_bipoly(qin, eliminate_x != 0);
+static Problem parse_problem(const ctg_bipoly* pin, const ctg_bipoly* qin, int32_t eliminate_x) {
+  Problem pr;
+  pr.p = parse_bipoly(pin, eliminate_x != 0);
+  pr.q = parse_bipoly(qin, eliminate_x != 0);
   // Conventions of elim.cpp:98-100.
-  if (p.empty() && q.empty()) throw ApiError(CTG_PRECONDITION, "resultant: both inputs identically zero");
-  pl->device = select_device(opts);
-  if (p.empty() || q.empty()) {
-    pl->trivial = true;
-    pl->trivial_kind = 0;
-    return pl.release();
+  if (pr.p.empty() && pr.q.empty()) throw ApiError(CTG_PRECONDITION, "resultant: both inputs identically zero");
+  if (pr.p.empty() || pr.q.empty()) {
+    pr.trivial = true;
+    return pr;
   }
-  int n = deg_y(p), m = deg_y(q);
-  if (n < m) {
-    std::swap(p, q);
-    std::swap(n, m);
-    pl->negate = (n & 1) && (m & 1);  // res(p,q) = (-1)^{nm} res(q,p)
+  pr.n = deg_y(pr.p);
+  pr.m = deg_y(pr.q);
+  if (pr.n < pr.m) {
+    std::swap(pr.p, pr.q);
+    std::swap(pr.n, pr.m);
+    pr.negate = (pr.n & 1) && (pr.m & 1);  // res(p,q) = (-1)^{nm} res(q,p)
   }
-  pl->n = n;
-  pl->m = m;
-  if (n > kGeneralMaxDeg) throw ApiError(CTG_UNSUPPORTED, "resultant: degree in the eliminated variable exceeds 128");
-  pl->deriv = (m == n - 1 && n >= 1 && is_y_derivative(p, q)) ? 1 : 0;
-
-  // Slots and limbs.
-  std::vector<int32_t> offp, lenp, offq, lenq;
-  std::vector<std::pair<int, const SBig*>> vals;
-  int S = 0;
-  build_slots(p, n, S, offp, lenp, vals);
-  if (!pl->deriv) {
-    build_slots(q, m, S, offq, lenq, vals);
-  } else {
-    offq.assign(m + 1, 0);
-    lenq.assign(m + 1, 0);
-  }
-  pl->S = S;
-  int L = 1;
-  for (auto& v : vals)
-    if (v.second) L = std::max<int>(L, static_cast<int>(v.second->mag.size()));
-  pl->L = L;
-  pl->h_limbs.assign(static_cast<size_t>(L) * S, 0u);
-  pl->h_sign.assign(S, 0);
-  for (int s = 0; s < S; ++s) {
-    if (!vals[s].second) continue;
-    const SBig& c = *vals[s].second;
-    pl->h_sign[s] = static_cast<int8_t>(c.sign);
-    for (size_t l = 0; l < c.mag.size(); ++l) pl->h_limbs[l * S + s] = c.mag[l];
-  }
-  pl->dir.clear();
-  pl->dir.insert(pl->dir.end(), offp.begin(), offp.end());
-  pl->dir.insert(pl->dir.end(), lenp.begin(), lenp.end());
-  pl->dir.insert(pl->dir.end(), offq.begin(), offq.end());
-  pl->dir.insert(pl->dir.end(), lenq.begin(), lenq.end());
-
+  if (pr.n > kGeneralMaxDeg) throw ApiError(CTG_UNSUPPORTED, "resultant: degree in the eliminated variable exceeds 128");
+  pr.deriv = (pr.m == pr.n - 1 && pr.n >= 1 && is_y_derivative(pr.p, pr.q)) ? 1 : 0;
   // Degree bound of the result (min of the Sylvester row bound and Bezout).
   int Xp = 0, Xq = 0, tp = 0, tq = 0;
-  for (const auto& [e, c] : p) {
+  for (const auto& [e, c] : pr.p) {
     Xp = std::max(Xp, e.second);
     tp = std::max(tp, e.first + e.second);
   }
-  for (const auto& [e, c] : q) {
+  for (const auto& [e, c] : pr.q) {
     Xq = std::max(Xq, e.second);
     tq = std::max(tq, e.first + e.second);
   }
-  const int64_t row_bound = static_cast<int64_t>(m) * Xp + static_cast<int64_t>(n) * Xq;
-  const int64_t bez = static_cast<int64_t>(tp) * tq;
-  const int64_t degb = std::min(row_bound, bez);
-  if (degb + 1 > kMaxNtt) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 16383");
-  pl->D = static_cast<uint32_t>(degb + 1);
-  pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
-
+  pr.degb = std::min(static_cast<int64_t>(pr.m) * Xp + static_cast<int64_t>(pr.n) * Xq,
+                     static_cast<int64_t>(tp) * tq);
   // Hadamard bound over |x| = 1.
   auto norm_bits = [](const TermMap& t, int deg) {
     std::vector<std::vector<double>> per(deg + 1);
@@ -218,30 +132,179 @@ ctg_plan* plan_build(const ctg_bipoly* pin, const ctg_bipoly* qin, int32_t elimi
     }
     return log2_sum_upper(sq);
   };
-  const double bp = norm_bits(p, n), bq = norm_bits(q, m);
-  pl->bound_bits = 0.5 * m * (std::isfinite(bp) ? bp : 0) + 0.5 * n * (std::isfinite(bq) ? bq : 0);
-  if (pl->bound_bits < 0) pl->bound_bits = 0;
-  const double need = pl->bound_bits + 1 + 36;
+  const double bp = norm_bits(pr.p, pr.n), bq = norm_bits(pr.q, pr.m);
+  pr.bound_bits = 0.5 * pr.m * (std::isfinite(bp) ? bp : 0) + 0.5 * pr.n * (std::isfinite(bq) ? bq : 0);
+  if (pr.bound_bits < 0) pr.bound_bits = 0;
+  return pr;
+}
+
+}  // namespace ctg
+
+using namespace ctg;
+
+struct ctg_plan {
+  int device = 0;
+  int B = 1;
+  bool trivial = false;  // (B == 1 only) one input zero: the result is the zero polynomial
+  int n = 0, m = 0, deriv = 0, negate = 0;
+  uint32_t D = 0, N = 0, r = 1, a = 0;
+  int P = 0, S = 0, L = 1;
+  double bound_bits = 0;
+  std::vector<int32_t> dir;
+  std::vector<uint32_t> h_limbs;  // [B][L][S]
+  std::vector<int8_t> h_sign;     // [B][S]
+  std::shared_ptr<CrtTables> tabs;
+  // device state
+  uint32_t* d_limbs = nullptr;
+  int8_t* d_sign = nullptr;
+  int32_t* d_dir = nullptr;
+  uint32_t* d_tab = nullptr;       // [B][P][S]
+  uint32_t* d_flags = nullptr;
+  uint32_t* d_counters = nullptr;
+  uint32_t flag_cap = 1u << 16;
+  uint32_t* d_Y = nullptr;         // [B][P][J]
+  double* d_upart = nullptr;       // [B][nchunk][J]
+  uint64_t* d_cols = nullptr;      // [B][J][L16]
+  uint32_t* d_vals = nullptr;      // K2 point values [B][P][nrows][N] (fast path only)
+  int nrows = 0, maxlen = 0;
+  bool fast_ok = false;
+  int crt_cap = 0;
+  int launches = 0;
+  bool uploaded = false;
+  // Device buffers come from the stream-ordered pool (cudaMallocAsync): no device-wide
+  // synchronisation per plan.  They are released on the last stream the plan used.
+  cudaStream_t last_stream = nullptr;
+  template <class T>
+  void palloc(T*& ptr, size_t count, cudaStream_t st) {
+    void* p = nullptr;
+    CTG_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(1, count) * sizeof(T), st));
+    ptr = static_cast<T*>(p);
+  }
+  template <class T>
+  void pfree(T*& ptr) {
+    if (ptr) cudaFreeAsync(ptr, last_stream);
+    ptr = nullptr;
+  }
+  ~ctg_plan() {
+    pfree(d_limbs);
+    pfree(d_sign);
+    pfree(d_dir);
+    pfree(d_tab);
+    pfree(d_flags);
+    pfree(d_counters);
+    pfree(d_Y);
+    pfree(d_upart);
+    pfree(d_cols);
+    pfree(d_vals);
+  }
+  int out_limbs() const { return tabs ? tabs->LM : 0; }
+  int out_words() const { return out_limbs() + 1; }
+};
+
+namespace ctg {
+
+// Builds a plan over problems[idx...] which must share (n, m, deriv, negate).
+ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& idx, int device) {
+  std::unique_ptr<ctg_plan> pl(new ctg_plan());
+  pl->device = device;
+  pl->B = static_cast<int>(idx.size());
+  const Problem& p0 = probs[idx[0]];
+  if (p0.trivial) {
+    if (pl->B != 1) throw ApiError(CTG_INVALID, "plan: batch plans need nonzero inputs");
+    pl->trivial = true;
+    return pl.release();
+  }
+  pl->n = p0.n;
+  pl->m = p0.m;
+  pl->deriv = p0.deriv;
+  pl->negate = p0.negate;
+  int64_t degb = 0;
+  double bound = 0;
+  for (int i : idx) {
+    const Problem& pr = probs[i];
+    if (pr.trivial || pr.n != pl->n || pr.m != pl->m || pr.deriv != pl->deriv || pr.negate != pl->negate)
+      throw ApiError(CTG_INVALID, "plan: batch members must have the same degrees in the eliminated variable");
+    degb = std::max(degb, pr.degb);
+    bound = std::max(bound, pr.bound_bits);
+  }
+  const int n = pl->n, m = pl->m;
+  // Union slot layout: y-degree j of p owns x-degrees 0..X_j (max over the batch).
+  std::vector<int32_t> Xp(n + 1, -1), Xq(m + 1, -1);
+  for (int i : idx) {
+    for (const auto& [e, c] : probs[i].p) Xp[e.first] = std::max(Xp[e.first], e.second);
+    if (!pl->deriv)
+      for (const auto& [e, c] : probs[i].q) Xq[e.first] = std::max(Xq[e.first], e.second);
+  }
+  std::vector<int32_t> offp(n + 1), lenp(n + 1), offq(m + 1, 0), lenq(m + 1, 0);
+  int S = 0;
+  for (int j = 0; j <= n; ++j) {
+    offp[j] = S;
+    lenp[j] = Xp[j] + 1;
+    S += lenp[j];
+  }
+  if (!pl->deriv)
+    for (int j = 0; j <= m; ++j) {
+      offq[j] = S;
+      lenq[j] = Xq[j] + 1;
+      S += lenq[j];
+    }
+  pl->S = S;
+  int L = 1;
+  for (int i : idx) {
+    for (const auto& [e, c] : probs[i].p) L = std::max<int>(L, static_cast<int>(c.mag.size()));
+    if (!pl->deriv)
+      for (const auto& [e, c] : probs[i].q) L = std::max<int>(L, static_cast<int>(c.mag.size()));
+  }
+  pl->L = L;
+  pl->h_limbs.assign(static_cast<size_t>(pl->B) * L * S, 0u);
+  pl->h_sign.assign(static_cast<size_t>(pl->B) * S, 0);
+  for (int b = 0; b < pl->B; ++b) {
+    uint32_t* lb = pl->h_limbs.data() + static_cast<size_t>(b) * L * S;
+    int8_t* sb = pl->h_sign.data() + static_cast<size_t>(b) * S;
+    auto put = [&](int s, const SBig& c) {
+      sb[s] = static_cast<int8_t>(c.sign);
+      for (size_t l = 0; l < c.mag.size(); ++l) lb[l * S + s] = c.mag[l];
+    };
+    for (const auto& [e, c] : probs[idx[b]].p) put(offp[e.first] + e.second, c);
+    if (!pl->deriv)
+      for (const auto& [e, c] : probs[idx[b]].q) put(offq[e.first] + e.second, c);
+  }
+  pl->dir.clear();
+  for (auto* v : {&offp, &lenp, &offq, &lenq}) pl->dir.insert(pl->dir.end(), v->begin(), v->end());
+  pl->nrows = pl->deriv ? n + 1 : n + m + 2;
+  pl->maxlen = 1;
+  for (int v : lenp) pl->maxlen = std::max(pl->maxlen, v);
+  for (int v : lenq) pl->maxlen = std::max(pl->maxlen, v);
+  pl->fast_ok = (m == n - 1) && n >= 2 && n <= kFastMaxDeg;
+
+  if (degb + 1 > kMaxNtt) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 16383");
+  pl->D = static_cast<uint32_t>(degb + 1);
+  pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
+  pl->bound_bits = bound;
+  const double need = bound + 1 + 36;
   std::vector<uint32_t> primes = select_primes(pl->N, need);
   pl->P = static_cast<int>(primes.size());
   pl->tabs = get_tables(pl->device, pl->N, pl->P, primes);
   return pl.release();
 }
 
-static void plan_alloc(ctg_plan* pl) {
+static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   if (pl->d_tab) return;
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_limbs, sizeof(uint32_t) * std::max<size_t>(1, pl->h_limbs.size())));
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_sign, std::max<size_t>(1, pl->h_sign.size())));
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_dir, sizeof(int32_t) * pl->dir.size()));
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_tab, sizeof(uint32_t) * std::max<size_t>(1, static_cast<size_t>(pl->P) * pl->S)));
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_flags, sizeof(uint32_t) * pl->flag_cap));
-  CTG_CUDA_CHECK(cudaMalloc(&pl->d_counters, sizeof(uint32_t) * 4));
-  CTG_CUDA_CHECK(cudaMemset(pl->d_counters, 0, sizeof(uint32_t) * 4));
+  pl->last_stream = st;
+  pl->palloc(pl->d_limbs, pl->h_limbs.size(), st);
+  pl->palloc(pl->d_sign, pl->h_sign.size(), st);
+  pl->palloc(pl->d_dir, pl->dir.size(), st);
+  pl->palloc(pl->d_tab, static_cast<size_t>(pl->B) * pl->P * pl->S, st);
+  pl->palloc(pl->d_flags, pl->flag_cap, st);
+  pl->palloc(pl->d_counters, 4, st);
+  if (pl->fast_ok) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
+  CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
 }
 
 void plan_upload(ctg_plan* pl, cudaStream_t st) {
   if (pl->trivial) return;
-  plan_alloc(pl);
+  plan_alloc(pl, st);
+  pl->last_stream = st;
   CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_limbs, pl->h_limbs.data(), sizeof(uint32_t) * pl->h_limbs.size(),
                                  cudaMemcpyHostToDevice, st));
   CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_sign, pl->h_sign.data(), pl->h_sign.size(), cudaMemcpyHostToDevice, st));
@@ -254,32 +317,40 @@ int64_t plan_h2d_bytes(const ctg_plan* pl) {
   return static_cast<int64_t>(sizeof(uint32_t) * pl->h_limbs.size() + pl->h_sign.size() + 4 * pl->dir.size());
 }
 
-void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, cudaStream_t st) {
+// Rows of curve b, prime k in [k0, k1): d_rows + b * curve_stride + (k - k0) * N  (curve_stride 0 = dense).
+void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st) {
   if (pl->trivial) return;
   if (!pl->uploaded) throw ApiError(CTG_INVALID, "plan: inputs not uploaded");
   if (k0 < 0 || k1 > pl->P || k0 > k1) throw ApiError(CTG_INVALID, "plan: prime range out of bounds");
   if (stage < 1 || stage > 3) throw ApiError(CTG_INVALID, "plan: stage must be 1, 2 or 3");
   const int nk = k1 - k0;
   if (nk == 0) return;
+  const size_t rows_bstride = curve_stride > 0 ? static_cast<size_t>(curve_stride) : static_cast<size_t>(nk) * pl->N;
+  pl->last_stream = st;
   if (stage == 1) {
-    pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, k0, nk, pl->d_tab, st);
+    pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, k0, nk, pl->d_tab,
+                                  static_cast<size_t>(pl->P) * pl->S, pl->B, st);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }
   if (stage == 3) {
-    pl->launches += launch_interp(d_rows, static_cast<int>(pl->N), nk, pl->tabs->d_pc, k0, static_cast<int>(pl->N),
-                                  static_cast<int>(pl->r), static_cast<int>(pl->a), static_cast<int>(pl->D),
-                                  pl->negate, pl->d_counters, st);
+    pl->launches += launch_interp(d_rows, rows_bstride, static_cast<int>(pl->N), nk, pl->B, pl->tabs->d_pc, k0,
+                                  static_cast<int>(pl->N), static_cast<int>(pl->r), static_cast<int>(pl->a),
+                                  static_cast<int>(pl->D), pl->negate, pl->d_counters, st);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t), st));
   ResParams rp{};
+  rp.B = pl->B;
   rp.tab = pl->d_tab;
+  rp.tab_bstride = static_cast<size_t>(pl->P) * pl->S;
   rp.S = pl->S;
   rp.pc = pl->tabs->d_pc;
   rp.k0 = k0;
+  rp.nk = nk;
   rp.rows = d_rows;
+  rp.rows_bstride = rows_bstride;
   rp.pitch = static_cast<int>(pl->N);
   rp.N = static_cast<int>(pl->N);
   rp.n = pl->n;
@@ -289,31 +360,43 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, cudaS
   rp.flag_list = pl->d_flags;
   rp.counters = pl->d_counters;
   rp.flag_cap = pl->flag_cap;
-  pl->launches += launch_modres(rp, nk, true, st);
+  rp.vals = pl->fast_ok ? pl->d_vals : nullptr;
+  rp.nrows = pl->nrows;
+  rp.maxlen = pl->maxlen;
+  pl->launches += launch_modres(rp, true, st);
   CTG_CUDA_CHECK(cudaGetLastError());
 }
 
-void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, cudaStream_t st) {
-  for (int stage = 1; stage <= 3; ++stage) plan_stage(pl, stage, k0, k1, d_rows, st);
+void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st) {
+  for (int stage = 1; stage <= 3; ++stage) plan_stage(pl, stage, k0, k1, d_rows, curve_stride, st);
 }
 
-void plan_crt(ctg_plan* pl, const uint32_t* d_all, int j0, int j1, uint32_t* d_out, cudaStream_t st,
-              int row_block = 0, long long block_stride = 0) {
+// Coefficients [j0, j1) of every curve.  Residues of curve b, prime k at d_all + b * curve_stride
+// + (k / row_block) * block_stride + (k % row_block) * N; output curve b at d_out + b * out_stride.
+void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int row_block, long long block_stride,
+              int j0, int j1, uint32_t* d_out, long long out_stride, cudaStream_t st) {
   if (pl->trivial) return;
   if (j0 < 0 || j1 > static_cast<int>(pl->D) || j0 > j1) throw ApiError(CTG_INVALID, "plan: coefficient range out of bounds");
   const int J = j1 - j0;
   if (J == 0) return;
+  const int W = pl->out_words();
+  if (out_stride > 0 && out_stride != static_cast<long long>(J) * W)
+    throw ApiError(CTG_INVALID, "plan: output curve stride must equal (j1 - j0) * (out_limbs + 1)");
+  const int nch = (pl->P + kCrtChunk - 1) / kCrtChunk;
   if (J > pl->crt_cap) {
-    cudaFree(pl->d_Y);
-    cudaFree(pl->d_tq);
-    cudaFree(pl->d_cols);
-    CTG_CUDA_CHECK(cudaMalloc(&pl->d_Y, sizeof(uint32_t) * static_cast<size_t>(pl->P) * J));
-    CTG_CUDA_CHECK(cudaMalloc(&pl->d_tq, sizeof(int64_t) * J));
-    CTG_CUDA_CHECK(cudaMalloc(&pl->d_cols, sizeof(uint64_t) * static_cast<size_t>(pl->tabs->L16) * J));
+    pl->pfree(pl->d_Y);
+    pl->pfree(pl->d_upart);
+    pl->pfree(pl->d_cols);
+    pl->palloc(pl->d_Y, static_cast<size_t>(pl->B) * pl->P * J, st);
+    pl->palloc(pl->d_upart, static_cast<size_t>(pl->B) * nch * J, st);
+    pl->palloc(pl->d_cols, static_cast<size_t>(pl->B) * pl->tabs->L16 * J, st);
     pl->crt_cap = J;
   }
+  pl->last_stream = st;
   CrtParams cp{};
+  cp.B = pl->B;
   cp.rows = d_all;
+  cp.curve_stride = curve_stride > 0 ? curve_stride : static_cast<long long>(pl->P) * pl->N;
   cp.pitch = static_cast<int>(pl->N);
   cp.P = pl->P;
   cp.row_block = row_block > 0 ? row_block : pl->P;
@@ -326,7 +409,7 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, int j0, int j1, uint32_t* d_o
   cp.M16 = pl->tabs->d_M16;
   cp.L16 = pl->tabs->L16;
   cp.Y = pl->d_Y;
-  cp.tq = pl->d_tq;
+  cp.upart = pl->d_upart;
   cp.cols = pl->d_cols;
   cp.out = d_out;
   cp.out_limbs = pl->tabs->LM;
@@ -343,10 +426,11 @@ uint32_t plan_error_bits(ctg_plan* pl, cudaStream_t st) {
   return c[1];
 }
 
+// h: one curve's CRT output (n_coeffs records of out_limbs + 1 words).
 void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
   std::vector<UCoeff> coeffs;
   if (!pl->trivial) {
-    const int W = pl->out_limbs() + 1;
+    const int W = pl->out_words();
     coeffs.resize(pl->D);
     for (uint32_t j = 0; j < pl->D; ++j) {
       const uint32_t* rec = h + static_cast<size_t>(j) * W;
@@ -361,6 +445,32 @@ void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
   fill_upoly(coeffs, out);
 }
 
+// Full on-device pipeline for one plan on the context stream: H2D, K1-K5, one D2H;
+// results decoded into out[0 .. B).
+void plan_run_all(ctg_plan* pl, Ctx& ctx, ctg_upoly_buf* out) {
+  cudaStream_t s = ctx.stream;
+  auto& st = stats_tls();
+  plan_upload(pl, s);
+  st.h2d_bytes += plan_h2d_bytes(pl);
+  const size_t rows_words = static_cast<size_t>(pl->B) * pl->P * pl->N;
+  const size_t per_curve = static_cast<size_t>(pl->D) * pl->out_words();
+  const size_t out_words = per_curve * pl->B;
+  uint32_t* d_rows = ctx.scratch_u32(0, rows_words);
+  uint32_t* d_out = ctx.scratch_u32(1, out_words);
+  plan_residues(pl, 0, pl->P, d_rows, 0, s);
+  plan_crt(pl, d_rows, 0, 0, 0, 0, static_cast<int>(pl->D), d_out, 0, s);
+  uint32_t* h_out = ctx.pinned_u32(out_words + 4);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(h_out, d_out, sizeof(uint32_t) * out_words, cudaMemcpyDeviceToHost, s));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(h_out + out_words, pl->d_counters, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, s));
+  CTG_CUDA_CHECK(cudaStreamSynchronize(s));
+  st.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (out_words + 2));
+  st.kernel_launches += pl->launches;
+  st.flagged_units += static_cast<int32_t>(h_out[out_words]);
+  const uint32_t bits = h_out[out_words + 1];
+  if (bits) throw ApiError(CTG_INTERNAL, "resultant: device self-check failed (error bits " + std::to_string(bits) + ")");
+  for (int b = 0; b < pl->B; ++b) plan_decode(pl, h_out + per_curve * b, &out[b]);
+}
+
 }  // namespace ctg
 
 // ---------------------------------------------------------------------------
@@ -368,12 +478,30 @@ void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
 // ---------------------------------------------------------------------------
 extern "C" {
 
+ctg_status ctg_plan_create_batch(int32_t batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                                 const ctg_opts* opts, ctg_plan** plan) {
+  return guarded([&] {
+    if (!plan || !p || !q || batch < 1) throw ApiError(CTG_INVALID, "plan: bad batch arguments");
+    DeviceGuard g(opts);
+    std::vector<Problem> probs;
+    std::vector<int> idx;
+    for (int b = 0; b < batch; ++b) {
+      probs.push_back(parse_problem(&p[b], &q[b], eliminate_x));
+      idx.push_back(b);
+    }
+    const int dev = select_device(opts);
+    *plan = plan_build(probs, idx, dev);
+  });
+}
+
 ctg_status ctg_plan_create(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x, const ctg_opts* opts,
                            ctg_plan** plan) {
   return guarded([&] {
     if (!plan) throw ApiError(CTG_INVALID, "plan: null output pointer");
     DeviceGuard g(opts);
-    *plan = plan_build(p, q, eliminate_x, opts);
+    std::vector<Problem> probs{parse_problem(p, q, eliminate_x)};
+    const int dev = select_device(opts);
+    *plan = plan_build(probs, {0}, dev);
   });
 }
 
@@ -391,8 +519,9 @@ ctg_status ctg_plan_get_info(const ctg_plan* pl, ctg_plan_info* info) {
     info->trivial = pl->trivial ? 1 : 0;
     info->bound_bits = pl->bound_bits;
     const double n = pl->n;
-    info->work_mulmods = static_cast<double>(pl->P) * pl->D * (n * n + n - 2);
+    info->work_mulmods = static_cast<double>(pl->B) * pl->P * pl->D * (n * n + n - 2);
     info->h2d_bytes = plan_h2d_bytes(pl);
+    info->batch = pl->B;
   });
 }
 
@@ -408,7 +537,7 @@ ctg_status ctg_plan_residues(ctg_plan* pl, int32_t k0, int32_t k1, uint32_t* d_r
   return guarded([&] {
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");
     PlanDeviceGuard g(pl->device);
-    plan_residues(pl, k0, k1, d_rows, resolve_stream(pl->device, stream));
+    plan_residues(pl, k0, k1, d_rows, 0, resolve_stream(pl->device, stream));
   });
 }
 
@@ -416,7 +545,16 @@ ctg_status ctg_plan_stage(ctg_plan* pl, int32_t stage, int32_t k0, int32_t k1, u
   return guarded([&] {
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");
     PlanDeviceGuard g(pl->device);
-    plan_stage(pl, stage, k0, k1, d_rows, resolve_stream(pl->device, stream));
+    plan_stage(pl, stage, k0, k1, d_rows, 0, resolve_stream(pl->device, stream));
+  });
+}
+
+ctg_status ctg_plan_stage_batch(ctg_plan* pl, int32_t stage, int32_t k0, int32_t k1, uint32_t* d_rows,
+                                int64_t curve_stride, void* stream) {
+  return guarded([&] {
+    if (!pl || curve_stride < 0) throw ApiError(CTG_INVALID, "plan: null or negative stride");
+    PlanDeviceGuard g(pl->device);
+    plan_stage(pl, stage, k0, k1, d_rows, curve_stride, resolve_stream(pl->device, stream));
   });
 }
 
@@ -424,7 +562,7 @@ ctg_status ctg_plan_crt(ctg_plan* pl, const uint32_t* d_all, int32_t j0, int32_t
   return guarded([&] {
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");
     PlanDeviceGuard g(pl->device);
-    plan_crt(pl, d_all, j0, j1, d_out, resolve_stream(pl->device, stream));
+    plan_crt(pl, d_all, 0, 0, 0, j0, j1, d_out, 0, resolve_stream(pl->device, stream));
   });
 }
 
@@ -434,7 +572,18 @@ ctg_status ctg_plan_crt_sharded(ctg_plan* pl, const uint32_t* d_all, int32_t row
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");
     if (row_block <= 0 || block_stride < 0) throw ApiError(CTG_INVALID, "plan: bad row_block / block_stride");
     PlanDeviceGuard g(pl->device);
-    plan_crt(pl, d_all, j0, j1, d_out, resolve_stream(pl->device, stream), row_block, block_stride);
+    plan_crt(pl, d_all, 0, row_block, block_stride, j0, j1, d_out, 0, resolve_stream(pl->device, stream));
+  });
+}
+
+ctg_status ctg_plan_crt_batch(ctg_plan* pl, const uint32_t* d_all, int64_t curve_stride, int32_t row_block,
+                              int64_t block_stride, int32_t j0, int32_t j1, uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    if (!pl || curve_stride < 0 || row_block < 0 || block_stride < 0)
+      throw ApiError(CTG_INVALID, "plan: null or negative layout argument");
+    PlanDeviceGuard g(pl->device);
+    plan_crt(pl, d_all, curve_stride, row_block, block_stride, j0, j1, d_out, 0,
+             resolve_stream(pl->device, stream));
   });
 }
 
@@ -465,49 +614,53 @@ void ctg_plan_destroy(ctg_plan* pl) {
   cudaSetDevice(prev);
 }
 
-ctg_status ctg_resultant(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x, ctg_upoly_buf* out,
-                         const ctg_opts* opts) {
+ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                               ctg_upoly_buf* out, const ctg_opts* opts) {
   return guarded([&] {
-    if (!out) throw ApiError(CTG_INVALID, "resultant: null output");
+    if (!out || !p || !q || batch < 0) throw ApiError(CTG_INVALID, "resultant_batch: bad arguments");
     CallTimer timer;
-    DeviceGuard g(opts);
-    std::unique_ptr<ctg_plan> pl(plan_build(p, q, eliminate_x, opts));
+    for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
+    std::vector<Problem> probs;
+    probs.reserve(batch);
+    for (int b = 0; b < batch; ++b) probs.push_back(parse_problem(&p[b], &q[b], eliminate_x));
+    // Group the nontrivial problems by shape; trivial ones are zero polynomials.
+    std::map<std::tuple<int, int, int, int>, std::vector<int>> groups;
+    for (int b = 0; b < batch; ++b) {
+      if (probs[b].trivial) {
+        fill_upoly({}, &out[b]);
+        continue;
+      }
+      groups[{probs[b].n, probs[b].m, probs[b].deriv, probs[b].negate}].push_back(b);
+    }
     timer.mark_setup();
-    auto& st = stats_tls();
-    st.n_primes = pl->P;
-    st.n_points = static_cast<int32_t>(pl->N);
-    st.n_coeffs = static_cast<int32_t>(pl->D);
-    st.out_limbs = pl->out_limbs();
-    if (pl->trivial) {
-      plan_decode(pl.get(), nullptr, out);
+    if (groups.empty()) {
       timer.finish();
       return;
     }
-    Ctx& ctx = context(pl->device);
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
     std::lock_guard<std::mutex> lock(ctx.mu);
-    cudaStream_t s = ctx.stream;
-    plan_upload(pl.get(), s);
-    st.h2d_bytes = plan_h2d_bytes(pl.get());
-    const size_t rows_words = static_cast<size_t>(pl->P) * pl->N;
-    const size_t out_words = static_cast<size_t>(pl->D) * (pl->out_limbs() + 1);
-    uint32_t* d_rows = ctx.scratch_u32(0, rows_words);
-    uint32_t* d_out = ctx.scratch_u32(1, out_words);
-    timer.mark_h2d();
-    plan_residues(pl.get(), 0, pl->P, d_rows, s);
-    plan_crt(pl.get(), d_rows, 0, static_cast<int>(pl->D), d_out, s);
-    uint32_t* h_out = ctx.pinned_u32(out_words + 4);
-    CTG_CUDA_CHECK(cudaMemcpyAsync(h_out, d_out, sizeof(uint32_t) * out_words, cudaMemcpyDeviceToHost, s));
-    CTG_CUDA_CHECK(cudaMemcpyAsync(h_out + out_words, pl->d_counters, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, s));
-    CTG_CUDA_CHECK(cudaStreamSynchronize(s));
+    auto& st = stats_tls();
+    std::vector<ctg_upoly_buf> tmp;
+    for (auto& [key, idx] : groups) {
+      std::unique_ptr<ctg_plan> pl(plan_build(probs, idx, dev));
+      st.n_primes = std::max(st.n_primes, pl->P);
+      st.n_points = static_cast<int32_t>(pl->N);
+      st.n_coeffs = static_cast<int32_t>(pl->D);
+      st.out_limbs = std::max(st.out_limbs, pl->out_limbs());
+      tmp.assign(idx.size(), ctg_upoly_buf{});
+      plan_run_all(pl.get(), ctx, tmp.data());
+      for (size_t i = 0; i < idx.size(); ++i) out[idx[i]] = tmp[i];
+    }
     timer.mark_device();
-    st.d2h_bytes = static_cast<int64_t>(sizeof(uint32_t) * (out_words + 2));
-    st.kernel_launches = pl->launches;
-    st.flagged_units = static_cast<int32_t>(h_out[out_words]);
-    const uint32_t bits = h_out[out_words + 1];
-    if (bits) throw ApiError(CTG_INTERNAL, "resultant: device self-check failed (error bits " + std::to_string(bits) + ")");
-    plan_decode(pl.get(), h_out, out);
     timer.finish();
   });
+}
+
+ctg_status ctg_resultant(const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x, ctg_upoly_buf* out,
+                         const ctg_opts* opts) {
+  return ctg_resultant_batch(1, p, q, eliminate_x, out, opts);
 }
 
 }  // extern "C"

@@ -149,7 +149,7 @@ uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launc
   uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
   CTG_CUDA_CHECK(cudaMemcpyAsync(d_limbs, limbs.data(), 4 * limbs.size(), cudaMemcpyHostToDevice, ar.st));
   CTG_CUDA_CHECK(cudaMemcpyAsync(d_sign, sign.data(), S, cudaMemcpyHostToDevice, ar.st));
-  L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, 0, tabs.P, d_tab, ar.st);
+  L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, 0, tabs.P, d_tab, static_cast<size_t>(tabs.P) * S, 1, ar.st);
   auto& st = stats_tls();
   st.h2d_bytes += static_cast<int64_t>(4 * limbs.size() + S);
   return d_tab;
@@ -182,12 +182,14 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   const int W = T->LM + 1;
   uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(cols) * W);
   uint32_t* d_Y = ar.alloc<uint32_t>(static_cast<size_t>(R) * cols);
-  int64_t* d_tq = ar.alloc<int64_t>(cols);
+  double* d_upart = ar.alloc<double>(static_cast<size_t>((R + kCrtChunk - 1) / kCrtChunk) * cols);
   uint64_t* d_cols = ar.alloc<uint64_t>(static_cast<size_t>(T->L16) * cols);
   uint32_t* d_cnt = ar.alloc<uint32_t>(4);
   CTG_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 16, ar.st));
   CrtParams cp{};
+  cp.B = 1;
   cp.rows = d_rows;
+  cp.curve_stride = static_cast<long long>(R) * cols;
   cp.pitch = cols;
   cp.P = R;
   cp.row_block = R;
@@ -200,7 +202,7 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   cp.M16 = T->d_M16;
   cp.L16 = T->L16;
   cp.Y = d_Y;
-  cp.tq = d_tq;
+  cp.upart = d_upart;
   cp.cols = d_cols;
   cp.out = d_out;
   cp.out_limbs = T->LM;

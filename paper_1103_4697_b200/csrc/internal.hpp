@@ -1,4 +1,8 @@
-// Internal declarations shared by the host API (api.cu) and the kernels.
+// Internal declarations shared by the host API (api_*.cu) and the kernels.
+//
+// Every resultant kernel processes a BATCH of B same-shape problems (curves): the
+// batch index is blockIdx.z and each per-curve array has a batch stride.  A single
+// ctg_resultant call is a batch of one.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -26,6 +30,7 @@ constexpr int kFastMaxDeg = 40;     // fast mod-p resultant templates: deg_y p i
 constexpr int kGeneralMaxDeg = 128; // general (formal-degree) kernel limit
 constexpr uint32_t kMaxNtt = 1u << 14;
 constexpr uint32_t kSentinel = 0xffffffffu;
+constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT rounding estimate
 
 // Device error bits (plan counters[1]).
 enum : uint32_t {
@@ -52,31 +57,33 @@ struct CrtTables {
 // Builds the tables for `primes` (in order) on `device`; N = NTT size (1 if unused).
 std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N);
 
-// Slot directory: y-degree j of a polynomial owns slots [off, off + len) of the
-// residue table; slot off + t holds the coefficient of x^t.
-struct SlotDir {
-  std::vector<int32_t> off, len;
-};
-
 struct ResParams {
-  const uint32_t* tab;      // [P][S] Montgomery residues of the slots
+  int B;                    // curves in the batch (blockIdx.z)
+  const uint32_t* tab;      // [B][P][S] Montgomery residues of the slots (global prime index)
+  size_t tab_bstride;       // = P * S
   int S;
   const PrimeConst* pc;     // [P]
-  int k0;                   // global index of the first prime of this launch
-  uint32_t* rows;           // output rows (k - k0) * pitch
+  int k0, nk;               // this launch covers primes [k0, k0 + nk)
+  uint32_t* rows;           // curve b, prime k: rows + b * rows_bstride + (k - k0) * pitch
+  size_t rows_bstride;
   int pitch;
   int N;                    // evaluation points per prime
   int n, m;                 // formal degrees in y (n >= m)
   int deriv;                // q == dp/dy: q_j(x) = (j+1) p_{j+1}(x)
-  const int32_t* dir;       // device slot directory: off_p[n+1], len_p[n+1], off_q[m+1], len_q[m+1]
+  const int32_t* dir;       // slot directory: off_p[n+1], len_p[n+1], off_q[m+1], len_q[m+1]
   uint32_t* flag_list;      // degenerate units (fast path) -> general kernel
   uint32_t* counters;       // [0] flagged count, [1] error bits
   uint32_t flag_cap;
+  uint32_t* vals;           // K2 output: [B][nk][nrows][N] point values (Montgomery); null = no fast path
+  int nrows;                // n + 1 (derivative mode) or n + m + 2
+  int maxlen;               // longest slot run (max x-degree + 1) over the rows
 };
 
 struct CrtParams {
-  const uint32_t* rows;  // full residue matrix, plain residues; row k at
-                         // rows + (k / row_block) * block_stride + (k % row_block) * pitch
+  int B;
+  const uint32_t* rows;  // plain residues; curve b, prime k at rows + b * curve_stride
+                         //   + (k / row_block) * block_stride + (k % row_block) * pitch
+  long long curve_stride;
   int pitch, P;
   int row_block;
   long long block_stride;
@@ -86,20 +93,20 @@ struct CrtParams {
   const uint32_t* Mk16;  // [P][L16] 16-bit digits of M / p_k
   const uint32_t* M16;   // [L16] 16-bit digits of M
   int L16;
-  uint32_t* Y;           // scratch [P][J]
-  int64_t* tq;           // scratch [J]
-  uint64_t* cols;        // scratch [J][L16]
-  uint32_t* out;         // [J][out_limbs + 1]
+  uint32_t* Y;           // scratch [B][P][J]
+  double* upart;         // scratch [B][ceil(P / kCrtChunk)][J]: partial sums of y_k / p_k
+  uint64_t* cols;        // scratch [B][J][L16]
+  uint32_t* out;         // [B][J][out_limbs + 1]
   int out_limbs;
   uint32_t* counters;
 };
 
 // Kernel launchers (kernels_res.cu).  Each returns the number of launches issued.
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0,
-                  int nk, uint32_t* d_tab, cudaStream_t st);
-int launch_modres(const ResParams& rp, int nk, bool fast, cudaStream_t st);
-int launch_interp(uint32_t* rows, int pitch, int nk, const PrimeConst* d_pc, int k0, int N, int r, int a, int D,
-                  int negate, uint32_t* counters, cudaStream_t st);
+                  int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st);
+int launch_modres(const ResParams& rp, bool fast, cudaStream_t st);
+int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc, int k0,
+                  int N, int r, int a, int D, int negate, uint32_t* counters, cudaStream_t st);
 int launch_crt(const CrtParams& cp, cudaStream_t st);
 
 }  // namespace ctg

@@ -1,17 +1,18 @@
-// sm_100a kernels of the multi-modular resultant (SURVEY.md §2 kernel table):
+// sm_100a kernels of the multi-modular resultant (SURVEY.md §2 kernel table).  Every
+// kernel processes a batch of B same-shape curves (blockIdx.z = curve).
 //
-//   K1 k_reduce        multiprecision coefficients -> residues mod each prime (Montgomery form)
-//   K2+K3 k_modres_fast<n>  per (prime, point): evaluate p, q at x = omega^i (Horner over the
-//                      residue table staged in shared memory) and run a division-free
-//                      Euclid on the two univariate images entirely in registers
-//   K3' k_modres_general  exact formal-degree resultant (degree drops, zero pivots, any shape)
-//                      for the units the fast path flags, or for shapes without a fast template
-//   K4 k_interp        inverse mixed-radix NTT (N = r * 2^a) per prime: values -> coefficients
-//   K5 k_crt_prep / k_crt_gemm / k_crt_carry  fixed-point CRT:  c = sum_k y_k (M/p_k) - t M
+//   K1 k_reduce          multiprecision coefficients -> residues mod each prime (Montgomery)
+//   K2 k_eval_ntt<LP>    y-coefficient rows evaluated at x = omega^i, i < N: coset
+//                        decomposition into LP-point NTTs in registers (k_eval_horner otherwise)
+//   K3 k_modres_fast<n>  (modres_fast.cuh) division-free Euclid per (prime, point) in registers
+//   K3' k_modres_general exact formal-degree resultant (degree drops, zero pivots, any shape)
+//                        for the units the fast path flags, or for shapes without a template
+//   K4 k_interp          inverse mixed-radix NTT (N = r 2^a) per prime: values -> coefficients
+//   K5 k_crt_prep / k_crt_gemm / k_crt_carry   fixed-point CRT  c = sum_k y_k (M/p_k) - t M
 //
 // The reference computes the same R = res_y(p, q) by a subresultant PRS over Z[x]
-// (/root/reference/proj/src/elim.cpp:95-136); R is unique, so the modular image of
-// the Sylvester determinant at every (prime, point) determines it bit-exactly.
+// (/root/reference/proj/src/elim.cpp:95-136); R is unique, so the modular images of the
+// Sylvester determinant at every (prime, point) determine it bit-exactly.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,27 +25,146 @@ namespace ctg {
 namespace {
 
 // ---------------------------------------------------------------------------
-// K1: reduce multiprecision slots modulo the primes.  limbs are stored limb-major
-// ([L][S]) so consecutive threads (slots) read consecutive words.
+// K1: reduce multiprecision slots modulo the primes.  Limbs are limb-major per curve
+// ([B][L][S]) so consecutive threads (slots) read consecutive words.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ limbs, const int8_t* __restrict__ sign,
                                                 int S, int L, const PrimeConst* __restrict__ pc, int k0,
-                                                uint32_t* __restrict__ tab) {
+                                                uint32_t* __restrict__ tab, size_t tab_bstride) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = k0 + blockIdx.y;
+  const int b = blockIdx.z;
   if (s >= S) return;
   const Mod M = load_mod(pc[k]);
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S;
   uint32_t acc = 0;
   // Horner over limbs from the top: acc <- acc * 2^32 + limb  (in Montgomery form:
   // mmul(acc, R^2) = acc*2^32, mmul(limb, R^2) = limb in Montgomery form).
   for (int l = L - 1; l >= 0; --l) {
-    uint32_t v = limbs[static_cast<size_t>(l) * S + s];
+    uint32_t v = lb[static_cast<size_t>(l) * S + s];
     v = v >= 2u * M.p ? v - 2u * M.p : v;  // p > 2^30: v < 4p
     v = csub(v, M.p);
     acc = mmul2(acc, M.r2, v, M.r2, M);
   }
-  if (sign[s] < 0) acc = mneg(acc, M.p);
-  tab[static_cast<size_t>(k) * S + s] = acc;
+  if (sign[static_cast<size_t>(b) * S + s] < 0) acc = mneg(acc, M.p);
+  tab[b * tab_bstride + static_cast<size_t>(k) * S + s] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K2: evaluate every y-coefficient row at all N points omega^i (Montgomery form).
+// Row r < n+1 is p_r(x); rows n+1.. are q_r(x) when q is not dp/dy.
+//
+// Coset decomposition: with LP = 2^b >= row length, LP | N and K = N / LP,
+//   V[u + K v] = sum_t (c_t omega^{t u}) (omega^K)^{t v} = NTT_LP(c_t omega^{t u})[v],
+// so each thread (prime, row, u) twists <= LP coefficients and runs one LP-point NTT
+// in registers: N (1 + log2(LP)/2) mulmods per row instead of N * len for Horner.
+// ---------------------------------------------------------------------------
+constexpr int bitrev_c(int t, int lg) {
+  int r = 0;
+  for (int i = 0; i < lg; ++i) r |= ((t >> i) & 1) << (lg - 1 - i);
+  return r;
+}
+
+__device__ __forceinline__ void row_slots(const ResParams& P, int r, int& off, int& len) {
+  const int nq = P.n + 1;
+  if (r < nq) {
+    off = P.dir[r];
+    len = P.dir[nq + r];
+  } else {
+    const int j = r - nq, base = 2 * nq;
+    off = P.dir[base + j];
+    len = P.dir[base + P.m + 1 + j];
+  }
+}
+
+__device__ __forceinline__ uint32_t* vals_row(const ResParams& P, int b, int kl, int r) {
+  return P.vals + ((static_cast<size_t>(b) * P.nk + kl) * P.nrows + r) * P.N;
+}
+
+template <int LP, int LG>
+__global__ void __launch_bounds__(128) k_eval_ntt(ResParams P, int K) {
+  const int kl = blockIdx.y, b = blockIdx.z;
+  const int k = P.k0 + kl;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P.nrows * K) return;
+  const int r = idx / K, u = idx - r * K;
+  const PrimeConst pcv = P.pc[k];
+  const Mod M = load_mod(pcv);
+  int off, len;
+  row_slots(P, r, off, len);
+  const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S + off;
+  uint32_t a[LP];
+  const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(u), M);
+  uint32_t xp = M.one;
+#pragma unroll
+  for (int t = 0; t < LP; ++t) {
+    const uint32_t c = (t < len) ? tab[t] : 0u;
+    a[bitrev_c(t, LG)] = mmul(c, xp, M);
+    xp = mmul(xp, x, M);
+  }
+  const uint32_t w = mpow(pcv.omega, static_cast<uint64_t>(K), M);  // order LP
+  uint32_t tw[LP / 2];
+  tw[0] = M.one;
+#pragma unroll
+  for (int e = 1; e < LP / 2; ++e) tw[e] = mmul(tw[e - 1], w, M);
+#pragma unroll
+  for (int len2 = 2; len2 <= LP; len2 <<= 1) {
+    const int half = len2 >> 1, step = LP / len2;
+#pragma unroll
+    for (int g = 0; g < LP; g += len2) {
+#pragma unroll
+      for (int t = 0; t < half; ++t) {
+        const uint32_t x0 = a[g + t], x1 = mmul(a[g + t + half], tw[t * step], M);
+        a[g + t] = madd(x0, x1, M.p);
+        a[g + t + half] = msub(x0, x1, M.p);
+      }
+    }
+  }
+  uint32_t* out = vals_row(P, b, kl, r) + u;
+#pragma unroll
+  for (int v = 0; v < LP; ++v) out[static_cast<size_t>(K) * v] = a[v];
+}
+
+// Fallback K2 (any row length / N): thread per (prime, row, point), Horner.
+__global__ void __launch_bounds__(128) k_eval_horner(ResParams P) {
+  const int r = blockIdx.y % P.nrows, kl = blockIdx.y / P.nrows, b = blockIdx.z;
+  const int k = P.k0 + kl;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.N) return;
+  const PrimeConst pcv = P.pc[k];
+  const Mod M = load_mod(pcv);
+  int off, len;
+  row_slots(P, r, off, len);
+  const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
+  vals_row(P, b, kl, r)[i] = horner(P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S, off, len, x, M);
+}
+
+template <int LP, int LG>
+void launch_eval_ntt(const ResParams& rp, cudaStream_t st) {
+  const int K = rp.N / LP;
+  dim3 grid((rp.nrows * K + 127) / 128, rp.nk, rp.B);
+  k_eval_ntt<LP, LG><<<grid, 128, 0, st>>>(rp, K);
+}
+
+int launch_eval(const ResParams& rp, cudaStream_t st) {
+  int lp = 4, lg = 2;
+  while (lp < rp.maxlen) {
+    lp <<= 1;
+    ++lg;
+  }
+  if ((rp.N % lp) == 0 && lp <= 64) {
+    switch (lp) {
+      case 4: launch_eval_ntt<4, 2>(rp, st); return 1;
+      case 8: launch_eval_ntt<8, 3>(rp, st); return 1;
+      case 16: launch_eval_ntt<16, 4>(rp, st); return 1;
+      case 32: launch_eval_ntt<32, 5>(rp, st); return 1;
+      case 64: launch_eval_ntt<64, 6>(rp, st); return 1;
+      default: break;
+    }
+  }
+  dim3 grid((rp.N + 127) / 128, rp.nrows * rp.nk, rp.B);
+  k_eval_horner<<<grid, 128, 0, st>>>(rp);
+  return 1;
 }
 
 // Exact resultant of univariate images with FORMAL degrees na, nb (Montgomery
@@ -105,18 +225,20 @@ __device__ uint32_t res_general(uint32_t* A, int na, uint32_t* B, int nb, const 
 }
 
 // General path: one thread per unit, either all units (use_list = 0) or the
-// degenerate units listed by the fast path.
+// degenerate units listed by the fast path.  Unit id = (b * nk + kl) * N + i.
 __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_list, uint32_t total_units) {
   const uint32_t count = use_list ? min(P.counters[0], P.flag_cap) : total_units;
   const int nq = P.n + 1;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < count; u += gridDim.x * blockDim.x) {
     const uint32_t unit = use_list ? P.flag_list[u] : u;
-    const int kl = static_cast<int>(unit / P.N), i = static_cast<int>(unit % P.N);
+    const uint32_t bk = unit / P.N;
+    const int i = static_cast<int>(unit % P.N);
+    const int kl = static_cast<int>(bk % P.nk), b = static_cast<int>(bk / P.nk);
     const int k = P.k0 + kl;
     const PrimeConst pcv = P.pc[k];
     const Mod M = load_mod(pcv);
     const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
-    const uint32_t* tab = P.tab + static_cast<size_t>(k) * P.S;
+    const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S;
     uint32_t bufA[kGeneralMaxDeg + 1], bufB[kGeneralMaxDeg + 1];
     for (int j = 0; j <= P.n; ++j) bufA[j] = horner(tab, P.dir[j], P.dir[nq + j], x, M);
     if (P.deriv) {
@@ -129,7 +251,7 @@ __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_lis
       const int base = 2 * nq;
       for (int j = 0; j <= P.m; ++j) bufB[j] = horner(tab, P.dir[base + j], P.dir[base + P.m + 1 + j], x, M);
     }
-    P.rows[static_cast<size_t>(kl) * P.pitch + i] = res_general(bufA, P.n, bufB, P.m, M);
+    P.rows[b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch + i] = res_general(bufA, P.n, bufB, P.m, M);
   }
 }
 
@@ -139,15 +261,16 @@ __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_lis
 //   u[i1] = radix-2 inverse NTT (root omega^{-r}) of v[r*i2 + i1],
 // with s = +-N^{-1}.  Coefficients j >= D must vanish (degree bound check).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_interp(uint32_t* rows, int pitch, const PrimeConst* __restrict__ pc, int k0,
-                                                int N, int r, int a, int D, int negate, uint32_t* counters) {
+__global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstride, int pitch,
+                                                const PrimeConst* __restrict__ pc, int k0, int N, int r, int a,
+                                                int D, int negate, uint32_t* counters) {
   extern __shared__ uint32_t sm[];
   uint32_t* tw = sm;      // omega^{-i}, i < N
   uint32_t* w = sm + N;   // work array
-  const int kl = blockIdx.x;
+  const int kl = blockIdx.x, b = blockIdx.y;
   const PrimeConst pcv = pc[k0 + kl];
   const Mod M = load_mod(pcv);
-  uint32_t* row = rows + static_cast<size_t>(kl) * pitch;
+  uint32_t* row = rows + b * rows_bstride + static_cast<size_t>(kl) * pitch;
   const int Mlen = 1 << a;
   const int tid = threadIdx.x, bs = blockDim.x;
   bool bad = false;
@@ -164,9 +287,9 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, int pitch, const
   const int halfM = Mlen >> 1;
   for (int len = 2; len <= Mlen; len <<= 1) {
     const int half = len >> 1, step = Mlen / len;
-    for (int b = tid; b < r * halfM; b += bs) {
-      const int rw = b / halfM, bb = b % halfM;
-      const int g = bb / half, t = bb % half;
+    for (int bb = tid; bb < r * halfM; bb += bs) {
+      const int rw = bb / halfM, q = bb % halfM;
+      const int g = q / half, t = q % half;
       uint32_t* base = w + rw * Mlen + g * len;
       const uint32_t u = base[t];
       const uint32_t v = mmul(base[t + half], tw[r * t * step], M);
@@ -199,19 +322,27 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, int pitch, const
 //   c = sum_k y_k (M/p_k) - t M      (|c| < M / 2^35 by the choice of primes, so
 //   u is within 2^-34 of an integer and the double sum rounds exactly).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ const uint32_t* crt_row(const CrtParams& C, int b, int k) {
+  return C.rows + b * C.curve_stride + static_cast<long long>(k / C.row_block) * C.block_stride +
+         static_cast<long long>(k % C.row_block) * C.pitch;
+}
+
+// grid (ceil(J/32), ceil(P/kCrtChunk), B), block (32, 8): y_k for 32 coefficients x 64 primes,
+// plus the partial sum of y_k / p_k over the chunk.
 __global__ void __launch_bounds__(256) k_crt_prep(CrtParams C) {
   __shared__ double red[8][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int jl = blockIdx.x * 32 + tx;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int kbeg = chunk * kCrtChunk, kend = min(kbeg + kCrtChunk, C.P);
   double u = 0;
   if (jl < C.J) {
-    for (int k = ty; k < C.P; k += 8) {
+    for (int k = kbeg + ty; k < kend; k += 8) {
       const PrimeConst& pcv = C.pc[k];
       const Mod M = load_mod(pcv);
-      const uint32_t v = C.rows[static_cast<long long>(k / C.row_block) * C.block_stride +
-                                static_cast<long long>(k % C.row_block) * C.pitch + C.j0 + jl];
+      const uint32_t v = crt_row(C, b, k)[C.j0 + jl];
       const uint32_t y = mmul(v, pcv.crt_c, M);
-      C.Y[static_cast<size_t>(k) * C.J + jl] = y;
+      C.Y[(static_cast<size_t>(b) * C.P + k) * C.J + jl] = y;
       u += static_cast<double>(y) * C.minv[k];
     }
   }
@@ -220,28 +351,34 @@ __global__ void __launch_bounds__(256) k_crt_prep(CrtParams C) {
   if (ty == 0 && jl < C.J) {
     double s = 0;
     for (int q = 0; q < 8; ++q) s += red[q][tx];
-    const double t = rint(s);
-    if (fabs(s - t) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
-    C.tq[jl] = static_cast<int64_t>(t);
+    const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+    C.upart[(static_cast<size_t>(b) * nch + chunk) * C.J + jl] = s;
   }
 }
 
-// cols[j][l] = sum_k Y[k][j] * Mk16[k][l]  (31-bit x 16-bit products, exact u64 sums)
-__global__ void __launch_bounds__(256) k_crt_gemm(CrtParams C) {
-  __shared__ __align__(16) uint32_t Ys[16][64];
+// cols[j][l] = sum_k Y[k][j] * Mk16[k][l]  (31-bit x 16-bit products, exact u64 sums:
+// one IMAD.WIDE.U32 with 64-bit accumulate per MAC).  Tile 32 j x 64 l, 128 threads,
+// 4 x 4 accumulators per thread, k staged through shared memory 16 primes at a time.
+__global__ void __launch_bounds__(128) k_crt_gemm(CrtParams C) {
+  __shared__ __align__(16) uint32_t Ys[16][32];
   __shared__ __align__(16) uint32_t Ms[16][64];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int jb = blockIdx.y * 64, lb = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // ty < 8
+  const int jb = blockIdx.y * 32, lb = blockIdx.x * 64, b = blockIdx.z;
+  const uint32_t* Yb = C.Y + static_cast<size_t>(b) * C.P * C.J;
   uint64_t acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0;
+    for (int q = 0; q < 4; ++q) acc[a][q] = 0;
   for (int k0 = 0; k0 < C.P; k0 += 16) {
-    for (int e = threadIdx.x; e < 1024; e += 256) {
+    for (int e = threadIdx.x; e < 16 * 32; e += 128) {
+      const int kk = e >> 5, c = e & 31;
+      const int k = k0 + kk;
+      Ys[kk][c] = (k < C.P && jb + c < C.J) ? Yb[static_cast<size_t>(k) * C.J + jb + c] : 0u;
+    }
+    for (int e = threadIdx.x; e < 16 * 64; e += 128) {
       const int kk = e >> 6, c = e & 63;
       const int k = k0 + kk;
-      Ys[kk][c] = (k < C.P && jb + c < C.J) ? C.Y[static_cast<size_t>(k) * C.J + jb + c] : 0u;
       Ms[kk][c] = (k < C.P && lb + c < C.L16) ? C.Mk16[static_cast<size_t>(k) * C.L16 + lb + c] : 0u;
     }
     __syncthreads();
@@ -254,94 +391,163 @@ __global__ void __launch_bounds__(256) k_crt_gemm(CrtParams C) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] += static_cast<uint64_t>(ya[a]) * ma[b];
+        for (int q = 0; q < 4; ++q) acc[a][q] += static_cast<uint64_t>(ya[a]) * ma[q];
     }
     __syncthreads();
   }
+  uint64_t* cols = C.cols + static_cast<size_t>(b) * C.J * C.L16;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int j = jb + ty * 4 + a;
     if (j >= C.J) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int l = lb + tx * 4 + b;
-      if (l < C.L16) C.cols[static_cast<size_t>(j) * C.L16 + l] = acc[a][b];
+    for (int q = 0; q < 4; ++q) {
+      const int l = lb + tx * 4 + q;
+      if (l < C.L16) cols[static_cast<size_t>(j) * C.L16 + l] = acc[a][q];
     }
   }
 }
 
-// Carry propagation (16-bit digits), subtraction of t*M, sign-magnitude output.
+// Carry propagation of sum_l cols[l] 2^(16 l) - t M, one warp per coefficient.
+// t = round(sum of the partial sums of y_k / p_k).  Lane i owns `chunk` 16-bit digits
+// (chunk even, >= 4, so a lane's value spans >= 64 bits): (1) local propagation with
+// carry-in 0 gives the lane's digits V_i and carry-out c_i; (2) the carry-ins follow
+// sequentially, C_{i+1} = c_i + floor((V_i + C_i) / 2^W), where |C_i| < 2^45 << 2^W makes
+// the floor -1, 0 or +1 -- decided from V_i's low 64 bits and whether its higher digits
+// are all ones / all zeros; (3) each lane adds its C_i; (4) a negative total is negated
+// in two's complement (sign-magnitude output).
 __global__ void __launch_bounds__(128) k_crt_carry(CrtParams C) {
-  const int jl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (jl >= C.J) return;
-  const uint64_t* col = C.cols + static_cast<size_t>(jl) * C.L16;
-  const int64_t t = C.tq[jl];
-  uint32_t* out = C.out + static_cast<size_t>(jl) * (C.out_limbs + 1);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= C.J * C.B) return;
+  const int b = gw / C.J, jl = gw - b * C.J;
+  const int L16 = C.L16, OL = C.out_limbs;
+  // rounding estimate t
+  const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+  double s = 0;
+  for (int q = lane; q < nch; q += 32) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const double tr = rint(s);
+  if (lane == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  const int64_t t = static_cast<int64_t>(tr);
+
+  int chunk = 2 * ((L16 + 63) / 64);
+  if (chunk < 4) chunk = 4;
+  const int d0 = lane * chunk;
+  const uint64_t* col = C.cols + (static_cast<size_t>(b) * C.J + jl) * L16;
+  uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1);
+  // (1) local propagation
   int64_t carry = 0;
-  uint32_t any = 0;
-  for (int w = 0; w < C.out_limbs; ++w) {
+  uint64_t low = 0;
+  bool ones = true, zeros = true;
+  for (int k = 0; k < chunk; k += 2) {
     uint32_t limb = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int l = 2 * w + h;
+      const int l = d0 + k + h;
       int64_t v = carry;
-      if (l < C.L16) v += static_cast<int64_t>(col[l]) - t * static_cast<int64_t>(C.M16[l]);
+      if (l < L16) v += static_cast<int64_t>(col[l]) - t * static_cast<int64_t>(C.M16[l]);
       limb |= static_cast<uint32_t>(v & 0xffff) << (16 * h);
       carry = v >> 16;
     }
-    out[1 + w] = limb;
-    any |= limb;
-  }
-  int sign = any ? 1 : 0;
-  if (carry < 0) {
-    uint32_t c = 1;
-    for (int w = 0; w < C.out_limbs; ++w) {
-      const uint64_t s = static_cast<uint64_t>(~out[1 + w]) + c;
-      out[1 + w] = static_cast<uint32_t>(s);
-      c = static_cast<uint32_t>(s >> 32);
+    const int w = (d0 + k) >> 1;
+    if (w < OL) out[1 + w] = limb;
+    if (k < 4) {
+      low |= static_cast<uint64_t>(limb) << (16 * k);
+    } else {
+      ones &= (limb == 0xffffffffu);
+      zeros &= (limb == 0u);
     }
-    sign = -1;
   }
-  out[0] = static_cast<uint32_t>(sign);
+  // (2) sequential carry-in scan over the lanes
+  int64_t cin = 0, my_cin = 0;
+  const uint32_t flags = (ones ? 1u : 0u) | (zeros ? 2u : 0u);
+  for (int i = 0; i < 32; ++i) {
+    const int64_t ci = __shfl_sync(0xffffffffu, carry, i);
+    const uint64_t lo = __shfl_sync(0xffffffffu, low, i);
+    const uint32_t fl = __shfl_sync(0xffffffffu, flags, i);
+    if (lane == i) my_cin = cin;
+    int64_t adj = 0;
+    if (cin > 0) {
+      adj = ((fl & 1u) && lo + static_cast<uint64_t>(cin) < lo) ? 1 : 0;
+    } else if (cin < 0) {
+      adj = ((fl & 2u) && lo < static_cast<uint64_t>(-cin)) ? -1 : 0;
+    }
+    cin = ci + adj;
+  }
+  const int64_t total_carry = cin;
+  // (3) add the carry-in to this lane's limbs
+  int64_t c = my_cin;
+  for (int k = 0; k < chunk && c != 0; k += 2) {
+    const int w = (d0 + k) >> 1;
+    if (w >= OL) break;
+    const int64_t v = static_cast<int64_t>(out[1 + w]) + c;
+    out[1 + w] = static_cast<uint32_t>(v);
+    c = v >> 32;
+  }
+  __syncwarp();
+  // (4) sign and magnitude
+  int lowest = OL;
+  for (int k = 0; k < chunk; k += 2) {
+    const int w = (d0 + k) >> 1;
+    if (w < OL && out[1 + w] != 0u) {
+      lowest = w;
+      break;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lowest = min(lowest, __shfl_xor_sync(0xffffffffu, lowest, off));
+  if (total_carry < 0) {
+    for (int k = 0; k < chunk; k += 2) {
+      const int w = (d0 + k) >> 1;
+      if (w >= OL || w < lowest) continue;
+      out[1 + w] = (w == lowest) ? (0u - out[1 + w]) : ~out[1 + w];
+    }
+  }
+  if (lane == 0) out[0] = static_cast<uint32_t>(lowest >= OL ? 0 : (total_carry < 0 ? -1 : 1));
 }
 
 }  // namespace
 
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0, int nk,
-                  uint32_t* d_tab, cudaStream_t st) {
-  if (S == 0 || nk == 0) return 0;
-  dim3 grid((S + 127) / 128, nk);
-  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, k0, d_tab);
+                  uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
+  if (S == 0 || nk == 0 || B == 0) return 0;
+  dim3 grid((S + 127) / 128, nk, B);
+  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, k0, d_tab, tab_bstride);
   return 1;
 }
 
-int launch_modres(const ResParams& rp, int nk, bool fast, cudaStream_t st) {
-  if (nk == 0) return 0;
-  if (fast && rp.m == rp.n - 1 && dispatch_fast_any(rp.n, rp, nk, st)) {
-    k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);
-    return 2;
+int launch_modres(const ResParams& rp, bool fast, cudaStream_t st) {
+  if (rp.nk == 0 || rp.B == 0) return 0;
+  if (fast && rp.vals && rp.m == rp.n - 1 && rp.n >= 2 && rp.n <= kFastMaxDeg) {
+    const int launches = launch_eval(rp, st);  // K2
+    if (dispatch_fast_any(rp.n, rp, st)) {     // K3
+      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);  // degenerate units, exact
+      return launches + 2;
+    }
   }
-  const uint32_t total = static_cast<uint32_t>(nk) * static_cast<uint32_t>(rp.N);
+  const uint32_t total = static_cast<uint32_t>(rp.B) * rp.nk * static_cast<uint32_t>(rp.N);
   const int blocks = static_cast<int>(std::min<uint32_t>((total + 127) / 128, 148u * 16u));
   k_modres_general<<<blocks, 128, 0, st>>>(rp, 0, total);
   return 1;
 }
 
-int launch_interp(uint32_t* rows, int pitch, int nk, const PrimeConst* d_pc, int k0, int N, int r, int a, int D,
-                  int negate, uint32_t* counters, cudaStream_t st) {
-  if (nk == 0) return 0;
+int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc, int k0,
+                  int N, int r, int a, int D, int negate, uint32_t* counters, cudaStream_t st) {
+  if (nk == 0 || B == 0) return 0;
   const size_t smem = static_cast<size_t>(2) * N * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_interp<<<nk, 256, smem, st>>>(rows, pitch, d_pc, k0, N, r, a, D, negate, counters);
+  k_interp<<<dim3(nk, B), 256, smem, st>>>(rows, rows_bstride, pitch, d_pc, k0, N, r, a, D, negate, counters);
   return 1;
 }
 
 int launch_crt(const CrtParams& cp, cudaStream_t st) {
-  if (cp.J == 0) return 0;
-  k_crt_prep<<<(cp.J + 31) / 32, dim3(32, 8), 0, st>>>(cp);
-  dim3 g2((cp.L16 + 63) / 64, (cp.J + 63) / 64);
-  k_crt_gemm<<<g2, 256, 0, st>>>(cp);
-  k_crt_carry<<<(cp.J + 127) / 128, 128, 0, st>>>(cp);
+  if (cp.J == 0 || cp.B == 0) return 0;
+  const int nch = (cp.P + kCrtChunk - 1) / kCrtChunk;
+  k_crt_prep<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
+  k_crt_gemm<<<dim3((cp.L16 + 63) / 64, (cp.J + 31) / 32, cp.B), 128, 0, st>>>(cp);
+  k_crt_carry<<<(cp.J * cp.B + 3) / 4, 128, 0, st>>>(cp);
   return 3;
 }
 

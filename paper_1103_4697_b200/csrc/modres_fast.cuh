@@ -19,24 +19,19 @@ namespace {
 // ---------------------------------------------------------------------------
 template <int NN>
 __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
-  extern __shared__ uint32_t sm[];
-  const int kl = blockIdx.y;
+  const int kl = blockIdx.y, b = blockIdx.z;
   const int k = P.k0 + kl;
-  const PrimeConst pcv = P.pc[k];
-  const Mod M = load_mod(pcv);
-  uint32_t* s_tab = sm;
-  int32_t* s_dir = reinterpret_cast<int32_t*>(sm + P.S);
-  constexpr int kDir = 2 * (NN + 1) + 2 * NN;
-  for (int s = threadIdx.x; s < P.S; s += blockDim.x) s_tab[s] = P.tab[static_cast<size_t>(k) * P.S + s];
-  for (int s = threadIdx.x; s < kDir; s += blockDim.x) s_dir[s] = P.dir[s];
-  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.N) return;
+  const PrimeConst pcv = P.pc[k];
+  const Mod M = load_mod(pcv);
 
-  const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
+  // Point values p_j(omega^i) (and q_j) from the K2 evaluation kernel: row j of this
+  // prime's block, column i -- consecutive threads read consecutive words.
+  const uint32_t* vals = P.vals + (static_cast<size_t>(b) * P.nk + kl) * P.nrows * P.N + i;
   uint32_t A[NN + 1], B[NN];
 #pragma unroll
-  for (int j = 0; j <= NN; ++j) A[j] = horner(s_tab, s_dir[j], s_dir[NN + 1 + j], x, M);
+  for (int j = 0; j <= NN; ++j) A[j] = vals[static_cast<size_t>(j) * P.N];
   if (P.deriv) {
     uint32_t c = M.one;
 #pragma unroll
@@ -46,7 +41,7 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < NN; ++j) B[j] = horner(s_tab, s_dir[2 * (NN + 1) + j], s_dir[2 * (NN + 1) + NN + j], x, M);
+    for (int j = 0; j < NN; ++j) B[j] = vals[static_cast<size_t>(NN + 1 + j) * P.N];
   }
 
   uint32_t flag = (A[NN] == 0u) | (B[NN - 1] == 0u);
@@ -73,35 +68,33 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
   }
   const uint32_t Ei = minv(E, M);
   const uint32_t res = mmul(B[0], mmul(Ei, Ei, M), M);
-  uint32_t* out = P.rows + static_cast<size_t>(kl) * P.pitch;
+  uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
   if (flag) {
     out[i] = kSentinel;
-    push_flag(P, static_cast<uint32_t>(kl) * P.N + i);
+    push_flag(P, (static_cast<uint32_t>(b) * P.nk + kl) * P.N + i);
   } else {
     out[i] = res;
   }
 }
 
 template <int NN>
-void launch_fast_n(const ResParams& rp, int nk, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(rp.S) * 4 + static_cast<size_t>(2 * (NN + 1) + 2 * NN) * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_modres_fast<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  dim3 grid((rp.N + 127) / 128, nk);
-  k_modres_fast<NN><<<grid, 128, smem, st>>>(rp);
+void launch_fast_n(const ResParams& rp, cudaStream_t st) {
+  dim3 grid((rp.N + 127) / 128, rp.nk, rp.B);
+  k_modres_fast<NN><<<grid, 128, 0, st>>>(rp);
 }
 
 template <int G, int NN>
-bool dispatch_group(int n, const ResParams& rp, int nk, cudaStream_t st) {
+bool dispatch_group(int n, const ResParams& rp, cudaStream_t st) {
   if constexpr (NN > kFastMaxDeg) {
     return false;
   } else {
     if constexpr (fast_group_of(NN) == G) {
       if (n == NN) {
-        launch_fast_n<NN>(rp, nk, st);
+        launch_fast_n<NN>(rp, st);
         return true;
       }
     }
-    return dispatch_group<G, NN + 1>(n, rp, nk, st);
+    return dispatch_group<G, NN + 1>(n, rp, st);
   }
 }
 
@@ -110,7 +103,7 @@ bool dispatch_group(int n, const ResParams& rp, int nk, cudaStream_t st) {
 
 #define CTG_DEFINE_FAST_GROUP(G)                                                                 \
   namespace ctg {                                                                                \
-  bool dispatch_fast_group_##G(int n, const ResParams& rp, int nk, cudaStream_t st) {            \
-    return dispatch_group<G, 2>(n, rp, nk, st);                                                  \
+  bool dispatch_fast_group_##G(int n, const ResParams& rp, cudaStream_t st) {                    \
+    return dispatch_group<G, 2>(n, rp, st);                                                      \
   }                                                                                              \
   }

@@ -30,10 +30,10 @@ constexpr int fast_group_of(int n) {
   const int idx = kFastMaxDeg - n, round = idx / kFastGroups, pos = idx % kFastGroups;
   return (round % 2 == 0) ? pos : kFastGroups - 1 - pos;
 }
-bool dispatch_fast_group(int group, int n, const ResParams& rp, int nk, cudaStream_t st);
-inline bool dispatch_fast_any(int n, const ResParams& rp, int nk, cudaStream_t st) {
+bool dispatch_fast_group(int group, int n, const ResParams& rp, cudaStream_t st);
+inline bool dispatch_fast_any(int n, const ResParams& rp, cudaStream_t st) {
   if (n < 2 || n > kFastMaxDeg) return false;
-  return dispatch_fast_group(fast_group_of(n), n, rp, nk, st);
+  return dispatch_fast_group(fast_group_of(n), n, rp, st);
 }
 
 }  // namespace ctg

@@ -62,3 +62,24 @@ def test_big_configs_digest(row):
     assert len(R) - 1 == row["deg"]
     assert format(R[-1], "x") == row["lc"] and format(R[0], "x") == row["c0"]
     assert _digest(R) == row["sha256"]
+
+
+def test_batch_api_mixed_shapes():
+    """ctg_resultant_batch groups same-shape problems into one batched plan; mixed shapes,
+    zero operands and Var::X must still match the reference one by one."""
+    rows = [r for r in load("resultant_random.jsonl") if r["op"] == "resultant_y" and "error" not in r]
+    rows += [r for r in load("worked.jsonl") if r["op"] == "resultant_y" and "error" not in r]
+    pairs = [(dec_bipoly(r["args"][0]), dec_bipoly(r["args"][1])) for r in rows]
+    got = P.resultant_batch(pairs)
+    assert got == [dec_upoly(r["result"]) for r in rows]
+
+
+def test_batch_plan_same_shape_curves():
+    small = [r for r in load("configs_small.jsonl") if r["curve"][:3] == ["dense", 10, 10]]
+    assert len(small) == 5
+    pairs = []
+    for r in small:
+        f = curves.make(*r["curve"])
+        pairs.append((f, curves.derive_y(f)))
+    got = P.resultant_batch(pairs)
+    assert got == [dec_upoly(r["result"]) for r in small]
