@@ -286,7 +286,7 @@ def main_ours(args):
             st = P.last_call_stats()
             h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
         e2e_ms = 1e3 * sum(walls) / len(walls)
-        e2e_phases = {k: st[k] for k in ("setup_ms", "device_ms", "decode_ms", "total_ms")}
+        e2e_phases = {k: st[k] for k in ("setup_ms", "h2d_ms", "device_ms", "d2h_ms", "decode_ms", "total_ms")}
     else:
         e2e_ms, h2d, d2h = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh,
                                        rank)

@@ -105,6 +105,7 @@ ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_
 ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ctg_opts* opts);
 
 void ctg_upoly_free(ctg_upoly_buf* buf);
+void ctg_upoly_free_batch(ctg_upoly_buf* bufs, int32_t n); /* = ctg_upoly_free on each */
 void ctg_sqf_free(ctg_sqf_buf* buf);
 const char* ctg_last_error(void); /* thread-local message of the last failing call */
 int32_t ctg_abi_version(void);

@@ -102,7 +102,7 @@ EXPORTS = (
     "ctg_plan_create", "ctg_plan_get_info", "ctg_plan_upload", "ctg_plan_residues", "ctg_plan_crt",
     "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy", "ctg_plan_stage",
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
-    "ctg_plan_stage_batch", "ctg_plan_crt_batch",
+    "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch",
 )
 
 _lib = None
@@ -128,6 +128,7 @@ def lib():
                                          C.POINTER(_Opts)]
         L.ctg_square_free_part.argtypes = [C.POINTER(_Upoly), C.POINTER(_UpolyBuf), C.POINTER(_Opts)]
         L.ctg_upoly_free.argtypes = [C.POINTER(_UpolyBuf)]
+        L.ctg_upoly_free_batch.argtypes = [C.POINTER(_UpolyBuf), C.c_int32]
         L.ctg_sqf_free.argtypes = [C.POINTER(_SqfBuf)]
         L.ctg_last_error.restype = C.c_char_p
         L.ctg_last_call_stats.argtypes = [C.POINTER(CallStats)]
@@ -302,10 +303,8 @@ def resultant_batch_raw(hb: HostBatch, var: str = "y", device=None) -> int:
     o = _opts(device)
     _check(lib().ctg_resultant_batch(hb.n, hb.p, hb.q, 1 if var in ("x", "X") else 0, outs, C.byref(o)),
            "resultant_batch")
-    total = 0
-    for i in range(hb.n):
-        total += outs[i].n_coeffs
-        lib().ctg_upoly_free(C.byref(outs[i]))
+    total = sum(outs[i].n_coeffs for i in range(hb.n))
+    lib().ctg_upoly_free_batch(outs, hb.n)
     return total
 
 

@@ -1,9 +1,13 @@
 #include "api_common.hpp"
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
+#include <thread>
 
 namespace ctg {
 
@@ -81,6 +85,29 @@ uint32_t* Ctx::pinned_u32(size_t words) {
   return static_cast<uint32_t*>(pinned);
 }
 
+cudaStream_t Ctx::copy_stream() {
+  if (!copy) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CTG_CUDA_CHECK(cudaSetDevice(device));
+    CTG_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    cudaSetDevice(prev);
+  }
+  return copy;
+}
+
+uint8_t* Ctx::pinned_input(size_t bytes) {
+  bytes = std::max<size_t>(16, bytes);
+  if (pinned_in_bytes < bytes) {
+    CTG_CUDA_CHECK(cudaStreamSynchronize(stream));
+    cudaFreeHost(pinned_in);
+    pinned_in = nullptr;
+    CTG_CUDA_CHECK(cudaMallocHost(&pinned_in, bytes));
+    pinned_in_bytes = bytes;
+  }
+  return static_cast<uint8_t*>(pinned_in);
+}
+
 Ctx& context(int device) {
   static std::mutex mu;
   static std::map<int, std::unique_ptr<Ctx>> ctxs;
@@ -122,9 +149,148 @@ double CallTimer::lap() {
 void CallTimer::mark_setup() { g_stats.setup_ms = lap(); }
 void CallTimer::mark_h2d() { g_stats.h2d_ms = lap(); }
 void CallTimer::mark_device() { g_stats.device_ms = lap(); }
+void CallTimer::finish_total() {
+  g_stats.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
 void CallTimer::finish() {
   g_stats.decode_ms = lap();
   g_stats.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+namespace {
+// Minimal persistent pool: workers pull indices from a shared counter.
+class Pool {
+ public:
+  Pool() {
+    unsigned hc = std::thread::hardware_concurrency();
+    nthreads_ = static_cast<int>(std::min(16u, std::max(1u, hc)));
+    for (int t = 1; t < nthreads_; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void run(int n, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel_for at a time
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(mu_);
+    done_cv_.wait(l, [&] { return done_ == n_; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    while (true) {
+      int i;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> l(mu_);
+        if (!fn_ || next_ >= n_) return;
+        i = next_++;
+        f = fn_;
+      }
+      (*f)(i);
+      {
+        std::lock_guard<std::mutex> l(mu_);
+        if (++done_ == n_) done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return stop_ || (gen_ != seen && fn_ != nullptr); });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  int nthreads_ = 1;
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+}  // namespace
+
+void parallel_for(int n, const std::function<void(int)>& fn) {
+  if (n <= 1) {
+    if (n == 1) fn(0);
+    return;
+  }
+  static Pool pool;
+  // Exceptions are captured per index and the first one rethrown on the caller's thread.
+  std::vector<std::exception_ptr> errs(n);
+  pool.run(n, [&](int i) {
+    try {
+      fn(i);
+    } catch (...) {
+      errs[i] = std::current_exception();
+    }
+  });
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+namespace {
+constexpr uint64_t kSingleMagic = 0x31666675625f6774ull;  // "tg_buff1"
+constexpr uint64_t kMemberMagic = 0x32666675625f6774ull;  // "tg_buff2"
+constexpr uint64_t kArenaMagic = 0x33666675625f6774ull;   // "tg_buff3"
+struct BufHdr {
+  uint64_t magic;
+  uint64_t aux;  // member: byte offset back to the arena header; arena: live members
+};
+size_t pad16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+void place_block(uint8_t* block, uint64_t magic, uint64_t aux, ctg_upoly_buf* out, size_t n, size_t total) {
+  auto* h = reinterpret_cast<BufHdr*>(block);
+  h->magic = magic;
+  h->aux = aux;
+  out->n_coeffs = static_cast<int32_t>(n);
+  out->limb_off = reinterpret_cast<uint32_t*>(block + sizeof(BufHdr));
+  out->limbs = out->limb_off + (n + 1);
+  out->sign = reinterpret_cast<int8_t*>(out->limbs + total);
+}
+}  // namespace
+
+size_t upoly_block_bytes(size_t n, size_t total) { return pad16(sizeof(BufHdr) + 4 * (n + 1) + 4 * total + n); }
+
+void upoly_alloc(ctg_upoly_buf* out, size_t n, size_t total) {
+  auto* block = static_cast<uint8_t*>(std::malloc(upoly_block_bytes(n, total)));
+  if (!block) throw std::bad_alloc();
+  place_block(block, kSingleMagic, 0, out, n, total);
+}
+
+void UpolyArena::create(size_t bytes, int64_t members) {
+  base = static_cast<uint8_t*>(std::malloc(sizeof(BufHdr) + bytes));
+  if (!base) throw std::bad_alloc();
+  auto* h = reinterpret_cast<BufHdr*>(base);
+  h->magic = kArenaMagic;
+  h->aux = static_cast<uint64_t>(members);
+}
+
+void UpolyArena::place(ctg_upoly_buf* out, size_t off, size_t n, size_t total) const {
+  uint8_t* block = base + sizeof(BufHdr) + off;
+  place_block(block, kMemberMagic, static_cast<uint64_t>(block - base), out, n, total);
 }
 
 void fill_upoly(const std::vector<UCoeff>& coeffs, ctg_upoly_buf* out) {
@@ -132,11 +298,7 @@ void fill_upoly(const std::vector<UCoeff>& coeffs, ctg_upoly_buf* out) {
   while (n > 0 && coeffs[n - 1].sign == 0) --n;
   size_t total = 0;
   for (size_t i = 0; i < n; ++i) total += coeffs[i].limbs.size();
-  out->n_coeffs = static_cast<int32_t>(n);
-  out->sign = static_cast<int8_t*>(std::malloc(std::max<size_t>(1, n)));
-  out->limb_off = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (n + 1)));
-  out->limbs = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<size_t>(1, total)));
-  if (!out->sign || !out->limb_off || !out->limbs) throw std::bad_alloc();
+  upoly_alloc(out, n, total);
   uint32_t off = 0;
   for (size_t i = 0; i < n; ++i) {
     out->sign[i] = coeffs[i].sign;
@@ -152,11 +314,30 @@ void fill_upoly(const std::vector<UCoeff>& coeffs, ctg_upoly_buf* out) {
 extern "C" {
 
 void ctg_upoly_free(ctg_upoly_buf* buf) {
+  using namespace ctg;
   if (!buf) return;
-  std::free(buf->sign);
-  std::free(buf->limb_off);
-  std::free(buf->limbs);
+  if (buf->limb_off) {
+    uint8_t* block = reinterpret_cast<uint8_t*>(buf->limb_off) - sizeof(BufHdr);
+    auto* h = reinterpret_cast<BufHdr*>(block);
+    if (h->magic == kSingleMagic) {
+      h->magic = 0;
+      std::free(block);
+    } else if (h->magic == kMemberMagic) {
+      h->magic = 0;
+      uint8_t* base = block - h->aux;
+      auto* ah = reinterpret_cast<BufHdr*>(base);
+      if (__atomic_sub_fetch(&ah->aux, 1, __ATOMIC_ACQ_REL) == 0) {
+        ah->magic = 0;
+        std::free(base);
+      }
+    }
+  }
   std::memset(buf, 0, sizeof(*buf));
+}
+
+void ctg_upoly_free_batch(ctg_upoly_buf* bufs, int32_t n) {
+  if (!bufs) return;
+  for (int32_t i = 0; i < n; ++i) ctg_upoly_free(&bufs[i]);
 }
 
 void ctg_sqf_free(ctg_sqf_buf* buf) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -71,8 +72,13 @@ struct Ctx {
   std::vector<size_t> scratch_bytes;
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  void* pinned_in = nullptr;
+  size_t pinned_in_bytes = 0;
+  cudaStream_t copy = nullptr;            // D2H stream (overlaps the next chunk's kernels)
+  cudaStream_t copy_stream();
   uint32_t* scratch_u32(int slot, size_t words);
-  uint32_t* pinned_u32(size_t words);
+  uint32_t* pinned_u32(size_t words);     // D2H staging
+  uint8_t* pinned_input(size_t bytes);    // H2D staging
 };
 Ctx& context(int device);
 cudaStream_t resolve_stream(int device, void* stream);
@@ -86,7 +92,12 @@ struct CallTimer {
   void mark_h2d();
   void mark_device();
   void finish();
+  void finish_total();  // total only (phases were accumulated by the callee)
 };
+
+// Runs fn(i) for i in [0, n) on a persistent host thread pool (inline when n <= 1).
+// Used for per-curve marshaling of batches (parsing, result decoding).
+void parallel_for(int n, const std::function<void(int)>& fn);
 
 // Decoded coefficient (sign-magnitude), used to fill library-owned result buffers.
 struct UCoeff {
@@ -95,5 +106,19 @@ struct UCoeff {
 };
 // Trims trailing zero coefficients and allocates/fills a ctg_upoly_buf.
 void fill_upoly(const std::vector<UCoeff>& coeffs, ctg_upoly_buf* out);
+
+// Result-buffer storage.  Every ctg_upoly_buf owns one block: a 16-byte header right
+// before limb_off, then limb_off[n+1], limbs[total], sign[n].  Blocks are either single
+// mallocs or members of a refcounted arena shared by one batch call (one allocation and
+// one release for the whole batch); ctg_upoly_free handles both.
+size_t upoly_block_bytes(size_t n_coeffs, size_t total_limbs);
+void upoly_alloc(ctg_upoly_buf* out, size_t n_coeffs, size_t total_limbs);  // single block
+struct UpolyArena {
+  uint8_t* base = nullptr;
+  // Creates an arena for `members` blocks totalling `bytes` (sum of upoly_block_bytes).
+  void create(size_t bytes, int64_t members);
+  // Places a block at byte offset `off` (from the first block) into out.
+  void place(ctg_upoly_buf* out, size_t off, size_t n_coeffs, size_t total_limbs) const;
+};
 
 }  // namespace ctg

@@ -258,7 +258,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   pl->L = L;
   pl->h_limbs.assign(static_cast<size_t>(pl->B) * L * S, 0u);
   pl->h_sign.assign(static_cast<size_t>(pl->B) * S, 0);
-  for (int b = 0; b < pl->B; ++b) {
+  parallel_for(pl->B, [&](int b) {
     uint32_t* lb = pl->h_limbs.data() + static_cast<size_t>(b) * L * S;
     int8_t* sb = pl->h_sign.data() + static_cast<size_t>(b) * S;
     auto put = [&](int s, const SBig& c) {
@@ -268,7 +268,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
     for (const auto& [e, c] : probs[idx[b]].p) put(offp[e.first] + e.second, c);
     if (!pl->deriv)
       for (const auto& [e, c] : probs[idx[b]].q) put(offq[e.first] + e.second, c);
-  }
+  });
   pl->dir.clear();
   for (auto* v : {&offp, &lenp, &offq, &lenq}) pl->dir.insert(pl->dir.end(), v->begin(), v->end());
   pl->nrows = pl->deriv ? n + 1 : n + m + 2;
@@ -301,15 +301,25 @@ static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
 }
 
-void plan_upload(ctg_plan* pl, cudaStream_t st) {
+// H2D of the plan's inputs; with `staging` (pinned, >= plan_h2d_bytes) the three copies go
+// through page-locked memory and stay asynchronous.
+void plan_upload(ctg_plan* pl, cudaStream_t st, uint8_t* staging = nullptr) {
   if (pl->trivial) return;
   plan_alloc(pl, st);
   pl->last_stream = st;
-  CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_limbs, pl->h_limbs.data(), sizeof(uint32_t) * pl->h_limbs.size(),
-                                 cudaMemcpyHostToDevice, st));
-  CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_sign, pl->h_sign.data(), pl->h_sign.size(), cudaMemcpyHostToDevice, st));
-  CTG_CUDA_CHECK(
-      cudaMemcpyAsync(pl->d_dir, pl->dir.data(), sizeof(int32_t) * pl->dir.size(), cudaMemcpyHostToDevice, st));
+  const size_t nl = sizeof(uint32_t) * pl->h_limbs.size(), ns = pl->h_sign.size(), nd = 4 * pl->dir.size();
+  const void *src_l = pl->h_limbs.data(), *src_s = pl->h_sign.data(), *src_d = pl->dir.data();
+  if (staging) {
+    std::memcpy(staging, src_l, nl);
+    std::memcpy(staging + nl, src_d, nd);
+    std::memcpy(staging + nl + nd, src_s, ns);
+    src_l = staging;
+    src_d = staging + nl;
+    src_s = staging + nl + nd;
+  }
+  CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_limbs, src_l, nl, cudaMemcpyHostToDevice, st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_dir, src_d, nd, cudaMemcpyHostToDevice, st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(pl->d_sign, src_s, ns, cudaMemcpyHostToDevice, st));
   pl->uploaded = true;
 }
 
@@ -426,49 +436,142 @@ uint32_t plan_error_bits(ctg_plan* pl, cudaStream_t st) {
   return c[1];
 }
 
-// h: one curve's CRT output (n_coeffs records of out_limbs + 1 words).
-void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
-  std::vector<UCoeff> coeffs;
-  if (!pl->trivial) {
-    const int W = pl->out_words();
-    coeffs.resize(pl->D);
-    for (uint32_t j = 0; j < pl->D; ++j) {
-      const uint32_t* rec = h + static_cast<size_t>(j) * W;
-      UCoeff& c = coeffs[j];
-      c.sign = static_cast<int8_t>(static_cast<int32_t>(rec[0]));
-      int n = W - 1;
-      while (n > 0 && rec[n] == 0) --n;
-      c.limbs.assign(rec + 1, rec + 1 + n);
-      if (c.limbs.empty()) c.sign = 0;
-    }
+// h: one curve's CRT output (n_coeffs records of out_limbs + 1 words) -> library-owned
+// CSR buffer, trimmed (two passes over the records, no per-coefficient allocation).
+struct DecodeSize {
+  std::vector<int> nl;  // limbs per coefficient
+  size_t nc = 0, total = 0;
+};
+
+DecodeSize decode_size(const ctg_plan* pl, const uint32_t* h) {
+  DecodeSize z;
+  const int W = pl->out_words();
+  z.nl.resize(pl->D);
+  int deg = -1;
+  for (uint32_t j = 0; j < pl->D; ++j) {
+    const uint32_t* rec = h + static_cast<size_t>(j) * W;
+    int n = W - 1;
+    while (n > 0 && rec[n] == 0) --n;
+    z.nl[j] = (rec[0] != 0u) ? n : 0;
+    if (z.nl[j]) deg = static_cast<int>(j);
   }
-  fill_upoly(coeffs, out);
+  z.nc = static_cast<size_t>(deg + 1);
+  for (size_t j = 0; j < z.nc; ++j) z.total += static_cast<size_t>(z.nl[j]);
+  return z;
 }
 
-// Full on-device pipeline for one plan on the context stream: H2D, K1-K5, one D2H;
-// results decoded into out[0 .. B).
-void plan_run_all(ctg_plan* pl, Ctx& ctx, ctg_upoly_buf* out) {
-  cudaStream_t s = ctx.stream;
+void decode_fill(const ctg_plan* pl, const uint32_t* h, const DecodeSize& z, ctg_upoly_buf* out) {
+  const int W = pl->out_words();
+  uint32_t off = 0;
+  for (size_t j = 0; j < z.nc; ++j) {
+    const uint32_t* rec = h + j * W;
+    out->sign[j] = z.nl[j] ? static_cast<int8_t>(static_cast<int32_t>(rec[0])) : 0;
+    out->limb_off[j] = off;
+    std::memcpy(out->limbs + off, rec + 1, 4 * static_cast<size_t>(z.nl[j]));
+    off += static_cast<uint32_t>(z.nl[j]);
+  }
+  out->limb_off[z.nc] = off;
+}
+
+void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
+  if (pl->trivial) {
+    fill_upoly({}, out);
+    return;
+  }
+  DecodeSize z = decode_size(pl, h);
+  upoly_alloc(out, z.nc, z.total);
+  decode_fill(pl, h, z, out);
+}
+
+// Pipelined execution of a list of chunk plans on one device context.  Compute runs on
+// ctx.stream; each chunk's D2H runs on ctx.copy after an event, so chunk c's copy and host
+// decode overlap chunk c+1's kernels.  Host staging (pinned, in and out) is carved from
+// one buffer per call; device scratch comes from the stream-ordered pool.
+struct Chunk {
+  std::unique_ptr<ctg_plan> pl;
+  std::vector<int> idx;  // positions in the caller's output array
+  size_t in_off = 0, out_off = 0, out_words = 0, per_curve = 0;
+  uint32_t* d_rows = nullptr;
+  uint32_t* d_out = nullptr;
+  cudaEvent_t computed = nullptr, copied = nullptr;
+};
+
+void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
+  using clk = std::chrono::steady_clock;
+  auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
   auto& st = stats_tls();
-  plan_upload(pl, s);
-  st.h2d_bytes += plan_h2d_bytes(pl);
-  const size_t rows_words = static_cast<size_t>(pl->B) * pl->P * pl->N;
-  const size_t per_curve = static_cast<size_t>(pl->D) * pl->out_words();
-  const size_t out_words = per_curve * pl->B;
-  uint32_t* d_rows = ctx.scratch_u32(0, rows_words);
-  uint32_t* d_out = ctx.scratch_u32(1, out_words);
-  plan_residues(pl, 0, pl->P, d_rows, 0, s);
-  plan_crt(pl, d_rows, 0, 0, 0, 0, static_cast<int>(pl->D), d_out, 0, s);
-  uint32_t* h_out = ctx.pinned_u32(out_words + 4);
-  CTG_CUDA_CHECK(cudaMemcpyAsync(h_out, d_out, sizeof(uint32_t) * out_words, cudaMemcpyDeviceToHost, s));
-  CTG_CUDA_CHECK(cudaMemcpyAsync(h_out + out_words, pl->d_counters, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, s));
-  CTG_CUDA_CHECK(cudaStreamSynchronize(s));
-  st.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (out_words + 2));
-  st.kernel_launches += pl->launches;
-  st.flagged_units += static_cast<int32_t>(h_out[out_words]);
-  const uint32_t bits = h_out[out_words + 1];
-  if (bits) throw ApiError(CTG_INTERNAL, "resultant: device self-check failed (error bits " + std::to_string(bits) + ")");
-  for (int b = 0; b < pl->B; ++b) plan_decode(pl, h_out + per_curve * b, &out[b]);
+  auto t0 = clk::now();
+  size_t in_bytes = 0, out_words = 0;
+  for (auto& c : chunks) {
+    c.in_off = in_bytes;
+    in_bytes += (static_cast<size_t>(plan_h2d_bytes(c.pl.get())) + 255) & ~static_cast<size_t>(255);
+    c.per_curve = static_cast<size_t>(c.pl->D) * c.pl->out_words();
+    c.out_words = c.per_curve * c.pl->B;
+    c.out_off = out_words;
+    out_words += c.out_words + 4;
+  }
+  uint8_t* h_in = ctx.pinned_input(in_bytes);
+  uint32_t* h_out = ctx.pinned_u32(out_words);
+  cudaStream_t s = ctx.stream, cp = ctx.copy_stream();
+  for (auto& c : chunks) {
+    ctg_plan* pl = c.pl.get();
+    plan_upload(pl, s, h_in + c.in_off);
+    st.h2d_bytes += plan_h2d_bytes(pl);
+    CTG_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.d_rows),
+                                   sizeof(uint32_t) * static_cast<size_t>(pl->B) * pl->P * pl->N, s));
+    CTG_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.d_out), sizeof(uint32_t) * c.out_words, s));
+    plan_residues(pl, 0, pl->P, c.d_rows, 0, s);
+    plan_crt(pl, c.d_rows, 0, 0, 0, 0, static_cast<int>(pl->D), c.d_out, 0, s);
+    CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
+    CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.copied, cudaEventDisableTiming));
+    CTG_CUDA_CHECK(cudaEventRecord(c.computed, s));
+    CTG_CUDA_CHECK(cudaStreamWaitEvent(cp, c.computed, 0));
+    uint32_t* ho = h_out + c.out_off;
+    CTG_CUDA_CHECK(cudaMemcpyAsync(ho + c.out_words, pl->d_counters, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
+    CTG_CUDA_CHECK(cudaMemcpyAsync(ho, c.d_out, sizeof(uint32_t) * c.out_words, cudaMemcpyDeviceToHost, cp));
+    CTG_CUDA_CHECK(cudaEventRecord(c.copied, cp));
+    CTG_CUDA_CHECK(cudaFreeAsync(c.d_rows, cp));
+    CTG_CUDA_CHECK(cudaFreeAsync(c.d_out, cp));
+    pl->last_stream = cp;  // the plan's own buffers are released after the copies
+    st.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
+  }
+  st.h2d_ms += ms_since(t0);
+  std::string err;
+  for (auto& c : chunks) {
+    t0 = clk::now();
+    CTG_CUDA_CHECK(cudaEventSynchronize(c.copied));
+    st.device_ms += ms_since(t0);
+    t0 = clk::now();
+    ctg_plan* pl = c.pl.get();
+    const uint32_t* ho = h_out + c.out_off;
+    st.kernel_launches += pl->launches;
+    st.flagged_units += static_cast<int32_t>(ho[c.out_words]);
+    const uint32_t bits = ho[c.out_words + 1];
+    if (bits && err.empty()) err = "resultant: device self-check failed (error bits " + std::to_string(bits) + ")";
+    if (!err.empty()) continue;
+    // Decode the chunk into one refcounted arena (one allocation for its curves).
+    std::vector<DecodeSize> sz(pl->B);
+    parallel_for(pl->B, [&](int b) { sz[b] = decode_size(pl, ho + c.per_curve * b); });
+    std::vector<size_t> off(pl->B + 1, 0);
+    for (int b = 0; b < pl->B; ++b) off[b + 1] = off[b] + upoly_block_bytes(sz[b].nc, sz[b].total);
+    UpolyArena arena;
+    arena.create(off[pl->B], pl->B);
+    parallel_for(pl->B, [&](int b) {
+      ctg_upoly_buf* o = &out[c.idx[b]];
+      arena.place(o, off[b], sz[b].nc, sz[b].total);
+      decode_fill(pl, ho + c.per_curve * b, sz[b], o);
+    });
+    st.decode_ms += ms_since(t0);
+  }
+  for (auto& c : chunks) {
+    cudaEventDestroy(c.computed);
+    cudaEventDestroy(c.copied);
+  }
+  if (!err.empty()) {
+    for (auto& c : chunks)
+      for (int i : c.idx) ctg_upoly_free(&out[i]);
+    throw ApiError(CTG_INTERNAL, err);
+  }
 }
 
 }  // namespace ctg
@@ -620,9 +723,8 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     if (!out || !p || !q || batch < 0) throw ApiError(CTG_INVALID, "resultant_batch: bad arguments");
     CallTimer timer;
     for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
-    std::vector<Problem> probs;
-    probs.reserve(batch);
-    for (int b = 0; b < batch; ++b) probs.push_back(parse_problem(&p[b], &q[b], eliminate_x));
+    std::vector<Problem> probs(batch);
+    parallel_for(batch, [&](int b) { probs[b] = parse_problem(&p[b], &q[b], eliminate_x); });
     // Group the nontrivial problems by shape; trivial ones are zero polynomials.
     std::map<std::tuple<int, int, int, int>, std::vector<int>> groups;
     for (int b = 0; b < batch; ++b) {
@@ -642,19 +744,25 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     Ctx& ctx = context(dev);
     std::lock_guard<std::mutex> lock(ctx.mu);
     auto& st = stats_tls();
-    std::vector<ctg_upoly_buf> tmp;
+    // Chunks of <= kChunk same-shape curves: each is one batched plan (one launch set).
+    constexpr int kChunk = 16;
+    std::vector<Chunk> chunks;
     for (auto& [key, idx] : groups) {
-      std::unique_ptr<ctg_plan> pl(plan_build(probs, idx, dev));
-      st.n_primes = std::max(st.n_primes, pl->P);
-      st.n_points = static_cast<int32_t>(pl->N);
-      st.n_coeffs = static_cast<int32_t>(pl->D);
-      st.out_limbs = std::max(st.out_limbs, pl->out_limbs());
-      tmp.assign(idx.size(), ctg_upoly_buf{});
-      plan_run_all(pl.get(), ctx, tmp.data());
-      for (size_t i = 0; i < idx.size(); ++i) out[idx[i]] = tmp[i];
+      for (size_t c0 = 0; c0 < idx.size(); c0 += kChunk) {
+        Chunk c;
+        c.idx.assign(idx.begin() + c0, idx.begin() + std::min(idx.size(), c0 + kChunk));
+        c.pl.reset(plan_build(probs, c.idx, dev));
+        st.n_primes = std::max(st.n_primes, c.pl->P);
+        st.n_points = static_cast<int32_t>(c.pl->N);
+        st.n_coeffs = static_cast<int32_t>(c.pl->D);
+        st.out_limbs = std::max(st.out_limbs, c.pl->out_limbs());
+        chunks.push_back(std::move(c));
+      }
     }
-    timer.mark_device();
-    timer.finish();
+    run_chunks(chunks, ctx, out);
+    chunks.clear();
+    parallel_for(batch, [&](int b) { probs[b] = Problem(); });  // release the parsed terms in parallel
+    timer.finish_total();
   });
 }
 
