@@ -171,7 +171,7 @@ def main_ours(args):
     import torch
 
     import paper_1103_4697_b200 as P
-    from paper_1103_4697_b200 import curves
+    from paper_1103_4697_b200 import curves, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,10 +202,8 @@ def main_ours(args):
     W = info["out_limbs"] + 1
     units_step = B * Pn * D  # mod-p resultants per step (P * D per curve)
     G = world
-    Pb = (Pn + G - 1) // G   # rows per rank block (uniform for the all-gather)
-    k0, k1 = min(rank * Pb, Pn), min((rank + 1) * Pb, Pn)
-    Jb = (D + G - 1) // G
-    j0, j1 = min(rank * Jb, D), min((rank + 1) * Jb, D)
+    k0, k1, Pb = sharding.prime_block(Pn, G, rank)  # rows per rank block (uniform for the all-gather)
+    j0, j1, Jb = sharding.coeff_block(D, G, rank)
     plan.upload(sh)
 
     send = torch.zeros((B, Pb, N), dtype=torch.int32, device=dev)
@@ -357,14 +355,9 @@ def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb
                        block_stride=B * Pb * N)
         dist.all_gather_into_tensor(gathered, out)
         if rank == 0:
-            import numpy as np
+            from paper_1103_4697_b200 import sharding
 
-            host = gathered.cpu().numpy().view("uint32")
-            blocks = []
-            for r in range(G):
-                Jr = max(0, min((r + 1) * Jb, D) - min(r * Jb, D))
-                blocks.append(host[r, :B * Jr * W].reshape(B, Jr, W))
-            full_host = np.concatenate(blocks, axis=1)
+            full_host = sharding.reassemble(gathered.cpu().numpy().view("uint32"), B, D, W, G)
             for bi in range(B):
                 plan.decode(full_host[bi])
         torch.cuda.synchronize()
