@@ -56,14 +56,37 @@ ZPoly parse_upoly(const ctg_upoly* p) {
 
 int zdeg(const ZPoly& p) { return static_cast<int>(p.size()) - 1; }
 
-// Positive gcd of all coefficients, stopping at 1 (upoly.cpp:59-66).
+// Positive gcd of all coefficients, stopping at 1 (upoly.cpp:59-66).  The coefficients are
+// visited shortest first, so the one full-size gcd is between the two smallest and every
+// later step is a cheap gcd of a big number with an already small content.
 Big zcontent(const ZPoly& p) {
-  Big g;
-  for (const auto& c : p) {
-    if (c.sign == 0) continue;
-    g = g.empty() ? c.mag : big_gcd(g, c.mag);
-    if (big_is_one(g)) break;
-  }
+  std::vector<const SBig*> order;
+  for (const auto& c : p)
+    if (c.sign != 0) order.push_back(&c);
+  std::stable_sort(order.begin(), order.end(),
+                   [](const SBig* a, const SBig* b) { return a->mag.size() < b->mag.size(); });
+  auto chain = [&](size_t i0, size_t i1) {
+    Big g;
+    for (size_t i = i0; i < i1; ++i) {
+      g = g.empty() ? order[i]->mag : big_gcd(g, order[i]->mag);
+      if (big_is_one(g)) break;
+    }
+    return g;
+  };
+  if (order.size() <= 32) return chain(0, order.size());
+  // Parallel tree: the two smallest coefficients first (usually enough), then groups.
+  Big g = chain(0, 2);
+  if (big_is_one(g)) return g;
+  const int groups = 16;
+  std::vector<Big> part(groups);
+  const size_t rest = order.size() - 2, per = (rest + groups - 1) / groups;
+  parallel_for(groups, [&](int t) {
+    const size_t i0 = 2 + t * per, i1 = std::min(order.size(), i0 + per);
+    Big h = g;
+    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = big_gcd(h, order[i]->mag);
+    part[t] = h;
+  });
+  for (const Big& h : part) g = big_gcd(g, h);
   return g;
 }
 
@@ -76,11 +99,21 @@ ZPoly zprimitive_positive(const ZPoly& p, Big* content = nullptr, int* lcsign = 
   if (lcsign) *lcsign = s;
   ZPoly q(p.size());
   const bool unit = big_is_one(c);
-  for (size_t i = 0; i < p.size(); ++i) {
-    if (p[i].sign == 0) continue;
-    q[i].sign = p[i].sign * s;
-    q[i].mag = unit ? p[i].mag : big_divexact(p[i].mag, c);
-  }
+  parallel_for(static_cast<int>(p.size() + 15) / 16, [&](int blk) {
+    const size_t i0 = static_cast<size_t>(blk) * 16, i1 = std::min(p.size(), i0 + 16);
+    for (size_t i = i0; i < i1; ++i) {
+      if (p[i].sign == 0) continue;
+      q[i].sign = p[i].sign * s;
+      if (unit) {
+        q[i].mag = p[i].mag;
+      } else if (c.size() == 1) {
+        uint32_t rem = 0;
+        q[i].mag = big_div_u32(p[i].mag, c[0], &rem);  // exact: c divides every coefficient
+      } else {
+        q[i].mag = big_divexact(p[i].mag, c);
+      }
+    }
+  });
   return q;
 }
 

@@ -1,5 +1,7 @@
 #include "hostmath.hpp"
 
+#include "gmp_host.hpp"
+
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -229,165 +231,52 @@ double log2_sum_upper(const std::vector<double>& xs) {
   return (mx + std::log2(s)) * (1 + 1e-14) + 1e-12;
 }
 
+// Multiplication, gcd and exact division on the host go through GMP (subquadratic; the
+// reference's own dependency) -- they serve contents, primitive parts and certificates.
+namespace {
+struct Mpz {
+  ctg_mpz_struct z;
+  Mpz() { __gmpz_init(&z); }
+  explicit Mpz(const Big& a) {
+    __gmpz_init(&z);
+    if (!a.empty()) __gmpz_import(&z, a.size(), -1, 4, 0, 0, a.data());
+  }
+  ~Mpz() { __gmpz_clear(&z); }
+  Big big() const {
+    Big r((__gmpz_sizeinbase(&z, 2) + 31) / 32 + 1, 0u);
+    size_t cnt = 0;
+    __gmpz_export(r.data(), &cnt, -1, 4, 0, 0, &z);
+    r.resize(cnt);
+    big_trim(r);
+    return r;
+  }
+  bool is_zero() const { return z._mp_size == 0; }
+};
+}  // namespace
+
 Big big_mul(const Big& a, const Big& b) {
   if (a.empty() || b.empty()) return Big();
-  Big r(a.size() + b.size(), 0u);
-  for (size_t i = 0; i < a.size(); ++i) {
-    uint64_t carry = 0;
-    const uint64_t ai = a[i];
-    for (size_t j = 0; j < b.size(); ++j) {
-      uint64_t t = ai * b[j] + r[i + j] + carry;
-      r[i + j] = static_cast<uint32_t>(t);
-      carry = t >> 32;
-    }
-    size_t k = i + b.size();
-    while (carry) {
-      uint64_t t = static_cast<uint64_t>(r[k]) + carry;
-      r[k] = static_cast<uint32_t>(t);
-      carry = t >> 32;
-      ++k;
-    }
-  }
-  big_trim(r);
-  return r;
+  Mpz x(a), y(b), r;
+  __gmpz_mul(&r.z, &x.z, &y.z);
+  return r.big();
 }
 
 double big_log2(const Big& a) { return log2_upper(a.data(), static_cast<int>(a.size())); }
 
-namespace {
-using W64 = std::vector<uint64_t>;
-W64 to_w64(const Big& a) {
-  W64 w((a.size() + 1) / 2, 0);
-  for (size_t i = 0; i < a.size(); ++i) w[i / 2] |= static_cast<uint64_t>(a[i]) << (32 * (i % 2));
-  while (!w.empty() && w.back() == 0) w.pop_back();
-  return w;
-}
-Big from_w64(const W64& w) {
-  Big a(2 * w.size());
-  for (size_t i = 0; i < w.size(); ++i) {
-    a[2 * i] = static_cast<uint32_t>(w[i]);
-    a[2 * i + 1] = static_cast<uint32_t>(w[i] >> 32);
-  }
-  big_trim(a);
-  return a;
-}
-size_t w_tz(const W64& a) {
-  size_t i = 0;
-  while (a[i] == 0) ++i;
-  return 64 * i + static_cast<size_t>(__builtin_ctzll(a[i]));
-}
-void w_shr(W64& a, size_t s) {
-  const size_t ws = s / 64, bs = s % 64;
-  if (ws) a.erase(a.begin(), a.begin() + static_cast<long>(std::min(ws, a.size())));
-  if (bs && !a.empty()) {
-    for (size_t i = 0; i + 1 < a.size(); ++i) a[i] = (a[i] >> bs) | (a[i + 1] << (64 - bs));
-    a.back() >>= bs;
-  }
-  while (!a.empty() && a.back() == 0) a.pop_back();
-}
-int w_cmp(const W64& a, const W64& b) {
-  if (a.size() != b.size()) return a.size() < b.size() ? -1 : 1;
-  for (size_t i = a.size(); i-- > 0;)
-    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
-  return 0;
-}
-void w_sub(W64& a, const W64& b) {  // a -= b, a >= b
-  unsigned char br = 0;
-  for (size_t i = 0; i < a.size(); ++i) {
-    const uint64_t bi = i < b.size() ? b[i] : 0;
-    const uint64_t t = a[i] - bi - br;
-    br = (a[i] < bi || (a[i] == bi && br)) ? 1 : 0;
-    a[i] = t;
-  }
-  while (!a.empty() && a.back() == 0) a.pop_back();
-}
-}  // namespace
-
-Big big_gcd(const Big& x, const Big& y) {
-  W64 a = to_w64(x), b = to_w64(y);
-  if (a.empty()) return from_w64(b);
-  if (b.empty()) return from_w64(a);
-  const size_t za = w_tz(a), zb = w_tz(b), shift = std::min(za, zb);
-  w_shr(a, za);
-  while (true) {
-    w_shr(b, w_tz(b));
-    if (w_cmp(a, b) > 0) std::swap(a, b);
-    w_sub(b, a);
-    if (b.empty()) break;
-  }
-  Big g = from_w64(a);
-  // g << shift
-  if (shift) {
-    const size_t ls = shift / 32, bs = shift % 32;
-    Big r(g.size() + ls + 1, 0u);
-    for (size_t i = 0; i < g.size(); ++i) {
-      r[i + ls] |= g[i] << bs;
-      if (bs) r[i + ls + 1] |= g[i] >> (32 - bs);
-    }
-    big_trim(r);
-    return r;
-  }
-  return g;
+Big big_gcd(const Big& a, const Big& b) {
+  Mpz x(a), y(b), r;
+  __gmpz_gcd(&r.z, &x.z, &y.z);
+  return r.big();
 }
 
 Big big_divexact(const Big& a, const Big& b) {
   if (b.empty()) throw std::runtime_error("big_divexact: zero divisor");
   if (a.empty()) return Big();
-  if (b.size() == 1) {
-    uint32_t rem = 0;
-    Big q = big_div_u32(a, b[0], &rem);
-    if (rem) throw std::runtime_error("big_divexact: inexact division");
-    return q;
-  }
-  // Schoolbook long division (Knuth D) with normalisation.
-  const int s = __builtin_clz(b.back());
-  auto shl = [](const Big& v, int sh, size_t extra) {
-    Big r(v.size() + extra, 0u);
-    for (size_t i = 0; i < v.size(); ++i) {
-      r[i] |= v[i] << sh;
-      if (sh && i + 1 < r.size()) r[i + 1] |= static_cast<uint32_t>(static_cast<uint64_t>(v[i]) >> (32 - sh));
-    }
-    return r;
-  };
-  Big vn = shl(b, s, 0), un = shl(a, s, 1);
-  const size_t n = vn.size(), m = a.size() - n + 1;
-  if (a.size() < n) throw std::runtime_error("big_divexact: inexact division");
-  Big q(m, 0u);
-  for (size_t j = m; j-- > 0;) {
-    const uint64_t num = (static_cast<uint64_t>(un[j + n]) << 32) | un[j + n - 1];
-    uint64_t qhat = num / vn[n - 1], rhat = num % vn[n - 1];
-    while (qhat >= (1ull << 32) || (n >= 2 && qhat * vn[n - 2] > ((rhat << 32) | un[j + n - 2]))) {
-      --qhat;
-      rhat += vn[n - 1];
-      if (rhat >= (1ull << 32)) break;
-    }
-    int64_t borrow = 0;
-    uint64_t carry = 0;
-    for (size_t i = 0; i < n; ++i) {
-      const uint64_t p = qhat * vn[i] + carry;
-      carry = p >> 32;
-      const int64_t t = static_cast<int64_t>(un[i + j]) - borrow - static_cast<int64_t>(p & 0xffffffffu);
-      un[i + j] = static_cast<uint32_t>(t);
-      borrow = t < 0 ? 1 : 0;
-    }
-    const int64_t t = static_cast<int64_t>(un[j + n]) - borrow - static_cast<int64_t>(carry);
-    un[j + n] = static_cast<uint32_t>(t);
-    if (t < 0) {
-      --qhat;
-      uint64_t c = 0;
-      for (size_t i = 0; i < n; ++i) {
-        const uint64_t sum = static_cast<uint64_t>(un[i + j]) + vn[i] + c;
-        un[i + j] = static_cast<uint32_t>(sum);
-        c = sum >> 32;
-      }
-      un[j + n] += static_cast<uint32_t>(c);
-    }
-    q[j] = static_cast<uint32_t>(qhat);
-  }
-  for (size_t i = 0; i < un.size(); ++i)
-    if (un[i]) throw std::runtime_error("big_divexact: inexact division");
-  big_trim(q);
-  return q;
+  Mpz x(a), y(b), r, q;
+  __gmpz_tdiv_r(&r.z, &x.z, &y.z);
+  if (!r.is_zero()) throw std::runtime_error("big_divexact: inexact division");
+  __gmpz_divexact(&q.z, &x.z, &y.z);
+  return q.big();
 }
 
 void sbig_add_inplace(SBig& acc, int sign, const uint32_t* limbs, int n) {
