@@ -282,7 +282,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
   pl->bound_bits = bound;
   const double need = bound + 1 + 36;
-  std::vector<uint32_t> primes = select_primes(pl->N, need);
+  std::vector<uint32_t> primes = select_primes(pl->N, need, kResPrimeMax);  // mmul3 window (modarith.cuh)
   pl->P = static_cast<int>(primes.size());
   pl->tabs = get_tables(pl->device, pl->N, pl->P, primes);
   return pl.release();

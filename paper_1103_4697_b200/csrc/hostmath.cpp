@@ -74,13 +74,14 @@ uint32_t primitive_root(uint32_t p) {
   throw std::runtime_error("primitive_root: none found");
 }
 
-std::vector<uint32_t> select_primes(uint32_t N, double need_bits) {
+std::vector<uint32_t> select_primes(uint32_t N, double need_bits, uint64_t hi) {
   static std::mutex mu;
-  static std::map<uint32_t, std::pair<std::vector<uint32_t>, uint64_t>> cache;  // N -> (primes, next c)
+  // (N, hi) -> (primes, next c)
+  static std::map<std::pair<uint32_t, uint64_t>, std::pair<std::vector<uint32_t>, uint64_t>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto& entry = cache[N];
+  auto& entry = cache[{N, hi}];
   auto& list = entry.first;
-  const uint64_t lo = (1ull << 30), hi = (1ull << 31);
+  const uint64_t lo = (1ull << 30);
   if (list.empty() && entry.second == 0) entry.second = (hi - 2) / N;
   std::vector<uint32_t> out;
   double bits = 0;

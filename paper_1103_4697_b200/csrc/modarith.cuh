@@ -46,6 +46,14 @@ CTG_HD uint32_t mmul2(uint32_t a, uint32_t b, uint32_t c, uint32_t d, const Mod&
   return redc(static_cast<uint64_t>(a) * b + static_cast<uint64_t>(c) * d, M.p, M.pneg);
 }
 
+// (a*b + c*d + e*f)*R^-1 mod p.  Requires p < 2^30.4 (kResPrimeMax): then
+// T < 3p^2 < 2^62.4, T + m p < 2^64 and the REDC output is < 1.99 p (one correction).
+CTG_HD uint32_t mmul3(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e, uint32_t f, const Mod& M) {
+  return redc(static_cast<uint64_t>(a) * b + static_cast<uint64_t>(c) * d + static_cast<uint64_t>(e) * f, M.p,
+              M.pneg);
+}
+constexpr uint32_t kResPrimeMax = 1416000000u;  // < 2^30.4 = 1,416,810,830
+
 CTG_HD uint32_t madd(uint32_t a, uint32_t b, uint32_t p) { return csub(a + b, p); }
 CTG_HD uint32_t msub(uint32_t a, uint32_t b, uint32_t p) {
   uint32_t s = a - b;

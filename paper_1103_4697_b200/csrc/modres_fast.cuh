@@ -13,9 +13,13 @@ namespace {
 //   A1 = b_k A - a_{k+1} y B,   r' = b_k A1 - A1_k B = b_k^2 (A mod B)
 //   res(A, B) = res(B, r') / b_k^(2k-2)
 // so res = r'_0 / E^2 with E = prod_{k=2}^{NN-1} b_k^(k-1), accumulated as
-// U <- U b_k, E <- E U.  Any vanishing leading coefficient (a degree drop mod p,
-// or a formal leading coefficient vanishing at the point) flags the unit for
-// the exact general kernel.  All arrays live in registers (fully unrolled).
+// U <- U b_k, E <- E U.  Both half-steps are fused into ONE pass over the coefficients,
+//   r'_i = (b_k^2) a_i + (-b_k a_{k+1}) b_{i-1} + (-A1_k) b_i,
+// a three-product sum with a single Montgomery reduction (mmul3: valid for p < 2^30.4,
+// the resultant's prime window): 3 IMAD.WIDE + IMAD + IMAD.HI per coefficient instead of
+// two two-product reductions.  Any vanishing leading coefficient (a degree drop mod p,
+// or a formal leading coefficient vanishing at the point) flags the unit for the exact
+// general kernel.  All arrays live in registers (fully unrolled).
 // ---------------------------------------------------------------------------
 template <int NN>
 __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
@@ -50,12 +54,12 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
   for (int kk = NN - 1; kk >= 1; --kk) {
     const uint32_t bk = B[kk];
     const uint32_t na = mneg(A[kk + 1], M.p);
-    A[0] = mmul(bk, A[0], M);
+    const uint32_t c1 = mmul(bk, bk, M);                                          // b_k^2
+    const uint32_t c2 = mmul(bk, na, M);                                          // -b_k a_{k+1}
+    const uint32_t c3 = mneg(mmul2(bk, A[kk], na, kk >= 1 ? B[kk - 1] : 0u, M), M.p);  // -A1_k
+    A[0] = mmul2(c1, A[0], c3, B[0], M);
 #pragma unroll
-    for (int t = 1; t <= kk; ++t) A[t] = mmul2(bk, A[t], na, B[t - 1], M);
-    const uint32_t nt = mneg(A[kk], M.p);
-#pragma unroll
-    for (int t = 0; t < kk; ++t) A[t] = mmul2(bk, A[t], nt, B[t], M);
+    for (int t = 1; t < kk; ++t) A[t] = mmul3(c1, A[t], c2, B[t - 1], c3, B[t], M);
     flag |= (A[kk - 1] == 0u);
     U = mmul(U, bk, M);
     if (kk >= 2) E = mmul(E, U, M);
