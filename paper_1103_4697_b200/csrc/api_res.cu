@@ -172,18 +172,40 @@ struct ctg_plan {
   int launches = 0;
   bool uploaded = false;
   // Device buffers come from the stream-ordered pool (cudaMallocAsync): no device-wide
-  // synchronisation per plan.  They are released on the last stream the plan used.
+  // synchronisation per plan; they are released on the last stream the plan used.  Plans
+  // run by ctg_resultant_batch instead bump-allocate from a grow-only per-context scratch
+  // region (`bump`), so steady-state calls allocate nothing.
   cudaStream_t last_stream = nullptr;
+  uint8_t* bump = nullptr;
+  size_t bump_off = 0, bump_cap = 0;
   template <class T>
   void palloc(T*& ptr, size_t count, cudaStream_t st) {
+    const size_t bytes = std::max<size_t>(1, count) * sizeof(T);
+    if (bump) {
+      if (bump_off + bytes > bump_cap) throw ApiError(CTG_INTERNAL, "plan: scratch region too small");
+      ptr = reinterpret_cast<T*>(bump + bump_off);
+      bump_off += (bytes + 255) & ~static_cast<size_t>(255);
+      return;
+    }
     void* p = nullptr;
-    CTG_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(1, count) * sizeof(T), st));
+    CTG_CUDA_CHECK(cudaMallocAsync(&p, bytes, st));
     ptr = static_cast<T*>(p);
   }
   template <class T>
   void pfree(T*& ptr) {
-    if (ptr) cudaFreeAsync(ptr, last_stream);
+    if (ptr && !bump) cudaFreeAsync(ptr, last_stream);
     ptr = nullptr;
+  }
+  // Bytes palloc will request for upload + residues + a CRT over J coefficients.
+  size_t scratch_bytes(int J) const {
+    auto r = [](size_t b) { return (std::max<size_t>(1, b) + 255) & ~static_cast<size_t>(255); };
+    const size_t nch = static_cast<size_t>((P + kCrtChunk - 1) / kCrtChunk);
+    size_t s = r(4 * h_limbs.size()) + r(h_sign.size()) + r(4 * dir.size()) + r(4ull * B * P * S) +
+               r(4ull * flag_cap) + r(16);
+    if (fast_ok) s += r(4ull * B * P * nrows * N);
+    s += r(4 * crt_y_words(*tabs, B, J)) + r(8 * static_cast<size_t>(B) * nch * J) +
+         r(8 * ((crt_cols_words(*tabs, B, J) + 1) / 2));
+    return s;
   }
   ~ctg_plan() {
     pfree(d_limbs);
@@ -397,9 +419,9 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int r
     pl->pfree(pl->d_Y);
     pl->pfree(pl->d_upart);
     pl->pfree(pl->d_cols);
-    pl->palloc(pl->d_Y, static_cast<size_t>(pl->B) * pl->P * J, st);
+    pl->palloc(pl->d_Y, crt_y_words(*pl->tabs, pl->B, J), st);
     pl->palloc(pl->d_upart, static_cast<size_t>(pl->B) * nch * J, st);
-    pl->palloc(pl->d_cols, static_cast<size_t>(pl->B) * pl->tabs->L16 * J, st);
+    pl->palloc(pl->d_cols, (crt_cols_words(*pl->tabs, pl->B, J) + 1) / 2, st);  // u64 elements
     pl->crt_cap = J;
   }
   pl->last_stream = st;
@@ -423,6 +445,13 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int r
   cp.cols = pl->d_cols;
   cp.out = d_out;
   cp.out_limbs = pl->tabs->LM;
+  cp.use_i8 = pl->tabs->use_i8 ? 1 : 0;
+  cp.Jp = (J + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+  cp.L8 = pl->tabs->L8;
+  cp.L8p = pl->tabs->L8p;
+  cp.Kp = pl->tabs->Kp;
+  cp.Bt8 = pl->tabs->d_Bt8;
+  cp.M8 = pl->tabs->d_M8;
   cp.counters = pl->d_counters;
   pl->launches += launch_crt(cp, st);
   CTG_CUDA_CHECK(cudaGetLastError());
@@ -510,6 +539,22 @@ void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
     c.out_off = out_words;
     out_words += c.out_words + 4;
   }
+  // Device scratch of every chunk (plan buffers + residue rows + CRT output) carved from one
+  // grow-only context region: chunks in flight at the same time never share memory.
+  std::vector<size_t> dev_off(chunks.size() + 1, 0);
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const ctg_plan* pl = chunks[i].pl.get();
+    const size_t rows = (4ull * pl->B * pl->P * pl->N + 255) & ~static_cast<size_t>(255);
+    const size_t outb = (4ull * chunks[i].out_words + 255) & ~static_cast<size_t>(255);
+    dev_off[i + 1] = dev_off[i] + pl->scratch_bytes(static_cast<int>(pl->D)) + rows + outb;
+  }
+  uint8_t* dev_base = reinterpret_cast<uint8_t*>(ctx.scratch_u32(2, dev_off.back() / 4 + 64));
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    ctg_plan* pl = chunks[i].pl.get();
+    pl->bump = dev_base + dev_off[i];
+    pl->bump_off = 0;
+    pl->bump_cap = dev_off[i + 1] - dev_off[i];
+  }
   uint8_t* h_in = ctx.pinned_input(in_bytes);
   uint32_t* h_out = ctx.pinned_u32(out_words);
   cudaStream_t s = ctx.stream, cp = ctx.copy_stream();
@@ -517,9 +562,8 @@ void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
     ctg_plan* pl = c.pl.get();
     plan_upload(pl, s, h_in + c.in_off);
     st.h2d_bytes += plan_h2d_bytes(pl);
-    CTG_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.d_rows),
-                                   sizeof(uint32_t) * static_cast<size_t>(pl->B) * pl->P * pl->N, s));
-    CTG_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&c.d_out), sizeof(uint32_t) * c.out_words, s));
+    pl->palloc(c.d_rows, static_cast<size_t>(pl->B) * pl->P * pl->N, s);
+    pl->palloc(c.d_out, c.out_words, s);
     plan_residues(pl, 0, pl->P, c.d_rows, 0, s);
     plan_crt(pl, c.d_rows, 0, 0, 0, 0, static_cast<int>(pl->D), c.d_out, 0, s);
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
@@ -530,8 +574,6 @@ void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
     CTG_CUDA_CHECK(cudaMemcpyAsync(ho + c.out_words, pl->d_counters, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
     CTG_CUDA_CHECK(cudaMemcpyAsync(ho, c.d_out, sizeof(uint32_t) * c.out_words, cudaMemcpyDeviceToHost, cp));
     CTG_CUDA_CHECK(cudaEventRecord(c.copied, cp));
-    CTG_CUDA_CHECK(cudaFreeAsync(c.d_rows, cp));
-    CTG_CUDA_CHECK(cudaFreeAsync(c.d_out, cp));
     pl->last_stream = cp;  // the plan's own buffers are released after the copies
     st.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
   }

@@ -214,9 +214,9 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   L.n += launch_gather_scale(d_src, src_pitch, d_idx, R, cols, d_seg, nseg, d_scale, T->d_pc, d_rows, ar.st);
   const int W = T->LM + 1;
   uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(cols) * W);
-  uint32_t* d_Y = ar.alloc<uint32_t>(static_cast<size_t>(R) * cols);
+  uint32_t* d_Y = ar.alloc<uint32_t>(crt_y_words(*T, 1, cols));
   double* d_upart = ar.alloc<double>(static_cast<size_t>((R + kCrtChunk - 1) / kCrtChunk) * cols);
-  uint64_t* d_cols = ar.alloc<uint64_t>(static_cast<size_t>(T->L16) * cols);
+  uint64_t* d_cols = ar.alloc<uint64_t>((crt_cols_words(*T, 1, cols) + 1) / 2);
   uint32_t* d_cnt = ar.alloc<uint32_t>(4);
   CTG_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 16, ar.st));
   CrtParams cp{};
@@ -239,6 +239,13 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   cp.cols = d_cols;
   cp.out = d_out;
   cp.out_limbs = T->LM;
+  cp.use_i8 = T->use_i8 ? 1 : 0;
+  cp.Jp = (cols + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+  cp.L8 = T->L8;
+  cp.L8p = T->L8p;
+  cp.Kp = T->Kp;
+  cp.Bt8 = T->d_Bt8;
+  cp.M8 = T->d_M8;
   cp.counters = d_cnt;
   L.n += launch_crt(cp, ar.st);
   CTG_CUDA_CHECK(cudaGetLastError());

@@ -31,6 +31,9 @@ constexpr int kGeneralMaxDeg = 128; // general (formal-degree) kernel limit
 constexpr uint32_t kMaxNtt = 1u << 14;
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT rounding estimate
+constexpr int kI8TileJ = 64;        // tensor-core CRT GEMM block tile: coefficients
+constexpr int kI8TileL = 128;       //                                   byte digits of the output
+constexpr int kI8MaxPrimes = 8192;  // s32 exactness: 4P * 255^2 < 2^31
 
 // Device error bits (plan counters[1]).
 enum : uint32_t {
@@ -50,6 +53,11 @@ struct CrtTables {
   double* d_minv = nullptr;
   uint32_t* d_Mk16 = nullptr;
   uint32_t* d_M16 = nullptr;
+  // tensor-core CRT operands (tables.cu): Bt8 [L8p][Kp] bytes, M8 [L8] byte digits of M
+  bool use_i8 = false;
+  int L8 = 0, L8p = 0, Kp = 0;
+  uint8_t* d_Bt8 = nullptr;
+  uint32_t* d_M8 = nullptr;
   std::vector<PrimeConst> h_pc;
   double log2M = 0;
   ~CrtTables();
@@ -93,13 +101,22 @@ struct CrtParams {
   const uint32_t* Mk16;  // [P][L16] 16-bit digits of M / p_k
   const uint32_t* M16;   // [L16] 16-bit digits of M
   int L16;
-  uint32_t* Y;           // scratch [B][P][J]
+  uint32_t* Y;           // scratch: IMAD path [B][P][J]; tensor path Yt [B][Jp][Kp/4] (k contiguous)
   double* upart;         // scratch [B][ceil(P / kCrtChunk)][J]: partial sums of y_k / p_k
-  uint64_t* cols;        // scratch [B][J][L16]
+  uint64_t* cols;        // scratch: IMAD path [B][J][L16] u64; tensor path [B][Jp][L8p] s32
   uint32_t* out;         // [B][J][out_limbs + 1]
   int out_limbs;
   uint32_t* counters;
+  // tensor-core path (use_i8): Jp = J rounded up to kI8TileJ
+  int use_i8;
+  int Jp, L8, L8p, Kp;
+  const uint8_t* Bt8;
+  const uint32_t* M8;
 };
+
+// Scratch words the CRT needs for J coefficients of B curves (Y and cols).
+size_t crt_y_words(const CrtTables& T, int B, int J);
+size_t crt_cols_words(const CrtTables& T, int B, int J);  // in 32-bit words
 
 // Kernel launchers (kernels_res.cu).  Each returns the number of launches issued.
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0,

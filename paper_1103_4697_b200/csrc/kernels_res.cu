@@ -508,7 +508,218 @@ __global__ void __launch_bounds__(128) k_crt_carry(CrtParams C) {
   if (lane == 0) out[0] = static_cast<uint32_t>(lowest >= OL ? 0 : (total_carry < 0 ? -1 : 1));
 }
 
+// ---------------------------------------------------------------------------
+// K5 on the tensor cores.  With Yt[j][k] = y_k (u32, k contiguous) read as bytes,
+//   A[j][4k+a] = byte a of y_k,   Bt8[l][4k+a] = byte (l-a) of M/p_k,
+//   C[j][l] = sum_{k,a} A[j][4k+a] Bt8[l][4k+a]  = the coefficient of 2^(8l) in sum_k y_k M/p_k
+// (u8 x u8 -> s32, exact while 4P * 255^2 < 2^31).  One mma.sync.m16n8k32 per 16x8x32.
+// ---------------------------------------------------------------------------
+
+// grid (ceil(J/32), ceil(P/64), B), block (32, 8): y_k for 32 coefficients x 64 primes,
+// transposed through shared memory into Yt (k contiguous), plus the partial sums of y_k/p_k.
+__global__ void __launch_bounds__(256) k_crt_prep_t(CrtParams C) {
+  __shared__ uint32_t tile[kCrtChunk][33];
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int jb = blockIdx.x * 32, jl = jb + tx;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int kbeg = chunk * kCrtChunk, kend = min(kbeg + kCrtChunk, C.P);
+  double u = 0;
+  for (int k = kbeg + ty; k < kbeg + kCrtChunk; k += 8) {
+    uint32_t y = 0;
+    if (k < kend && jl < C.J) {
+      const PrimeConst& pcv = C.pc[k];
+      const Mod M = load_mod(pcv);
+      y = mmul(crt_row(C, b, k)[C.j0 + jl], pcv.crt_c, M);
+      u += static_cast<double>(y) * C.minv[k];
+    }
+    tile[k - kbeg][tx] = y;
+  }
+  red[ty][tx] = u;
+  __syncthreads();
+  if (ty == 0 && jl < C.J) {
+    double s = 0;
+    for (int q = 0; q < 8; ++q) s += red[q][tx];
+    const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+    C.upart[(static_cast<size_t>(b) * nch + chunk) * C.J + jl] = s;
+  }
+  const int ppad = C.Kp / 4;
+  const int t = ty * 32 + tx;
+  for (int e = t; e < 32 * kCrtChunk; e += 256) {
+    const int jj = e / kCrtChunk, kk = e % kCrtChunk;
+    if (jb + jj < C.Jp && kbeg + kk < ppad)
+      C.Y[(static_cast<size_t>(b) * C.Jp + jb + jj) * ppad + kbeg + kk] = tile[kk][jj];
+  }
+}
+
+__device__ __forceinline__ void mma_u8(int32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// grid (L8p / 128, Jp / 64, B), 256 threads (8 warps, 2 x 4), warp tile 32 j x 32 l.
+__global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
+  constexpr int PW = 9;  // smem row pitch in words (32 bytes + 4 pad: conflict-free fragments)
+  __shared__ uint32_t As[kI8TileJ * PW];
+  __shared__ uint32_t Bs[kI8TileL * PW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int jb = blockIdx.y * kI8TileJ, lb = blockIdx.x * kI8TileL, b = blockIdx.z;
+  const int kw = C.Kp / 4;  // u32 words per row
+  const uint32_t* Ab = C.Y + (static_cast<size_t>(b) * C.Jp + jb) * kw;
+  const uint32_t* Bb = reinterpret_cast<const uint32_t*>(C.Bt8) + static_cast<size_t>(lb) * kw;
+  int32_t acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0;
+  for (int k0 = 0; k0 < kw; k0 += 8) {
+#pragma unroll
+    for (int e = tid; e < kI8TileJ * 8; e += 256) As[(e >> 3) * PW + (e & 7)] = Ab[static_cast<size_t>(e >> 3) * kw + k0 + (e & 7)];
+#pragma unroll
+    for (int e = tid; e < kI8TileL * 8; e += 256) Bs[(e >> 3) * PW + (e & 7)] = Bb[static_cast<size_t>(e >> 3) * kw + k0 + (e & 7)];
+    __syncthreads();
+    uint32_t af[2][4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = wm * 32 + mi * 16 + g;
+      af[mi][0] = As[r * PW + tig];
+      af[mi][1] = As[(r + 8) * PW + tig];
+      af[mi][2] = As[r * PW + 4 + tig];
+      af[mi][3] = As[(r + 8) * PW + 4 + tig];
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int cidx = wn * 32 + ni * 8 + g;
+      const uint32_t b0 = Bs[cidx * PW + tig], b1 = Bs[cidx * PW + 4 + tig];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) mma_u8(acc[mi][ni], af[mi], b0, b1);
+    }
+    __syncthreads();
+  }
+  int32_t* Cb = reinterpret_cast<int32_t*>(C.cols) + static_cast<size_t>(b) * C.Jp * C.L8p;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = jb + wm * 32 + mi * 16 + g;
+      const int c = lb + wn * 32 + ni * 8 + tig * 2;
+      *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r) * C.L8p + c]) = make_int2(acc[mi][ni][0], acc[mi][ni][1]);
+      *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r + 8) * C.L8p + c]) = make_int2(acc[mi][ni][2], acc[mi][ni][3]);
+    }
+}
+
+// Carry propagation of sum_l C[l] 2^(8 l) - t M over byte digits (one warp per coefficient;
+// same lane-chunk carry-lookahead scan as k_crt_carry, chunk = multiple of 4 digits, >= 8).
+__global__ void __launch_bounds__(128) k_crt_carry8(CrtParams C) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= C.J * C.B) return;
+  const int b = gw / C.J, jl = gw - b * C.J;
+  const int L8 = C.L8, OL = C.out_limbs;
+  const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+  double s = 0;
+  for (int q = lane; q < nch; q += 32) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const double tr = rint(s);
+  if (lane == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  const int64_t t = static_cast<int64_t>(tr);
+
+  int chunk = 4 * ((L8 + 127) / 128);
+  if (chunk < 8) chunk = 8;
+  const int d0 = lane * chunk;
+  const int32_t* col = reinterpret_cast<const int32_t*>(C.cols) + (static_cast<size_t>(b) * C.Jp + jl) * C.L8p;
+  uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1);
+  int64_t carry = 0;
+  uint64_t low = 0;
+  bool ones = true, zeros = true;
+  for (int k = 0; k < chunk; k += 4) {
+    uint32_t limb = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int l = d0 + k + h;
+      int64_t v = carry;
+      if (l < L8) v += static_cast<int64_t>(col[l]) - t * static_cast<int64_t>(C.M8[l]);
+      limb |= static_cast<uint32_t>(v & 0xff) << (8 * h);
+      carry = v >> 8;
+    }
+    const int w = (d0 + k) >> 2;
+    if (w < OL) out[1 + w] = limb;
+    if (k < 8) {
+      low |= static_cast<uint64_t>(limb) << (8 * k);
+    } else {
+      ones &= (limb == 0xffffffffu);
+      zeros &= (limb == 0u);
+    }
+  }
+  int64_t cin = 0, my_cin = 0;
+  const uint32_t flags = (ones ? 1u : 0u) | (zeros ? 2u : 0u);
+  for (int i = 0; i < 32; ++i) {
+    const int64_t ci = __shfl_sync(0xffffffffu, carry, i);
+    const uint64_t lo = __shfl_sync(0xffffffffu, low, i);
+    const uint32_t fl = __shfl_sync(0xffffffffu, flags, i);
+    if (lane == i) my_cin = cin;
+    int64_t adj = 0;
+    if (cin > 0) {
+      adj = ((fl & 1u) && lo + static_cast<uint64_t>(cin) < lo) ? 1 : 0;
+    } else if (cin < 0) {
+      adj = ((fl & 2u) && lo < static_cast<uint64_t>(-cin)) ? -1 : 0;
+    }
+    cin = ci + adj;
+  }
+  const int64_t total_carry = cin;
+  int64_t c = my_cin;
+  for (int k = 0; k < chunk && c != 0; k += 4) {
+    const int w = (d0 + k) >> 2;
+    if (w >= OL) break;
+    const int64_t v = static_cast<int64_t>(out[1 + w]) + c;
+    out[1 + w] = static_cast<uint32_t>(v);
+    c = v >> 32;
+  }
+  __syncwarp();
+  int lowest = OL;
+  for (int k = 0; k < chunk; k += 4) {
+    const int w = (d0 + k) >> 2;
+    if (w < OL && out[1 + w] != 0u) {
+      lowest = w;
+      break;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lowest = min(lowest, __shfl_xor_sync(0xffffffffu, lowest, off));
+  if (total_carry < 0) {
+    for (int k = 0; k < chunk; k += 4) {
+      const int w = (d0 + k) >> 2;
+      if (w >= OL || w < lowest) continue;
+      out[1 + w] = (w == lowest) ? (0u - out[1 + w]) : ~out[1 + w];
+    }
+  }
+  if (lane == 0) out[0] = static_cast<uint32_t>(lowest >= OL ? 0 : (total_carry < 0 ? -1 : 1));
+}
+
 }  // namespace
+
+size_t crt_y_words(const CrtTables& T, int B, int J) {
+  if (T.use_i8) {
+    const size_t Jp = (static_cast<size_t>(J) + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+    return static_cast<size_t>(B) * Jp * (T.Kp / 4);
+  }
+  return static_cast<size_t>(B) * T.P * J;
+}
+
+size_t crt_cols_words(const CrtTables& T, int B, int J) {
+  if (T.use_i8) {
+    const size_t Jp = (static_cast<size_t>(J) + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+    return static_cast<size_t>(B) * Jp * T.L8p;
+  }
+  return static_cast<size_t>(B) * J * T.L16 * 2;
+}
 
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0, int nk,
                   uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
@@ -545,6 +756,12 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
 int launch_crt(const CrtParams& cp, cudaStream_t st) {
   if (cp.J == 0 || cp.B == 0) return 0;
   const int nch = (cp.P + kCrtChunk - 1) / kCrtChunk;
+  if (cp.use_i8) {
+    k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
+    k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
+    k_crt_carry8<<<(cp.J * cp.B + 3) / 4, 128, 0, st>>>(cp);
+    return 3;
+  }
   k_crt_prep<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
   k_crt_gemm<<<dim3((cp.L16 + 63) / 64, (cp.J + 31) / 32, cp.B), 128, 0, st>>>(cp);
   k_crt_carry<<<(cp.J * cp.B + 3) / 4, 128, 0, st>>>(cp);

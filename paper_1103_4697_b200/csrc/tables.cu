@@ -1,5 +1,10 @@
 // Prime tables: Montgomery constants, roots of unity (for the NTT size N) and the
-// fixed-point CRT constants M/p_k (16-bit digits), (M/p_k)^{-1} mod p_k, 1/p_k.
+// fixed-point CRT constants: (M/p_k)^{-1} mod p_k, 1/p_k and the digits of M/p_k in two
+// layouts -- 16-bit digits for the IMAD GEMM, and the byte-sliced, shift-expanded
+// operand of the tensor-core GEMM:
+//   Bt8[l][4k + a] = byte (l - a) of M/p_k,
+// so that  sum_k y_k (M/p_k) = sum_l 2^(8 l) sum_{k,a} byte_a(y_k) Bt8[l][4k+a]
+// is ONE u8 x u8 -> s32 matrix product (exact: 4P * 255^2 < 2^31 for P < 8250).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -14,11 +19,9 @@ CrtTables::~CrtTables() {
   cudaFree(d_minv);
   cudaFree(d_Mk16);
   cudaFree(d_M16);
+  cudaFree(d_Bt8);
+  cudaFree(d_M8);
 }
-
-// ---------------------------------------------------------------------------
-// Per-prime constants and fixed-point CRT tables for an ordered prime set.
-// ---------------------------------------------------------------------------
 
 std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N) {
   const int P = static_cast<int>(primes.size());
@@ -32,12 +35,19 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   for (uint32_t p : primes) Mb = big_mul_u32(Mb, p);
   T->LM = static_cast<int>(Mb.size());
   T->L16 = 2 * T->LM;
+  T->L8 = 4 * T->LM;
+  T->L8p = (T->L8 + kI8TileL - 1) / kI8TileL * kI8TileL;
+  T->Kp = (4 * P + 31) / 32 * 32;
+  T->use_i8 = P <= kI8MaxPrimes;
   std::vector<PrimeConst> pc(P);
   std::vector<double> minv(P);
-  std::vector<uint32_t> Mk16(static_cast<size_t>(P) * T->L16, 0u), M16(T->L16, 0u);
+  std::vector<uint32_t> Mk16(static_cast<size_t>(P) * T->L16, 0u), M16(T->L16, 0u), M8(T->L8, 0u);
+  std::vector<uint8_t> Bt8;
+  if (T->use_i8) Bt8.assign(static_cast<size_t>(T->L8p) * T->Kp, 0u);
   for (int l = 0; l < T->LM; ++l) {
     M16[2 * l] = Mb[l] & 0xffffu;
     M16[2 * l + 1] = Mb[l] >> 16;
+    for (int a = 0; a < 4; ++a) M8[4 * l + a] = (Mb[l] >> (8 * a)) & 0xffu;
   }
   for (int k = 0; k < P; ++k) {
     const uint32_t p = primes[k];
@@ -63,6 +73,17 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
       Mk16[static_cast<size_t>(k) * T->L16 + 2 * l] = Mk[l] & 0xffffu;
       Mk16[static_cast<size_t>(k) * T->L16 + 2 * l + 1] = Mk[l] >> 16;
     }
+    if (T->use_i8) {
+      const int nbytes = 4 * static_cast<int>(Mk.size());
+      for (int i = 0; i < nbytes; ++i) {
+        const uint8_t byte = static_cast<uint8_t>(Mk[i / 4] >> (8 * (i % 4)));
+        if (!byte) continue;
+        for (int a = 0; a < 4; ++a) {
+          const int l = i + a;
+          if (l < T->L8) Bt8[static_cast<size_t>(l) * T->Kp + 4 * k + a] = byte;
+        }
+      }
+    }
   }
   T->h_pc = pc;
   T->log2M = 0;
@@ -71,10 +92,16 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   CTG_CUDA_CHECK(cudaMalloc(&T->d_minv, sizeof(double) * P));
   CTG_CUDA_CHECK(cudaMalloc(&T->d_Mk16, sizeof(uint32_t) * Mk16.size()));
   CTG_CUDA_CHECK(cudaMalloc(&T->d_M16, sizeof(uint32_t) * M16.size()));
+  CTG_CUDA_CHECK(cudaMalloc(&T->d_M8, sizeof(uint32_t) * M8.size()));
   CTG_CUDA_CHECK(cudaMemcpy(T->d_pc, pc.data(), sizeof(PrimeConst) * P, cudaMemcpyHostToDevice));
   CTG_CUDA_CHECK(cudaMemcpy(T->d_minv, minv.data(), sizeof(double) * P, cudaMemcpyHostToDevice));
   CTG_CUDA_CHECK(cudaMemcpy(T->d_Mk16, Mk16.data(), sizeof(uint32_t) * Mk16.size(), cudaMemcpyHostToDevice));
   CTG_CUDA_CHECK(cudaMemcpy(T->d_M16, M16.data(), sizeof(uint32_t) * M16.size(), cudaMemcpyHostToDevice));
+  CTG_CUDA_CHECK(cudaMemcpy(T->d_M8, M8.data(), sizeof(uint32_t) * M8.size(), cudaMemcpyHostToDevice));
+  if (T->use_i8) {
+    CTG_CUDA_CHECK(cudaMalloc(&T->d_Bt8, Bt8.size()));
+    CTG_CUDA_CHECK(cudaMemcpy(T->d_Bt8, Bt8.data(), Bt8.size(), cudaMemcpyHostToDevice));
+  }
   return T;
 }
 
