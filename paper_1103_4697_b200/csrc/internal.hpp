@@ -31,7 +31,7 @@ constexpr int kGeneralMaxDeg = 128; // general (formal-degree) kernel limit
 constexpr uint32_t kMaxNtt = 1u << 14;
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT rounding estimate
-constexpr int kI8TileJ = 64;        // tensor-core CRT GEMM block tile: coefficients
+constexpr int kI8TileJ = 128;       // tensor-core CRT GEMM block tile: coefficients
 constexpr int kI8TileL = 128;       //                                   byte digits of the output
 constexpr int kI8MaxPrimes = 8192;  // s32 exactness: 4P * 255^2 < 2^31
 

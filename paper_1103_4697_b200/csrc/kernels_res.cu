@@ -559,55 +559,94 @@ __device__ __forceinline__ void mma_u8(int32_t (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// grid (L8p / 128, Jp / 64, B), 256 threads (8 warps, 2 x 4), warp tile 32 j x 32 l.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* smem) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+
+// grid (L8p / 128, Jp / 128, B), 256 threads = 8 warps (2 along j x 4 along l), warp tile
+// 64 j x 32 l (4 x 4 mma tiles).  K is staged 64 bytes per step through a 2-deep cp.async
+// pipeline; fragments come from ldmatrix (row pitch 80 B: conflict-free).
 __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
-  constexpr int PW = 9;  // smem row pitch in words (32 bytes + 4 pad: conflict-free fragments)
-  __shared__ uint32_t As[kI8TileJ * PW];
-  __shared__ uint32_t Bs[kI8TileL * PW];
+  constexpr int kBK = 64, kPitch = 80;
+  __shared__ __align__(128) uint8_t As[2][kI8TileJ * kPitch];
+  __shared__ __align__(128) uint8_t Bs[2][kI8TileL * kPitch];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
   const int jb = blockIdx.y * kI8TileJ, lb = blockIdx.x * kI8TileL, b = blockIdx.z;
-  const int kw = C.Kp / 4;  // u32 words per row
-  const uint32_t* Ab = C.Y + (static_cast<size_t>(b) * C.Jp + jb) * kw;
-  const uint32_t* Bb = reinterpret_cast<const uint32_t*>(C.Bt8) + static_cast<size_t>(lb) * kw;
-  int32_t acc[2][4][4];
+  const uint8_t* Ab = reinterpret_cast<const uint8_t*>(C.Y) + (static_cast<size_t>(b) * C.Jp + jb) * C.Kp;
+  const uint8_t* Bb = C.Bt8 + static_cast<size_t>(lb) * C.Kp;
+  const int nst = C.Kp / kBK;
+  auto load = [&](int stage, int buf) {
+    const int k0 = stage * kBK;
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+    for (int e = tid; e < 1024; e += 256) {
+      const bool isB = e >= 512;
+      const int ee = e & 511, row = ee >> 2, ch = ee & 3;
+      const uint8_t* src = (isB ? Bb : Ab) + static_cast<size_t>(row) * C.Kp + k0 + ch * 16;
+      uint8_t* dst = (isB ? Bs[buf] : As[buf]) + row * kPitch + ch * 16;
+      cp_async16(dst, src);
+    }
+    cp_async_commit();
+  };
+  int32_t acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[i][j][q] = 0;
-  for (int k0 = 0; k0 < kw; k0 += 8) {
-#pragma unroll
-    for (int e = tid; e < kI8TileJ * 8; e += 256) As[(e >> 3) * PW + (e & 7)] = Ab[static_cast<size_t>(e >> 3) * kw + k0 + (e & 7)];
-#pragma unroll
-    for (int e = tid; e < kI8TileL * 8; e += 256) Bs[(e >> 3) * PW + (e & 7)] = Bb[static_cast<size_t>(e >> 3) * kw + k0 + (e & 7)];
-    __syncthreads();
-    uint32_t af[2][4];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      const int r = wm * 32 + mi * 16 + g;
-      af[mi][0] = As[r * PW + tig];
-      af[mi][1] = As[(r + 8) * PW + tig];
-      af[mi][2] = As[r * PW + 4 + tig];
-      af[mi][3] = As[(r + 8) * PW + 4 + tig];
+  load(0, 0);
+  for (int s = 0; s < nst; ++s) {
+    if (s + 1 < nst) {
+      load(s + 1, (s + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const uint8_t* as = As[s & 1];
+    const uint8_t* bs = Bs[s & 1];
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int cidx = wn * 32 + ni * 8 + g;
-      const uint32_t b0 = Bs[cidx * PW + tig], b1 = Bs[cidx * PW + 4 + tig];
+    for (int kk = 0; kk < kBK; kk += 32) {
+      uint32_t af[4][4], bf[4][2];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) mma_u8(acc[mi][ni], af[mi], b0, b1);
+      for (int mi = 0; mi < 4; ++mi)
+        ldmatrix_x4(af[mi], as + (wm * 64 + mi * 16 + (lane & 15)) * kPitch + kk + (lane >> 4) * 16);
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        uint32_t t[4];
+        ldmatrix_x4(t, bs + (wn * 32 + nj * 16 + ((lane >> 4) << 3) + (lane & 7)) * kPitch + kk + ((lane >> 3) & 1) * 16);
+        bf[2 * nj][0] = t[0];
+        bf[2 * nj][1] = t[1];
+        bf[2 * nj + 1][0] = t[2];
+        bf[2 * nj + 1][1] = t[3];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) mma_u8(acc[mi][ni], af[mi], bf[ni][0], bf[ni][1]);
     }
     __syncthreads();
   }
   int32_t* Cb = reinterpret_cast<int32_t*>(C.cols) + static_cast<size_t>(b) * C.Jp * C.L8p;
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
-      const int r = jb + wm * 32 + mi * 16 + g;
+      const int r = jb + wm * 64 + mi * 16 + g;
       const int c = lb + wn * 32 + ni * 8 + tig * 2;
       *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r) * C.L8p + c]) = make_int2(acc[mi][ni][0], acc[mi][ni][1]);
       *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r + 8) * C.L8p + c]) = make_int2(acc[mi][ni][2], acc[mi][ni][3]);

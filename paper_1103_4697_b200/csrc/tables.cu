@@ -37,7 +37,7 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   T->L16 = 2 * T->LM;
   T->L8 = 4 * T->LM;
   T->L8p = (T->L8 + kI8TileL - 1) / kI8TileL * kI8TileL;
-  T->Kp = (4 * P + 31) / 32 * 32;
+  T->Kp = (4 * P + 63) / 64 * 64;  // 64-byte K stages of the GEMM pipeline
   T->use_i8 = P <= kI8MaxPrimes;
   std::vector<PrimeConst> pc(P);
   std::vector<double> minv(P);
