@@ -366,9 +366,9 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
     return;
   }
   if (stage == 3) {
-    pl->launches += launch_interp(d_rows, rows_bstride, static_cast<int>(pl->N), nk, pl->B, pl->tabs->d_pc, k0,
-                                  static_cast<int>(pl->N), static_cast<int>(pl->r), static_cast<int>(pl->a),
-                                  static_cast<int>(pl->D), pl->negate, pl->d_counters, st);
+    pl->launches += launch_interp(d_rows, rows_bstride, static_cast<int>(pl->N), nk, pl->B, pl->tabs->d_pc,
+                                  pl->tabs->d_twinv, k0, static_cast<int>(pl->N), static_cast<int>(pl->r),
+                                  static_cast<int>(pl->a), static_cast<int>(pl->D), pl->negate, pl->d_counters, st);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }

@@ -58,6 +58,7 @@ struct CrtTables {
   int L8 = 0, L8p = 0, Kp = 0;
   uint8_t* d_Bt8 = nullptr;
   uint32_t* d_M8 = nullptr;
+  uint32_t* d_twinv = nullptr;  // [P][N] omega_k^{-i} (Montgomery), N > 1 only
   std::vector<PrimeConst> h_pc;
   double log2M = 0;
   ~CrtTables();
@@ -122,8 +123,11 @@ size_t crt_cols_words(const CrtTables& T, int B, int J);  // in 32-bit words
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0,
                   int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st);
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st);
-int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc, int k0,
-                  int N, int r, int a, int D, int negate, uint32_t* counters, cudaStream_t st);
+int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
+                  const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
+                  cudaStream_t st);
+// Fills twinv[k][i] = omega_k^{-i} for all primes of a table (one launch, at table build).
+void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv);
 int launch_crt(const CrtParams& cp, cudaStream_t st);
 
 }  // namespace ctg

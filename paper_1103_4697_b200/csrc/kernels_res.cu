@@ -261,8 +261,17 @@ __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_lis
 //   u[i1] = radix-2 inverse NTT (root omega^{-r}) of v[r*i2 + i1],
 // with s = +-N^{-1}.  Coefficients j >= D must vanish (degree bound check).
 // ---------------------------------------------------------------------------
+__global__ void k_twiddles(const PrimeConst* __restrict__ pc, int P, int N, uint32_t* twinv) {
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<size_t>(P) * N) return;
+  const int k = static_cast<int>(idx / N), i = static_cast<int>(idx % N);
+  const PrimeConst pcv = pc[k];
+  twinv[idx] = mpow(pcv.omega_inv, static_cast<uint64_t>(i), load_mod(pcv));
+}
+
 __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstride, int pitch,
-                                                const PrimeConst* __restrict__ pc, int k0, int N, int r, int a,
+                                                const PrimeConst* __restrict__ pc,
+                                                const uint32_t* __restrict__ twinv, int k0, int N, int r, int a,
                                                 int D, int negate, uint32_t* counters) {
   extern __shared__ uint32_t sm[];
   uint32_t* tw = sm;      // omega^{-i}, i < N
@@ -271,11 +280,12 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
   const PrimeConst pcv = pc[k0 + kl];
   const Mod M = load_mod(pcv);
   uint32_t* row = rows + b * rows_bstride + static_cast<size_t>(kl) * pitch;
+  const uint32_t* twk = twinv + static_cast<size_t>(k0 + kl) * N;
   const int Mlen = 1 << a;
   const int tid = threadIdx.x, bs = blockDim.x;
   bool bad = false;
   for (int i = tid; i < N; i += bs) {
-    tw[i] = mpow(pcv.omega_inv, static_cast<uint64_t>(i), M);
+    tw[i] = twk[i];
     const uint32_t val = row[i];
     bad |= (val == kSentinel);
     const int i1 = i % r, i2 = i / r;
@@ -783,13 +793,20 @@ int launch_modres(const ResParams& rp, bool fast, cudaStream_t st) {
   return 1;
 }
 
-int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc, int k0,
-                  int N, int r, int a, int D, int negate, uint32_t* counters, cudaStream_t st) {
+int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
+                  const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
+                  cudaStream_t st) {
   if (nk == 0 || B == 0) return 0;
   const size_t smem = static_cast<size_t>(2) * N * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_interp<<<dim3(nk, B), 256, smem, st>>>(rows, rows_bstride, pitch, d_pc, k0, N, r, a, D, negate, counters);
+  k_interp<<<dim3(nk, B), 256, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, r, a, D, negate,
+                                           counters);
   return 1;
+}
+
+void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv) {
+  const size_t total = static_cast<size_t>(P) * N;
+  k_twiddles<<<static_cast<unsigned>((total + 255) / 256), 256>>>(d_pc, P, N, d_twinv);
 }
 
 int launch_crt(const CrtParams& cp, cudaStream_t st) {

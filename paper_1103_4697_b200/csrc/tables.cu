@@ -21,6 +21,7 @@ CrtTables::~CrtTables() {
   cudaFree(d_M16);
   cudaFree(d_Bt8);
   cudaFree(d_M8);
+  cudaFree(d_twinv);
 }
 
 std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N) {
@@ -101,6 +102,12 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   if (T->use_i8) {
     CTG_CUDA_CHECK(cudaMalloc(&T->d_Bt8, Bt8.size()));
     CTG_CUDA_CHECK(cudaMemcpy(T->d_Bt8, Bt8.data(), Bt8.size(), cudaMemcpyHostToDevice));
+  }
+  if (N >= 1 && P > 0) {
+    CTG_CUDA_CHECK(cudaMalloc(&T->d_twinv, sizeof(uint32_t) * static_cast<size_t>(P) * N));
+    launch_twiddles(T->d_pc, P, static_cast<int>(N), T->d_twinv);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    CTG_CUDA_CHECK(cudaDeviceSynchronize());
   }
   return T;
 }
