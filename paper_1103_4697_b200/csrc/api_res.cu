@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -29,12 +30,12 @@
 
 namespace ctg {
 
-// Cached per-(device, N, P) prime tables for the resultant path.
-static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, int P, const std::vector<uint32_t>& primes) {
+// Cached per-(device, N, prime list) tables for the resultant path.
+static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, const std::vector<uint32_t>& primes) {
   static std::mutex mu;
-  static std::map<std::tuple<int, uint32_t, int>, std::shared_ptr<CrtTables>> cache;
+  static std::map<std::tuple<int, uint32_t, std::vector<uint32_t>>, std::shared_ptr<CrtTables>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(device, N, P);
+  auto key = std::make_tuple(device, N, primes);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   auto T = build_tables(device, primes, N);
@@ -306,7 +307,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   const double need = bound + 1 + 36;
   std::vector<uint32_t> primes = select_primes(pl->N, need, kResPrimeMax);  // mmul3 window (modarith.cuh)
   pl->P = static_cast<int>(primes.size());
-  pl->tabs = get_tables(pl->device, pl->N, pl->P, primes);
+  pl->tabs = get_tables(pl->device, pl->N, primes);
   return pl.release();
 }
 
@@ -801,10 +802,17 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
         chunks.push_back(std::move(c));
       }
     }
+    const double t_plan = timer.lap();
     run_chunks(chunks, ctx, out);
+    const double t_run = timer.lap();
     chunks.clear();
     parallel_for(batch, [&](int b) { probs[b] = Problem(); });  // release the parsed terms in parallel
+    const double t_rel = timer.lap();
     timer.finish_total();
+    static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
+    if (trace)
+      std::fprintf(stderr, "[ctg] batch %d: plan %.3f ms, run %.3f ms, release %.3f ms, total %.3f ms\n", batch, t_plan,
+                   t_run, t_rel, st.total_ms);
   });
 }
 

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <limits>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <stdexcept>
 
@@ -74,41 +75,44 @@ uint32_t primitive_root(uint32_t p) {
   throw std::runtime_error("primitive_root: none found");
 }
 
-std::vector<uint32_t> select_primes(uint32_t N, double need_bits, uint64_t hi) {
+// Cached, lazily extended sequence of the primes c*N + 1 in (lo, hi), decreasing.
+static uint32_t prime_seq_at(uint32_t N, uint64_t hi, uint64_t lo, size_t i) {
   static std::mutex mu;
-  // (N, hi) -> (primes, next c)
-  static std::map<std::pair<uint32_t, uint64_t>, std::pair<std::vector<uint32_t>, uint64_t>> cache;
+  // (N, hi, lo) -> (primes, next c)
+  static std::map<std::tuple<uint32_t, uint64_t, uint64_t>, std::pair<std::vector<uint32_t>, uint64_t>> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto& entry = cache[{N, hi}];
+  auto& entry = cache[{N, hi, lo}];
   auto& list = entry.first;
-  const uint64_t lo = (1ull << 30);
   if (list.empty() && entry.second == 0) entry.second = (hi - 2) / N;
+  while (i >= list.size()) {
+    bool found = false;
+    while (entry.second > 0) {
+      uint64_t c = entry.second--;
+      uint64_t p = c * N + 1;
+      if (p >= hi) continue;
+      if (p <= lo) {
+        entry.second = 0;
+        break;
+      }
+      if (is_prime_u32(static_cast<uint32_t>(p))) {
+        list.push_back(static_cast<uint32_t>(p));
+        found = true;
+        break;
+      }
+    }
+    if (!found) return 0u;
+  }
+  return list[i];
+}
+
+std::vector<uint32_t> select_primes(uint32_t N, double need_bits, uint64_t hi, uint64_t lo) {
   std::vector<uint32_t> out;
   double bits = 0;
-  size_t i = 0;
-  while (bits < need_bits) {
-    if (i == list.size()) {
-      // Extend the cached sequence.
-      bool found = false;
-      while (entry.second > 0) {
-        uint64_t c = entry.second--;
-        uint64_t p = c * N + 1;
-        if (p >= hi) continue;
-        if (p <= lo) {
-          entry.second = 0;
-          break;
-        }
-        if (is_prime_u32(static_cast<uint32_t>(p))) {
-          list.push_back(static_cast<uint32_t>(p));
-          found = true;
-          break;
-        }
-      }
-      if (!found) throw std::runtime_error("select_primes: ran out of primes p = c*N+1 in (2^30, 2^31)");
-    }
-    out.push_back(list[i]);
-    bits += std::log2(static_cast<double>(list[i]));
-    ++i;
+  for (size_t i = 0; bits < need_bits; ++i) {
+    const uint32_t p = prime_seq_at(N, hi, lo, i);
+    if (!p) throw std::runtime_error("select_primes: ran out of primes p = c*N+1 in the window");
+    out.push_back(p);
+    bits += std::log2(static_cast<double>(p));
   }
   return out;
 }

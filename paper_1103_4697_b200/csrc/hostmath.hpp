@@ -18,11 +18,11 @@ uint32_t inv_mod_u32(uint32_t a, uint32_t p);
 // Primitive root modulo the prime p.
 uint32_t primitive_root(uint32_t p);
 
-// All primes p = c*N + 1 in (2^30, hi), in decreasing order, as many as
+// All primes p = c*N + 1 in (lo, hi), in decreasing order, as many as
 // needed so that sum(log2 p) >= need_bits.  Deterministic: the list for a
-// given (N, hi) is always a prefix of the same sequence.  The resultant uses
+// given (N, hi, lo) is always a prefix of the same sequence.  The resultant uses
 // hi = kResPrimeMax (three-product reductions), the gcd / Yun path hi = 2^31.
-std::vector<uint32_t> select_primes(uint32_t N, double need_bits, uint64_t hi = (1ull << 31));
+std::vector<uint32_t> select_primes(uint32_t N, double need_bits, uint64_t hi = (1ull << 31), uint64_t lo = (1ull << 30));
 
 // Smallest N = r * 2^a >= D with r in {1, 3, 5, 7} (the NTT sizes the
 // interpolation kernel supports).  Returns r and a through the pointers.

@@ -665,9 +665,13 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
 
 // Carry propagation of sum_l C[l] 2^(8 l) - t M over byte digits (one warp per coefficient;
 // same lane-chunk carry-lookahead scan as k_crt_carry, chunk = multiple of 4 digits, >= 8).
+// The warp first stages v_l = C[l] - t M8[l] through shared memory with coalesced loads
+// (int32: 0 <= C[l] < 2^31, 0 <= t M8[l] < 2^21); slot l lives at l + l / chunk so the
+// lanes' chunk walks (stride chunk + 1, odd) are bank-conflict-free.
 __global__ void __launch_bounds__(128) k_crt_carry8(CrtParams C) {
+  extern __shared__ int32_t sv[];
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   if (gw >= C.J * C.B) return;
   const int b = gw / C.J, jl = gw - b * C.J;
   const int L8 = C.L8, OL = C.out_limbs;
@@ -678,12 +682,16 @@ __global__ void __launch_bounds__(128) k_crt_carry8(CrtParams C) {
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   const double tr = rint(s);
   if (lane == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
-  const int64_t t = static_cast<int64_t>(tr);
+  const int32_t t = static_cast<int32_t>(tr);
 
   int chunk = 4 * ((L8 + 127) / 128);
   if (chunk < 8) chunk = 8;
   const int d0 = lane * chunk;
   const int32_t* col = reinterpret_cast<const int32_t*>(C.cols) + (static_cast<size_t>(b) * C.Jp + jl) * C.L8p;
+  int32_t* v_s = sv + wib * (32 * chunk + 32);
+  for (int l = lane; l < 32 * chunk; l += 32)
+    v_s[l + l / chunk] = (l < L8) ? col[l] - t * static_cast<int32_t>(C.M8[l]) : 0;
+  __syncwarp();
   uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1);
   int64_t carry = 0;
   uint64_t low = 0;
@@ -693,8 +701,7 @@ __global__ void __launch_bounds__(128) k_crt_carry8(CrtParams C) {
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const int l = d0 + k + h;
-      int64_t v = carry;
-      if (l < L8) v += static_cast<int64_t>(col[l]) - t * static_cast<int64_t>(C.M8[l]);
+      const int64_t v = carry + v_s[l + lane];  // l / chunk == lane
       limb |= static_cast<uint32_t>(v & 0xff) << (8 * h);
       carry = v >> 8;
     }
@@ -815,7 +822,14 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
   if (cp.use_i8) {
     k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
     k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
-    k_crt_carry8<<<(cp.J * cp.B + 3) / 4, 128, 0, st>>>(cp);
+    int chunk = 4 * ((cp.L8 + 127) / 128);
+    if (chunk < 8) chunk = 8;
+    const size_t warp_smem = static_cast<size_t>(32 * chunk + 32) * sizeof(int32_t);
+    const int wpb = warp_smem * 4 <= 160 * 1024 ? 4 : 1;  // P <= 8192: one warp needs <= 127 KB
+    const size_t smem = warp_smem * wpb;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_crt_carry8, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_crt_carry8<<<(cp.J * cp.B + wpb - 1) / wpb, 32 * wpb, smem, st>>>(cp);
     return 3;
   }
   k_crt_prep<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);

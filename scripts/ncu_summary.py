@@ -38,6 +38,16 @@ def summarize(path):
         if k in hdr:
             i = hdr.index(k)
             out.append(f"  {short:12s} {vals[i]} {units[i]}")
+    pipes = []
+    for i, k in enumerate(hdr):
+        if (k.startswith("sm__pipe_") or k.startswith("sm__inst_executed_pipe_")) and k.endswith("pct_of_peak_sustained_active"):
+            try:
+                v = float(vals[i])
+            except ValueError:
+                continue
+            if v >= 1.0:
+                pipes.append(f"{k.replace('.avg.pct_of_peak_sustained_active', '')}={v:.1f}")
+    out.append("  pipes% " + " ".join(pipes))
     st = []
     for s in STALLS:
         k = f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
