@@ -208,6 +208,34 @@ class HostBipoly:
                               self.limbs.ctypes.data_as(_u32p))
         self.nbytes = self.dx.nbytes + self.dy.nbytes + self.sign.nbytes + self.off.nbytes + self.limbs.nbytes
 
+    @classmethod
+    def from_terms(cls, terms, pad_limbs: int = 0):
+        """Raw CSR operand from [(dx, dy, value), ...] in the given order -- duplicates,
+        explicit zeros and ``pad_limbs`` high zero limbs per term are kept (the library
+        must sum / drop / trim them like the reference's map insertion)."""
+        self = cls.__new__(cls)
+        n = len(terms)
+        self.dx = np.array([t[0] for t in terms], dtype=np.int32)
+        self.dy = np.array([t[1] for t in terms], dtype=np.int32)
+        self.sign = np.zeros(n, dtype=np.int8)
+        self.off = np.zeros(n + 1, dtype=np.uint32)
+        chunks, pos = [], 0
+        for i, (_, _, v) in enumerate(terms):
+            mag = -v if v < 0 else v
+            self.sign[i] = -1 if v < 0 else (1 if v > 0 else 0)
+            nl = (mag.bit_length() + 31) >> 5
+            nl += pad_limbs if v else 0
+            chunks.append(mag.to_bytes(nl * 4, "little"))
+            pos += nl
+            self.off[i + 1] = pos
+        raw = b"".join(chunks)
+        self.limbs = np.ascontiguousarray(np.frombuffer(raw, dtype=np.uint32) if raw else np.zeros(1, np.uint32))
+        self.struct = _Bipoly(n, self.dx.ctypes.data_as(_i32p), self.dy.ctypes.data_as(_i32p),
+                              self.sign.ctypes.data_as(_i8p), self.off.ctypes.data_as(_u32p),
+                              self.limbs.ctypes.data_as(_u32p))
+        self.nbytes = self.dx.nbytes + self.dy.nbytes + self.sign.nbytes + self.off.nbytes + self.limbs.nbytes
+        return self
+
 
 class HostUpoly:
     def __init__(self, p):

@@ -1,6 +1,8 @@
 #include "api_common.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -158,7 +160,11 @@ void CallTimer::finish() {
 }
 
 namespace {
-// Minimal persistent pool: workers pull indices from a shared counter.
+// Persistent pool for per-curve host work.  A call publishes a Job; workers claim indices
+// with an atomic counter (no lock per item) and, after a job, spin ~200 us for the next one
+// before sleeping, so the back-to-back parallel_for calls of one batch do not pay a
+// futex wake-up each.  `active_` guards the stack-allocated Job: the caller unpublishes it
+// and waits until no worker still holds it.
 class Pool {
  public:
   Pool() {
@@ -169,66 +175,64 @@ class Pool {
   ~Pool() {
     {
       std::lock_guard<std::mutex> l(mu_);
-      stop_ = true;
+      stop_.store(true);
     }
     cv_.notify_all();
     for (auto& w : workers_) w.join();
   }
   void run(int n, const std::function<void(int)>& fn) {
-    std::unique_lock<std::mutex> call(call_mu_);  // one parallel_for at a time
+    std::lock_guard<std::mutex> call(call_mu_);  // one parallel_for at a time
+    Job job{&fn, n};
+    job_.store(&job);
     {
       std::lock_guard<std::mutex> l(mu_);
-      fn_ = &fn;
-      n_ = n;
-      next_ = 0;
-      done_ = 0;
-      ++gen_;
+      gen_.fetch_add(1);
     }
     cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> l(mu_);
-    done_cv_.wait(l, [&] { return done_ == n_; });
-    fn_ = nullptr;
+    work(&job);
+    while (job.done.load(std::memory_order_acquire) < n) std::this_thread::yield();
+    job_.store(nullptr);
+    while (active_.load() != 0) std::this_thread::yield();
   }
 
  private:
-  void work() {
-    while (true) {
-      int i;
-      const std::function<void(int)>* f;
-      {
-        std::lock_guard<std::mutex> l(mu_);
-        if (!fn_ || next_ >= n_) return;
-        i = next_++;
-        f = fn_;
-      }
-      (*f)(i);
-      {
-        std::lock_guard<std::mutex> l(mu_);
-        if (++done_ == n_) done_cv_.notify_all();
-      }
+  struct Job {
+    const std::function<void(int)>* fn;
+    int n;
+    std::atomic<int> next{0}, done{0};
+  };
+  static void work(Job* j) {
+    for (int i = j->next.fetch_add(1); i < j->n; i = j->next.fetch_add(1)) {
+      (*j->fn)(i);
+      j->done.fetch_add(1, std::memory_order_release);
     }
   }
   void loop() {
-    uint64_t seen = 0;
+    using clk = std::chrono::steady_clock;
+    uint64_t seen = gen_.load();
     while (true) {
-      {
+      const auto t_end = clk::now() + std::chrono::microseconds(200);
+      while (gen_.load(std::memory_order_acquire) == seen && !stop_.load() && clk::now() < t_end)
+        std::this_thread::yield();
+      if (gen_.load() == seen && !stop_.load()) {
         std::unique_lock<std::mutex> l(mu_);
-        cv_.wait(l, [&] { return stop_ || (gen_ != seen && fn_ != nullptr); });
-        if (stop_) return;
-        seen = gen_;
+        cv_.wait(l, [&] { return stop_.load() || gen_.load() != seen; });
       }
-      work();
+      if (stop_.load()) return;
+      seen = gen_.load();
+      active_.fetch_add(1);
+      if (Job* j = job_.load()) work(j);
+      active_.fetch_sub(1);
     }
   }
   int nthreads_ = 1;
   std::vector<std::thread> workers_;
   std::mutex mu_, call_mu_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(int)>* fn_ = nullptr;
-  int n_ = 0, next_ = 0, done_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::condition_variable cv_;
+  std::atomic<Job*> job_{nullptr};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> active_{0};
+  std::atomic<bool> stop_{false};
 };
 }  // namespace
 
@@ -261,6 +265,68 @@ struct BufHdr {
 };
 size_t pad16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
+// Arena blocks: [ArenaHdr | members...].  Released arenas are kept in a small cache and
+// handed to the next batch call, so steady-state batches write into pages that are already
+// mapped (a fresh multi-MB malloc is an mmap whose first-touch faults cost more than the
+// decode itself).
+struct ArenaHdr {
+  BufHdr h;         // magic, live members
+  uint64_t cap;     // usable bytes after the header
+  uint64_t pad;
+};
+class ArenaCache {
+ public:
+  uint8_t* take(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      size_t best = blocks_.size();
+      for (size_t i = 0; i < blocks_.size(); ++i) {
+        const uint64_t cap = reinterpret_cast<ArenaHdr*>(blocks_[i])->cap;
+        if (cap >= bytes && cap <= 4 * bytes + (1u << 20) &&
+            (best == blocks_.size() || cap < reinterpret_cast<ArenaHdr*>(blocks_[best])->cap))
+          best = i;
+      }
+      if (best < blocks_.size()) {
+        uint8_t* b = blocks_[best];
+        held_ -= reinterpret_cast<ArenaHdr*>(b)->cap;
+        blocks_.erase(blocks_.begin() + static_cast<std::ptrdiff_t>(best));
+        return b;
+      }
+    }
+    const size_t cap = (bytes + 65535) & ~static_cast<size_t>(65535);
+    auto* b = static_cast<uint8_t*>(std::malloc(sizeof(ArenaHdr) + cap));
+    if (!b) throw std::bad_alloc();
+    reinterpret_cast<ArenaHdr*>(b)->cap = cap;
+    return b;
+  }
+  void give(uint8_t* b) {
+    const uint64_t cap = reinterpret_cast<ArenaHdr*>(b)->cap;
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      if (blocks_.size() < kMaxBlocks && held_ + cap <= kMaxHeld) {
+        blocks_.push_back(b);
+        held_ += cap;
+        return;
+      }
+    }
+    std::free(b);
+  }
+  ~ArenaCache() {
+    for (uint8_t* b : blocks_) std::free(b);
+  }
+
+ private:
+  static constexpr size_t kMaxBlocks = 8;
+  static constexpr uint64_t kMaxHeld = 1ull << 30;
+  std::mutex mu_;
+  std::vector<uint8_t*> blocks_;
+  uint64_t held_ = 0;
+};
+ArenaCache& arena_cache() {
+  static ArenaCache* c = new ArenaCache();  // never destroyed: results may be freed at exit
+  return *c;
+}
+
 void place_block(uint8_t* block, uint64_t magic, uint64_t aux, ctg_upoly_buf* out, size_t n, size_t total) {
   auto* h = reinterpret_cast<BufHdr*>(block);
   h->magic = magic;
@@ -281,15 +347,14 @@ void upoly_alloc(ctg_upoly_buf* out, size_t n, size_t total) {
 }
 
 void UpolyArena::create(size_t bytes, int64_t members) {
-  base = static_cast<uint8_t*>(std::malloc(sizeof(BufHdr) + bytes));
-  if (!base) throw std::bad_alloc();
+  base = arena_cache().take(bytes);
   auto* h = reinterpret_cast<BufHdr*>(base);
   h->magic = kArenaMagic;
   h->aux = static_cast<uint64_t>(members);
 }
 
 void UpolyArena::place(ctg_upoly_buf* out, size_t off, size_t n, size_t total) const {
-  uint8_t* block = base + sizeof(BufHdr) + off;
+  uint8_t* block = base + sizeof(ArenaHdr) + off;
   place_block(block, kMemberMagic, static_cast<uint64_t>(block - base), out, n, total);
 }
 
@@ -328,7 +393,7 @@ void ctg_upoly_free(ctg_upoly_buf* buf) {
       auto* ah = reinterpret_cast<BufHdr*>(base);
       if (__atomic_sub_fetch(&ah->aux, 1, __ATOMIC_ACQ_REL) == 0) {
         ah->magic = 0;
-        std::free(base);
+        arena_cache().give(base);
       }
     }
   }

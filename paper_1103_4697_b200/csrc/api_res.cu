@@ -44,47 +44,136 @@ static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, const std::
 }
 
 // ---------------------------------------------------------------------------
-// Input parsing (sparse map keyed (dy, dx), zero terms dropped -- bipoly.cpp:7-15)
+// Input parsing (sparse terms keyed (dy, dx), zero terms dropped -- bipoly.cpp:7-15).
+// Terms are kept flat and sorted by (dy, dx): batch calls parse and lay out thousands
+// of terms per curve, and a node-per-term map made that pointer chasing the host cost.
 // ---------------------------------------------------------------------------
-using TermMap = std::map<std::pair<int, int>, SBig>;  // (dy, dx) -> coefficient
+struct Terms {
+  std::vector<int32_t> dy, dx;
+  std::vector<int8_t> sign;
+  std::vector<uint32_t> off{0};  // limbs of term i: limbs[off[i] .. off[i+1]), trimmed
+  std::vector<uint32_t> limbs;
+  size_t size() const { return dy.size(); }
+  bool empty() const { return dy.empty(); }
+  int nlimbs(size_t i) const { return static_cast<int>(off[i + 1] - off[i]); }
+  const uint32_t* mag(size_t i) const { return limbs.data() + off[i]; }
+  void push(int y, int x, int sg, const uint32_t* l, int n) {
+    dy.push_back(y);
+    dx.push_back(x);
+    sign.push_back(static_cast<int8_t>(sg));
+    limbs.insert(limbs.end(), l, l + n);
+    off.push_back(static_cast<uint32_t>(limbs.size()));
+  }
+};
 
-static TermMap parse_bipoly(const ctg_bipoly* f, bool swap_xy) {
-  TermMap t;
+static Terms parse_bipoly(const ctg_bipoly* f, bool swap_xy) {
+  Terms t;
   if (!f || f->n_terms == 0) return t;
   if (f->n_terms < 0 || !f->dx || !f->dy || !f->sign || !f->limb_off || (!f->limbs && f->limb_off[f->n_terms] > 0))
     throw ApiError(CTG_INVALID, "bipoly: null pointer or negative term count");
-  for (int i = 0; i < f->n_terms; ++i) {
+  const int nt = f->n_terms;
+  auto key = [&](int i) {
     int dx = f->dx[i], dy = f->dy[i];
-    if (dx < 0 || dy < 0) throw ApiError(CTG_INVALID, "bipoly: negative exponent");
     if (swap_xy) std::swap(dx, dy);
-    const uint32_t b = f->limb_off[i], e = f->limb_off[i + 1];
-    if (e < b) throw ApiError(CTG_INVALID, "bipoly: limb_off not monotone");
-    int s = f->sign[i];
-    if (s < -1 || s > 1) throw ApiError(CTG_INVALID, "bipoly: sign must be -1, 0 or +1");
-    sbig_add_inplace(t[{dy, dx}], s, f->limbs + b, static_cast<int>(e - b));
+    return std::make_pair(dy, dx);
+  };
+  // Unique keys in (dy, dx) order, or in (dx, dy) order (a map keyed x-first, the usual
+  // CSR of the reference's BiPoly): then a counting sort by dy yields (dy, dx) order.
+  bool yx = true, xy = true;
+  int maxdy = 0;
+  for (int i = 0; i < nt; ++i) {
+    if (f->dx[i] < 0 || f->dy[i] < 0) throw ApiError(CTG_INVALID, "bipoly: negative exponent");
+    if (f->limb_off[i + 1] < f->limb_off[i]) throw ApiError(CTG_INVALID, "bipoly: limb_off not monotone");
+    if (f->sign[i] < -1 || f->sign[i] > 1) throw ApiError(CTG_INVALID, "bipoly: sign must be -1, 0 or +1");
+    const auto k = key(i);
+    maxdy = std::max(maxdy, k.first);
+    if (i > 0) {
+      const auto k0 = key(i - 1);
+      if (!(k0 < k)) yx = false;
+      if (!(std::make_pair(k0.second, k0.first) < std::make_pair(k.second, k.first))) xy = false;
+    }
   }
-  for (auto it = t.begin(); it != t.end();) it = (it->second.sign == 0) ? t.erase(it) : std::next(it);
+  t.dy.reserve(nt);
+  t.dx.reserve(nt);
+  t.sign.reserve(nt);
+  t.off.reserve(nt + 1);
+  t.limbs.reserve(f->limb_off[nt] - f->limb_off[0]);
+  auto trimmed = [&](int i, const uint32_t*& l) {
+    l = f->limbs + f->limb_off[i];
+    int n = static_cast<int>(f->limb_off[i + 1] - f->limb_off[i]);
+    while (n > 0 && l[n - 1] == 0) --n;
+    return n;
+  };
+  auto copy_in = [&](int i) {
+    const uint32_t* l;
+    const int n = trimmed(i, l);
+    if (n > 0 && f->sign[i] != 0) t.push(key(i).first, key(i).second, f->sign[i], l, n);
+  };
+  if (yx) {
+    for (int i = 0; i < nt; ++i) copy_in(i);
+    return t;
+  }
+  if (xy && maxdy <= 4 * nt + 64) {
+    std::vector<int> start(maxdy + 2, 0), order(nt);
+    for (int i = 0; i < nt; ++i) ++start[key(i).first + 1];
+    for (int d = 0; d <= maxdy; ++d) start[d + 1] += start[d];
+    for (int i = 0; i < nt; ++i) order[start[key(i).first]++] = i;
+    for (int i : order) copy_in(i);
+    return t;
+  }
+  // General input: stable sort by key, sum the terms of equal keys.
+  std::vector<int> order(nt);
+  for (int i = 0; i < nt; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+  for (int a = 0; a < nt;) {
+    int b = a + 1;
+    while (b < nt && key(order[b]) == key(order[a])) ++b;
+    SBig acc;
+    for (int r = a; r < b; ++r) {
+      const uint32_t* l;
+      const int n = trimmed(order[r], l);
+      sbig_add_inplace(acc, f->sign[order[r]], l, n);
+    }
+    if (acc.sign != 0) {
+      const auto k = key(order[a]);
+      t.push(k.first, k.second, acc.sign, acc.mag.data(), static_cast<int>(acc.mag.size()));
+    }
+    a = b;
+  }
   return t;
 }
 
-static int deg_y(const TermMap& t) { return t.empty() ? -1 : t.rbegin()->first.first; }
+static int deg_y(const Terms& t) { return t.empty() ? -1 : t.dy.back(); }
 
-static bool is_y_derivative(const TermMap& p, const TermMap& q) {
-  size_t cnt = 0;
-  for (const auto& [e, c] : p) {
-    if (e.first == 0) continue;
-    ++cnt;
-    auto it = q.find({e.first - 1, e.second});
-    if (it == q.end() || it->second.sign != c.sign) return false;
-    Big want = big_mul_small(c.mag.data(), static_cast<int>(c.mag.size()), static_cast<uint32_t>(e.first));
-    if (big_cmp(want, it->second.mag) != 0) return false;
+// a * s == b for magnitudes (no allocation).
+static bool mul_small_equals(const uint32_t* a, int na, uint32_t s, const uint32_t* b, int nb) {
+  uint64_t carry = 0;
+  int i = 0;
+  for (; i < na; ++i) {
+    const uint64_t v = static_cast<uint64_t>(a[i]) * s + carry;
+    if (i >= nb || b[i] != static_cast<uint32_t>(v)) return false;
+    carry = v >> 32;
   }
-  return cnt == q.size();
+  for (; carry; ++i, carry >>= 32)
+    if (i >= nb || b[i] != static_cast<uint32_t>(carry)) return false;
+  return i == nb;
+}
+
+// q == dp/dy term by term: the terms of p with dy >= 1 map in order onto q's terms.
+static bool is_y_derivative(const Terms& p, const Terms& q) {
+  size_t k = 0;
+  for (size_t i = 0; i < p.size(); ++i) {
+    if (p.dy[i] == 0) continue;
+    if (k >= q.size() || q.dy[k] != p.dy[i] - 1 || q.dx[k] != p.dx[i] || q.sign[k] != p.sign[i]) return false;
+    if (!mul_small_equals(p.mag(i), p.nlimbs(i), static_cast<uint32_t>(p.dy[i]), q.mag(k), q.nlimbs(k))) return false;
+    ++k;
+  }
+  return k == q.size();
 }
 
 // One parsed problem, normalised so that deg_y p >= deg_y q.
 struct Problem {
-  TermMap p, q;
+  Terms p, q;
   int n = -1, m = -1, deriv = 0, negate = 0;
   bool trivial = false;  // one input zero -> zero polynomial
   int64_t degb = 0;      // degree bound of the result
@@ -112,28 +201,31 @@ static Problem parse_problem(const ctg_bipoly* pin, const ctg_bipoly* qin, int32
   pr.deriv = (pr.m == pr.n - 1 && pr.n >= 1 && is_y_derivative(pr.p, pr.q)) ? 1 : 0;
   // Degree bound of the result (min of the Sylvester row bound and Bezout).
   int Xp = 0, Xq = 0, tp = 0, tq = 0;
-  for (const auto& [e, c] : pr.p) {
-    Xp = std::max(Xp, e.second);
-    tp = std::max(tp, e.first + e.second);
+  for (size_t i = 0; i < pr.p.size(); ++i) {
+    Xp = std::max(Xp, pr.p.dx[i]);
+    tp = std::max(tp, pr.p.dy[i] + pr.p.dx[i]);
   }
-  for (const auto& [e, c] : pr.q) {
-    Xq = std::max(Xq, e.second);
-    tq = std::max(tq, e.first + e.second);
+  for (size_t i = 0; i < pr.q.size(); ++i) {
+    Xq = std::max(Xq, pr.q.dx[i]);
+    tq = std::max(tq, pr.q.dy[i] + pr.q.dx[i]);
   }
   pr.degb = std::min(static_cast<int64_t>(pr.m) * Xp + static_cast<int64_t>(pr.n) * Xq,
                      static_cast<int64_t>(tp) * tq);
   // Hadamard bound over |x| = 1.
-  auto norm_bits = [](const TermMap& t, int deg) {
-    std::vector<std::vector<double>> per(deg + 1);
-    for (const auto& [e, c] : t) per[e.first].push_back(log2_upper(c.mag.data(), static_cast<int>(c.mag.size())));
-    std::vector<double> sq;
-    for (auto& v : per) {
-      double l1 = log2_sum_upper(v);
+  auto norm_bits = [](const Terms& t) {
+    // Terms are sorted by dy: each y-degree is one contiguous run.
+    std::vector<double> run, sq;
+    for (size_t a = 0; a < t.size();) {
+      size_t b = a;
+      run.clear();
+      for (; b < t.size() && t.dy[b] == t.dy[a]; ++b) run.push_back(log2_upper(t.mag(b), t.nlimbs(b)));
+      const double l1 = log2_sum_upper(run);
       if (std::isfinite(l1)) sq.push_back(2 * l1);
+      a = b;
     }
     return log2_sum_upper(sq);
   };
-  const double bp = norm_bits(pr.p, pr.n), bq = norm_bits(pr.q, pr.m);
+  const double bp = norm_bits(pr.p), bq = norm_bits(pr.q);
   pr.bound_bits = 0.5 * pr.m * (std::isfinite(bp) ? bp : 0) + 0.5 * pr.n * (std::isfinite(bq) ? bq : 0);
   if (pr.bound_bits < 0) pr.bound_bits = 0;
   return pr;
@@ -251,12 +343,17 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
     bound = std::max(bound, pr.bound_bits);
   }
   const int n = pl->n, m = pl->m;
+  using tclk = std::chrono::steady_clock;
+  const auto tb0 = tclk::now();
   // Union slot layout: y-degree j of p owns x-degrees 0..X_j (max over the batch).
   std::vector<int32_t> Xp(n + 1, -1), Xq(m + 1, -1);
   for (int i : idx) {
-    for (const auto& [e, c] : probs[i].p) Xp[e.first] = std::max(Xp[e.first], e.second);
-    if (!pl->deriv)
-      for (const auto& [e, c] : probs[i].q) Xq[e.first] = std::max(Xq[e.first], e.second);
+    const Terms& tp = probs[i].p;
+    for (size_t t = 0; t < tp.size(); ++t) Xp[tp.dy[t]] = std::max(Xp[tp.dy[t]], tp.dx[t]);
+    if (!pl->deriv) {
+      const Terms& tq = probs[i].q;
+      for (size_t t = 0; t < tq.size(); ++t) Xq[tq.dy[t]] = std::max(Xq[tq.dy[t]], tq.dx[t]);
+    }
   }
   std::vector<int32_t> offp(n + 1), lenp(n + 1), offq(m + 1, 0), lenq(m + 1, 0);
   int S = 0;
@@ -274,9 +371,12 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   pl->S = S;
   int L = 1;
   for (int i : idx) {
-    for (const auto& [e, c] : probs[i].p) L = std::max<int>(L, static_cast<int>(c.mag.size()));
-    if (!pl->deriv)
-      for (const auto& [e, c] : probs[i].q) L = std::max<int>(L, static_cast<int>(c.mag.size()));
+    const Terms& tp = probs[i].p;
+    for (size_t t = 0; t < tp.size(); ++t) L = std::max(L, tp.nlimbs(t));
+    if (!pl->deriv) {
+      const Terms& tq = probs[i].q;
+      for (size_t t = 0; t < tq.size(); ++t) L = std::max(L, tq.nlimbs(t));
+    }
   }
   pl->L = L;
   pl->h_limbs.assign(static_cast<size_t>(pl->B) * L * S, 0u);
@@ -284,14 +384,18 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   parallel_for(pl->B, [&](int b) {
     uint32_t* lb = pl->h_limbs.data() + static_cast<size_t>(b) * L * S;
     int8_t* sb = pl->h_sign.data() + static_cast<size_t>(b) * S;
-    auto put = [&](int s, const SBig& c) {
-      sb[s] = static_cast<int8_t>(c.sign);
-      for (size_t l = 0; l < c.mag.size(); ++l) lb[l * S + s] = c.mag[l];
+    auto put = [&](const Terms& t, const std::vector<int32_t>& off) {
+      for (size_t i = 0; i < t.size(); ++i) {
+        const int s = off[t.dy[i]] + t.dx[i];
+        sb[s] = t.sign[i];
+        const uint32_t* m = t.mag(i);
+        for (int l = 0; l < t.nlimbs(i); ++l) lb[static_cast<size_t>(l) * S + s] = m[l];
+      }
     };
-    for (const auto& [e, c] : probs[idx[b]].p) put(offp[e.first] + e.second, c);
-    if (!pl->deriv)
-      for (const auto& [e, c] : probs[idx[b]].q) put(offq[e.first] + e.second, c);
+    put(probs[idx[b]].p, offp);
+    if (!pl->deriv) put(probs[idx[b]].q, offq);
   });
+  const auto tb1 = tclk::now();
   pl->dir.clear();
   for (auto* v : {&offp, &lenp, &offq, &lenq}) pl->dir.insert(pl->dir.end(), v->begin(), v->end());
   pl->nrows = pl->deriv ? n + 1 : n + m + 2;
@@ -305,9 +409,17 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
   pl->bound_bits = bound;
   const double need = bound + 1 + 36;
+  const auto tb2 = tclk::now();
   std::vector<uint32_t> primes = select_primes(pl->N, need, kResPrimeMax);  // mmul3 window (modarith.cuh)
   pl->P = static_cast<int>(primes.size());
+  const auto tb3 = tclk::now();
   pl->tabs = get_tables(pl->device, pl->N, primes);
+  const auto tb4 = tclk::now();
+  static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
+  auto us = [](tclk::time_point a, tclk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  if (trace)
+    std::fprintf(stderr, "[ctg] plan_build B=%d: layout+fill %.1f us, dims %.1f us, primes %.1f us, tables %.1f us\n", pl->B,
+                 us(tb0, tb1), us(tb1, tb2), us(tb2, tb3), us(tb3, tb4));
   return pl.release();
 }
 

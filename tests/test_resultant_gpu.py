@@ -83,3 +83,44 @@ def test_batch_plan_same_shape_curves():
         pairs.append((f, curves.derive_y(f)))
     got = P.resultant_batch(pairs)
     assert got == [dec_upoly(r["result"]) for r in small]
+
+
+def _term_orders(f, rng):
+    """The same polynomial as raw CSR operands in several term orders and encodings."""
+    items = [(k[0], k[1], v) for k, v in f.items() if v]
+    yx = sorted(items, key=lambda t: (t[1], t[0]))
+    shuffled = items[:]
+    rng.shuffle(shuffled)
+    # every coefficient split into two duplicate-key terms, plus explicit zero terms
+    split = []
+    for dx, dy, v in shuffled:
+        a = rng.randrange(-abs(v) - 5, abs(v) + 5)
+        split += [(dx, dy, a), (dx, dy, v - a), (dx + 1, dy, 0)]
+    # a term cancelled by a duplicate: (dx, dy) present with total zero
+    split += [(0, 0, 7), (0, 0, -7)] if (0, 0) not in f else []
+    return {"xy": P.HostBipoly.from_terms(sorted(items)), "yx": P.HostBipoly.from_terms(yx),
+            "yx_padded": P.HostBipoly.from_terms(yx, pad_limbs=2),
+            "shuffled": P.HostBipoly.from_terms(shuffled), "split_dups_zeros": P.HostBipoly.from_terms(split)}
+
+
+def test_input_term_order_and_duplicates():
+    """ctg_bipoly with unsorted, duplicated, zero and zero-padded terms: the parse sums
+    equal keys and drops zeros (bipoly.cpp map insertion) -- same result as the canonical form."""
+    import random
+    rng = random.Random(5)
+    rows = [r for r in load("resultant_random.jsonl") if r["op"] == "resultant_y" and "error" not in r][:12]
+    rows += [r for r in load("resultant_random.jsonl") if r["op"] == "resultant_x" and "error" not in r][:6]
+    assert rows
+    for r in rows:
+        f, g = (dec_bipoly(a) for a in r["args"])
+        var = "x" if r["op"] == "resultant_x" else "y"
+        want = dec_upoly(r["result"])
+        fo, go = _term_orders(f, rng), _term_orders(g, rng)
+        for kind in fo:
+            assert P.resultant_host(fo[kind], go[kind], var) == want, (kind, r)
+    # the f_y shape (derivative detection) through the permuted encodings
+    f = curves.make("dense", 8, 40, 3)
+    want = P.resultant(f, curves.derive_y(f))
+    fo, go = _term_orders(f, rng), _term_orders(curves.derive_y(f), rng)
+    for kind in fo:
+        assert P.resultant_host(fo[kind], go[kind]) == want, kind
