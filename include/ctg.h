@@ -11,6 +11,9 @@
  *                                   upoly.hpp:92, elim.cpp:80-93
  *   ctg_square_free_part  replaces  curvetop::square_free_part(p)
  *                                   elim.hpp:45, elim.cpp:204-210
+ *   ctg_gcd_bivariate     replaces  curvetop::gcd_bivariate(f, g) when the gcd of the
+ *                                   primitive parts is trivial (the square-free-curve case of
+ *                                   lift.cpp:85 and pipeline.cpp:321); elim.hpp:42, elim.cpp:178-202
  *
  * The C++ TU paper_1103_4697_b200/cxx/curvetop_elim_gpu.cpp defines those
  * curvetop:: symbols with the reference's exact signatures on top of this ABI
@@ -83,6 +86,16 @@ typedef struct {
   ctg_upoly_buf* factors; /* primitive, positive leading coefficient, square-free */
 } ctg_sqf_buf;
 
+/* Library-allocated bivariate result, terms sorted by (dx, dy), no zero terms. */
+typedef struct {
+  int32_t n_terms;
+  int32_t* dx;
+  int32_t* dy;
+  int8_t* sign;
+  uint32_t* limb_off; /* n_terms + 1 */
+  uint32_t* limbs;
+} ctg_bipoly_buf;
+
 typedef struct {
   int32_t device;   /* CUDA device ordinal; -1 = current device */
   int32_t verify;   /* 1 (default) = run the on-device self-checks; 0 = skip the optional ones */
@@ -103,8 +116,17 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
 ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_buf* out,
                               const ctg_opts* opts);
 ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ctg_opts* opts);
+/* gcd_bivariate (elim.cpp:178-202): y-contents by GPU univariate gcds, then a GPU probe of
+ * gcd(f(a, y), g(a, y)) mod p at several (p, a) with lc_y(f)(a) or lc_y(g)(a) nonzero mod p.
+ * A degree-0 image certifies that the primitive parts are coprime; the result is then
+ * gcd_univariate(content_y f, content_y g).  Returns CTG_UNSUPPORTED (out untouched) when
+ * every probe has positive degree: the primitive parts share a factor, and the caller runs
+ * the reference's PRS (the drop-in TU does). */
+ctg_status ctg_gcd_bivariate(const ctg_bipoly* f, const ctg_bipoly* g, ctg_bipoly_buf* out,
+                             const ctg_opts* opts);
 
 void ctg_upoly_free(ctg_upoly_buf* buf);
+void ctg_bipoly_free(ctg_bipoly_buf* buf);
 void ctg_upoly_free_batch(ctg_upoly_buf* bufs, int32_t n); /* = ctg_upoly_free on each */
 void ctg_sqf_free(ctg_sqf_buf* buf);
 const char* ctg_last_error(void); /* thread-local message of the last failing call */

@@ -8,6 +8,9 @@ algorithms for the path this repo accelerates:
   * ``gcd_univariate``   -- elim.cpp:80-93 (primitive PRS)
   * ``square_free_part`` -- elim.cpp:204-210
   * ``reconstruct``      -- elim.cpp:74-78
+  * ``gcd_bivariate``    -- elim.cpp:178-202 (PRS in y over Z[x] after content_y, bipoly.cpp:192-201)
+  * ``curve_q``          -- CurveContext::resultant_q / q_factorization, lift.cpp:76-101
+                            (h = gcd_bivariate(f_x, f_y), Q = res(f_x/h, f_y/h), Yun(Q))
   * the Z[x] substrate they use -- upoly.cpp:30-120, bipoly.cpp:103-190
 
 Parity status: PINNED.  ``tests/test_oracle.py`` checks every function here
@@ -413,3 +416,108 @@ def reconstruct(unit, factors):
     for poly, mult in factors:
         r = u_mul(r, u_pow(poly, mult))
     return r
+
+
+# ----------------------------------------------------------------------------
+# Bivariate gcd and the Teissier resultant
+# ----------------------------------------------------------------------------
+
+def from_y_coeffs(rows):
+    """bipoly.cpp from_y_coeffs: {(x, y): c}."""
+    return b_clean({(ex, ey): c for ey, r in enumerate(rows) for ex, c in enumerate(r)})
+
+
+def content_y(f):
+    """bipoly.cpp:192-201: gcd_univariate chain over the y-coefficients (stops at 1), then
+    primitive_positive(g) * content(g) -- the chain's gcd with positive leading coefficient."""
+    if not f:
+        raise PreconditionError("content_y: zero polynomial")
+    g = []
+    for fi in y_coeffs(f):
+        if not fi:
+            continue
+        g = fi if not g else gcd_univariate(g, fi)
+        if g == [1]:
+            break
+    return u_scale(primitive_positive(g), content(g))
+
+
+def divexact_univariate_x(f, d):
+    """bipoly.cpp:236-244."""
+    return from_y_coeffs([r if not r else divexact(r, d) for r in y_coeffs(f)])
+
+
+def gcd_bivariate(f, g):
+    """elim.cpp:178-202."""
+    f, g = b_clean(f), b_clean(g)
+    if not f and not g:
+        raise PreconditionError("gcd_bivariate: both inputs zero")
+    if not f:
+        return g
+    if not g:
+        return f
+    cf, cg = content_y(f), content_y(g)
+    a = y_coeffs(divexact_univariate_x(f, cf))
+    b = y_coeffs(divexact_univariate_x(g, cg))
+    if _yv_degree(a) < _yv_degree(b):
+        a, b = b, a
+    while _yv_degree(b) >= 0:
+        r = _yv_prem(a, b)
+        c = _yv_content(r)
+        a = b
+        b = [] if not c else _yv_divexact_scalar(r, c)
+    ca = _yv_content(a)
+    pp = _yv_divexact_scalar(a, ca)
+    res = b_mul(from_y_coeffs(pp), {(i, 0): c for i, c in enumerate(gcd_univariate(cf, cg)) if c})
+    lead = y_coeffs(res)[degree_y(res)]
+    if lead[-1] < 0:
+        res = {k: -v for k, v in res.items()}
+    return res
+
+
+def b_mul(f, g):
+    out = {}
+    for (a, b), c in f.items():
+        for (d, e), v in g.items():
+            out[(a + d, b + e)] = out.get((a + d, b + e), 0) + c * v
+    return b_clean(out)
+
+
+def divexact_bivariate(p, d):
+    """bipoly.cpp:246-266: long division in y over Z[x], every quotient exact."""
+    if not d:
+        raise Error("divexact: zero divisor")
+    if not p:
+        return p
+    if degree_y(d) == 0:
+        return divexact_univariate_x(p, y_coeffs(d)[0])
+    rem = y_coeffs(p)
+    dc = y_coeffs(d)
+    dn, dl = len(dc) - 1, dc[-1]
+    if len(rem) - 1 < dn:
+        raise Error("divexact: inexact division (degree)")
+    quo = [[] for _ in range(len(rem) - dn)]
+    for i in range(len(rem) - 1, dn - 1, -1):
+        if not rem[i]:
+            continue
+        q = divexact(rem[i], dl)
+        quo[i - dn] = q
+        for j in range(dn + 1):
+            rem[i - dn + j] = u_sub(rem[i - dn + j], u_mul(q, dc[j]))
+    if any(r for r in rem):
+        raise Error("divexact: inexact division")
+    return from_y_coeffs(quo)
+
+
+def curve_q(f):
+    """lift.cpp:76-101: (h, Q, Yun(Q)) with h = gcd_bivariate(f_x, f_y), Q = res(f_x*, f_y*)."""
+    fx, fy = derive_x(f), derive_y(f)
+    if not fx:
+        q = [1]
+        h = {}
+    else:
+        h = gcd_bivariate(fx, fy)
+        if degree_x(h) > 0 or degree_y(h) > 0:
+            fx, fy = divexact_bivariate(fx, h), divexact_bivariate(fy, h)
+        q = resultant(fx, fy, "y")
+    return h, q, yun_squarefree(q)

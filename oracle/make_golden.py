@@ -16,6 +16,9 @@ Fixture files (JSON lines):
   univariate_random.jsonl yun / gcd / square_free_part on structured random inputs
   configs_small.jsonl   res(f, f_y) (+ Yun) on the BASELINE configs that finish in seconds
   configs_big.jsonl     sha256 digests of res(f, f_y) at the full BASELINE sizes
+  bivariate_gcd.jsonl   gcd_bivariate (elim.cpp:178-202) on coprime / content-sharing / factor-sharing pairs
+  teissier.jsonl        CurveContext::resultant_q + q_factorization (lift.cpp:76-101): h = gcd(f_x, f_y),
+                        Q = res(f_x / h, f_y / h), Yun(Q) -- SURVEY.md §8(f) rank 1
 """
 
 from __future__ import annotations
@@ -292,6 +295,91 @@ def configs_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
     return rows
 
 
+def bivariate_gcd() -> list[dict]:
+    rng = random.Random(178_202)
+    reqs, meta = [], []
+    for t in range(90):
+        kind = t % 9
+        if kind == 0:     # generic coprime pair
+            f = rand_bipoly(rng, rng.randint(0, 4), rng.randint(1, 5), rng.randint(2, 40))
+            g = rand_bipoly(rng, rng.randint(0, 4), rng.randint(1, 5), rng.randint(2, 40))
+        elif kind == 1:   # x-contents sharing a factor, coprime primitive parts
+            c = rand_bipoly(rng, rng.randint(1, 3), 0, 6)
+            f = curves._bmul(rand_bipoly(rng, 2, rng.randint(1, 4), 10), curves._bmul(c, rand_bipoly(rng, 1, 0, 5)))
+            g = curves._bmul(rand_bipoly(rng, 2, rng.randint(1, 4), 10), c)
+        elif kind == 2:   # integer contents only (gcd_univariate drops them)
+            k1, k2 = rng.randint(2, 30), rng.randint(2, 30)
+            f = {e: k1 * v for e, v in rand_bipoly(rng, 2, rng.randint(1, 3), 8).items()}
+            g = {e: k2 * v for e, v in rand_bipoly(rng, 2, rng.randint(1, 3), 8).items()}
+        elif kind == 3:   # one operand of degree 0 in y
+            f = rand_bipoly(rng, rng.randint(0, 4), rng.randint(1, 4), 12)
+            g = rand_bipoly(rng, rng.randint(1, 4), 0, 12)
+        elif kind == 4:   # single y-coefficient operands (content = the coefficient itself)
+            f = {(ex, 3): v for (ex, _), v in rand_bipoly(rng, 3, 0, 10).items()}
+            g = rand_bipoly(rng, 2, 2, 10)
+        elif kind == 5:   # common bivariate factor (primitive parts NOT coprime)
+            c = rand_bipoly(rng, rng.randint(0, 2), rng.randint(1, 2), 5)
+            f = curves._bmul(rand_bipoly(rng, 2, rng.randint(1, 3), 6), c)
+            g = curves._bmul(rand_bipoly(rng, 2, rng.randint(1, 3), 6), c)
+        elif kind == 6:   # (f, f_y) of random curves, lc_y depending on x
+            f = rand_bipoly(rng, rng.randint(1, 5), rng.randint(2, 6), 16, 0.7)
+            g = curves.derive_y(f)
+        elif kind == 7:   # (f_x, f_y) of dense curves
+            f0 = curves.make("dense", rng.randint(3, 7), 10, rng.randint(1, 99))
+            f, g = curves.derive_x(f0), curves.derive_y(f0)
+        else:             # a zero operand / negative leading coefficients
+            f = {e: -v for e, v in rand_bipoly(rng, 2, 2, 10).items()}
+            g = {} if t % 2 else {e: -abs(v) for e, v in rand_bipoly(rng, 1, 1, 10).items()}
+        if not f and not g:
+            continue
+        reqs.append(("gcd_bivariate", [f, g]))
+        meta.append({"kind": kind})
+    rows = emit(reqs, meta)
+    reqs = [("gcd_bivariate", [{}, {}])]
+    rows += emit(reqs, [{"kind": "both_zero"}])
+    return rows
+
+
+def teissier_curves() -> list:
+    out = [("dense", 6, 10, s) for s in (1, 2, 3)] + [("dense", 8, 10, 1), ("dense", 10, 10, 1),
+                                                       ("sheared", 2, 0, 1), ("dense", 5, 300, 1)]
+    return out
+
+
+def special_curves() -> dict:
+    s = lambda *t: bp(*t)
+    return {
+        "circle": s((2, 0, 1), (0, 2, 1), (0, 0, -1)),
+        "cusp": s((0, 2, 1), (3, 0, -1)),
+        "nodal": s((0, 2, 1), (3, 0, -1), (2, 0, -1)),
+        "hyperbola": s((1, 1, 1), (0, 0, -1)),
+        # f = s^3 - 2 s + 1 with s = x + y: f_x = f_y, h = f_x, Q = res(1, 1) = 1
+        "diagonal": s((3, 0, 1), (2, 1, 3), (1, 2, 3), (0, 3, 1), (1, 0, -2), (0, 1, -2), (0, 0, 1)),
+        "lc_x": s((1, 2, 1), (0, 2, 3), (2, 1, -1), (0, 0, 5), (3, 0, 1)),
+    }
+
+
+def teissier() -> list[dict]:
+    reqs, meta = [], []
+    for c in teissier_curves():
+        reqs.append(("curve_q", [curves.make(*c)]))
+        meta.append({"curve": list(c)})
+    for name, f in special_curves().items():
+        reqs.append(("curve_q", [f]))
+        meta.append({"name": name, "f": enc_bipoly(f)})
+    res = run_batch(reqs)
+    rows = []
+    for m, r in zip(meta, res):
+        row = dict(m)
+        if "error" in r:
+            row["error"] = r["error"]
+        else:
+            row["result"], row["h"], row["qsf"] = r["result"], r["h"], r["qsf"]
+        row["ref_seconds"] = r["seconds"]
+        rows.append(row)
+    return rows
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -304,6 +392,8 @@ def main() -> None:
     write("resultant_random.jsonl", resultant_random())
     write("univariate_random.jsonl", univariate_random())
     write("configs_small.jsonl", configs_small())
+    write("bivariate_gcd.jsonl", bivariate_gcd())
+    write("teissier.jsonl", teissier())
     if args.big:
         write("configs_big.jsonl", configs_big(args.cache, args.cached_only))
 

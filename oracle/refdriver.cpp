@@ -14,7 +14,7 @@
 //                                          (+ yun_squarefree(R) when "yun" is given)
 //
 // Request format (text):
-//   OP <resultant_y|resultant_x|resultant_fy|yun|gcd|sqfp>
+//   OP <resultant_y|resultant_x|resultant_fy|yun|gcd|sqfp|gcd_bivariate|curve_q>
 //   B <nterms>  followed by nterms lines "dx dy hexcoeff"        (bivariate operand)
 //   U <ncoeffs> followed by ncoeffs lines "hexcoeff" low->high   (univariate operand)
 //   END
@@ -28,6 +28,7 @@
 
 #include "curvetop/bipoly.hpp"
 #include "curvetop/elim.hpp"
+#include "curvetop/lift.hpp"
 #include "oracles.hpp"
 
 using namespace curvetop;
@@ -189,6 +190,15 @@ int cmd_batch() {
         body = std::string("\"result\":") + json_upoly(gcd_univariate(args.at(0).u, args.at(1).u));
       } else if (op == "sqfp") {
         body = std::string("\"result\":") + json_upoly(square_free_part(args.at(0).u));
+      } else if (op == "gcd_bivariate") {
+        body = std::string("\"result\":") + json_bipoly(gcd_bivariate(args.at(0).b, args.at(1).b));
+      } else if (op == "curve_q") {  // CurveContext::resultant_q / q_factorization (lift.cpp:76-101)
+        const BPoly& f = args.at(0).b;
+        BPoly h = gcd_bivariate(derive(f, Var::X, 1), derive(f, Var::Y, 1));
+        CurveContext ctx(f);
+        const UPoly& q = ctx.resultant_q();
+        body = std::string("\"result\":") + json_upoly(q) + ",\"h\":" + json_bipoly(h) +
+               ",\"qsf\":" + json_sqf(ctx.q_factorization());
       } else {
         body = "\"error\":\"unknown op\"";
       }

@@ -30,7 +30,7 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libctg.so")
+LIB_PATH = os.environ.get("CTG_LIBRARY") or os.path.join(_PKG, "libctg.so")  # CTG_LIBRARY: A/B experiments
 
 
 class Error(RuntimeError):
@@ -43,6 +43,10 @@ class PreconditionError(Error):
 
 class CudaError(Error):
     """A CUDA failure or no device: libctg has no CPU fallback."""
+
+
+class UnsupportedError(Error):
+    """CTG_UNSUPPORTED: outside the library's GPU path (message says which limit)."""
 
 
 CTG_OK, CTG_PRECONDITION, CTG_INVALID, CTG_UNSUPPORTED, CTG_INTERNAL, CTG_CUDA = range(6)
@@ -63,6 +67,11 @@ class _Upoly(C.Structure):
 
 class _UpolyBuf(C.Structure):
     _fields_ = [("n_coeffs", C.c_int32), ("sign", _i8p), ("limb_off", _u32p), ("limbs", _u32p)]
+
+
+class _BipolyBuf(C.Structure):
+    _fields_ = [("n_terms", C.c_int32), ("dx", _i32p), ("dy", _i32p), ("sign", _i8p), ("limb_off", _u32p),
+                ("limbs", _u32p)]
 
 
 class _SqfBuf(C.Structure):
@@ -102,7 +111,7 @@ EXPORTS = (
     "ctg_plan_create", "ctg_plan_get_info", "ctg_plan_upload", "ctg_plan_residues", "ctg_plan_crt",
     "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy", "ctg_plan_stage",
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
-    "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch",
+    "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch", "ctg_gcd_bivariate", "ctg_bipoly_free",
 )
 
 _lib = None
@@ -130,6 +139,9 @@ def lib():
         L.ctg_upoly_free.argtypes = [C.POINTER(_UpolyBuf)]
         L.ctg_upoly_free_batch.argtypes = [C.POINTER(_UpolyBuf), C.c_int32]
         L.ctg_sqf_free.argtypes = [C.POINTER(_SqfBuf)]
+        L.ctg_gcd_bivariate.argtypes = [C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.POINTER(_BipolyBuf),
+                                        C.POINTER(_Opts)]
+        L.ctg_bipoly_free.argtypes = [C.POINTER(_BipolyBuf)]
         L.ctg_last_error.restype = C.c_char_p
         L.ctg_last_call_stats.argtypes = [C.POINTER(CallStats)]
         L.ctg_plan_create.argtypes = [C.POINTER(_Bipoly), C.POINTER(_Bipoly), C.c_int32, C.POINTER(_Opts),
@@ -165,6 +177,8 @@ def _raise(status: int, what: str):
         raise PreconditionError(msg)
     if status == CTG_CUDA:
         raise CudaError(msg)
+    if status == CTG_UNSUPPORTED:
+        raise UnsupportedError(msg)
     raise Error(msg)
 
 
@@ -359,6 +373,30 @@ def resultant(p: dict, q: dict, var: str = "y", device=None) -> list:
     both of degree 0 in var -> [1]; degree-0 operand q -> q^deg(p).
     """
     return resultant_host(HostBipoly(p), HostBipoly(q), var, device)
+
+
+def gcd_bivariate(f: dict, g: dict, device=None) -> dict:
+    """curvetop::gcd_bivariate (elim.hpp:42, elim.cpp:178-202) when the primitive parts are
+    coprime (square-free curves: lift.cpp:85, pipeline.cpp:321); raises UnsupportedError
+    when they share a factor (the drop-in C++ TU then runs the reference's PRS)."""
+    hf, hg = HostBipoly(f), HostBipoly(g)
+    out = _BipolyBuf()
+    o = _opts(device)
+    _check(lib().ctg_gcd_bivariate(C.byref(hf.struct), C.byref(hg.struct), C.byref(out), C.byref(o)),
+           "gcd_bivariate")
+    try:
+        n = out.n_terms
+        res = {}
+        if n:
+            off = np.ctypeslib.as_array(out.limb_off, shape=(n + 1,))
+            total = int(off[n])
+            raw = bytes(np.ctypeslib.as_array(out.limbs, shape=(max(total, 1),)).tobytes()) if total else b""
+            for t in range(n):
+                v = int.from_bytes(raw[int(off[t]) * 4:int(off[t + 1]) * 4], "little")
+                res[(int(out.dx[t]), int(out.dy[t]))] = -v if out.sign[t] < 0 else v
+        return res
+    finally:
+        lib().ctg_bipoly_free(C.byref(out))
 
 
 def yun_squarefree(p: list, device=None):

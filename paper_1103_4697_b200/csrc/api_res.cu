@@ -402,7 +402,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   pl->maxlen = 1;
   for (int v : lenp) pl->maxlen = std::max(pl->maxlen, v);
   for (int v : lenq) pl->maxlen = std::max(pl->maxlen, v);
-  pl->fast_ok = (m == n - 1) && n >= 2 && n <= kFastMaxDeg;
+  pl->fast_ok = (m == n - 1 || m == n) && n >= 2 && n <= kFastMaxDeg;
 
   if (degb + 1 > kMaxNtt) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 16383");
   pl->D = static_cast<uint32_t>(degb + 1);

@@ -475,6 +475,164 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
   throw ApiError(CTG_INTERNAL, "gcd: could not find enough lucky primes");
 }
 
+
+// ---------------------------------------------------------------------------
+// gcd_bivariate (elim.cpp:178-202) for coprime primitive parts.
+// ---------------------------------------------------------------------------
+using YPoly = std::vector<ZPoly>;  // y-degree -> coefficient in Z[x] (trimmed), bipoly.hpp y_coeffs
+
+YPoly parse_bipoly_y(const ctg_bipoly* f) {
+  YPoly out;
+  if (!f || f->n_terms == 0) return out;
+  if (f->n_terms < 0 || !f->dx || !f->dy || !f->sign || !f->limb_off || (!f->limbs && f->limb_off[f->n_terms] > 0))
+    throw ApiError(CTG_INVALID, "bipoly: null pointer or negative term count");
+  for (int i = 0; i < f->n_terms; ++i) {
+    const int dx = f->dx[i], dy = f->dy[i];
+    if (dx < 0 || dy < 0) throw ApiError(CTG_INVALID, "bipoly: negative exponent");
+    const uint32_t b = f->limb_off[i], e = f->limb_off[i + 1];
+    if (e < b) throw ApiError(CTG_INVALID, "bipoly: limb_off not monotone");
+    const int sg = f->sign[i];
+    if (sg < -1 || sg > 1) throw ApiError(CTG_INVALID, "bipoly: sign must be -1, 0 or +1");
+    if (static_cast<int>(out.size()) <= dy) out.resize(dy + 1);
+    if (static_cast<int>(out[dy].size()) <= dx) out[dy].resize(dx + 1);
+    sbig_add_inplace(out[dy][dx], sg, f->limbs + b, static_cast<int>(e - b));
+  }
+  for (auto& c : out)
+    while (!c.empty() && c.back().sign == 0) c.pop_back();
+  while (!out.empty() && out.back().empty()) out.pop_back();
+  return out;
+}
+
+// curvetop::gcd_univariate semantics (elim.cpp:80-93) on the GPU path.
+ZPoly gcd_uni(const ZPoly& a, const ZPoly& b, int dev, cudaStream_t st, Launches& L) {
+  if (a.empty() && b.empty()) throw ApiError(CTG_PRECONDITION, "gcd_univariate: both inputs zero");
+  if (a.empty() || b.empty()) return zprimitive_positive(a.empty() ? b : a);
+  ZPoly A = zprimitive_positive(a), B = zprimitive_positive(b);
+  if (zdeg(A) == 0 || zdeg(B) == 0) return ZPoly{SBig{1, Big{1u}}};
+  return gcd_modular(A, B, dev, st, L);
+}
+
+bool zis_one(const ZPoly& g) { return g.size() == 1 && g[0].sign == 1 && big_is_one(g[0].mag); }
+
+// content_y (bipoly.cpp:192-201): gcd chain over the nonzero y-coefficients (stopping at 1),
+// returned with positive leading coefficient and its full integer content.
+ZPoly content_y(const YPoly& f, int dev, cudaStream_t st, Launches& L) {
+  ZPoly g;
+  for (const auto& fi : f) {
+    if (fi.empty()) continue;
+    g = g.empty() ? fi : gcd_uni(g, fi, dev, st, L);
+    if (zis_one(g)) break;
+  }
+  if (!g.empty() && g.back().sign < 0)
+    for (auto& c : g) c.sign = -c.sign;
+  return g;
+}
+
+// deg_y gcd(f/cf, g/cg) == 0, certified by one (p, a) image of degree 0 whose formal leading
+// y-coefficient survives: the image of the primitive gcd H then has degree deg_y H.
+bool primitive_parts_coprime(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, Launches& L) {
+  const int nf = static_cast<int>(f.size()) - 1, ng = static_cast<int>(g.size()) - 1;
+  if (std::max(nf, ng) > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: y-degree exceeds 6000");
+  ZPoly slots;
+  std::vector<int32_t> dir;
+  std::vector<int32_t> off, len;
+  for (const YPoly* h : {&f, &g}) {
+    std::vector<int32_t> o, l;
+    for (const auto& row : *h) {
+      o.push_back(static_cast<int32_t>(slots.size()));
+      l.push_back(static_cast<int32_t>(row.size()));
+      slots.insert(slots.end(), row.begin(), row.end());
+    }
+    dir.insert(dir.end(), o.begin(), o.end());
+    dir.insert(dir.end(), l.begin(), l.end());
+  }
+  if (slots.empty()) return false;
+  DevArena ar(st);
+  const std::vector<uint32_t> primes = select_primes(1, 4 * 30.0);
+  auto T = build_tables(dev, primes, 1);
+  uint32_t* tab = reduce_poly(ar, slots, *T, L);
+  int32_t* d_dir = ar.alloc<int32_t>(dir.size());
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_dir, dir.data(), 4 * dir.size(), cudaMemcpyHostToDevice, ar.st));
+  constexpr int kPoints = 8;
+  const int units = T->P * kPoints;
+  int32_t* d_deg = ar.alloc<int32_t>(units);
+  L.n += launch_bigcd_probe(tab, static_cast<int>(slots.size()), d_dir, nf, ng, T->d_pc, T->P, kPoints, d_deg, ar.st);
+  CTG_CUDA_CHECK(cudaGetLastError());
+  std::vector<int32_t> deg(units);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * units, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+  for (int d : deg)
+    if (d == 0) return true;
+  return false;
+}
+
+void fill_bipoly_x(const ZPoly& c, ctg_bipoly_buf* out) {
+  std::vector<int> idx;
+  size_t total = 0;
+  for (size_t i = 0; i < c.size(); ++i)
+    if (c[i].sign != 0) {
+      idx.push_back(static_cast<int>(i));
+      total += c[i].mag.size();
+    }
+  const size_t n = idx.size();
+  const size_t bytes = 8 * n + 4 * (n + 1) + 4 * total + n + 16;
+  auto* base = static_cast<uint8_t*>(std::malloc(bytes));
+  if (!base) throw std::bad_alloc();
+  out->n_terms = static_cast<int32_t>(n);
+  out->dx = reinterpret_cast<int32_t*>(base);
+  out->dy = out->dx + n;
+  out->limb_off = reinterpret_cast<uint32_t*>(out->dy + n);
+  out->limbs = out->limb_off + n + 1;
+  out->sign = reinterpret_cast<int8_t*>(out->limbs + total);
+  uint32_t pos = 0;
+  for (size_t t = 0; t < n; ++t) {
+    const SBig& v = c[idx[t]];
+    out->dx[t] = idx[t];
+    out->dy[t] = 0;
+    out->sign[t] = static_cast<int8_t>(v.sign);
+    out->limb_off[t] = pos;
+    std::memcpy(out->limbs + pos, v.mag.data(), 4 * v.mag.size());
+    pos += static_cast<uint32_t>(v.mag.size());
+  }
+  out->limb_off[n] = pos;
+}
+
+// Copy of a parsed operand, terms sorted by (dx, dy) (the reference returns it as is).
+void fill_bipoly(const YPoly& f, ctg_bipoly_buf* out) {
+  struct T {
+    int dx, dy;
+    const SBig* c;
+  };
+  std::vector<T> terms;
+  size_t total = 0;
+  for (size_t y = 0; y < f.size(); ++y)
+    for (size_t x = 0; x < f[y].size(); ++x)
+      if (f[y][x].sign != 0) {
+        terms.push_back({static_cast<int>(x), static_cast<int>(y), &f[y][x]});
+        total += f[y][x].mag.size();
+      }
+  std::sort(terms.begin(), terms.end(), [](const T& a, const T& b) { return a.dx != b.dx ? a.dx < b.dx : a.dy < b.dy; });
+  const size_t n = terms.size();
+  auto* base = static_cast<uint8_t*>(std::malloc(8 * n + 4 * (n + 1) + 4 * total + n + 16));
+  if (!base) throw std::bad_alloc();
+  out->n_terms = static_cast<int32_t>(n);
+  out->dx = reinterpret_cast<int32_t*>(base);
+  out->dy = out->dx + n;
+  out->limb_off = reinterpret_cast<uint32_t*>(out->dy + n);
+  out->limbs = out->limb_off + n + 1;
+  out->sign = reinterpret_cast<int8_t*>(out->limbs + total);
+  uint32_t pos = 0;
+  for (size_t t = 0; t < n; ++t) {
+    out->dx[t] = terms[t].dx;
+    out->dy[t] = terms[t].dy;
+    out->sign[t] = static_cast<int8_t>(terms[t].c->sign);
+    out->limb_off[t] = pos;
+    std::memcpy(out->limbs + pos, terms[t].c->mag.data(), 4 * terms[t].c->mag.size());
+    pos += static_cast<uint32_t>(terms[t].c->mag.size());
+  }
+  out->limb_off[n] = pos;
+}
+
 void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly, int>>& factors, ctg_sqf_buf* out) {
   std::memset(out, 0, sizeof(*out));
   out->unit_sign = static_cast<int8_t>(unit.empty() ? 0 : unit_sign);
@@ -582,6 +740,44 @@ ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_
     fill_upoly(to_ucoeffs(r), out);
     timer.finish();
   });
+}
+
+ctg_status ctg_gcd_bivariate(const ctg_bipoly* f, const ctg_bipoly* g, ctg_bipoly_buf* out, const ctg_opts* opts) {
+  return guarded([&] {
+    if (!out) throw ApiError(CTG_INVALID, "gcd_bivariate: null output");
+    CallTimer timer;
+    YPoly a = parse_bipoly_y(f), b = parse_bipoly_y(g);
+    // elim.cpp:179-181
+    if (a.empty() && b.empty()) throw ApiError(CTG_PRECONDITION, "gcd_bivariate: both inputs zero");
+    if (a.empty() || b.empty()) {
+      fill_bipoly(a.empty() ? b : a, out);
+      timer.finish();
+      return;
+    }
+    timer.mark_setup();
+    DeviceGuard guard(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    Launches L;
+    const ZPoly cf = content_y(a, dev, ctx.stream, L), cg = content_y(b, dev, ctx.stream, L);
+    if (!primitive_parts_coprime(a, b, dev, ctx.stream, L)) {
+      stats_tls().kernel_launches = L.n;
+      throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: the primitive parts share a factor (no GPU path)");
+    }
+    // elim.cpp:193-201: pp = +-1, result = gcd_univariate(cf, cg) with positive leading coefficient
+    const ZPoly c = gcd_uni(cf, cg, dev, ctx.stream, L);
+    timer.mark_device();
+    stats_tls().kernel_launches = L.n;
+    fill_bipoly_x(c, out);
+    timer.finish();
+  });
+}
+
+void ctg_bipoly_free(ctg_bipoly_buf* buf) {
+  if (!buf) return;
+  std::free(buf->dx);
+  std::memset(buf, 0, sizeof(*buf));
 }
 
 }  // extern "C"

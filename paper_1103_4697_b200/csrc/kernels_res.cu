@@ -787,7 +787,7 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
 
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st) {
   if (rp.nk == 0 || rp.B == 0) return 0;
-  if (fast && rp.vals && rp.m == rp.n - 1 && rp.n >= 2 && rp.n <= kFastMaxDeg) {
+  if (fast && rp.vals && (rp.m == rp.n - 1 || (rp.m == rp.n && !rp.deriv)) && rp.n >= 2 && rp.n <= kFastMaxDeg) {
     const int launches = launch_eval(rp, st);  // K2
     if (dispatch_fast_any(rp.n, rp, st)) {     // K3
       k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);  // degenerate units, exact

@@ -248,6 +248,40 @@ __global__ void k_gather_scale(const uint32_t* __restrict__ src, int src_pitch, 
   dst[static_cast<size_t>(r) * cols + c] = mmul(v, scale[static_cast<size_t>(r) * nseg + s], M);
 }
 
+
+// Bivariate gcd probe (ctg_gcd_bivariate): CTA per unit (prime k, point j).  The y-rows of
+// f and g (slot runs of the reduced coefficient table, x-degree ascending) are evaluated at
+// a_j by Horner, then gcd(f(a_j, y), g(a_j, y)) mod p_k runs in shared memory.  deg[unit] is
+// the gcd degree, or -1 when the unit proves nothing (both formal leading y-coefficients
+// vanish at a_j, or an image is identically zero).
+__global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ dir, int nf,
+                              int ng, const PrimeConst* __restrict__ pc, int npts, int32_t* __restrict__ deg) {
+  extern __shared__ uint32_t sm[];
+  const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
+  const Mod M = load_mod_u(pc[k]);
+  const int w = (nf > ng ? nf : ng) + 2;
+  uint32_t* X = sm;
+  uint32_t* Y = sm + w;
+  const int32_t *offf = dir, *lenf = dir + nf + 1, *offg = dir + 2 * (nf + 1), *leng = offg + ng + 1;
+  // a_j: distinct small integers 2, 3, ... in Montgomery form
+  const uint32_t a = mmul(static_cast<uint32_t>(j + 2), M.r2, M);
+  const uint32_t* t = tab + static_cast<size_t>(k) * S;
+  for (int r = threadIdx.x; r <= nf + ng + 1; r += blockDim.x) {
+    const bool isf = r <= nf;
+    const int row = isf ? r : r - nf - 1;
+    const int off = isf ? offf[row] : offg[row], len = isf ? lenf[row] : leng[row];
+    uint32_t acc = 0u;
+    for (int i = len - 1; i >= 0; --i) acc = madd(mmul(acc, a, M), t[off + i], M.p);
+    (isf ? X : Y)[row] = acc;
+  }
+  __syncthreads();
+  const bool lc_ok = X[nf] != 0u || Y[ng] != 0u;
+  const int dx = blk_trim(X, nf), dy = blk_trim(Y, ng);
+  int d = -1;
+  if (dx >= 0 && dy >= 0) d = blk_gcd(X, dx, Y, dy, M);
+  if (threadIdx.x == 0) deg[unit] = lc_ok ? d : -1;
+}
+
 }  // namespace
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
@@ -266,6 +300,15 @@ int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, co
   const size_t smem = modgcd_smem(na, nb);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_modgcd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_modgcd<<<nk, 256, smem, st>>>(tabA, na, tabB, nb, pc, deg, out, pitch);
+  return 1;
+}
+
+int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
+                       int nk, int npts, int32_t* deg, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_bigcd_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_bigcd_probe<<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg);
   return 1;
 }
 

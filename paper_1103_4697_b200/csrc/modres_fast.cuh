@@ -21,7 +21,14 @@ namespace {
 // or a formal leading coefficient vanishing at the point) flags the unit for the exact
 // general kernel.  All arrays live in registers (fully unrolled).
 // ---------------------------------------------------------------------------
-template <int NN>
+// Resident blocks per SM requested from ptxas (caps registers at 65536 / (128 * minB)).
+constexpr int fast_min_blocks(int n) { return n <= 12 ? 8 : n <= 20 ? 6 : n <= 26 ? 5 : n <= 32 ? 4 : 3; }
+
+//
+// EQ = true: deg_y p = deg_y q = NN (e.g. Q = res(f_x, f_y) of a curve whose y^n
+// coefficient is constant).  One extra elimination A' = b_n A - a_n B (deg NN - 1) reduces
+// it to the shape above:  res(A, B) = (-1)^NN b_n^-(NN-1) res(B, A')  (A = (a_n/b_n) B + A'/b_n).
+template <int NN, bool EQ>
 __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
   const int kl = blockIdx.y, b = blockIdx.z;
   const int k = P.k0 + kl;
@@ -33,22 +40,37 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
   // Point values p_j(omega^i) (and q_j) from the K2 evaluation kernel: row j of this
   // prime's block, column i -- consecutive threads read consecutive words.
   const uint32_t* vals = P.vals + (static_cast<size_t>(b) * P.nk + kl) * P.nrows * P.N + i;
-  uint32_t A[NN + 1], B[NN];
+  uint32_t A[NN + 1], B[NN + 1];
+  uint32_t flag = 0u, bn = 0u;
+  if constexpr (EQ) {
 #pragma unroll
-  for (int j = 0; j <= NN; ++j) A[j] = vals[static_cast<size_t>(j) * P.N];
-  if (P.deriv) {
-    uint32_t c = M.one;
+    for (int j = 0; j <= NN; ++j) B[j] = vals[static_cast<size_t>(j) * P.N];            // p
 #pragma unroll
-    for (int j = 0; j < NN; ++j) {
-      B[j] = mmul(A[j + 1], c, M);
-      c = madd(c, M.one, M.p);
-    }
+    for (int j = 0; j <= NN; ++j) A[j] = vals[static_cast<size_t>(NN + 1 + j) * P.N];   // q
+    // (A, B) <- (q, b_n p - a_n q) with a_n = lc p, b_n = lc q
+    const uint32_t an = B[NN];
+    bn = A[NN];
+    flag = (an == 0u) | (bn == 0u);
+    const uint32_t nan = mneg(an, M.p);
+#pragma unroll
+    for (int j = 0; j < NN; ++j) B[j] = mmul2(bn, B[j], nan, A[j], M);
   } else {
 #pragma unroll
-    for (int j = 0; j < NN; ++j) B[j] = vals[static_cast<size_t>(NN + 1 + j) * P.N];
+    for (int j = 0; j <= NN; ++j) A[j] = vals[static_cast<size_t>(j) * P.N];
+    if (P.deriv) {
+      uint32_t c = M.one;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        B[j] = mmul(A[j + 1], c, M);
+        c = madd(c, M.one, M.p);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NN; ++j) B[j] = vals[static_cast<size_t>(NN + 1 + j) * P.N];
+    }
   }
 
-  uint32_t flag = (A[NN] == 0u) | (B[NN - 1] == 0u);
+  flag |= (A[NN] == 0u) | (B[NN - 1] == 0u);
   uint32_t U = M.one, E = M.one;
 #pragma unroll
   for (int kk = NN - 1; kk >= 1; --kk) {
@@ -70,8 +92,10 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
       B[t] = tmp;
     }
   }
-  const uint32_t Ei = minv(E, M);
-  const uint32_t res = mmul(B[0], mmul(Ei, Ei, M), M);
+  uint32_t den = mmul(E, E, M);
+  if constexpr (EQ) den = mmul(den, mpow(bn, NN - 1, M), M);
+  uint32_t res = mmul(B[0], minv(den, M), M);
+  if constexpr (EQ && (NN & 1)) res = mneg(res, M.p);
   uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
   if (flag) {
     out[i] = kSentinel;
@@ -84,7 +108,10 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
 template <int NN>
 void launch_fast_n(const ResParams& rp, cudaStream_t st) {
   dim3 grid((rp.N + 127) / 128, rp.nk, rp.B);
-  k_modres_fast<NN><<<grid, 128, 0, st>>>(rp);
+  if (rp.m == rp.n)
+    k_modres_fast<NN, true><<<grid, 128, 0, st>>>(rp);
+  else
+    k_modres_fast<NN, false><<<grid, 128, 0, st>>>(rp);
 }
 
 template <int G, int NN>

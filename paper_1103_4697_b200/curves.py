@@ -114,6 +114,10 @@ def derive_y(f: dict) -> dict:
     return {(ex, ey - 1): c * ey for (ex, ey), c in f.items() if ey >= 1 and c * ey != 0}
 
 
+def derive_x(f: dict) -> dict:
+    return {(ex - 1, ey): c * ex for (ex, ey), c in f.items() if ex >= 1 and c * ex != 0}
+
+
 # BASELINE.json configs -> (kind, a, b)
 CONFIGS = {
     "d10_b10": ("dense", 10, 10),

@@ -12,8 +12,10 @@
 //   square_free_part  -> ctg_square_free_part  (GPU, elim.cpp:204-210)
 //   SquareFreeFactorization::reconstruct, multiplicity_at: same semantics as elim.cpp:74-78,
 //     167-176 (products / sign tests on the host, gcds on the GPU)
-//   gcd_bivariate: the reference's PRS over Z[x][y] (elim.cpp:178-202) with its univariate
-//     contents on the GPU -- the bivariate GPU gcd is a "next" row.
+//   gcd_bivariate     -> ctg_gcd_bivariate     (GPU: contents + modular coprimality probe,
+//     elim.cpp:178-202) when the primitive parts are coprime -- every square-free curve's
+//     (f_x, f_y) and (f', f'_y) (lift.cpp:85, pipeline.cpp:321); when they share a factor
+//     (CTG_UNSUPPORTED) the reference's PRS over Z[x][y] runs here with GPU contents.
 //
 // Status codes map to the reference's exceptions: CTG_PRECONDITION -> PreconditionError,
 // anything else -> Error (there is no CPU fallback: a CUDA failure throws).
@@ -223,6 +225,19 @@ BivariatePolynomial gcd_bivariate(const BivariatePolynomial& f, const BivariateP
   if (f.is_zero() && g.is_zero()) throw PreconditionError("gcd_bivariate: both inputs zero");
   if (f.is_zero()) return g;
   if (g.is_zero()) return f;
+  {
+    BiMarshal mf(f), mg(g);
+    ctg_bipoly_buf out{};
+    const ctg_status st = ctg_gcd_bivariate(&mf.view, &mg.view, &out, nullptr);
+    if (st == CTG_OK) {
+      BivariatePolynomial::TermMap t;
+      for (int i = 0; i < out.n_terms; ++i)
+        t[{out.dx[i], out.dy[i]}] = from_limbs(out.sign[i], out.limbs + out.limb_off[i], out.limb_off[i + 1] - out.limb_off[i]);
+      ctg_bipoly_free(&out);
+      return BivariatePolynomial(std::move(t));
+    }
+    if (st != CTG_UNSUPPORTED) raise(st, "gcd_bivariate");
+  }
   // Primitive PRS in y over Z[x] on the x-primitive parts; the x-content gcd is
   // multiplied back and the leading (y, then x) coefficient made positive.
   const UnivariatePolynomial cf = content_y(f), cg = content_y(g);

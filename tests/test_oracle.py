@@ -76,3 +76,31 @@ def test_restatement_on_small_configs():
         assert R == dec_upoly(r["result"])
         if "yun" in r and a <= 8:
             assert O.yun_squarefree(R) == dec_sqf(r["yun"])
+
+
+def test_restatement_gcd_bivariate():
+    """elim.cpp:178-202 restated (PRS in y over Z[x]) against the reference's outputs."""
+    rows = load("bivariate_gcd.jsonl")
+    assert len(rows) > 80
+    for r in rows:
+        f, g = (dec_bipoly(a) for a in r["args"])
+        if "error" in r:
+            with pytest.raises(O.PreconditionError):
+                O.gcd_bivariate(f, g)
+        else:
+            assert O.gcd_bivariate(f, g) == dec_bipoly(r["result"]), r
+
+
+def _teissier_curve(r):
+    return curves.make(*r["curve"]) if "curve" in r else dec_bipoly(r["f"])
+
+
+def test_restatement_curve_q():
+    """CurveContext::resultant_q / q_factorization (lift.cpp:76-101) on the small curves."""
+    rows = [r for r in load("teissier.jsonl") if "curve" not in r or r["curve"][0] == "dense" and r["curve"][1] <= 8]
+    assert len(rows) >= 8
+    for r in rows:
+        h, q, qsf = O.curve_q(_teissier_curve(r))
+        assert h == dec_bipoly(r["h"]), r.get("curve", r.get("name"))
+        assert q == dec_upoly(r["result"])
+        assert qsf == dec_sqf(r["qsf"])
