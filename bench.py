@@ -120,6 +120,20 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # reference arm: the reference's own CPU implementation (oracle/_ref), all host cores
 # ----------------------------------------------------------------------------
+def traffic_for(workload, batch):
+    """DRAM bytes (read + write) per K3 launch from one ncu --set full capture of the same
+    bench command (profiles/traffic.json, written by scripts/traffic.sh), or None."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh).get(workload)
+    except (OSError, ValueError):
+        return None
+    if not t or t.get("batch") != batch:
+        return None
+    return t.get("k3_dram_bytes_per_launch")
+
+
 def run_refdriver(kind, a, b, seed, reps=1, yun=False, timeout=None):
     cmd = [REFDRIVER, "time_res", kind, str(a), str(b), str(seed), str(reps)] + (["yun"] if yun else [])
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, check=True).stdout
@@ -211,8 +225,10 @@ def main_ours(args):
     out = torch.zeros((B * Jb * W,), dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-    stage_ms = [0.0] * 5
+    # events: start | K1 reduce | K2 eval | K3 mod-p resultant | K4 interp | exchange | K5 CRT
+    STAGES = ("reduce", "eval", "modres", "interp", "exchange", "crt")
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
+    stage_ms = [0.0] * len(STAGES)
 
     def crt():
         if G > 1:
@@ -224,17 +240,17 @@ def main_ours(args):
     def step(timed=False):
         if timed:
             evs[0].record(stream)
-        for s_ in (1, 2, 3):
+        for i, s_ in enumerate((1, 4, 5, 3)):  # K1, K2, K3 (+ exact fallback), K4
             plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
             if timed:
-                evs[s_].record(stream)
+                evs[i + 1].record(stream)
         if G > 1:
             dist.all_gather_into_tensor(full, send)
         if timed:
-            evs[4].record(stream)
+            evs[5].record(stream)
         crt()
         if timed:
-            evs[5].record(stream)
+            evs[6].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -257,8 +273,8 @@ def main_ours(args):
             torch.cuda.synchronize()
             step(timed=True)
             torch.cuda.synchronize()
-            total_ms += evs[0].elapsed_time(evs[5])
-            for i in range(5):
+            total_ms += evs[0].elapsed_time(evs[-1])
+            for i in range(len(STAGES)):
                 stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
     gpu_launches = plan.launches - launches0
     t_max = total_ms
@@ -290,23 +306,28 @@ def main_ours(args):
                                        rank)
     e2e_value = units_step / (e2e_ms * 1e-3)
 
-    # --- roofline of the dominant kernel (stage 2: K2 eval + K3 mod-p resultant) ---------
+    # --- roofline of the dominant kernel: K3, the mod-p resultant (north_star: >= 50% of IMAD peak)
     peaks = P.microbench_int(dev)
     n = info["deg_p"]
-    k3_ms_per_launch = stage_ms[1] / args.steps  # one batched launch set per step
+    sm = {nm: v / args.steps for nm, v in zip(STAGES, stage_ms)}
     units_launch = B * (k1 - k0) * N
     imad_launch = 4.0 * units_launch * (n * n + n - 2)
-    achieved = imad_launch / (k3_ms_per_launch * 1e-3) / 1e12
+    achieved = imad_launch / (sm["modres"] * 1e-3) / 1e12
     peak = peaks["imad_per_s"] / 1e12
+    # K2 against the same peak with its own count: P * N * (d(d+1)/2 + d) mulmods
+    d_tot = a if kind == "dense" else 6 * a
+    k2_mulmods = units_launch * (d_tot * (d_tot + 1) / 2 + d_tot)
+    k2_frac = 4.0 * k2_mulmods / (sm["eval"] * 1e-3) / 1e12 / peak if sm["eval"] > 0 else None
     roofline = {"bound": "int32-imad", "achieved": achieved, "peak": peak, "unit": "TIMAD/s",
-                "frac": achieved / peak, "traffic": None,
-                "kernel": f"stage 2 = k_eval_ntt (K2) + k_modres_fast<{n}> (K3) + k_modres_general (flagged units)",
+                "frac": achieved / peak, "traffic": traffic_for(args.workload, B),
+                "kernel": f"K3 = k_modres_fast<{n}> (fused division-free Euclid) + k_modres_general (flagged units)",
                 "algorithmic": f"4 IMAD x (n^2+n-2) mulmods x {units_launch} units per launch, n={n} (SURVEY §8d)",
                 "peak_source": "measured live: ctg_microbench_int (8 IMAD chains/thread, all SMs)",
                 "imad_wide_peak_T": peaks["imad_wide_per_s"] / 1e12,
                 "mmul2_peak_G": peaks["mmul2_per_s"] / 1e9,
-                "stage_ms_per_step": {nm: v / args.steps for nm, v in
-                                      zip(("reduce", "modres", "interp", "exchange", "crt"), stage_ms)}}
+                "k2_eval_frac": k2_frac,
+                "stage2_frac": imad_launch / ((sm["eval"] + sm["modres"]) * 1e-3) / 1e12 / peak,
+                "stage_ms_per_step": sm}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,

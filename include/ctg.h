@@ -165,7 +165,9 @@ ctg_status ctg_plan_upload(ctg_plan* plan, void* stream);
 /* Rows [k0, k1) of the residue matrix into d_rows (device, (k1-k0) x n_points words). */
 ctg_status ctg_plan_residues(ctg_plan* plan, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream);
 /* One stage of ctg_plan_residues (for per-kernel timing): 1 = reduce (K1),
- * 2 = evaluate + mod-p resultant (K2/K3 + the exact fallback), 3 = interpolate (K4). */
+ * 2 = evaluate + mod-p resultant (K2/K3 + the exact fallback), 3 = interpolate (K4);
+ * stage 2 split in two: 4 = evaluate only (K2; nothing without the fast path),
+ * 5 = mod-p resultant only (K3 + the exact fallback; needs stage 4 first). */
 ctg_status ctg_plan_stage(ctg_plan* plan, int32_t stage, int32_t k0, int32_t k1, uint32_t* d_rows, void* stream);
 /* Coefficients [j0, j1) from the full residue matrix d_all (device, n_primes x n_points):
  * d_out gets (j1-j0) x (out_limbs + 1) words: word 0 = sign (as int32), then magnitude limbs. */

@@ -380,6 +380,27 @@ def teissier() -> list[dict]:
     return rows
 
 
+def teissier_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
+    """Digests of Q = res(f_x, f_y) (h = 1 for these curves) at BASELINE sizes."""
+    rows = []
+    for (kind, a, b, s) in [("dense", 20, 64, 1), ("sheared", 3, 0, 1)]:
+        name = f"{kind}_{a}_{b}_{s}"
+        cached = os.path.join(cache_dir, f"outq_{name}.txt")
+        if os.path.exists(cached) and os.path.getsize(cached) > 0:
+            r = json.loads(open(cached).read().splitlines()[0])
+        elif cached_only:
+            print(f"skip Q {name}: no cached reference output")
+            continue
+        else:
+            f = curves.make(kind, a, b, s)
+            r = run_batch([("resultant_y", [curves.derive_x(f), curves.derive_y(f)])])[0]
+        res = r["result"]
+        ints = [int(c, 16) for c in res]
+        rows.append({"curve": [kind, a, b, s], "deg": len(res) - 1, "max_bits": max(abs(c).bit_length() for c in ints),
+                     "sha256": digest(res), "lc": res[-1], "c0": res[0], "ref_seconds": r["seconds"]})
+    return rows
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -396,6 +417,7 @@ def main() -> None:
     write("teissier.jsonl", teissier())
     if args.big:
         write("configs_big.jsonl", configs_big(args.cache, args.cached_only))
+        write("teissier_big.jsonl", teissier_big(args.cache, args.cached_only))
 
 
 if __name__ == "__main__":

@@ -467,7 +467,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   if (pl->trivial) return;
   if (!pl->uploaded) throw ApiError(CTG_INVALID, "plan: inputs not uploaded");
   if (k0 < 0 || k1 > pl->P || k0 > k1) throw ApiError(CTG_INVALID, "plan: prime range out of bounds");
-  if (stage < 1 || stage > 3) throw ApiError(CTG_INVALID, "plan: stage must be 1, 2 or 3");
+  if (stage < 1 || stage > 5) throw ApiError(CTG_INVALID, "plan: stage must be 1..5");
   const int nk = k1 - k0;
   if (nk == 0) return;
   const size_t rows_bstride = curve_stride > 0 ? static_cast<size_t>(curve_stride) : static_cast<size_t>(nk) * pl->N;
@@ -485,7 +485,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }
-  CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t), st));
+  if (stage != 4) CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t), st));
   ResParams rp{};
   rp.B = pl->B;
   rp.tab = pl->d_tab;
@@ -508,7 +508,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   rp.vals = pl->fast_ok ? pl->d_vals : nullptr;
   rp.nrows = pl->nrows;
   rp.maxlen = pl->maxlen;
-  pl->launches += launch_modres(rp, true, st);
+  pl->launches += launch_modres(rp, true, st, stage == 4 ? 1 : stage == 5 ? 2 : 0);
   CTG_CUDA_CHECK(cudaGetLastError());
 }
 

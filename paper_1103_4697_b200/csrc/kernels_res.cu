@@ -785,15 +785,17 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
   return 1;
 }
 
-int launch_modres(const ResParams& rp, bool fast, cudaStream_t st) {
+int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
   if (rp.nk == 0 || rp.B == 0) return 0;
   if (fast && rp.vals && (rp.m == rp.n - 1 || (rp.m == rp.n && !rp.deriv)) && rp.n >= 2 && rp.n <= kFastMaxDeg) {
-    const int launches = launch_eval(rp, st);  // K2
-    if (dispatch_fast_any(rp.n, rp, st)) {     // K3
-      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);  // degenerate units, exact
+    const int launches = part == 2 ? 0 : launch_eval(rp, st);  // K2
+    if (part == 1) return launches;
+    if (dispatch_fast_any(rp.n, rp, st)) {                      // K3
+      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);          // degenerate units, exact
       return launches + 2;
     }
   }
+  if (part == 1) return 0;
   const uint32_t total = static_cast<uint32_t>(rp.B) * rp.nk * static_cast<uint32_t>(rp.N);
   const int blocks = static_cast<int>(std::min<uint32_t>((total + 127) / 128, 148u * 16u));
   k_modres_general<<<blocks, 128, 0, st>>>(rp, 0, total);

@@ -95,3 +95,19 @@ def test_equal_degree_fast_kernel_matches_general():
         p = {k: v for k, v in p.items() if v}
         q = {k: v for k, v in q.items() if v}
         assert P.resultant(p, q) == O.resultant(p, q, "y")
+
+
+def test_teissier_q_big_digests():
+    """Q = res(f_x, f_y) at d20/64 (EQ fast kernel, n = 19) and the sheared K=3 curve
+    against sha256 digests of the reference's outputs (tests/golden/teissier_big.jsonl)."""
+    import hashlib
+    rows = load("teissier_big.jsonl")
+    assert len(rows) == 2
+    for r in rows:
+        f = curves.make(*r["curve"])
+        fx, fy = curves.derive_x(f), curves.derive_y(f)
+        assert P.gcd_bivariate(fx, fy) == {(0, 0): 1}
+        q = P.resultant(fx, fy)
+        hexes = [format(c, "x") for c in q]
+        assert len(q) - 1 == r["deg"] and hexes[-1] == r["lc"] and hexes[0] == r["c0"]
+        assert hashlib.sha256(",".join(hexes).encode()).hexdigest() == r["sha256"], r["curve"]
