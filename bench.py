@@ -347,6 +347,7 @@ def main_ours(args):
     }
     if rank == 0 and G == 1 and not args.no_headline:
         line["headline"] = headline(P, curves)
+        line["yun"] = yun_line(P, curves, args.workload)
     if rank == 0 and G == 1:
         line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args.workload, Pn * D)
     if rank == 0:
@@ -410,6 +411,28 @@ def headline(P, curves):
             "reference_cpu_s": ref_s,
             "reference_cpu_source": "oracle/_ref/refdriver, 1 core of the build container (not re-run: 28 min)",
             "speedup_vs_reference_1gpu": ref_s * 1e3 / ms}
+
+
+def yun_line(P, curves, workload):
+    """Second §8 row: yun_squarefree(R) through the C ABI for the workload's seed-1 curve
+    (and the singular sheared K=3 family, the Yun stress config), GPU wall ms (median of 5)."""
+    out = {}
+    kind, a, b, _, _ = WORKLOADS[workload]
+    for name, (k_, a_, b_) in ((workload, (kind, a, b)), ("sheared_k3", ("sheared", 3, 0))):
+        f = curves.make(k_, a_, b_, 1)
+        R = P.resultant(f, curves.derive_y(f))
+        for _ in range(2):
+            P.yun_squarefree(R)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            unit, fac = P.yun_squarefree(R)
+            ts.append(1e3 * (time.perf_counter() - t0))
+        out[name] = {"deg_R": len(R) - 1, "gpu_ms_median": statistics.median(ts),
+                     "pattern": "".join(f"({len(p_) - 1})^{m}" for p_, m in fac),
+                     "kernel_launches": P.last_call_stats()["kernel_launches"]}
+    out["sheared_k3"]["reference_cpu_s"] = 29.2  # SURVEY §6.2, oracle/_ref in the build container
+    return out
 
 
 def cpu_baseline(workload, units_per_curve):

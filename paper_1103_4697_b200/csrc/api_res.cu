@@ -565,6 +565,8 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int r
   cp.Kp = pl->tabs->Kp;
   cp.Bt8 = pl->tabs->d_Bt8;
   cp.M8 = pl->tabs->d_M8;
+  // Hadamard bound (plan_build): |coefficient| < 2^bound_bits
+  cp.top_digit = std::min(cp.L8, static_cast<int>(std::ceil((pl->bound_bits + 1) / 8.0)) + 1);
   cp.counters = pl->d_counters;
   pl->launches += launch_crt(cp, st);
   CTG_CUDA_CHECK(cudaGetLastError());

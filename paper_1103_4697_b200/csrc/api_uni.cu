@@ -246,6 +246,7 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   cp.Kp = T->Kp;
   cp.Bt8 = T->d_Bt8;
   cp.M8 = T->d_M8;
+  cp.top_digit = cp.L8;
   cp.counters = d_cnt;
   L.n += launch_crt(cp, ar.st);
   CTG_CUDA_CHECK(cudaGetLastError());

@@ -113,6 +113,7 @@ struct CrtParams {
   int Jp, L8, L8p, Kp;
   const uint8_t* Bt8;
   const uint32_t* M8;
+  int top_digit;         // |value| < 2^(8 top_digit) (coefficient bound; L8 when unknown)
 };
 
 // Scratch words the CRT needs for J coefficients of B curves (Y and cols).

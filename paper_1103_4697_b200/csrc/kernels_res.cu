@@ -15,6 +15,8 @@
 // Sylvester determinant at every (prime, point) determine it bit-exactly.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <algorithm>
 
 #include "internal.hpp"
@@ -663,100 +665,78 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
     }
 }
 
-// Carry propagation of sum_l C[l] 2^(8 l) - t M over byte digits (one warp per coefficient;
-// same lane-chunk carry-lookahead scan as k_crt_carry, chunk = multiple of 4 digits, >= 8).
-// The warp first stages v_l = C[l] - t M8[l] through shared memory with coalesced loads
-// (int32: 0 <= C[l] < 2^31, 0 <= t M8[l] < 2^21); slot l lives at l + l / chunk so the
-// lanes' chunk walks (stride chunk + 1, odd) are bank-conflict-free.
-__global__ void __launch_bounds__(128) k_crt_carry8(CrtParams C) {
-  extern __shared__ int32_t sv[];
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  if (gw >= C.J * C.B) return;
-  const int b = gw / C.J, jl = gw - b * C.J;
-  const int L8 = C.L8, OL = C.out_limbs;
+
+
+// Carry propagation of V = sum_l C[l] 2^(8 l) - t M (K5 epilogue), one THREAD per coefficient:
+// a sequential walk over the L8 byte digits (16 per limb step, int4 loads of the GEMM
+// columns with 8 in flight per thread, M8 broadcast from L1), then, for V < 0, a two's-
+// complement pass over the limbs the same thread just wrote.  Each coefficient is a few
+// hundred to a few thousand digits; thousands of independent walks hide the carry-chain
+// latency.  (Measured on B200 against a warp-per-coefficient lookahead scan, SEG threads per
+// coefficient with a segment scan, shared-memory row tiles, and a variant that settles the
+// sign first to avoid the second pass: this is the fastest at d20 / d30 / d16.)
+// WIDE: 64-bit carry arithmetic (needed when 4P * 255^2 + 2^25 >= 2^31).
+template <bool WIDE>
+__global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= C.J * C.B) return;
+  const int b = g / C.J, jl = g - b * C.J;
+  const int OL = C.out_limbs;
   const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
   double s = 0;
-  for (int q = lane; q < nch; q += 32) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  for (int q = 0; q < nch; ++q) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
   const double tr = rint(s);
-  if (lane == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  if (fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
   const int32_t t = static_cast<int32_t>(tr);
-
-  int chunk = 4 * ((L8 + 127) / 128);
-  if (chunk < 8) chunk = 8;
-  const int d0 = lane * chunk;
-  const int32_t* col = reinterpret_cast<const int32_t*>(C.cols) + (static_cast<size_t>(b) * C.Jp + jl) * C.L8p;
-  int32_t* v_s = sv + wib * (32 * chunk + 32);
-  for (int l = lane; l < 32 * chunk; l += 32)
-    v_s[l + l / chunk] = (l < L8) ? col[l] - t * static_cast<int32_t>(C.M8[l]) : 0;
-  __syncwarp();
-  uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1);
-  int64_t carry = 0;
-  uint64_t low = 0;
-  bool ones = true, zeros = true;
-  for (int k = 0; k < chunk; k += 4) {
-    uint32_t limb = 0;
+  const int4* col = reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(C.cols) +
+                                                  (static_cast<size_t>(b) * C.Jp + jl) * C.L8p);
+  const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
+  uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1) + 1;
+  using acc_t = typename std::conditional<WIDE, long long, int>::type;
+  acc_t carry = 0;
+  uint32_t any = 0;
+  constexpr int kBatch = 8;
+  for (int w0 = 0; w0 < OL; w0 += kBatch) {
+    int4 cb[kBatch];
+    uint4 mb[kBatch];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int l = d0 + k + h;
-      const int64_t v = carry + v_s[l + lane];  // l / chunk == lane
-      limb |= static_cast<uint32_t>(v & 0xff) << (8 * h);
+    for (int i = 0; i < kBatch; ++i) {
+      if (w0 + i < OL) {
+        cb[i] = col[w0 + i];
+        mb[i] = __ldg(&m8[w0 + i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      if (w0 + i >= OL) break;
+      const int4 c = cb[i];
+      const uint4 m = mb[i];
+      uint32_t limb;
+      acc_t v = carry + c.x - static_cast<acc_t>(t) * static_cast<int>(m.x);
+      limb = static_cast<uint32_t>(v) & 0xffu;
+      v = (v >> 8) + c.y - static_cast<acc_t>(t) * static_cast<int>(m.y);
+      limb |= (static_cast<uint32_t>(v) & 0xffu) << 8;
+      v = (v >> 8) + c.z - static_cast<acc_t>(t) * static_cast<int>(m.z);
+      limb |= (static_cast<uint32_t>(v) & 0xffu) << 16;
+      v = (v >> 8) + c.w - static_cast<acc_t>(t) * static_cast<int>(m.w);
+      limb |= static_cast<uint32_t>(v) << 24;
       carry = v >> 8;
-    }
-    const int w = (d0 + k) >> 2;
-    if (w < OL) out[1 + w] = limb;
-    if (k < 8) {
-      low |= static_cast<uint64_t>(limb) << (8 * k);
-    } else {
-      ones &= (limb == 0xffffffffu);
-      zeros &= (limb == 0u);
+      out[w0 + i] = limb;
+      any |= limb;
     }
   }
-  int64_t cin = 0, my_cin = 0;
-  const uint32_t flags = (ones ? 1u : 0u) | (zeros ? 2u : 0u);
-  for (int i = 0; i < 32; ++i) {
-    const int64_t ci = __shfl_sync(0xffffffffu, carry, i);
-    const uint64_t lo = __shfl_sync(0xffffffffu, low, i);
-    const uint32_t fl = __shfl_sync(0xffffffffu, flags, i);
-    if (lane == i) my_cin = cin;
-    int64_t adj = 0;
-    if (cin > 0) {
-      adj = ((fl & 1u) && lo + static_cast<uint64_t>(cin) < lo) ? 1 : 0;
-    } else if (cin < 0) {
-      adj = ((fl & 2u) && lo < static_cast<uint64_t>(-cin)) ? -1 : 0;
-    }
-    cin = ci + adj;
-  }
-  const int64_t total_carry = cin;
-  int64_t c = my_cin;
-  for (int k = 0; k < chunk && c != 0; k += 4) {
-    const int w = (d0 + k) >> 2;
-    if (w >= OL) break;
-    const int64_t v = static_cast<int64_t>(out[1 + w]) + c;
-    out[1 + w] = static_cast<uint32_t>(v);
-    c = v >> 32;
-  }
-  __syncwarp();
-  int lowest = OL;
-  for (int k = 0; k < chunk; k += 4) {
-    const int w = (d0 + k) >> 2;
-    if (w < OL && out[1 + w] != 0u) {
-      lowest = w;
-      break;
+  // |V| < M / 2 < 2^(32 OL - 1): the final carry is 0 (V >= 0) or -1 (V < 0); -V = ~V + 1.
+  int sign = any ? 1 : 0;
+  if (carry < 0) {
+    sign = -1;
+    uint32_t cin = 1;
+    for (int w = 0; w < OL; ++w) {
+      const uint32_t x = ~out[w] + cin;
+      cin = (cin && x == 0u) ? 1u : 0u;
+      out[w] = x;
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) lowest = min(lowest, __shfl_xor_sync(0xffffffffu, lowest, off));
-  if (total_carry < 0) {
-    for (int k = 0; k < chunk; k += 4) {
-      const int w = (d0 + k) >> 2;
-      if (w >= OL || w < lowest) continue;
-      out[1 + w] = (w == lowest) ? (0u - out[1 + w]) : ~out[1 + w];
-    }
-  }
-  if (lane == 0) out[0] = static_cast<uint32_t>(lowest >= OL ? 0 : (total_carry < 0 ? -1 : 1));
+  out[-1] = static_cast<uint32_t>(sign);
 }
 
 }  // namespace
@@ -824,14 +804,13 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
   if (cp.use_i8) {
     k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
     k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
-    int chunk = 4 * ((cp.L8 + 127) / 128);
-    if (chunk < 8) chunk = 8;
-    const size_t warp_smem = static_cast<size_t>(32 * chunk + 32) * sizeof(int32_t);
-    const int wpb = warp_smem * 4 <= 160 * 1024 ? 4 : 1;  // P <= 8192: one warp needs <= 127 KB
-    const size_t smem = warp_smem * wpb;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_crt_carry8, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_crt_carry8<<<(cp.J * cp.B + wpb - 1) / wpb, 32 * wpb, smem, st>>>(cp);
+    // 4P * 255^2 + 2^25 < 2^31: the per-digit sum fits int32
+    const bool wide = static_cast<double>(cp.P) * 4 * 255 * 255 + 33554432.0 >= 2147483648.0;
+    const unsigned blocks = static_cast<unsigned>((static_cast<long long>(cp.J) * cp.B + 127) / 128);
+    if (wide)
+      k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
+    else
+      k_crt_carry_seq<false><<<blocks, 128, 0, st>>>(cp);
     return 3;
   }
   k_crt_prep<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);

@@ -31,7 +31,10 @@ STALLS = ["wait", "math_pipe_throttle", "long_scoreboard", "short_scoreboard", "
 def summarize(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    return "\n\n".join(summarize_row(rows[0], rows[1], v, path) for v in rows[2:] if v)
+
+
+def summarize_row(hdr, units, vals, path):
     name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else path
     out = [f"kernel: {name[:90]}"]
     for k, short in KEYS:
