@@ -508,6 +508,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   rp.vals = pl->fast_ok ? pl->d_vals : nullptr;
   rp.nrows = pl->nrows;
   rp.maxlen = pl->maxlen;
+  rp.twinv = pl->tabs->d_twinv;
   pl->launches += launch_modres(rp, true, st, stage == 4 ? 1 : stage == 5 ? 2 : 0);
   CTG_CUDA_CHECK(cudaGetLastError());
 }

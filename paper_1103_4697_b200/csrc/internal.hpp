@@ -86,6 +86,7 @@ struct ResParams {
   uint32_t* vals;           // K2 output: [B][nk][nrows][N] point values (Montgomery); null = no fast path
   int nrows;                // n + 1 (derivative mode) or n + m + 2
   int maxlen;               // longest slot run (max x-degree + 1) over the rows
+  const uint32_t* twinv;    // [P][N] omega_k^{-i} (Montgomery; global prime index k)
 };
 
 struct CrtParams {

@@ -96,19 +96,20 @@ __global__ void __launch_bounds__(128) k_eval_ntt(ResParams P, int K) {
   row_slots(P, r, off, len);
   const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S + off;
   uint32_t a[LP];
-  const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(u), M);
+  // omega^j = omega^{-(N - j)}: powers come from the per-prime inverse-twiddle table
+  const uint32_t* twr = P.twinv + static_cast<size_t>(k) * P.N;
+  const uint32_t x = u ? __ldg(&twr[P.N - u]) : M.one;
+  uint32_t tw[LP / 2];  // w^e, w = omega^K of order LP
+  tw[0] = M.one;
+#pragma unroll
+  for (int e = 1; e < LP / 2; ++e) tw[e] = __ldg(&twr[P.N - K * e]);
   uint32_t xp = M.one;
 #pragma unroll
-  for (int t = 0; t < LP; ++t) {
+  for (int t = 0; t < LP; ++t) {  // c_t x^t
     const uint32_t c = (t < len) ? tab[t] : 0u;
     a[bitrev_c(t, LG)] = mmul(c, xp, M);
     xp = mmul(xp, x, M);
   }
-  const uint32_t w = mpow(pcv.omega, static_cast<uint64_t>(K), M);  // order LP
-  uint32_t tw[LP / 2];
-  tw[0] = M.one;
-#pragma unroll
-  for (int e = 1; e < LP / 2; ++e) tw[e] = mmul(tw[e - 1], w, M);
 #pragma unroll
   for (int len2 = 2; len2 <= LP; len2 <<= 1) {
     const int half = len2 >> 1, step = LP / len2;
