@@ -15,7 +15,11 @@
 // Sylvester determinant at every (prime, point) determine it bit-exactly.
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+
 #include <type_traits>
+
+#include "crt_gemm_tma.cuh"
 
 #include <algorithm>
 
@@ -799,12 +803,53 @@ void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv) {
   k_twiddles<<<static_cast<unsigned>((total + 255) / 256), 256>>>(d_pc, P, N, d_twinv);
 }
 
+// 2D u8 tensor map (K-major rows of `kbytes` bytes), SWIZZLE_128B boxes of 128 B x box_rows.
+static bool make_u8_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kbytes, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return f;
+  }();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {kbytes, rows};
+  cuuint64_t strides[1] = {kbytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(tma::kBK), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The CRT product as ONE TMA-fed tcgen05 GEMM over every curve of the batch:
+// cols[B * Jp][L8p] = Yt[B * Jp][Kp] x Bt8[L8p][Kp]^T.
+template <int BN>
+static bool launch_gemm_tma(const CrtParams& cp, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  const uint64_t rows = static_cast<uint64_t>(cp.B) * cp.Jp;
+  if (!make_u8_map(&ta, cp.Y, rows, cp.Kp, tma::kBM) || !make_u8_map(&tb, cp.Bt8, cp.L8p, cp.Kp, BN)) return false;
+  static const bool attr = [] {
+    return cudaFuncSetAttribute(tma::k_gemm_u8_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(tma::smem_bytes<BN>())) == cudaSuccess;
+  }();
+  if (!attr) return false;
+  tma::k_gemm_u8_tma<BN><<<dim3(cp.L8p / BN, static_cast<unsigned>(rows / tma::kBM)), 128, tma::smem_bytes<BN>(), st>>>(
+      ta, tb, reinterpret_cast<int32_t*>(cp.cols), cp.L8p, cp.Kp);
+  return true;
+}
+
 int launch_crt(const CrtParams& cp, cudaStream_t st) {
   if (cp.J == 0 || cp.B == 0) return 0;
   const int nch = (cp.P + kCrtChunk - 1) / kCrtChunk;
   if (cp.use_i8) {
     k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
-    k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
+    // Long K (>= 8 stages): TMA + tcgen05; short K: the mma.sync kernel has less fixed cost.
+    bool done = false;
+    if (cp.Kp >= 1024) done = (cp.L8p % 256 == 0) ? launch_gemm_tma<256>(cp, st) : launch_gemm_tma<128>(cp, st);
+    if (!done) k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
     // 4P * 255^2 + 2^25 < 2^31: the per-digit sum fits int32
     const bool wide = static_cast<double>(cp.P) * 4 * 255 * 255 + 33554432.0 >= 2147483648.0;
     const unsigned blocks = static_cast<unsigned>((static_cast<long long>(cp.J) * cp.B + 127) / 128);

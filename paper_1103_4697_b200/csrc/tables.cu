@@ -38,7 +38,7 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   T->L16 = 2 * T->LM;
   T->L8 = 4 * T->LM;
   T->L8p = (T->L8 + kI8TileL - 1) / kI8TileL * kI8TileL;
-  T->Kp = (4 * P + 63) / 64 * 64;  // 64-byte K stages of the GEMM pipeline
+  T->Kp = (4 * P + 127) / 128 * 128;  // 128-byte K stages (TMA / tcgen05 GEMM; 2 mma.sync stages)
   T->use_i8 = P <= kI8MaxPrimes;
   std::vector<PrimeConst> pc(P);
   std::vector<double> minv(P);
