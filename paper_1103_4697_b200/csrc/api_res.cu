@@ -473,7 +473,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   const size_t rows_bstride = curve_stride > 0 ? static_cast<size_t>(curve_stride) : static_cast<size_t>(nk) * pl->N;
   pl->last_stream = st;
   if (stage == 1) {
-    pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, k0, nk, pl->d_tab,
+    pl->launches += launch_reduce(pl->d_limbs, pl->d_sign, pl->S, pl->L, pl->tabs->d_pc, pl->tabs->d_rpow, k0, nk, pl->d_tab,
                                   static_cast<size_t>(pl->P) * pl->S, pl->B, st);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;

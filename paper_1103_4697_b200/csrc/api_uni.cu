@@ -182,7 +182,8 @@ uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launc
   uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
   CTG_CUDA_CHECK(cudaMemcpyAsync(d_limbs, limbs.data(), 4 * limbs.size(), cudaMemcpyHostToDevice, ar.st));
   CTG_CUDA_CHECK(cudaMemcpyAsync(d_sign, sign.data(), S, cudaMemcpyHostToDevice, ar.st));
-  L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, 0, tabs.P, d_tab, static_cast<size_t>(tabs.P) * S, 1, ar.st);
+  L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, tabs.d_rpow, 0, tabs.P, d_tab, static_cast<size_t>(tabs.P) * S, 1,
+                       ar.st);
   auto& st = stats_tls();
   st.h2d_bytes += static_cast<int64_t>(4 * limbs.size() + S);
   return d_tab;

@@ -34,6 +34,7 @@ constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT roundin
 constexpr int kI8TileJ = 128;       // tensor-core CRT GEMM block tile: coefficients
 constexpr int kI8TileL = 128;       //                                   byte digits of the output
 constexpr int kI8MaxPrimes = 8192;  // s32 exactness: 4P * 255^2 < 2^31
+constexpr int kRedL = 64;           // limb powers tabulated per prime for K1 (longer inputs extend on the fly)
 
 // Device error bits (plan counters[1]).
 enum : uint32_t {
@@ -59,6 +60,7 @@ struct CrtTables {
   uint8_t* d_Bt8 = nullptr;
   uint32_t* d_M8 = nullptr;
   uint32_t* d_twinv = nullptr;  // [P][N] omega_k^{-i} (Montgomery), N > 1 only
+  uint32_t* d_rpow = nullptr;   // [P][kRedL] R^(l+2) mod p_k (plain): mmul(limb_l, .) = limb_l 2^(32 l) R
   std::vector<PrimeConst> h_pc;
   double log2M = 0;
   ~CrtTables();
@@ -122,8 +124,8 @@ size_t crt_y_words(const CrtTables& T, int B, int J);
 size_t crt_cols_words(const CrtTables& T, int B, int J);  // in 32-bit words
 
 // Kernel launchers (kernels_res.cu).  Each returns the number of launches issued.
-int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0,
-                  int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st);
+int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc,
+                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st);
 // part: 0 = K2 + K3 (+ general), 1 = K2 only, 2 = K3 (+ general) only.
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part = 0);
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,

@@ -34,23 +34,33 @@ namespace {
 // K1: reduce multiprecision slots modulo the primes.  Limbs are limb-major per curve
 // ([B][L][S]) so consecutive threads (slots) read consecutive words.
 // ---------------------------------------------------------------------------
+// K1: every coefficient (L little-endian 32-bit limbs, sign) modulo every prime, Montgomery
+// form.  One thread per (prime, slot) over a flat index (no idle lanes when S is small):
+//   value R = sum_l limb_l 2^(32 l) R = sum_l mmul(limb_l, R^(l+2))
+// with the weights from a per-prime table: independent products (no Horner chain), each
+// REDC exact for any 32-bit limb (limb * w < 2^32 p), summed with a conditional subtract.
 __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ limbs, const int8_t* __restrict__ sign,
-                                                int S, int L, const PrimeConst* __restrict__ pc, int k0,
+                                                int S, int L, const PrimeConst* __restrict__ pc,
+                                                const uint32_t* __restrict__ rpow, int k0, int nk,
                                                 uint32_t* __restrict__ tab, size_t tab_bstride) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = k0 + blockIdx.y;
-  const int b = blockIdx.z;
-  if (s >= S) return;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (idx >= static_cast<long long>(nk) * S) return;
+  const int kl = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<long long>(kl) * S);
+  const int k = k0 + kl;
   const Mod M = load_mod(pc[k]);
-  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S;
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + s;
+  const uint32_t* w = rpow + static_cast<size_t>(k) * kRedL;
   uint32_t acc = 0;
-  // Horner over limbs from the top: acc <- acc * 2^32 + limb  (in Montgomery form:
-  // mmul(acc, R^2) = acc*2^32, mmul(limb, R^2) = limb in Montgomery form).
-  for (int l = L - 1; l >= 0; --l) {
-    uint32_t v = lb[static_cast<size_t>(l) * S + s];
-    v = v >= 2u * M.p ? v - 2u * M.p : v;  // p > 2^30: v < 4p
-    v = csub(v, M.p);
-    acc = mmul2(acc, M.r2, v, M.r2, M);
+  const int Lt = L < kRedL ? L : kRedL;
+#pragma unroll 4
+  for (int l = 0; l < Lt; ++l) acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], __ldg(&w[l]), M), M.p);
+  if (L > kRedL) {  // very long coefficients: extend the weights by R per limb
+    uint32_t wl = __ldg(&w[kRedL - 1]);
+    for (int l = kRedL; l < L; ++l) {
+      wl = mmul(wl, M.r2, M);
+      acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], wl, M), M.p);
+    }
   }
   if (sign[static_cast<size_t>(b) * S + s] < 0) acc = mneg(acc, M.p);
   tab[b * tab_bstride + static_cast<size_t>(k) * S + s] = acc;
@@ -762,11 +772,12 @@ size_t crt_cols_words(const CrtTables& T, int B, int J) {
   return static_cast<size_t>(B) * J * T.L16 * 2;
 }
 
-int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc, int k0, int nk,
-                  uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
+int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc,
+                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
   if (S == 0 || nk == 0 || B == 0) return 0;
-  dim3 grid((S + 127) / 128, nk, B);
-  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, k0, d_tab, tab_bstride);
+  const long long n = static_cast<long long>(nk) * S;
+  dim3 grid(static_cast<unsigned>((n + 127) / 128), B);
+  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
   return 1;
 }
 

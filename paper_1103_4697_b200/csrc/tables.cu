@@ -22,6 +22,7 @@ CrtTables::~CrtTables() {
   cudaFree(d_Bt8);
   cudaFree(d_M8);
   cudaFree(d_twinv);
+  cudaFree(d_rpow);
 }
 
 std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N) {
@@ -86,6 +87,18 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
       }
     }
   }
+  // K1 limb weights: R^(l+2) mod p, so that mmul(limb, w_l) = limb * 2^(32 l) in Montgomery form.
+  std::vector<uint32_t> rpow(static_cast<size_t>(P) * kRedL);
+  for (int k = 0; k < P; ++k) {
+    const uint64_t p = primes[k], r = (static_cast<uint64_t>(1) << 32) % p;
+    uint64_t x = (r * r) % p;
+    for (int l = 0; l < kRedL; ++l) {
+      rpow[static_cast<size_t>(k) * kRedL + l] = static_cast<uint32_t>(x);
+      x = (x * r) % p;
+    }
+  }
+  CTG_CUDA_CHECK(cudaMalloc(&T->d_rpow, sizeof(uint32_t) * rpow.size()));
+  CTG_CUDA_CHECK(cudaMemcpy(T->d_rpow, rpow.data(), sizeof(uint32_t) * rpow.size(), cudaMemcpyHostToDevice));
   T->h_pc = pc;
   T->log2M = 0;
   for (uint32_t p : primes) T->log2M += std::log2(static_cast<double>(p));
