@@ -286,9 +286,10 @@ __global__ void k_twiddles(const PrimeConst* __restrict__ pc, int P, int N, uint
   twinv[idx] = mpow(pcv.omega_inv, static_cast<uint64_t>(i), load_mod(pcv));
 }
 
+template <int R>
 __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstride, int pitch,
                                                 const PrimeConst* __restrict__ pc,
-                                                const uint32_t* __restrict__ twinv, int k0, int N, int r, int a,
+                                                const uint32_t* __restrict__ twinv, int k0, int N, int a,
                                                 int D, int negate, uint32_t* counters) {
   extern __shared__ uint32_t sm[];
   uint32_t* tw = sm;      // omega^{-i}, i < N
@@ -305,21 +306,22 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
     tw[i] = twk[i];
     const uint32_t val = row[i];
     bad |= (val == kSentinel);
-    const int i1 = i % r, i2 = i / r;
+    const int i1 = i % R, i2 = i / R;  // R is a compile-time 1, 3, 5 or 7
     const int br = a ? static_cast<int>(__brev(static_cast<uint32_t>(i2)) >> (32 - a)) : 0;
     w[i1 * Mlen + br] = val;
   }
   if (bad) atomicOr(&counters[1], kErrSentinel);
   __syncthreads();
-  const int halfM = Mlen >> 1;
-  for (int len = 2; len <= Mlen; len <<= 1) {
-    const int half = len >> 1, step = Mlen / len;
-    for (int bb = tid; bb < r * halfM; bb += bs) {
-      const int rw = bb / halfM, q = bb % halfM;
-      const int g = q / half, t = q % half;
-      uint32_t* base = w + rw * Mlen + g * len;
+  // R radix-2 inverse NTTs of length Mlen (index math by shifts: every length is a power of 2)
+  const int lgh = a - 1;  // log2(Mlen / 2)
+  for (int lg = 1; lg <= a; ++lg) {
+    const int half = 1 << (lg - 1), lgstep = a - lg;
+    for (int bb = tid; bb < (R << lgh); bb += bs) {
+      const int rw = bb >> lgh, q = bb & ((1 << lgh) - 1);
+      const int g = q >> (lg - 1), t = q & (half - 1);
+      uint32_t* base = w + rw * Mlen + (g << lg);
       const uint32_t u = base[t];
-      const uint32_t v = mmul(base[t + half], tw[r * t * step], M);
+      const uint32_t v = mmul(base[t + half], tw[(R * t) << lgstep], M);
       base[t] = madd(u, v, M.p);
       base[t + half] = msub(u, v, M.p);
     }
@@ -328,10 +330,18 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
   bool tail = false;
   for (int j = tid; j < N; j += bs) {
     const int j1 = j & (Mlen - 1);
-    uint32_t acc = 0;
-    for (int i1 = 0; i1 < r; ++i1) {
-      const uint32_t e = static_cast<uint32_t>((static_cast<uint64_t>(i1) * j) % N);
-      acc = madd(acc, mmul(w[i1 * Mlen + j1], tw[e], M), M.p);
+    uint32_t acc;
+    if (R == 1) {
+      acc = w[j1];
+    } else {
+      acc = 0;
+      int e = 0;  // i1 * j mod N, stepped (j < N)
+#pragma unroll
+      for (int i1 = 0; i1 < R; ++i1) {
+        acc = madd(acc, mmul(w[i1 * Mlen + j1], tw[e], M), M.p);
+        e += j;
+        if (e >= N) e -= N;
+      }
     }
     uint32_t c = mmul(acc, pcv.scale, M);  // Montgomery x plain -> plain
     if (negate) c = mneg(c, M.p);
@@ -803,9 +813,19 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
                   cudaStream_t st) {
   if (nk == 0 || B == 0) return 0;
   const size_t smem = static_cast<size_t>(2) * N * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_interp<<<dim3(nk, B), 256, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, r, a, D, negate,
-                                           counters);
+  // one radix-2 butterfly per thread per stage where possible (r * 2^(a-1) of them)
+  int threads = (r << a) / 2;
+  threads = threads < 32 ? 32 : (threads > 256 ? 256 : (threads + 31) / 32 * 32);
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<dim3(nk, B), threads, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, a, D, negate, counters);
+  };
+  switch (r) {
+    case 1: go(k_interp<1>); break;
+    case 3: go(k_interp<3>); break;
+    case 5: go(k_interp<5>); break;
+    default: go(k_interp<7>); break;
+  }
   return 1;
 }
 
