@@ -124,3 +124,27 @@ def test_input_term_order_and_duplicates():
     fo, go = _term_orders(f, rng), _term_orders(curves.derive_y(f), rng)
     for kind in fo:
         assert P.resultant_host(fo[kind], go[kind]) == want, kind
+
+
+def _eval_x(f, x0):
+    """f(x0, y) as a bivariate of x-degree 0."""
+    out = {}
+    for (ex, ey), c in f.items():
+        out[(0, ey)] = out.get((0, ey), 0) + c * x0 ** ex
+    return {k: v for k, v in out.items() if v}
+
+
+@pytest.mark.parametrize("d", [44, 60])
+def test_specialisation_beyond_fast_degrees(d):
+    """deg_y > 40 runs the general formal-degree kernel for every unit.  R(x0) must equal
+    res_y(f(x0, y), f_y(x0, y)) (lc_y f constant: specialisation commutes),
+    checked exactly with the oracle restatement on the univariate specialisations."""
+    import curvetop_oracle as O
+    f = curves.make("dense", d, 8, 7)
+    R = P.resultant(f, curves.derive_y(f))
+    assert len(R) - 1 <= d * (d - 1)
+    for x0 in (0, 1, -2, 3):
+        fx0 = _eval_x(f, x0)
+        want = O.resultant(fx0, O.derive_y(fx0), "y")
+        got = sum(c * x0 ** i for i, c in enumerate(R))
+        assert [got] == want or (got == 0 and want == []), x0
