@@ -54,7 +54,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="d20_b64", choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=64, help="curves per step (seeds 1..B)")
+    ap.add_argument("--batch", type=int, default=256, help="curves per step (seeds 1..B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-headline", action="store_true")
     return ap.parse_args()

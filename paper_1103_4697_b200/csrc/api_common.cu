@@ -316,7 +316,7 @@ class ArenaCache {
   }
 
  private:
-  static constexpr size_t kMaxBlocks = 8;
+  static constexpr size_t kMaxBlocks = 32;
   static constexpr uint64_t kMaxHeld = 1ull << 30;
   std::mutex mu_;
   std::vector<uint8_t*> blocks_;

@@ -902,13 +902,14 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     Ctx& ctx = context(dev);
     std::lock_guard<std::mutex> lock(ctx.mu);
     auto& st = stats_tls();
-    // Chunks of <= kChunk same-shape curves: each is one batched plan (one launch set).
-    constexpr int kChunk = 16;
+    // Chunks of same-shape curves, each one batched plan (one launch set): about four per
+    // group so that D2H + decode of one overlap the kernels of the next, 16..64 curves each.
     std::vector<Chunk> chunks;
     for (auto& [key, idx] : groups) {
-      for (size_t c0 = 0; c0 < idx.size(); c0 += kChunk) {
+      const size_t chunk = std::min<size_t>(64, std::max<size_t>(16, (idx.size() + 3) / 4));
+      for (size_t c0 = 0; c0 < idx.size(); c0 += chunk) {
         Chunk c;
-        c.idx.assign(idx.begin() + c0, idx.begin() + std::min(idx.size(), c0 + kChunk));
+        c.idx.assign(idx.begin() + c0, idx.begin() + std::min(idx.size(), c0 + chunk));
         c.pl.reset(plan_build(probs, c.idx, dev));
         st.n_primes = std::max(st.n_primes, c.pl->P);
         st.n_points = static_cast<int32_t>(c.pl->N);
