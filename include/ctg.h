@@ -11,9 +11,9 @@
  *                                   upoly.hpp:92, elim.cpp:80-93
  *   ctg_square_free_part  replaces  curvetop::square_free_part(p)
  *                                   elim.hpp:45, elim.cpp:204-210
- *   ctg_gcd_bivariate     replaces  curvetop::gcd_bivariate(f, g) when the gcd of the
- *                                   primitive parts is trivial (the square-free-curve case of
- *                                   lift.cpp:85 and pipeline.cpp:321); elim.hpp:42, elim.cpp:178-202
+ *   ctg_gcd_bivariate     replaces  curvetop::gcd_bivariate(f, g)
+ *                                   elim.hpp:42, elim.cpp:178-202 (callers lift.cpp:85,
+ *                                   pipeline.cpp:321)
  *
  * The C++ TU paper_1103_4697_b200/cxx/curvetop_elim_gpu.cpp defines those
  * curvetop:: symbols with the reference's exact signatures on top of this ABI
@@ -119,9 +119,11 @@ ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ct
 /* gcd_bivariate (elim.cpp:178-202): y-contents by GPU univariate gcds, then a GPU probe of
  * gcd(f(a, y), g(a, y)) mod p at several (p, a) with lc_y(f)(a) or lc_y(g)(a) nonzero mod p.
  * A degree-0 image certifies that the primitive parts are coprime; the result is then
- * gcd_univariate(content_y f, content_y g).  Returns CTG_UNSUPPORTED (out untouched) when
- * every probe has positive degree: the primitive parts share a factor, and the caller runs
- * the reference's PRS (the drop-in TU does). */
+ * gcd_univariate(content_y f, content_y g).  Otherwise Brown's modular gcd runs on the GPU
+ * (images gamma(a) * gcd(f(a, y), g(a, y)) mod p with cofactors, Newton interpolation in x,
+ * CRT) and an exactness certificate proves the result; output terms sorted by (dx, dy).
+ * CTG_UNSUPPORTED only beyond the shared-memory limits (y-degree > 6000 or an x-degree
+ * bound above ~1700). */
 ctg_status ctg_gcd_bivariate(const ctg_bipoly* f, const ctg_bipoly* g, ctg_bipoly_buf* out,
                              const ctg_opts* opts);
 

@@ -376,9 +376,8 @@ def resultant(p: dict, q: dict, var: str = "y", device=None) -> list:
 
 
 def gcd_bivariate(f: dict, g: dict, device=None) -> dict:
-    """curvetop::gcd_bivariate (elim.hpp:42, elim.cpp:178-202) when the primitive parts are
-    coprime (square-free curves: lift.cpp:85, pipeline.cpp:321); raises UnsupportedError
-    when they share a factor (the drop-in C++ TU then runs the reference's PRS)."""
+    """curvetop::gcd_bivariate (elim.hpp:42, elim.cpp:178-202): a modular coprimality probe,
+    and Brown's modular bivariate gcd (certified) when the primitive parts share a factor."""
     hf, hg = HostBipoly(f), HostBipoly(g)
     out = _BipolyBuf()
     o = _opts(device)

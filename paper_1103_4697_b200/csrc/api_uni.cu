@@ -568,6 +568,223 @@ bool primitive_parts_coprime(const YPoly& f, const YPoly& g, int dev, cudaStream
   return false;
 }
 
+// ---- small signed Z[x] helpers for the Brown gcd's normalisation (degrees ~ tens) ----
+SBig sb_mul(const SBig& a, const SBig& b) {
+  if (a.sign == 0 || b.sign == 0) return SBig{};
+  return SBig{a.sign * b.sign, big_mul(a.mag, b.mag)};
+}
+
+ZPoly zmul(const ZPoly& a, const ZPoly& b) {
+  if (a.empty() || b.empty()) return ZPoly{};
+  ZPoly r(a.size() + b.size() - 1);
+  for (size_t i = 0; i < a.size(); ++i)
+    for (size_t j = 0; j < b.size(); ++j) {
+      const SBig t = sb_mul(a[i], b[j]);
+      if (t.sign) sbig_add_inplace(r[i + j], t.sign, t.mag.data(), static_cast<int>(t.mag.size()));
+    }
+  while (!r.empty() && r.back().sign == 0) r.pop_back();
+  return r;
+}
+
+// a / c in Z[x] for an exact divisor c (throws CTG_INTERNAL otherwise).
+ZPoly zdivexact(ZPoly a, const ZPoly& c) {
+  const int dc = zdeg(c);
+  if (dc < 0) throw ApiError(CTG_INTERNAL, "zdivexact: zero divisor");
+  if (zdeg(a) < dc) {
+    if (!a.empty()) throw ApiError(CTG_INTERNAL, "zdivexact: inexact division");
+    return a;
+  }
+  ZPoly q(a.size() - dc);
+  for (int t = zdeg(a) - dc; t >= 0; --t) {
+    SBig& top = a[t + dc];
+    if (top.sign == 0) continue;
+    SBig qt{top.sign * c[dc].sign, big_divexact(top.mag, c[dc].mag)};
+    for (int i = 0; i <= dc; ++i) {
+      const SBig m = sb_mul(qt, c[i]);
+      if (m.sign) sbig_add_inplace(a[t + i], -m.sign, m.mag.data(), static_cast<int>(m.mag.size()));
+    }
+    q[t] = std::move(qt);
+  }
+  for (const auto& r : a)
+    if (r.sign != 0) throw ApiError(CTG_INTERNAL, "zdivexact: inexact division");
+  while (!q.empty() && q.back().sign == 0) q.pop_back();
+  return q;
+}
+
+double ylog2_l1(const YPoly& f) {
+  std::vector<double> v;
+  for (const auto& r : f)
+    for (const auto& c : r)
+      if (c.sign) v.push_back(big_log2(c.mag));
+  return log2_sum_upper(v);
+}
+double ylog2_linf(const YPoly& f) {
+  double m = -INFINITY;
+  for (const auto& r : f) m = std::max(m, zlog2_linf(r));
+  return m;
+}
+int ydeg_x(const YPoly& f) {
+  int d = -1;
+  for (const auto& r : f) d = std::max(d, zdeg(r));
+  return d;
+}
+
+uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Brown's modular gcd of f, g in Z[x][y] (replaces the PRS of
+// elim.cpp:184-190 when the primitive parts share a factor).  Returns H = pp_{Z[x]} gcd(f, g)
+// with lc_x(lc_y H) > 0.
+//   gamma = gcd_{Z[x]}(lc_y f, lc_y g) (GPU univariate gcd times the integer gcd of contents)
+//   is a multiple of lc_y gcd(f, g); for every prime p and point a with gamma(a) != 0 the GPU
+//   computes h = gamma(a) * monic gcd(f(a, y), g(a, y)) and the cofactors u = f(a, y) / g,
+//   w = g(a, y) / g (k_bigcd_images); primes whose N points all reach the minimal degree are
+//   interpolated in x (k_newton_interp) and CRT'd (K5) to Ht, U, W in Z[x][y].
+//   Certificate: deg_x Ht <= bH, deg_x U <= deg_x f, deg_x W <= deg_x g with N > bH + max
+//   makes Ht U = gamma f and Ht W = gamma g hold mod every CRT prime as polynomials, and the
+//   norm bounds ||Ht||_1 ||U||_1 < M/2, ||gamma||_1 ||f||_inf < M/2 (same for g) make them exact
+//   over Z; then pp(Ht) divides f and g and has y-degree = the minimal modular degree >=
+//   deg_y gcd(f, g), so it IS the primitive gcd (up to sign).
+YPoly bigcd_modular(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, Launches& L) {
+  const int nf = static_cast<int>(f.size()) - 1, ng = static_cast<int>(g.size()) - 1;
+  const ZPoly& lf = f.back();
+  const ZPoly& lg = g.back();
+  // gamma = gcd(cont lf, cont lg) * gcd_uni(lf, lg)
+  ZPoly gamma = gcd_uni(lf, lg, dev, st, L);
+  {
+    const Big ci = big_gcd(zcontent(lf), zcontent(lg));
+    for (auto& c : gamma) c.mag = big_mul(c.mag, ci);
+  }
+  const int dxf = ydeg_x(f), dxg = ydeg_x(g), dgam = zdeg(gamma);
+  const int bH = dgam + std::min(dxf, dxg);
+  const int N = bH + std::max(dxf, dxg) + 1;
+  if (std::max(nf, ng) > kMaxUniDeg || newton_smem(N) > 227 * 1024)
+    throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: degrees exceed the modular gcd's shared-memory limits");
+  // slot table: rows of f, rows of g, gamma
+  ZPoly slots;
+  std::vector<int32_t> dir;
+  for (const YPoly* h : {&f, &g}) {
+    std::vector<int32_t> o, l;
+    for (const auto& row : *h) {
+      o.push_back(static_cast<int32_t>(slots.size()));
+      l.push_back(static_cast<int32_t>(row.size()));
+      slots.insert(slots.end(), row.begin(), row.end());
+    }
+    dir.insert(dir.end(), o.begin(), o.end());
+    dir.insert(dir.end(), l.begin(), l.end());
+  }
+  const int gam_off = static_cast<int>(slots.size()), gam_len = static_cast<int>(gamma.size());
+  slots.insert(slots.end(), gamma.begin(), gamma.end());
+  const double lgam = zlog2_l1(gamma);
+  const double need = 2 * lgam + ylog2_l1(f) + ylog2_l1(g) + (dxf + nf + dxg + ng) + 2 + 40;
+  double extra = 62;
+  for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
+    DevArena ar(st);
+    const std::vector<uint32_t> primes = select_primes(1, need + extra);
+    const int nk = static_cast<int>(primes.size());
+    auto T = build_tables(dev, primes, 1);
+    uint32_t* tab = reduce_poly(ar, slots, *T, L);
+    std::vector<uint32_t> offs(nk);
+    for (int k = 0; k < nk; ++k)
+      offs[k] = 1u + static_cast<uint32_t>(mix64((static_cast<uint64_t>(primes[k]) << 8) ^ attempt) %
+                                            (primes[k] - static_cast<uint32_t>(N) - 2u));
+    int32_t* d_dir = ar.alloc<int32_t>(dir.size());
+    uint32_t* d_offs = ar.alloc<uint32_t>(nk);
+    CTG_CUDA_CHECK(cudaMemcpyAsync(d_dir, dir.data(), 4 * dir.size(), cudaMemcpyHostToDevice, ar.st));
+    CTG_CUDA_CHECK(cudaMemcpyAsync(d_offs, offs.data(), 4 * nk, cudaMemcpyHostToDevice, ar.st));
+    const int pitch = nf + ng + 3;
+    int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * N);
+    uint32_t* d_img = ar.alloc<uint32_t>(static_cast<size_t>(nk) * N * pitch);
+    L.n += launch_bigcd_images(tab, static_cast<int>(slots.size()), d_dir, nf, ng, gam_off, gam_len, T->d_pc, d_offs,
+                               nk, N, d_deg, d_img, pitch, ar.st);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    std::vector<int32_t> deg(static_cast<size_t>(nk) * N);
+    CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * deg.size(), cudaMemcpyDeviceToHost, ar.st));
+    CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+    stats_tls().d2h_bytes += static_cast<int64_t>(4 * deg.size());
+    int dmin = INT32_MAX;
+    for (int d : deg)
+      if (d >= 0) dmin = std::min(dmin, d);
+    if (dmin == INT32_MAX) continue;
+    if (dmin == 0) return YPoly{ZPoly{SBig{1, Big{1u}}}};
+    std::vector<int> lucky;
+    double bits = 0;
+    for (int k = 0; k < nk; ++k) {
+      bool ok = true;
+      for (int j = 0; j < N && ok; ++j) ok = deg[static_cast<size_t>(k) * N + j] == dmin;
+      if (ok) {
+        lucky.push_back(k);
+        bits += std::log2(static_cast<double>(primes[k]));
+      }
+    }
+    if (bits < need) continue;
+    const int cols = nf + ng - dmin + 3;
+    int32_t* d_idx = ar.alloc<int32_t>(lucky.size());
+    CTG_CUDA_CHECK(cudaMemcpyAsync(d_idx, lucky.data(), 4 * lucky.size(), cudaMemcpyHostToDevice, ar.st));
+    uint32_t* d_coef = ar.alloc<uint32_t>(static_cast<size_t>(nk) * N * cols);
+    L.n += launch_newton_interp(d_img, pitch, d_idx, static_cast<int>(lucky.size()), T->d_pc, d_offs, N, cols, d_coef,
+                                ar.st);
+    CTG_CUDA_CHECK(cudaGetLastError());
+    double log2M = 0;
+    const int total = N * cols;
+    ZPoly all = crt_rows(ar, d_coef, total, lucky, primes, total, {total}, std::vector<uint32_t>(lucky.size(), 1u), dev,
+                         &log2M, L);
+    // unpack: column c = y-row of Ht (c <= dmin), U, W; coefficient t = x-degree
+    auto unpack = [&](int c0, int rows, int bound, YPoly* out) {
+      out->assign(rows, ZPoly{});
+      for (int r = 0; r < rows; ++r) {
+        ZPoly& z = (*out)[r];
+        z.resize(N);
+        for (int t = 0; t < N; ++t) z[t] = std::move(all[static_cast<size_t>(t) * cols + c0 + r]);
+        while (!z.empty() && z.back().sign == 0) z.pop_back();
+        if (zdeg(z) > bound) return false;
+      }
+      while (!out->empty() && out->back().empty()) out->pop_back();
+      return true;
+    };
+    YPoly Ht, U, W;
+    if (!unpack(0, dmin + 1, bH, &Ht) || !unpack(dmin + 1, nf - dmin + 1, dxf, &U) ||
+        !unpack(nf + 2, ng - dmin + 1, dxg, &W))
+      continue;  // an undetected unlucky prime: retry with a fresh prime set
+    if (static_cast<int>(Ht.size()) != dmin + 1) throw ApiError(CTG_INTERNAL, "gcd_bivariate: degree mismatch after CRT");
+    const double lH = ylog2_l1(Ht);
+    const bool ok = lH + ylog2_l1(U) + 1 < log2M - 1 && lH + ylog2_l1(W) + 1 < log2M - 1 &&
+                    lgam + ylog2_linf(f) + 1 < log2M - 1 && lgam + ylog2_linf(g) + 1 < log2M - 1;
+    if (!ok) continue;  // bound too small for these coefficients: more primes
+    // H = pp_{Z[x]}(Ht): integer content, then the primitive gcd of the rows (GPU chain)
+    Big ci;
+    for (const auto& r : Ht)
+      if (!r.empty()) {
+        const Big c = zcontent(r);
+        ci = ci.empty() ? c : big_gcd(ci, c);
+      }
+    ZPoly cx;
+    for (const auto& r : Ht) {
+      if (r.empty()) continue;
+      cx = cx.empty() ? zprimitive_positive(r) : gcd_uni(cx, r, dev, st, L);
+      if (zdeg(cx) == 0) break;
+    }
+    YPoly H(Ht.size());
+    const bool unit_ci = big_is_one(ci);
+    for (size_t r = 0; r < Ht.size(); ++r) {
+      ZPoly row = Ht[r];
+      if (!unit_ci)
+        for (auto& c : row)
+          if (c.sign) c.mag = big_divexact(c.mag, ci);
+      H[r] = zdeg(cx) > 0 ? zdivexact(std::move(row), cx) : std::move(row);
+    }
+    if (H.back().back().sign < 0)
+      for (auto& r : H)
+        for (auto& c : r) c.sign = -c.sign;
+    return H;
+  }
+  throw ApiError(CTG_INTERNAL, "gcd_bivariate: could not certify the modular gcd");
+}
+
 void fill_bipoly_x(const ZPoly& c, ctg_bipoly_buf* out) {
   std::vector<int> idx;
   size_t total = 0;
@@ -763,15 +980,22 @@ ctg_status ctg_gcd_bivariate(const ctg_bipoly* f, const ctg_bipoly* g, ctg_bipol
     std::lock_guard<std::mutex> lock(ctx.mu);
     Launches L;
     const ZPoly cf = content_y(a, dev, ctx.stream, L), cg = content_y(b, dev, ctx.stream, L);
-    if (!primitive_parts_coprime(a, b, dev, ctx.stream, L)) {
-      stats_tls().kernel_launches = L.n;
-      throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: the primitive parts share a factor (no GPU path)");
-    }
-    // elim.cpp:193-201: pp = +-1, result = gcd_univariate(cf, cg) with positive leading coefficient
+    // elim.cpp:193-201: result = pp(gcd) * gcd_univariate(cf, cg), leading (y, then x)
+    // coefficient positive (gcd_univariate's leading coefficient is positive).
     const ZPoly c = gcd_uni(cf, cg, dev, ctx.stream, L);
+    if (primitive_parts_coprime(a, b, dev, ctx.stream, L)) {  // pp = +-1
+      timer.mark_device();
+      stats_tls().kernel_launches = L.n;
+      fill_bipoly_x(c, out);
+      timer.finish();
+      return;
+    }
+    YPoly H = bigcd_modular(a, b, dev, ctx.stream, L);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
-    fill_bipoly_x(c, out);
+    if (!(c.size() == 1 && big_is_one(c[0].mag)))
+      for (auto& r : H) r = zmul(r, c);
+    fill_bipoly(H, out);
     timer.finish();
   });
 }

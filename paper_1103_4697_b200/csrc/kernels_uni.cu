@@ -282,6 +282,117 @@ __global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int
   if (threadIdx.x == 0) deg[unit] = lc_ok ? d : -1;
 }
 
+// ---------------------------------------------------------------------------
+// Modular bivariate gcd (Brown), ctg_gcd_bivariate when the primitive parts share a factor.
+// CTA per unit (prime k, point a = off_k + j): the y-rows of A, B and gamma (gcd of the
+// leading y-coefficients, slot run `gam`) are evaluated at a by Horner; then
+//   g = monic gcd(A(a, y), B(a, y)),  h = gamma(a) g,  u = A(a, y) / g,  w = B(a, y) / g
+// are stored (plain) as h (dg+1) | u (na-dg+1) | w (nb-dg+1) at out[k][j][...], pitch words.
+// deg[k][j] = dg, or -2 when gamma(a) = 0 mod p (then A(a, y) or B(a, y) may drop degree).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bigcd_images(const uint32_t* __restrict__ tab, int S,
+                                                      const int32_t* __restrict__ dir, int na, int nb, int gam_off,
+                                                      int gam_len, const PrimeConst* __restrict__ pc,
+                                                      const uint32_t* __restrict__ offs, int npts,
+                                                      int32_t* __restrict__ deg, uint32_t* __restrict__ out,
+                                                      int pitch) {
+  extern __shared__ uint32_t sm[];
+  __shared__ uint32_t s_gam;
+  const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
+  const Mod M = load_mod_u(pc[k]);
+  const int cap = (na > nb ? na : nb) + 2;
+  uint32_t *A = sm, *Bv = sm + cap, *X = sm + 2 * cap, *Y = sm + 3 * cap, *Q = sm + 4 * cap;
+  const int32_t *offa = dir, *lena = dir + na + 1, *offb = dir + 2 * (na + 1), *lenb = offb + nb + 1;
+  uint32_t av = offs[k] + static_cast<uint32_t>(j);
+  if (av >= M.p) av -= M.p;
+  const uint32_t a = mmul(av, M.r2, M);
+  const uint32_t* t = tab + static_cast<size_t>(k) * S;
+  for (int r = threadIdx.x; r <= na + nb + 2; r += blockDim.x) {
+    const int which = r <= na ? 0 : (r <= na + nb + 1 ? 1 : 2);
+    const int row = which == 0 ? r : r - na - 1;
+    const int off = which == 0 ? offa[row] : (which == 1 ? offb[row] : gam_off);
+    const int len = which == 0 ? lena[row] : (which == 1 ? lenb[row] : gam_len);
+    uint32_t acc = 0u;
+    for (int i = len - 1; i >= 0; --i) acc = madd(mmul(acc, a, M), t[off + i], M.p);
+    if (which == 0) {
+      A[row] = X[row] = acc;
+    } else if (which == 1) {
+      Bv[row] = Y[row] = acc;
+    } else {
+      s_gam = acc;
+    }
+  }
+  __syncthreads();
+  int32_t* dk = deg + static_cast<size_t>(k) * npts + j;
+  if (s_gam == 0u || A[na] == 0u || Bv[nb] == 0u) {
+    if (threadIdx.x == 0) *dk = -2;
+    return;
+  }
+  const uint32_t gam = s_gam;
+  const int dg = blk_gcd(X, na, Y, nb, M);
+  uint32_t* o = out + (static_cast<size_t>(k) * npts + j) * pitch;
+  for (int i = threadIdx.x; i <= dg; i += blockDim.x) o[i] = from_mont(mmul(X[i], gam, M), M);
+  const int du = blk_divexact_monic(A, na, X, dg, Q, M);
+  blk_store_plain(o + dg + 1, Q, du, M);
+  __syncthreads();
+  const int dw = blk_divexact_monic(Bv, nb, X, dg, Q, M);
+  blk_store_plain(o + dg + 1 + du + 1, Q, dw, M);
+  if (threadIdx.x == 0) *dk = dg;
+}
+
+// Newton interpolation in x on the consecutive points a_j = off_k + j (j < N): for row r
+// (prime idx[r]) and column c, the values src[idx[r]][j][c] (plain, pitch src_pitch) become
+// the monomial coefficients dst[idx[r]][t][c] (t < N, plain).  CTA = (32 columns, one row);
+// column c of the CTA lives in shared memory v[j * 32 + lane]: divided differences with
+// spacing j - i (inverses 1..N-1 from a per-CTA table), then Horner with (x - a_i) in place,
+// the growing coefficient array stored reversed in the slots the consumed values free up.
+constexpr int kNewtonCols = 32;
+__global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* __restrict__ src, int src_pitch,
+                                                               const int32_t* __restrict__ idx,
+                                                               const PrimeConst* __restrict__ pc,
+                                                               const uint32_t* __restrict__ offs, int N, int cols,
+                                                               uint32_t* __restrict__ dst) {
+  extern __shared__ uint32_t sm[];
+  const int k = idx[blockIdx.y];
+  const Mod M = load_mod_u(pc[k]);
+  const int lane = threadIdx.x, c = blockIdx.x * kNewtonCols + lane;
+  uint32_t* inv = sm;              // inv[i] = 1 / i (Montgomery), i < N
+  uint32_t* v = sm + N;            // [N][32]
+  for (int i = lane + 1; i < N; i += kNewtonCols) inv[i] = minv(mmul(static_cast<uint32_t>(i), M.r2, M), M);
+  const uint32_t* s = src + static_cast<size_t>(k) * N * src_pitch;
+  for (int j = 0; j < N; ++j) v[j * kNewtonCols + lane] = c < cols ? mmul(s[static_cast<size_t>(j) * src_pitch + c], M.r2, M) : 0u;
+  __syncthreads();
+  // divided differences: v[i] <- (v[i] - v[i-1]) / (a_i - a_{i-d}) = ... / d
+  for (int d = 1; d < N; ++d) {
+    const uint32_t id = inv[d];
+    for (int i = N - 1; i >= d; --i) {
+      const uint32_t x1 = v[i * kNewtonCols + lane], x0 = v[(i - 1) * kNewtonCols + lane];
+      v[i * kNewtonCols + lane] = mmul(msub(x1, x0, M.p), id, M);
+    }
+  }
+  // Horner: cf(x) = v_{N-1}; cf <- cf (x - a_i) + v_i for i = N-2..0.  cf[t] at slot N-1-t.
+  uint32_t ob = offs[k];
+  for (int i = N - 2; i >= 0; --i) {
+    uint32_t ai = ob + static_cast<uint32_t>(i);
+    if (ai >= M.p) ai -= M.p;
+    const uint32_t nai = mneg(mmul(ai, M.r2, M), M.p);
+    const uint32_t vi = v[i * kNewtonCols + lane];
+    const int dgn = N - 1 - i;  // new degree
+    // newcf[t] = cf[t-1] - a_i cf[t]  (cf[dgn] = 0), t = dgn..1;  newcf[0] = v_i - a_i cf[0]
+    uint32_t hi = 0u;  // cf[t] for the t being written (cf[dgn] = 0)
+    for (int t = dgn; t >= 1; --t) {
+      const uint32_t lo = v[(N - 1 - (t - 1)) * kNewtonCols + lane];  // cf[t-1]
+      v[(N - 1 - t) * kNewtonCols + lane] = mmul2(hi, nai, lo, M.one, M);
+      hi = lo;
+    }
+    v[(N - 1) * kNewtonCols + lane] = madd(mmul(hi, nai, M), vi, M.p);
+  }
+  if (c < cols) {
+    uint32_t* o = dst + static_cast<size_t>(k) * N * cols;
+    for (int t = 0; t < N; ++t) o[static_cast<size_t>(t) * cols + c] = from_mont(v[(N - 1 - t) * kNewtonCols + lane], M);
+  }
+}
+
 }  // namespace
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
@@ -309,6 +420,29 @@ int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, i
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_bigcd_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_bigcd_probe<<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg);
+  return 1;
+}
+
+int launch_bigcd_images(const uint32_t* tab, int S, const int32_t* dir, int na, int nb, int gam_off, int gam_len,
+                        const PrimeConst* pc, const uint32_t* offs, int nk, int npts, int32_t* deg, uint32_t* out,
+                        int pitch, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_bigcd_images, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_bigcd_images<<<nk * npts, 128, smem, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg, out, pitch);
+  return 1;
+}
+
+size_t newton_smem(int N) { return static_cast<size_t>(N) * (kNewtonCols + 1) * 4; }
+
+int launch_newton_interp(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, const PrimeConst* pc,
+                         const uint32_t* offs, int N, int cols, uint32_t* dst, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return 0;
+  const size_t smem = newton_smem(N);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_newton_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  dim3 grid((cols + kNewtonCols - 1) / kNewtonCols, rows);
+  k_newton_interp<<<grid, kNewtonCols, smem, st>>>(src, src_pitch, idx, pc, offs, N, cols, dst);
   return 1;
 }
 

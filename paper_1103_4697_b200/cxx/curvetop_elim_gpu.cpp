@@ -12,10 +12,9 @@
 //   square_free_part  -> ctg_square_free_part  (GPU, elim.cpp:204-210)
 //   SquareFreeFactorization::reconstruct, multiplicity_at: same semantics as elim.cpp:74-78,
 //     167-176 (products / sign tests on the host, gcds on the GPU)
-//   gcd_bivariate     -> ctg_gcd_bivariate     (GPU: contents + modular coprimality probe,
-//     elim.cpp:178-202) when the primitive parts are coprime -- every square-free curve's
-//     (f_x, f_y) and (f', f'_y) (lift.cpp:85, pipeline.cpp:321); when they share a factor
-//     (CTG_UNSUPPORTED) the reference's PRS over Z[x][y] runs here with GPU contents.
+//   gcd_bivariate     -> ctg_gcd_bivariate     (GPU, elim.cpp:178-202: contents by modular
+//     univariate gcds, a modular coprimality probe, and Brown's modular bivariate gcd with
+//     an exactness certificate when the primitive parts share a factor)
 //
 // Status codes map to the reference's exceptions: CTG_PRECONDITION -> PreconditionError,
 // anything else -> Error (there is no CPU fallback: a CUDA failure throws).
@@ -107,57 +106,6 @@ UnivariatePolynomial take(ctg_upoly_buf& b) {
   return UnivariatePolynomial(std::move(c));
 }
 
-// ---- Z[x][y] helpers for gcd_bivariate (same results as elim.cpp:17-70) ----
-using ZxY = std::vector<UnivariatePolynomial>;  // y-coefficients in Z[x]
-
-int top_y(const ZxY& a) {
-  int d = static_cast<int>(a.size()) - 1;
-  while (d >= 0 && a[static_cast<size_t>(d)].is_zero()) --d;
-  return d;
-}
-
-// Full content in Z[x] (primitive gcd of the y-coefficients times their integer gcd).
-UnivariatePolynomial content_zx(const ZxY& a) {
-  UnivariatePolynomial g;
-  BigInt ig(0);
-  for (const auto& c : a) {
-    if (c.is_zero()) continue;
-    g = g.is_zero() ? c : gcd_univariate(g, c);  // GPU
-    const BigInt cc = c.content();
-    mpz_gcd(ig.get_mpz_t(), ig.get_mpz_t(), cc.get_mpz_t());
-  }
-  return g.is_zero() ? g : g.primitive_positive() * ig;
-}
-
-ZxY divide_zx(ZxY a, const UnivariatePolynomial& s) {
-  for (auto& c : a)
-    if (!c.is_zero()) c = c.divexact(s);
-  return a;
-}
-
-// lc_y(D)^(deg A - deg D + 1) * A  mod D  in Z[x][y].
-ZxY prem_y(ZxY A, const ZxY& D) {
-  const int dd = top_y(D);
-  if (dd < 0) throw Error("yv_prem: zero divisor");
-  int da = top_y(A);
-  if (da < dd) return A;
-  A.resize(static_cast<size_t>(da) + 1);
-  const UnivariatePolynomial& lead = D[static_cast<size_t>(dd)];
-  for (; da >= dd; --da) {
-    const UnivariatePolynomial t = std::move(A[static_cast<size_t>(da)]);
-    A[static_cast<size_t>(da)] = UnivariatePolynomial();
-    for (int j = 0; j < da; ++j) A[static_cast<size_t>(j)] = A[static_cast<size_t>(j)] * lead;
-    if (t.is_zero()) continue;
-    for (int j = 0; j < dd; ++j) {
-      auto& slot = A[static_cast<size_t>(da - dd + j)];
-      slot = slot - t * D[static_cast<size_t>(j)];
-    }
-  }
-  A.resize(static_cast<size_t>(dd));
-  A.resize(static_cast<size_t>(top_y(A) + 1));
-  return A;
-}
-
 UnivariatePolynomial power(const UnivariatePolynomial& p, int k) {
   UnivariatePolynomial r = UnivariatePolynomial::constant(1);
   while (k-- > 0) r = r * p;
@@ -225,35 +173,14 @@ BivariatePolynomial gcd_bivariate(const BivariatePolynomial& f, const BivariateP
   if (f.is_zero() && g.is_zero()) throw PreconditionError("gcd_bivariate: both inputs zero");
   if (f.is_zero()) return g;
   if (g.is_zero()) return f;
-  {
-    BiMarshal mf(f), mg(g);
-    ctg_bipoly_buf out{};
-    const ctg_status st = ctg_gcd_bivariate(&mf.view, &mg.view, &out, nullptr);
-    if (st == CTG_OK) {
-      BivariatePolynomial::TermMap t;
-      for (int i = 0; i < out.n_terms; ++i)
-        t[{out.dx[i], out.dy[i]}] = from_limbs(out.sign[i], out.limbs + out.limb_off[i], out.limb_off[i + 1] - out.limb_off[i]);
-      ctg_bipoly_free(&out);
-      return BivariatePolynomial(std::move(t));
-    }
-    if (st != CTG_UNSUPPORTED) raise(st, "gcd_bivariate");
-  }
-  // Primitive PRS in y over Z[x] on the x-primitive parts; the x-content gcd is
-  // multiplied back and the leading (y, then x) coefficient made positive.
-  const UnivariatePolynomial cf = content_y(f), cg = content_y(g);
-  ZxY u = divexact_univariate_x(f, cf).y_coeffs();
-  ZxY v = divexact_univariate_x(g, cg).y_coeffs();
-  if (top_y(u) < top_y(v)) std::swap(u, v);
-  while (top_y(v) >= 0) {
-    ZxY r = prem_y(std::move(u), v);
-    const UnivariatePolynomial c = content_zx(r);
-    u = std::move(v);
-    v = c.is_zero() ? ZxY{} : divide_zx(std::move(r), c);
-  }
-  BivariatePolynomial h = BivariatePolynomial::from_y_coeffs(divide_zx(u, content_zx(u))) *
-                          BivariatePolynomial::from_univariate(gcd_univariate(cf, cg), Var::X);
-  if (h.y_coeffs()[static_cast<size_t>(h.degree_y())].leading() < 0) h = -h;
-  return h;
+  BiMarshal mf(f), mg(g);
+  ctg_bipoly_buf out{};
+  check(ctg_gcd_bivariate(&mf.view, &mg.view, &out, nullptr), "gcd_bivariate");
+  BivariatePolynomial::TermMap t;
+  for (int i = 0; i < out.n_terms; ++i)
+    t[{out.dx[i], out.dy[i]}] = from_limbs(out.sign[i], out.limbs + out.limb_off[i], out.limb_off[i + 1] - out.limb_off[i]);
+  ctg_bipoly_free(&out);
+  return BivariatePolynomial(std::move(t));
 }
 
 }  // namespace curvetop

@@ -1,15 +1,22 @@
 #!/bin/bash
-# Round profile capture (run under gpurun): launch list of the default bench command and one
-# ncu --set full capture per hot kernel at d30/128 (batch 4).  Plain runs first (exit 0 gate).
+# Round profile capture (run under gpurun, one GPU): plain runs first (exit-0 gate), then
+#   1. the launch list of the DEFAULT bench command (ncu --metrics gpu__time_duration.sum),
+#   2. K3 DRAM traffic at the default batch (profiles/traffic.json, copied to gpurun_out/prof),
+#   3. one ncu --set full capture per hot kernel of the default workload (first launch each).
+# usage: scripts/profile_round.sh [tag]
 set -e
-mkdir -p gpurun_out/prof
-DEF="python bench.py --steps 2 --warmup 1 --batch 64 --no-cpu-baseline --no-headline"
-$DEF > gpurun_out/prof/plain_default.json 2> gpurun_out/prof/plain_default.err
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv \
-    --log-file gpurun_out/prof/launches_default.csv $DEF > gpurun_out/prof/ncu_default.log 2>&1
-D30="python bench.py --workload d30_b128 --batch 4 --steps 1 --warmup 1 --no-cpu-baseline --no-headline"
-$D30 > gpurun_out/prof/plain_d30.json 2> gpurun_out/prof/plain_d30.err
-for k in k_modres_fast k_eval_ntt k_crt_gemm_i8 k_crt_carry8 k_interp k_reduce; do
-  ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/prof/full_d30_$k $D30 \
-      > gpurun_out/prof/ncu_d30_$k.log 2>&1 || true
+T=${1:-r01}
+O=gpurun_out/prof_$T
+mkdir -p $O
+DEF="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-headline"
+$DEF > $O/plain_default.json 2> $O/plain_default.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $O/launches_default.csv $DEF > $O/ncu_default.log 2>&1
+B=$(python -c "import json;print(json.load(open('$O/plain_default.json'))['config']['curves_per_step'])")
+ONE="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-headline"
+for k in k_modres_fast k_eval_ntt k_gemm_u8_tma k_crt_carry_seq k_crt_prep_t k_interp k_reduce; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o $O/full_$k $ONE \
+      > $O/ncu_full_$k.log 2>&1 || true
 done
+python scripts/traffic_json.py d20_b64 $B $O/full_k_modres_fast.ncu-rep > $O/traffic.log 2>&1 || true
+cp profiles/traffic.json $O/traffic.json || true

@@ -23,7 +23,7 @@ def _sqf(res):
 def test_gcd_bivariate_against_reference():
     rows = load("bivariate_gcd.jsonl")
     assert len(rows) > 80
-    n_gpu = n_unsupported = 0
+    n_coprime = n_shared = 0
     for r in rows:
         f, g = (dec_bipoly(a) for a in r["args"])
         if "error" in r:
@@ -32,15 +32,40 @@ def test_gcd_bivariate_against_reference():
             continue
         want = dec_bipoly(r["result"])
         shares_factor = f and g and any(ey > 0 for (_, ey) in want)
-        if shares_factor:
-            # primitive parts not coprime: outside the GPU path, reported (never a wrong answer)
-            with pytest.raises(P.UnsupportedError):
-                P.gcd_bivariate(f, g)
-            n_unsupported += 1
-        else:
-            assert P.gcd_bivariate(f, g) == want, r
-            n_gpu += 1
-    assert n_gpu >= 60 and n_unsupported >= 5
+        # coprime primitive parts: the probe; a shared factor: Brown's modular gcd + certificate
+        assert P.gcd_bivariate(f, g) == want, r
+        n_shared += bool(shares_factor)
+        n_coprime += not shares_factor
+    assert n_coprime >= 60 and n_shared >= 5
+
+
+def _rand_bipoly(rng, dx, dy, c):
+    return {(i, j): v for i in range(dx + 1) for j in range(dy + 1) if (v := rng.randint(-c, c))}
+
+
+def test_gcd_bivariate_shared_factor_random():
+    """Brown's modular gcd on f = h a, g = h b (h with a non-constant leading y-coefficient,
+    contents in x and integers, lc_y vanishing at small integers) against the oracle's PRS."""
+    import random
+    rng = random.Random(2024)
+    for t in range(24):
+        h = _rand_bipoly(rng, rng.randint(0, 3), rng.randint(1, 3), 30)
+        a = _rand_bipoly(rng, rng.randint(0, 3), rng.randint(0, 3), 30)
+        b = _rand_bipoly(rng, rng.randint(0, 3), rng.randint(0, 3), 30)
+        if t % 4 == 1:  # x-content on both sides (gcd_univariate(cf, cg) factor)
+            a = O.b_mul(a, {(1, 0): 1, (0, 0): -2})
+            b = O.b_mul(b, {(1, 0): 3, (0, 0): -6})
+        if t % 4 == 2:  # integer contents
+            a = {k: 6 * v for k, v in a.items()}
+            b = {k: 10 * v for k, v in b.items()}
+        if t % 4 == 3:  # lc_y(h) = x - 3: vanishes at an integer point
+            dy = max(j for _, j in h)
+            h = {k: v for k, v in h.items() if k[1] != dy}
+            h[(1, dy)], h[(0, dy)] = 1, -3
+        f, g = O.b_mul(h, a), O.b_mul(h, b)
+        if not f or not g:
+            continue
+        assert P.gcd_bivariate(f, g) == O.gcd_bivariate(f, g), t
 
 
 def test_gcd_bivariate_of_config_curve_derivatives():
@@ -66,12 +91,8 @@ def test_teissier_q_against_reference():
         f = _teissier_curve(r)
         fx, fy = curves.derive_x(f), curves.derive_y(f)
         h_ref = dec_bipoly(r["h"])
-        try:
-            h = P.gcd_bivariate(fx, fy)
-            assert h == h_ref
-        except P.UnsupportedError:
-            assert any(ey > 0 for (_, ey) in h_ref)  # only when f_x, f_y share a factor
-            h = h_ref
+        h = P.gcd_bivariate(fx, fy)
+        assert h == h_ref
         if max((ex for ex, _ in h), default=0) > 0 or max((ey for _, ey in h), default=0) > 0:
             fx, fy = O.divexact_bivariate(fx, h), O.divexact_bivariate(fy, h)
         q = P.resultant(fx, fy)
