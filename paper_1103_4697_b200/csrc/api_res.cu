@@ -261,6 +261,7 @@ struct ctg_plan {
   uint32_t* d_vals = nullptr;      // K2 point values [B][P][nrows][N] (fast path only)
   int nrows = 0, maxlen = 0;
   bool fast_ok = false;
+  bool fused = false;              // K2 folded into K3 (k_modres_fused): no d_vals
   int crt_cap = 0;
   int launches = 0;
   bool uploaded = false;
@@ -295,7 +296,7 @@ struct ctg_plan {
     const size_t nch = static_cast<size_t>((P + kCrtChunk - 1) / kCrtChunk);
     size_t s = r(4 * h_limbs.size()) + r(h_sign.size()) + r(4 * dir.size()) + r(4ull * B * P * S) +
                r(4ull * flag_cap) + r(16);
-    if (fast_ok) s += r(4ull * B * P * nrows * N);
+    if (fast_ok && !fused) s += r(4ull * B * P * nrows * N);
     s += r(4 * crt_y_words(*tabs, B, J)) + r(8 * static_cast<size_t>(B) * nch * J) +
          r(8 * ((crt_cols_words(*tabs, B, J) + 1) / 2));
     return s;
@@ -407,6 +408,14 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   if (degb + 1 > kMaxNtt) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 16383");
   pl->D = static_cast<uint32_t>(degb + 1);
   pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
+  {
+    int lp = 4;  // coset NTT length of the fused kernel (res_common.cuh coset_lp(n + 1))
+    while (lp < n + 1) lp <<= 1;
+    // Opt-in (CTG_FUSE=1): measured equal to K2 + K3 on B200 (both are bound by the FMA-heavy
+    // pipe, not by the point-value round trip), but it never materialises the point values.
+    static const bool fuse = std::getenv("CTG_FUSE") != nullptr && std::getenv("CTG_FUSE")[0] == '1';
+    pl->fused = pl->fast_ok && pl->deriv && m == n - 1 && pl->maxlen <= lp && pl->N % lp == 0 && fuse;
+  }
   pl->bound_bits = bound;
   const double need = bound + 1 + 36;
   const auto tb2 = tclk::now();
@@ -432,7 +441,7 @@ static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   pl->palloc(pl->d_tab, static_cast<size_t>(pl->B) * pl->P * pl->S, st);
   pl->palloc(pl->d_flags, pl->flag_cap, st);
   pl->palloc(pl->d_counters, 4, st);
-  if (pl->fast_ok) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
+  if (pl->fast_ok && !pl->fused) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
 }
 
@@ -505,7 +514,8 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   rp.flag_list = pl->d_flags;
   rp.counters = pl->d_counters;
   rp.flag_cap = pl->flag_cap;
-  rp.vals = pl->fast_ok ? pl->d_vals : nullptr;
+  rp.vals = pl->fast_ok && !pl->fused ? pl->d_vals : nullptr;
+  rp.fused = pl->fused ? 1 : 0;
   rp.nrows = pl->nrows;
   rp.maxlen = pl->maxlen;
   rp.twinv = pl->tabs->d_twinv;

@@ -89,6 +89,7 @@ struct ResParams {
   int nrows;                // n + 1 (derivative mode) or n + m + 2
   int maxlen;               // longest slot run (max x-degree + 1) over the rows
   const uint32_t* twinv;    // [P][N] omega_k^{-i} (Montgomery; global prime index k)
+  int fused;                // K2 folded into the K3 launch (k_modres_fused); vals unused
 };
 
 struct CrtParams {

@@ -75,12 +75,6 @@ __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ lim
 // so each thread (prime, row, u) twists <= LP coefficients and runs one LP-point NTT
 // in registers: N (1 + log2(LP)/2) mulmods per row instead of N * len for Horner.
 // ---------------------------------------------------------------------------
-constexpr int bitrev_c(int t, int lg) {
-  int r = 0;
-  for (int i = 0; i < lg; ++i) r |= ((t >> i) & 1) << (lg - 1 - i);
-  return r;
-}
-
 __device__ __forceinline__ void row_slots(const ResParams& P, int r, int& off, int& len) {
   const int nq = P.n + 1;
   if (r < nq) {
@@ -99,47 +93,25 @@ __device__ __forceinline__ uint32_t* vals_row(const ResParams& P, int b, int kl,
 
 template <int LP, int LG>
 __global__ void __launch_bounds__(128) k_eval_ntt(ResParams P, int K) {
+  __shared__ uint32_t tw[LP / 2];
   const int kl = blockIdx.y, b = blockIdx.z;
   const int k = P.k0 + kl;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= P.nrows * K) return;
-  const int r = idx / K, u = idx - r * K;
   const PrimeConst pcv = P.pc[k];
   const Mod M = load_mod(pcv);
+  const uint32_t* twr = P.twinv + static_cast<size_t>(k) * P.N;
+  load_coset_twiddles<LP>(tw, twr, P.N, K, M);
+  __syncthreads();
+  if (idx >= P.nrows * K) return;
+  const int r = idx / K, u = idx - r * K;
   int off, len;
   row_slots(P, r, off, len);
   const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S + off;
   uint32_t a[LP];
-  // omega^j = omega^{-(N - j)}: powers come from the per-prime inverse-twiddle table
-  const uint32_t* twr = P.twinv + static_cast<size_t>(k) * P.N;
-  const uint32_t x = u ? __ldg(&twr[P.N - u]) : M.one;
-  uint32_t tw[LP / 2];  // w^e, w = omega^K of order LP
-  tw[0] = M.one;
-#pragma unroll
-  for (int e = 1; e < LP / 2; ++e) tw[e] = __ldg(&twr[P.N - K * e]);
-  uint32_t xp = M.one;
-#pragma unroll
-  for (int t = 0; t < LP; ++t) {  // c_t x^t
-    const uint32_t c = (t < len) ? tab[t] : 0u;
-    a[bitrev_c(t, LG)] = mmul(c, xp, M);
-    xp = mmul(xp, x, M);
-  }
-#pragma unroll
-  for (int len2 = 2; len2 <= LP; len2 <<= 1) {
-    const int half = len2 >> 1, step = LP / len2;
-#pragma unroll
-    for (int g = 0; g < LP; g += len2) {
-#pragma unroll
-      for (int t = 0; t < half; ++t) {
-        const uint32_t x0 = a[g + t], x1 = mmul(a[g + t + half], tw[t * step], M);
-        a[g + t] = madd(x0, x1, M.p);
-        a[g + t + half] = msub(x0, x1, M.p);
-      }
-    }
-  }
+  coset_ntt<LP, LG>(tab, len, u ? __ldg(&twr[P.N - u]) : M.one, tw, M, a);
   uint32_t* out = vals_row(P, b, kl, r) + u;
 #pragma unroll
-  for (int v = 0; v < LP; ++v) out[static_cast<size_t>(K) * v] = a[v];
+  for (int j = 0; j < LP; ++j) out[static_cast<size_t>(K) * bitrev_c(j, LG)] = a[j];
 }
 
 // Fallback K2 (any row length / N): thread per (prime, row, point), Horner.
@@ -793,6 +765,13 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
 
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
   if (rp.nk == 0 || rp.B == 0) return 0;
+  if (fast && rp.fused) {  // K2 folded into K3: the point values never leave shared memory
+    if (part == 1) return 0;
+    if (dispatch_fused_any(rp.n, rp, st)) {
+      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);
+      return 2;
+    }
+  }
   if (fast && rp.vals && (rp.m == rp.n - 1 || (rp.m == rp.n && !rp.deriv)) && rp.n >= 2 && rp.n <= kFastMaxDeg) {
     const int launches = part == 2 ? 0 : launch_eval(rp, st);  // K2
     if (part == 1) return launches;

@@ -24,6 +24,41 @@ namespace {
 // Resident blocks per SM requested from ptxas (caps registers at 65536 / (128 * minB)).
 constexpr int fast_min_blocks(int n) { return n <= 12 ? 8 : n <= 20 ? 6 : n <= 26 ? 5 : n <= 32 ? 4 : 3; }
 
+// The fused division-free Euclid on A (deg NN), B (deg NN - 1) in registers; returns
+// res(A, B) (EQ: the caller's pre-elimination folded in via bn).  flag != 0 marks a degree
+// drop (the unit goes to the exact general kernel).
+template <int NN, bool EQ>
+__device__ __forceinline__ uint32_t fast_euclid(uint32_t (&A)[NN + 1], uint32_t (&B)[NN + 1], uint32_t bn,
+                                                uint32_t& flag, const Mod& M) {
+  flag |= (A[NN] == 0u) | (B[NN - 1] == 0u);
+  uint32_t U = M.one, E = M.one;
+#pragma unroll
+  for (int kk = NN - 1; kk >= 1; --kk) {
+    const uint32_t bk = B[kk];
+    const uint32_t na = mneg(A[kk + 1], M.p);
+    const uint32_t c1 = mmul(bk, bk, M);                                          // b_k^2
+    const uint32_t c2 = mmul(bk, na, M);                                          // -b_k a_{k+1}
+    const uint32_t c3 = mneg(mmul2(bk, A[kk], na, kk >= 1 ? B[kk - 1] : 0u, M), M.p);  // -A1_k
+    A[0] = mmul2(c1, A[0], c3, B[0], M);
+#pragma unroll
+    for (int t = 1; t < kk; ++t) A[t] = mmul3(c1, A[t], c2, B[t - 1], c3, B[t], M);
+    flag |= (A[kk - 1] == 0u);
+    U = mmul(U, bk, M);
+    if (kk >= 2) E = mmul(E, U, M);
+#pragma unroll
+    for (int t = 0; t <= kk; ++t) {
+      const uint32_t tmp = A[t];
+      A[t] = B[t];
+      B[t] = tmp;
+    }
+  }
+  uint32_t den = mmul(E, E, M);
+  if constexpr (EQ) den = mmul(den, mpow(bn, NN - 1, M), M);
+  uint32_t res = mmul(B[0], minv(den, M), M);
+  if constexpr (EQ && (NN & 1)) res = mneg(res, M.p);
+  return res;
+}
+
 //
 // EQ = true: deg_y p = deg_y q = NN (e.g. Q = res(f_x, f_y) of a curve whose y^n
 // coefficient is constant).  One extra elimination A' = b_n A - a_n B (deg NN - 1) reduces
@@ -70,38 +105,96 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
     }
   }
 
-  flag |= (A[NN] == 0u) | (B[NN - 1] == 0u);
-  uint32_t U = M.one, E = M.one;
-#pragma unroll
-  for (int kk = NN - 1; kk >= 1; --kk) {
-    const uint32_t bk = B[kk];
-    const uint32_t na = mneg(A[kk + 1], M.p);
-    const uint32_t c1 = mmul(bk, bk, M);                                          // b_k^2
-    const uint32_t c2 = mmul(bk, na, M);                                          // -b_k a_{k+1}
-    const uint32_t c3 = mneg(mmul2(bk, A[kk], na, kk >= 1 ? B[kk - 1] : 0u, M), M.p);  // -A1_k
-    A[0] = mmul2(c1, A[0], c3, B[0], M);
-#pragma unroll
-    for (int t = 1; t < kk; ++t) A[t] = mmul3(c1, A[t], c2, B[t - 1], c3, B[t], M);
-    flag |= (A[kk - 1] == 0u);
-    U = mmul(U, bk, M);
-    if (kk >= 2) E = mmul(E, U, M);
-#pragma unroll
-    for (int t = 0; t <= kk; ++t) {
-      const uint32_t tmp = A[t];
-      A[t] = B[t];
-      B[t] = tmp;
-    }
-  }
-  uint32_t den = mmul(E, E, M);
-  if constexpr (EQ) den = mmul(den, mpow(bn, NN - 1, M), M);
-  uint32_t res = mmul(B[0], minv(den, M), M);
-  if constexpr (EQ && (NN & 1)) res = mneg(res, M.p);
+  const uint32_t res = fast_euclid<NN, EQ>(A, B, bn, flag, M);
   uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
   if (flag) {
     out[i] = kSentinel;
     push_flag(P, (static_cast<uint32_t>(b) * P.nk + kl) * P.N + i);
   } else {
     out[i] = res;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused K2+K3 for res(f, f_y) (deg_y q = NN - 1, q = dp/dy, rows of <= LP slots).
+// CTA = (tile of TU = 128 / LP cosets, prime, curve): 128 points {u + K v : u in tile, v < LP}.
+//   phase 1: thread (row r, coset u) evaluates row r at the tile's LP points of coset u by
+//            one LP-point NTT in registers (coset_ntt, as K2) and stores them to shared
+//            memory sv[r][v * TU + (u - u0)] (row stride 128 + TU: conflict-free stores);
+//   phase 2: thread i runs the Euclid of K3 on its point's NN + 1 values sv[.][i].
+// The [B][P][NN+1][N] point-value array of the two-kernel path (K2 store + K3 load, 8 (NN+1)
+// bytes of HBM traffic per unit) is never materialised.
+// ---------------------------------------------------------------------------
+constexpr int fused_min_blocks(int n) { return n <= 24 ? 8 : n <= 32 ? 6 : 4; }
+template <int NN>
+__global__ void __launch_bounds__(128, fused_min_blocks(NN)) k_modres_fused(ResParams P, int K) {
+  constexpr int LP = coset_lp(NN + 1), LG = ilog2_c(LP), TU = 128 / LP, RS = 128 + TU;
+  __shared__ uint32_t sv[(NN + 1) * RS];
+  __shared__ uint32_t tw[LP / 2];
+  const int kl = blockIdx.y, b = blockIdx.z;
+  const int k = P.k0 + kl;
+  const int u0 = blockIdx.x * TU;
+  const PrimeConst pcv = P.pc[k];
+  const Mod M = load_mod(pcv);
+  const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S;
+  const uint32_t* twr = P.twinv + static_cast<size_t>(k) * P.N;
+  load_coset_twiddles<LP>(tw, twr, P.N, K, M);
+  __syncthreads();
+  {
+    const int r = threadIdx.x / TU, uu = threadIdx.x - r * TU, u = u0 + uu;
+    if (r <= NN && u < K) {
+      uint32_t a[LP];
+      coset_ntt<LP, LG>(tab + P.dir[r], P.dir[NN + 1 + r], u ? __ldg(&twr[P.N - u]) : M.one, tw, M, a);
+#pragma unroll
+      for (int j = 0; j < LP; ++j) sv[r * RS + bitrev_c(j, LG) * TU + uu] = a[j];
+    }
+  }
+  __syncthreads();
+  const int uu = threadIdx.x % TU, v = threadIdx.x / TU, u = u0 + uu;
+  if (u >= K) return;
+  const int i = u + K * v;  // the point omega^i of this thread
+  uint32_t A[NN + 1], B[NN + 1];
+#pragma unroll
+  for (int j = 0; j <= NN; ++j) A[j] = sv[j * RS + threadIdx.x];
+  {
+    uint32_t c = M.one;
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      B[j] = mmul(A[j + 1], c, M);
+      c = madd(c, M.one, M.p);
+    }
+  }
+  uint32_t flag = 0u;
+  const uint32_t res = fast_euclid<NN, false>(A, B, 0u, flag, M);
+  uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
+  if (flag) {
+    out[i] = kSentinel;
+    push_flag(P, (static_cast<uint32_t>(b) * P.nk + kl) * P.N + i);
+  } else {
+    out[i] = res;
+  }
+}
+
+template <int NN>
+void launch_fused_n(const ResParams& rp, cudaStream_t st) {
+  constexpr int LP = coset_lp(NN + 1), TU = 128 / LP;
+  const int K = rp.N / LP;
+  dim3 grid((K + TU - 1) / TU, rp.nk, rp.B);
+  k_modres_fused<NN><<<grid, 128, 0, st>>>(rp, K);
+}
+
+template <int G, int NN>
+bool dispatch_fused(int n, const ResParams& rp, cudaStream_t st) {
+  if constexpr (NN > kFastMaxDeg) {
+    return false;
+  } else {
+    if constexpr (fast_group_of(NN) == G) {
+      if (n == NN) {
+        launch_fused_n<NN>(rp, st);
+        return true;
+      }
+    }
+    return dispatch_fused<G, NN + 1>(n, rp, st);
   }
 }
 
@@ -136,5 +229,8 @@ bool dispatch_group(int n, const ResParams& rp, cudaStream_t st) {
   namespace ctg {                                                                                \
   bool dispatch_fast_group_##G(int n, const ResParams& rp, cudaStream_t st) {                    \
     return dispatch_group<G, 2>(n, rp, st);                                                      \
+  }                                                                                              \
+  bool dispatch_fused_group_##G(int n, const ResParams& rp, cudaStream_t st) {                   \
+    return dispatch_fused<G, 2>(n, rp, st);                                                      \
   }                                                                                              \
   }

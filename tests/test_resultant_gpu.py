@@ -148,3 +148,46 @@ def test_specialisation_beyond_fast_degrees(d):
         want = O.resultant(fx0, O.derive_y(fx0), "y")
         got = sum(c * x0 ** i for i, c in enumerate(R))
         assert [got] == want or (got == 0 and want == []), x0
+
+
+_FUSED_CHILD = r"""
+import hashlib, json, sys
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+import paper_1103_4697_b200 as P
+from golden_io import dec_bipoly, dec_upoly, load
+from paper_1103_4697_b200 import curves
+n = 0
+for r in load("configs_small.jsonl"):
+    f = curves.make(*r["curve"])
+    assert P.resultant(f, curves.derive_y(f)) == dec_upoly(r["result"]), r["curve"]
+    n += 1
+for r in load("resultant_random.jsonl"):
+    if r["op"] == "resultant_fy" and "error" not in r:
+        f = dec_bipoly(r["args"][0])
+        assert P.resultant(f, curves.derive_y(f)) == dec_upoly(r["result"]), r
+        n += 1
+for r in load("configs_big.jsonl"):
+    if True:
+        f = curves.make(*r["curve"])
+        R = P.resultant(f, curves.derive_y(f))
+        h = hashlib.sha256(",".join(format(c, "x") for c in R).encode()).hexdigest()
+        assert h == r["sha256"], r["curve"]
+        n += 1
+print(json.dumps({"checked": n, "launches": P.last_call_stats()["kernel_launches"]}))
+"""
+
+
+def test_fused_k2_k3_kernel():
+    """The opt-in fused evaluation + Euclid kernel (CTG_FUSE=1, read once per process) on the
+    res(f, f_y) fixtures and the reference digests of the four big configs."""
+    import json
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CTG_FUSE="1")
+    out = subprocess.run([sys.executable, "-c", _FUSED_CHILD, repo], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["checked"] >= 6
