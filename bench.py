@@ -421,15 +421,19 @@ def yun_line(P, curves, workload):
     for name, (k_, a_, b_) in ((workload, (kind, a, b)), ("sheared_k3", ("sheared", 3, 0))):
         f = curves.make(k_, a_, b_, 1)
         R = P.resultant(f, curves.derive_y(f))
+        hp = P.HostUpoly(R)
         for _ in range(2):
-            P.yun_squarefree(R)
-        ts = []
+            P.yun_squarefree_raw(hp)
+        ts, dev = [], []
         for _ in range(5):
             t0 = time.perf_counter()
-            unit, fac = P.yun_squarefree(R)
+            fac = P.yun_squarefree_raw(hp)
             ts.append(1e3 * (time.perf_counter() - t0))
+            dev.append(P.last_call_stats()["device_ms"])
         out[name] = {"deg_R": len(R) - 1, "gpu_ms_median": statistics.median(ts),
-                     "pattern": "".join(f"({len(p_) - 1})^{m}" for p_, m in fac),
+                     "device_phase_ms_median": statistics.median(dev),
+                     "path": "ctg_yun_squarefree (C ABI), host CSR limbs in/out",
+                     "pattern": "".join(f"({d})^{m}" for d, m in fac),
                      "kernel_launches": P.last_call_stats()["kernel_launches"]}
     out["sheared_k3"]["reference_cpu_s"] = 29.2  # SURVEY §6.2, oracle/_ref in the build container
     return out

@@ -327,6 +327,18 @@ def resultant_raw(p: HostBipoly, q: HostBipoly, var: str = "y", device=None) -> 
     return n
 
 
+def yun_squarefree_raw(p: HostUpoly, device=None) -> list:
+    """ctg_yun_squarefree into library buffers that are freed again (no Python-int decoding):
+    the C-ABI call a C/C++ caller (the drop-in TU) makes.  Returns [(degree, multiplicity)]."""
+    out = _SqfBuf()
+    o = _opts(device)
+    _check(lib().ctg_yun_squarefree(C.byref(p.struct), C.byref(out), C.byref(o)), "yun_squarefree")
+    try:
+        return [(int(out.factors[i].n_coeffs) - 1, int(out.mult[i])) for i in range(out.n_factors)]
+    finally:
+        lib().ctg_sqf_free(C.byref(out))
+
+
 class HostBatch:
     """Caller-owned host operands of a batch of resultants (arrays of ctg_bipoly)."""
 

@@ -30,19 +30,6 @@
 
 namespace ctg {
 
-// Cached per-(device, N, prime list) tables for the resultant path.
-static std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, const std::vector<uint32_t>& primes) {
-  static std::mutex mu;
-  static std::map<std::tuple<int, uint32_t, std::vector<uint32_t>>, std::shared_ptr<CrtTables>> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(device, N, primes);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  auto T = build_tables(device, primes, N);
-  cache[key] = T;
-  return T;
-}
-
 // ---------------------------------------------------------------------------
 // Input parsing (sparse terms keyed (dy, dx), zero terms dropped -- bipoly.cpp:7-15).
 // Terms are kept flat and sorted by (dy, dx): batch calls parse and lay out thousands

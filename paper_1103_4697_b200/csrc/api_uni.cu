@@ -37,6 +37,10 @@ namespace {
 
 using ZPoly = std::vector<SBig>;  // low -> high, trimmed
 
+// Primes of the univariate path: (2^30, 2^30.4), the window where the fused two-elimination
+// pass of blk_gcd (a three-product sum, mmul3) needs one Montgomery reduction.
+std::vector<uint32_t> select_uni_primes(double need_bits) { return select_primes(1, need_bits, kResPrimeMax); }
+
 ZPoly parse_upoly(const ctg_upoly* p) {
   ZPoly out;
   if (!p || p->n_coeffs == 0) return out;
@@ -196,7 +200,7 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
                const std::vector<uint32_t>& scale_plain, int device, double* log2M, Launches& L) {
   std::vector<uint32_t> lp;
   for (int k : lucky) lp.push_back(primes[k]);
-  auto T = build_tables(device, lp, 1);
+  auto T = get_tables(device, 1, lp);
   const int R = static_cast<int>(lp.size());
   const int nseg = static_cast<int>(seg_end.size());
   std::vector<uint32_t> scale_m(static_cast<size_t>(R) * nseg);
@@ -293,7 +297,7 @@ struct YunImages {
 
 YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& primes, int device, Launches& L) {
   const int n = zdeg(P);
-  auto T = build_tables(device, primes, 1);
+  auto T = get_tables(device, 1, primes);
   uint32_t* d_tab = reduce_poly(ar, P, *T, L);
   const int nk = static_cast<int>(primes.size());
   YunImages im;
@@ -317,7 +321,7 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
   YunResult res;
   // Probe: a square-free P is certified by one prime p with p !| lc(P) and deg gcd(P, P') = 0 mod p.
   {
-    std::vector<uint32_t> probe = select_primes(1, 3 * 30.0);
+    std::vector<uint32_t> probe = select_uni_primes(3 * 30.0);
     YunImages im = run_modyun(ar, P, probe, device, L);
     for (size_t k = 0; k < probe.size(); ++k) {
       const int32_t* d = im.deg.data() + k * (n + 1);
@@ -332,7 +336,7 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
   const double need = big_log2(lcP) + n + zlog2_l2(P) + 2 + 40;
   double extra = 62;
   for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
-    std::vector<uint32_t> primes = select_primes(1, need + extra);
+    std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
     YunImages im = run_modyun(ar, P, primes, device, L);
     // lucky pattern: maximal square-free-part degree, then the most frequent pattern
@@ -422,9 +426,9 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
   const double need = std::max({lg + std::min(na, nb) + std::min(la, lb), lg + na + la, lg + nb + lb}) + 2 + 40;
   double extra = 62;
   for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
-    std::vector<uint32_t> primes = select_primes(1, need + extra);
+    std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
-    auto T = build_tables(device, primes, 1);
+    auto T = get_tables(device, 1, primes);
     uint32_t* tA = reduce_poly(ar, A, *T, L);
     uint32_t* tB = reduce_poly(ar, B, *T, L);
     const int pitch = na + nb + 3;
@@ -550,8 +554,8 @@ bool primitive_parts_coprime(const YPoly& f, const YPoly& g, int dev, cudaStream
   }
   if (slots.empty()) return false;
   DevArena ar(st);
-  const std::vector<uint32_t> primes = select_primes(1, 4 * 30.0);
-  auto T = build_tables(dev, primes, 1);
+  const std::vector<uint32_t> primes = select_uni_primes(4 * 30.0);
+  auto T = get_tables(dev, 1, primes);
   uint32_t* tab = reduce_poly(ar, slots, *T, L);
   int32_t* d_dir = ar.alloc<int32_t>(dir.size());
   CTG_CUDA_CHECK(cudaMemcpyAsync(d_dir, dir.data(), 4 * dir.size(), cudaMemcpyHostToDevice, ar.st));
@@ -684,9 +688,9 @@ YPoly bigcd_modular(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, La
   double extra = 62;
   for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
     DevArena ar(st);
-    const std::vector<uint32_t> primes = select_primes(1, need + extra);
+    const std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
-    auto T = build_tables(dev, primes, 1);
+    auto T = get_tables(dev, 1, primes);
     uint32_t* tab = reduce_poly(ar, slots, *T, L);
     std::vector<uint32_t> offs(nk);
     for (int k = 0; k < nk; ++k)

@@ -67,6 +67,10 @@ struct CrtTables {
 };
 // Builds the tables for `primes` (in order) on `device`; N = NTT size (1 if unused).
 std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>& primes, uint32_t N);
+// Cached build_tables (per device, N, prime list; least recently used entries beyond 64 are
+// dropped).  Building costs device allocations and synchronous copies, so every caller --
+// resultant plans, the gcd / Yun images, their CRTs -- goes through the cache.
+std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, const std::vector<uint32_t>& primes);
 
 struct ResParams {
   int B;                    // curves in the batch (blockIdx.z)

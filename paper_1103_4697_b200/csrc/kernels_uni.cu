@@ -27,6 +27,7 @@ __device__ __forceinline__ void swp(uint32_t*& a, uint32_t*& b) {
   b = t;
 }
 
+// Primes p < kResPrimeMax (2^30.4): the fused pass uses mmul3 (modarith.cuh).
 // Monic gcd of X (degree dx) and Y (degree dy), destroying both; the result ends
 // up in X (pointers are swapped as the remainder sequence proceeds).  Degrees are
 // exact (top coefficient nonzero) or -1.  Returns the gcd's degree (-1 if both zero).
@@ -41,6 +42,19 @@ __device__ int blk_gcd(uint32_t*& X, int dx, uint32_t*& Y, int dy, const Mod& M)
   }
   while (dy >= 0) {
     while (dx >= dy) {
+      if (dx == dy + 1 && dy >= 1) {
+        // Two eliminations in one pass (the normal remainder step, as K3):
+        //   X1 = b X - a_{k+1} y Y,  r = b X1 - X1_k Y = b^2 (X mod Y)   (k = dy, b = lc Y)
+        //   r_i = b^2 x_i - b a_{k+1} y_{i-1} - X1_k y_i: three products, one reduction (mmul3).
+        const uint32_t b = Y[dy], na = mneg(X[dx], M.p);
+        const uint32_t c1 = mmul(b, b, M), c2 = mmul(b, na, M);
+        const uint32_t c3 = mneg(mmul2(b, X[dy], na, Y[dy - 1], M), M.p);
+        for (int i = tid; i < dy; i += bs)
+          X[i] = i ? mmul3(c1, X[i], c2, Y[i - 1], c3, Y[i], M) : mmul2(c1, X[0], c3, Y[0], M);
+        __syncthreads();
+        dx = blk_trim(X, dy - 1);
+        continue;
+      }
       // X <- c X - t y^(dx-dy) Y   (c = lc Y, t = lc X): the top coefficient cancels.
       const uint32_t c = Y[dy], t = mneg(X[dx], M.p);
       const int sh = dx - dy;

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "api_common.hpp"
 #include "internal.hpp"
@@ -122,6 +125,30 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
     CTG_CUDA_CHECK(cudaGetLastError());
     CTG_CUDA_CHECK(cudaDeviceSynchronize());
   }
+  return T;
+}
+
+std::shared_ptr<CrtTables> get_tables(int device, uint32_t N, const std::vector<uint32_t>& primes) {
+  using Key = std::tuple<int, uint32_t, std::vector<uint32_t>>;
+  static std::mutex mu;
+  static std::map<Key, std::pair<std::shared_ptr<CrtTables>, uint64_t>> cache;
+  static uint64_t tick = 0;
+  constexpr size_t kCap = 64;
+  std::lock_guard<std::mutex> lock(mu);
+  Key key = std::make_tuple(device, N, primes);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    it->second.second = ++tick;
+    return it->second.first;
+  }
+  auto T = build_tables(device, primes, N);
+  if (cache.size() >= kCap) {
+    auto lru = cache.begin();
+    for (auto j = cache.begin(); j != cache.end(); ++j)
+      if (j->second.second < lru->second.second) lru = j;
+    cache.erase(lru);  // in-flight users hold their own reference
+  }
+  cache.emplace(std::move(key), std::make_pair(T, ++tick));
   return T;
 }
 
