@@ -98,6 +98,17 @@ cudaStream_t Ctx::copy_stream() {
   return copy;
 }
 
+cudaStream_t Ctx::aux_stream() {
+  if (!aux) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CTG_CUDA_CHECK(cudaSetDevice(device));
+    CTG_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    cudaSetDevice(prev);
+  }
+  return aux;
+}
+
 uint8_t* Ctx::pinned_input(size_t bytes) {
   bytes = std::max<size_t>(16, bytes);
   if (pinned_in_bytes < bytes) {

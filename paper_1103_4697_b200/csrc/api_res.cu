@@ -625,10 +625,12 @@ void plan_decode(const ctg_plan* pl, const uint32_t* h, ctg_upoly_buf* out) {
   decode_fill(pl, h, z, out);
 }
 
-// Pipelined execution of a list of chunk plans on one device context.  Compute runs on
-// ctx.stream; each chunk's D2H runs on ctx.copy after an event, so chunk c's copy and host
-// decode overlap chunk c+1's kernels.  Host staging (pinned, in and out) is carved from
-// one buffer per call; device scratch comes from the stream-ordered pool.
+// Streaming execution of chunk plans on one device context.  The caller parses and plans
+// block after block; each chunk is enqueued as soon as its plan exists (H2D from pinned
+// staging, kernels on ctx.stream / ctx.aux alternately, D2H of the exact result on ctx.copy after an event), so
+// the host's parsing / planning of block c+1 and its decoding of block c overlap the GPU.
+// Device scratch and pinned staging are carved from grow-only context regions reserved
+// once per call; a chunk that does not fit drains the pipeline and regrows them.
 struct Chunk {
   std::unique_ptr<ctg_plan> pl;
   std::vector<int> idx;  // positions in the caller's output array
@@ -636,45 +638,79 @@ struct Chunk {
   uint32_t* d_rows = nullptr;
   uint32_t* d_out = nullptr;
   cudaEvent_t computed = nullptr, copied = nullptr;
+  cudaEvent_t t_begin = nullptr, t_computed = nullptr, t_copied = nullptr;  // CTG_TRACE_HOST only
+  double host_enqueued_ms = 0;
 };
 
-void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
-  using clk = std::chrono::steady_clock;
-  auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
-  auto& st = stats_tls();
-  auto t0 = clk::now();
-  size_t in_bytes = 0, out_words = 0;
-  for (auto& c : chunks) {
-    c.in_off = in_bytes;
-    in_bytes += (static_cast<size_t>(plan_h2d_bytes(c.pl.get())) + 255) & ~static_cast<size_t>(255);
-    c.per_curve = static_cast<size_t>(c.pl->D) * c.pl->out_words();
-    c.out_words = c.per_curve * c.pl->B;
-    c.out_off = out_words;
-    out_words += c.out_words + 4;
+struct ChunkNeeds {
+  size_t dev = 0, in = 0, out = 0;  // bytes, bytes, u32 words
+};
+
+ChunkNeeds chunk_needs(const ctg_plan* pl) {
+  ChunkNeeds n;
+  const size_t rows = (4ull * pl->B * pl->P * pl->N + 255) & ~static_cast<size_t>(255);
+  const size_t outw = static_cast<size_t>(pl->D) * pl->out_words() * pl->B;
+  n.dev = pl->scratch_bytes(static_cast<int>(pl->D)) + rows + ((4 * outw + 255) & ~static_cast<size_t>(255));
+  n.in = (static_cast<size_t>(plan_h2d_bytes(pl)) + 255) & ~static_cast<size_t>(255);
+  n.out = outw + 4;
+  return n;
+}
+
+class ChunkPipeline {
+ public:
+  ChunkPipeline(Ctx& ctx, ctg_upoly_buf* out) : ctx_(ctx), out_(out), st_(stats_tls()) {}
+  ~ChunkPipeline() {
+    for (auto& c : inflight_) {  // error path: let the copies finish before the buffers go
+      if (c.copied) cudaEventSynchronize(c.copied);
+      destroy_events(c);
+    }
+    if (t0_) cudaEventDestroy(t0_);
   }
-  // Device scratch of every chunk (plan buffers + residue rows + CRT output) carved from one
-  // grow-only context region: chunks in flight at the same time never share memory.
-  std::vector<size_t> dev_off(chunks.size() + 1, 0);
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    const ctg_plan* pl = chunks[i].pl.get();
-    const size_t rows = (4ull * pl->B * pl->P * pl->N + 255) & ~static_cast<size_t>(255);
-    const size_t outb = (4ull * chunks[i].out_words + 255) & ~static_cast<size_t>(255);
-    dev_off[i + 1] = dev_off[i] + pl->scratch_bytes(static_cast<int>(pl->D)) + rows + outb;
+  // Regions for `need` (nothing may be in flight: growing synchronises and reallocates).
+  void reserve(const ChunkNeeds& need) {
+    drain();
+    dev_ = reinterpret_cast<uint8_t*>(ctx_.scratch_u32(2, need.dev / 4 + 64));
+    dev_cap_ = need.dev + 256;
+    in_ = ctx_.pinned_input(need.in);
+    in_cap_ = need.in;
+    hout_ = ctx_.pinned_u32(need.out);
+    out_cap_ = need.out;
+    dev_used_ = in_used_ = out_used_ = 0;
   }
-  uint8_t* dev_base = reinterpret_cast<uint8_t*>(ctx.scratch_u32(2, dev_off.back() / 4 + 64));
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    ctg_plan* pl = chunks[i].pl.get();
-    pl->bump = dev_base + dev_off[i];
-    pl->bump_off = 0;
-    pl->bump_cap = dev_off[i + 1] - dev_off[i];
-  }
-  uint8_t* h_in = ctx.pinned_input(in_bytes);
-  uint32_t* h_out = ctx.pinned_u32(out_words);
-  cudaStream_t s = ctx.stream, cp = ctx.copy_stream();
-  for (auto& c : chunks) {
+  void enqueue(Chunk&& c) {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     ctg_plan* pl = c.pl.get();
-    plan_upload(pl, s, h_in + c.in_off);
-    st.h2d_bytes += plan_h2d_bytes(pl);
+    const ChunkNeeds n = chunk_needs(pl);
+    if (dev_used_ + n.dev > dev_cap_ || in_used_ + n.in > in_cap_ || out_used_ + n.out > out_cap_) {
+      drain();
+      if (n.dev > dev_cap_ || n.in > in_cap_ || n.out > out_cap_)
+        reserve({std::max(n.dev, dev_cap_), std::max(n.in, in_cap_), std::max(n.out, out_cap_)});
+    }
+    pl->bump = dev_ + dev_used_;
+    pl->bump_off = 0;
+    pl->bump_cap = n.dev;
+    dev_used_ += n.dev;
+    c.in_off = in_used_;
+    in_used_ += n.in;
+    c.per_curve = static_cast<size_t>(pl->D) * pl->out_words();
+    c.out_words = c.per_curve * pl->B;
+    c.out_off = out_used_;
+    out_used_ += n.out;
+    // Chunks alternate between two compute streams, so one chunk's low-occupancy tail (K4,
+    // the CRT carry) overlaps the next chunk's first kernels.
+    cudaStream_t s = (n_enqueued_++ % 2 == 0) ? ctx_.stream : ctx_.aux_stream(), cp = ctx_.copy_stream();
+    if (trace()) {
+      for (cudaEvent_t* e : {&c.t_begin, &c.t_computed, &c.t_copied}) CTG_CUDA_CHECK(cudaEventCreate(e));
+      if (!t0_) {
+        CTG_CUDA_CHECK(cudaEventCreate(&t0_));
+        CTG_CUDA_CHECK(cudaEventRecord(t0_, s));
+        host0_ = t0;
+      }
+      CTG_CUDA_CHECK(cudaEventRecord(c.t_begin, s));
+    }
+    plan_upload(pl, s, in_ + c.in_off);
+    st_.h2d_bytes += plan_h2d_bytes(pl);
     pl->palloc(c.d_rows, static_cast<size_t>(pl->B) * pl->P * pl->N, s);
     pl->palloc(c.d_out, c.out_words, s);
     plan_residues(pl, 0, pl->P, c.d_rows, 0, s);
@@ -682,52 +718,94 @@ void run_chunks(std::vector<Chunk>& chunks, Ctx& ctx, ctg_upoly_buf* out) {
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.copied, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventRecord(c.computed, s));
+    if (trace()) CTG_CUDA_CHECK(cudaEventRecord(c.t_computed, s));
     CTG_CUDA_CHECK(cudaStreamWaitEvent(cp, c.computed, 0));
-    uint32_t* ho = h_out + c.out_off;
+    uint32_t* ho = hout_ + c.out_off;
     CTG_CUDA_CHECK(cudaMemcpyAsync(ho + c.out_words, pl->d_counters, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
     CTG_CUDA_CHECK(cudaMemcpyAsync(ho, c.d_out, sizeof(uint32_t) * c.out_words, cudaMemcpyDeviceToHost, cp));
     CTG_CUDA_CHECK(cudaEventRecord(c.copied, cp));
-    pl->last_stream = cp;  // the plan's own buffers are released after the copies
-    st.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
+    if (trace()) {
+      CTG_CUDA_CHECK(cudaEventRecord(c.t_copied, cp));
+      c.host_enqueued_ms = std::chrono::duration<double, std::milli>(clk::now() - host0_).count();
+    }
+    pl->last_stream = cp;
+    st_.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
+    inflight_.push_back(std::move(c));
+    st_.h2d_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
   }
-  st.h2d_ms += ms_since(t0);
-  std::string err;
-  for (auto& c : chunks) {
-    t0 = clk::now();
-    CTG_CUDA_CHECK(cudaEventSynchronize(c.copied));
-    st.device_ms += ms_since(t0);
-    t0 = clk::now();
-    ctg_plan* pl = c.pl.get();
-    const uint32_t* ho = h_out + c.out_off;
-    st.kernel_launches += pl->launches;
-    st.flagged_units += static_cast<int32_t>(ho[c.out_words]);
-    const uint32_t bits = ho[c.out_words + 1];
-    if (bits && err.empty()) err = "resultant: device self-check failed (error bits " + std::to_string(bits) + ")";
-    if (!err.empty()) continue;
-    // Decode the chunk into one refcounted arena (one allocation for its curves).
-    std::vector<DecodeSize> sz(pl->B);
-    parallel_for(pl->B, [&](int b) { sz[b] = decode_size(pl, ho + c.per_curve * b); });
-    std::vector<size_t> off(pl->B + 1, 0);
-    for (int b = 0; b < pl->B; ++b) off[b + 1] = off[b] + upoly_block_bytes(sz[b].nc, sz[b].total);
-    UpolyArena arena;
-    arena.create(off[pl->B], pl->B);
-    parallel_for(pl->B, [&](int b) {
-      ctg_upoly_buf* o = &out[c.idx[b]];
-      arena.place(o, off[b], sz[b].nc, sz[b].total);
-      decode_fill(pl, ho + c.per_curve * b, sz[b], o);
-    });
-    st.decode_ms += ms_since(t0);
+  // Waits for and decodes every chunk in flight (in order), then frees the regions for reuse.
+  void drain() {
+    using clk = std::chrono::steady_clock;
+    auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
+    for (auto& c : inflight_) {
+      auto t0 = clk::now();
+      CTG_CUDA_CHECK(cudaEventSynchronize(c.copied));
+      st_.device_ms += ms_since(t0);
+      t0 = clk::now();
+      ctg_plan* pl = c.pl.get();
+      const uint32_t* ho = hout_ + c.out_off;
+      st_.kernel_launches += pl->launches;
+      st_.flagged_units += static_cast<int32_t>(ho[c.out_words]);
+      const uint32_t bits = ho[c.out_words + 1];
+      if (bits && err_.empty()) err_ = "resultant: device self-check failed (error bits " + std::to_string(bits) + ")";
+      if (err_.empty()) {
+        // Decode the chunk into one refcounted arena (one allocation for its curves).
+        std::vector<DecodeSize> sz(pl->B);
+        parallel_for(pl->B, [&](int b) { sz[b] = decode_size(pl, ho + c.per_curve * b); });
+        std::vector<size_t> off(pl->B + 1, 0);
+        for (int b = 0; b < pl->B; ++b) off[b + 1] = off[b] + upoly_block_bytes(sz[b].nc, sz[b].total);
+        UpolyArena arena;
+        arena.create(off[pl->B], pl->B);
+        parallel_for(pl->B, [&](int b) {
+          ctg_upoly_buf* o = &out_[c.idx[b]];
+          arena.place(o, off[b], sz[b].nc, sz[b].total);
+          decode_fill(pl, ho + c.per_curve * b, sz[b], o);
+        });
+      }
+      if (trace()) {
+        float a = 0, b = 0, d = 0;
+        cudaEventElapsedTime(&a, t0_, c.t_begin);
+        cudaEventElapsedTime(&b, t0_, c.t_computed);
+        cudaEventElapsedTime(&d, t0_, c.t_copied);
+        std::fprintf(stderr, "[ctg]   chunk B=%d: host enqueued %.3f | gpu begin %.3f computed %.3f copied %.3f | host decoded %.3f ms\n",
+                     pl->B, c.host_enqueued_ms, a, b, d, std::chrono::duration<double, std::milli>(clk::now() - host0_).count());
+      }
+      destroy_events(c);
+      st_.decode_ms += ms_since(t0);
+    }
+    inflight_.clear();
+    dev_used_ = in_used_ = out_used_ = 0;
   }
-  for (auto& c : chunks) {
-    cudaEventDestroy(c.computed);
-    cudaEventDestroy(c.copied);
+  // Drains; throws if a chunk failed its device self-check (the caller frees the results).
+  void finish() {
+    drain();
+    if (!err_.empty()) throw ApiError(CTG_INTERNAL, err_);
   }
-  if (!err.empty()) {
-    for (auto& c : chunks)
-      for (int i : c.idx) ctg_upoly_free(&out[i]);
-    throw ApiError(CTG_INTERNAL, err);
+
+ private:
+  static bool trace() {
+    static const bool t = std::getenv("CTG_TRACE_HOST") != nullptr;
+    return t;
   }
-}
+  static void destroy_events(Chunk& c) {
+    for (cudaEvent_t* e : {&c.computed, &c.copied, &c.t_begin, &c.t_computed, &c.t_copied}) {
+      if (*e) cudaEventDestroy(*e);
+      *e = nullptr;
+    }
+  }
+  Ctx& ctx_;
+  ctg_upoly_buf* out_;
+  ctg_call_stats& st_;
+  std::vector<Chunk> inflight_;
+  std::string err_;
+  uint8_t* dev_ = nullptr;
+  uint8_t* in_ = nullptr;
+  uint32_t* hout_ = nullptr;
+  size_t dev_cap_ = 0, in_cap_ = 0, out_cap_ = 0, dev_used_ = 0, in_used_ = 0, out_used_ = 0;
+  cudaEvent_t t0_ = nullptr;  // trace origin
+  int n_enqueued_ = 0;
+  std::chrono::steady_clock::time_point host0_;
+};
 
 }  // namespace ctg
 
@@ -879,53 +957,93 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     CallTimer timer;
     for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
     std::vector<Problem> probs(batch);
-    parallel_for(batch, [&](int b) { probs[b] = parse_problem(&p[b], &q[b], eliminate_x); });
-    // Group the nontrivial problems by shape; trivial ones are zero polynomials.
-    std::map<std::tuple<int, int, int, int>, std::vector<int>> groups;
-    for (int b = 0; b < batch; ++b) {
-      if (probs[b].trivial) {
-        fill_upoly({}, &out[b]);
-        continue;
-      }
-      groups[{probs[b].n, probs[b].m, probs[b].deriv, probs[b].negate}].push_back(b);
-    }
-    timer.mark_setup();
-    if (groups.empty()) {
-      timer.finish();
-      return;
-    }
-    DeviceGuard g(opts);
-    const int dev = select_device(opts);
-    Ctx& ctx = context(dev);
-    std::lock_guard<std::mutex> lock(ctx.mu);
     auto& st = stats_tls();
-    // Chunks of same-shape curves, each one batched plan (one launch set): about four per
-    // group so that D2H + decode of one overlap the kernels of the next, 16..64 curves each.
-    std::vector<Chunk> chunks;
-    for (auto& [key, idx] : groups) {
-      const size_t chunk = std::min<size_t>(64, std::max<size_t>(16, (idx.size() + 3) / 4));
-      for (size_t c0 = 0; c0 < idx.size(); c0 += chunk) {
-        Chunk c;
-        c.idx.assign(idx.begin() + c0, idx.begin() + std::min(idx.size(), c0 + chunk));
-        c.pl.reset(plan_build(probs, c.idx, dev));
-        st.n_primes = std::max(st.n_primes, c.pl->P);
-        st.n_points = static_cast<int32_t>(c.pl->N);
-        st.n_coeffs = static_cast<int32_t>(c.pl->D);
-        st.out_limbs = std::max(st.out_limbs, c.pl->out_limbs());
-        chunks.push_back(std::move(c));
+    // The device is touched only once a nontrivial problem exists (zero inputs and input
+    // errors behave as before, without a GPU).
+    std::unique_ptr<DeviceGuard> guard;
+    std::unique_lock<std::mutex> lock;
+    std::unique_ptr<ChunkPipeline> pipe;
+    int dev = -1;
+    auto pipeline = [&]() -> ChunkPipeline& {
+      if (!pipe) {
+        guard = std::make_unique<DeviceGuard>(opts);
+        dev = select_device(opts);
+        Ctx& ctx = context(dev);
+        lock = std::unique_lock<std::mutex>(ctx.mu);
+        pipe = std::make_unique<ChunkPipeline>(ctx, out);
       }
+      return *pipe;
+    };
+    // Blocks of consecutive curves: parse, group by shape, plan and enqueue one block while the
+    // GPU runs the previous one (each shape group of a block is one batched plan = one launch
+    // set).  The first and last blocks are small (they are the exposed head -- host parsing
+    // before the GPU starts -- and tail -- the last D2H and decode); the middle ones are large
+    // (fewer, fuller launches).  E.g. 256 curves -> 32 | 96 | 96 | 32.
+    std::vector<int> bounds{0};
+    if (batch <= 32) {
+      bounds.push_back(batch);
+    } else {
+      const int s0 = std::min(32, std::max(8, batch / 8));
+      const int mid = batch - 2 * s0, nm = (mid + 127) / 128, per = (mid + nm - 1) / nm;
+      bounds.push_back(s0);
+      for (int k = 0; k < nm; ++k) bounds.push_back(std::min(s0 + mid, bounds.back() + per));
+      bounds.push_back(batch);
     }
-    const double t_plan = timer.lap();
-    run_chunks(chunks, ctx, out);
-    const double t_run = timer.lap();
-    chunks.clear();
-    parallel_for(batch, [&](int b) { probs[b] = Problem(); });  // release the parsed terms in parallel
-    const double t_rel = timer.lap();
+    bool reserved = false;
+    double t_parse = 0, t_plan = 0;
+    using tclk = std::chrono::steady_clock;
+    try {
+      for (size_t blk = 0; blk + 1 < bounds.size(); ++blk) {
+        const int b0 = bounds[blk], b1 = bounds[blk + 1];
+        if (b1 <= b0) continue;
+        auto t0 = tclk::now();
+        parallel_for(b1 - b0, [&](int i) { probs[b0 + i] = parse_problem(&p[b0 + i], &q[b0 + i], eliminate_x); });
+        std::map<std::tuple<int, int, int, int>, std::vector<int>> groups;
+        for (int b = b0; b < b1; ++b) {
+          if (probs[b].trivial) {
+            fill_upoly({}, &out[b]);
+            continue;
+          }
+          groups[{probs[b].n, probs[b].m, probs[b].deriv, probs[b].negate}].push_back(b);
+        }
+        auto t1 = tclk::now();
+        t_parse += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        for (auto& [key, idx] : groups) {
+          ChunkPipeline& pl_run = pipeline();
+          Chunk c;
+          c.idx = idx;
+          c.pl.reset(plan_build(probs, c.idx, dev));
+          st.n_primes = std::max(st.n_primes, c.pl->P);
+          st.n_points = static_cast<int32_t>(c.pl->N);
+          st.n_coeffs = static_cast<int32_t>(c.pl->D);
+          st.out_limbs = std::max(st.out_limbs, c.pl->out_limbs());
+          if (!reserved) {  // size the regions for the whole call from the first plan
+            const ChunkNeeds n = chunk_needs(c.pl.get());
+            const double f = 1.1 * batch / c.pl->B;
+            pl_run.reserve({static_cast<size_t>(f * n.dev) + n.dev, static_cast<size_t>(f * n.in) + n.in,
+                            static_cast<size_t>(f * n.out) + n.out});
+            reserved = true;
+          }
+          t_plan += std::chrono::duration<double, std::milli>(tclk::now() - t1).count();
+          pl_run.enqueue(std::move(c));
+          t1 = tclk::now();
+        }
+        // the plans hold their own copies of the limbs: release this block's parsed terms
+        // now, while the GPU works, instead of after the last decode
+        parallel_for(b1 - b0, [&](int i) { probs[b0 + i] = Problem(); });
+      }
+      if (pipe) pipe->finish();
+    } catch (...) {
+      pipe.reset();  // waits for copies in flight
+      for (int b = 0; b < batch; ++b) ctg_upoly_free(&out[b]);
+      throw;
+    }
+    st.setup_ms = t_parse + t_plan;
     timer.finish_total();
     static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
     if (trace)
-      std::fprintf(stderr, "[ctg] batch %d: plan %.3f ms, run %.3f ms, release %.3f ms, total %.3f ms\n", batch, t_plan,
-                   t_run, t_rel, st.total_ms);
+      std::fprintf(stderr, "[ctg] batch %d: parse %.3f ms, plan %.3f ms, enqueue %.3f ms, wait %.3f ms, decode %.3f ms, total %.3f ms\n",
+                   batch, t_parse, t_plan, st.h2d_ms, st.device_ms, st.decode_ms, st.total_ms);
   });
 }
 
