@@ -24,12 +24,53 @@ namespace {
 // Resident blocks per SM requested from ptxas (caps registers at 65536 / (128 * minB)).
 constexpr int fast_min_blocks(int n) { return n <= 12 ? 8 : n <= 20 ? 6 : n <= 26 ? 5 : n <= 32 ? 4 : 3; }
 
-// The fused division-free Euclid on A (deg NN), B (deg NN - 1) in registers; returns
-// res(A, B) (EQ: the caller's pre-elimination folded in via bn).  flag != 0 marks a degree
-// drop (the unit goes to the exact general kernel).
+// Montgomery's batch inversion across the CTA (blockDim = 128, all threads call it): returns
+// 1/d for every thread's d (nonzero; threads with nothing to invert pass M.one).  In-warp
+// prefix / suffix products by shuffles, one Fermat inversion of the CTA product by thread 0,
+// then 1/d_i = 1/T * (product of all others): ~13 multiplications per unit instead of the
+// ~45 of a Fermat inversion per unit (the SIMT lanes would each run their own).
+__device__ __forceinline__ uint32_t cta_batch_inverse(uint32_t d, const Mod& M) {
+  constexpr int kWarps = 4;
+  __shared__ uint32_t s_w[kWarps], s_c[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t pf = d, sf = d;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, pf, off);
+    const uint32_t c = __shfl_down_sync(0xffffffffu, sf, off);
+    if (lane >= off) pf = mmul(pf, a, M);
+    if (lane + off < 32) sf = mmul(sf, c, M);
+  }
+  if (lane == 31) s_w[warp] = pf;
+  uint32_t pe = __shfl_up_sync(0xffffffffu, pf, 1), se = __shfl_down_sync(0xffffffffu, sf, 1);
+  if (lane == 0) pe = M.one;
+  if (lane == 31) se = M.one;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t T = M.one;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) T = mmul(T, s_w[w], M);
+    const uint32_t inv = minv(T, M);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      uint32_t c = inv;
+#pragma unroll
+      for (int v = 0; v < kWarps; ++v)
+        if (v != w) c = mmul(c, s_w[v], M);
+      s_c[w] = c;
+    }
+  }
+  __syncthreads();
+  return mmul(mmul(s_c[warp], pe, M), se, M);
+}
+
+// The fused division-free Euclid on A (deg NN), B (deg NN - 1) in registers; returns the
+// numerator of res(A, B) and its (nonzero unless flagged) denominator through den_out (EQ:
+// the caller's pre-elimination folded in via bn).  flag != 0 marks a degree drop (the unit
+// goes to the exact general kernel).
 template <int NN, bool EQ>
 __device__ __forceinline__ uint32_t fast_euclid(uint32_t (&A)[NN + 1], uint32_t (&B)[NN + 1], uint32_t bn,
-                                                uint32_t& flag, const Mod& M) {
+                                                uint32_t& flag, const Mod& M, uint32_t& den_out) {
   flag |= (A[NN] == 0u) | (B[NN - 1] == 0u);
   uint32_t U = M.one, E = M.one;
 #pragma unroll
@@ -54,9 +95,10 @@ __device__ __forceinline__ uint32_t fast_euclid(uint32_t (&A)[NN + 1], uint32_t 
   }
   uint32_t den = mmul(E, E, M);
   if constexpr (EQ) den = mmul(den, mpow(bn, NN - 1, M), M);
-  uint32_t res = mmul(B[0], minv(den, M), M);
-  if constexpr (EQ && (NN & 1)) res = mneg(res, M.p);
-  return res;
+  den_out = den;
+  uint32_t num = B[0];
+  if constexpr (EQ && (NN & 1)) num = mneg(num, M.p);
+  return num;
 }
 
 //
@@ -68,13 +110,16 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
   const int kl = blockIdx.y, b = blockIdx.z;
   const int k = P.k0 + kl;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P.N) return;
+  // Threads past the last point (N < 128 or not a multiple of it) redo point N - 1 and stay
+  // in the CTA for the batch inversion; they store nothing.
+  const bool active = i < P.N;
+  const int ic = active ? i : P.N - 1;
   const PrimeConst pcv = P.pc[k];
   const Mod M = load_mod(pcv);
 
   // Point values p_j(omega^i) (and q_j) from the K2 evaluation kernel: row j of this
   // prime's block, column i -- consecutive threads read consecutive words.
-  const uint32_t* vals = P.vals + (static_cast<size_t>(b) * P.nk + kl) * P.nrows * P.N + i;
+  const uint32_t* vals = P.vals + (static_cast<size_t>(b) * P.nk + kl) * P.nrows * P.N + ic;
   uint32_t A[NN + 1], B[NN + 1];
   uint32_t flag = 0u, bn = 0u;
   if constexpr (EQ) {
@@ -105,13 +150,16 @@ __global__ void __launch_bounds__(128) k_modres_fast(ResParams P) {
     }
   }
 
-  const uint32_t res = fast_euclid<NN, EQ>(A, B, bn, flag, M);
+  uint32_t den;
+  const uint32_t num = fast_euclid<NN, EQ>(A, B, bn, flag, M, den);
+  const uint32_t inv = cta_batch_inverse(flag ? M.one : den, M);
+  if (!active) return;
   uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
   if (flag) {
     out[i] = kSentinel;
     push_flag(P, (static_cast<uint32_t>(b) * P.nk + kl) * P.N + i);
   } else {
-    out[i] = res;
+    out[i] = mmul(num, inv, M);
   }
 }
 
@@ -151,11 +199,12 @@ __global__ void __launch_bounds__(128, fused_min_blocks(NN)) k_modres_fused(ResP
   }
   __syncthreads();
   const int uu = threadIdx.x % TU, v = threadIdx.x / TU, u = u0 + uu;
-  if (u >= K) return;
-  const int i = u + K * v;  // the point omega^i of this thread
+  const bool active = u < K;  // inactive threads redo the tile's first coset (batch inversion)
+  const int i = u + K * v;    // the point omega^i of this thread
   uint32_t A[NN + 1], B[NN + 1];
+  const int col = active ? threadIdx.x : v * TU;
 #pragma unroll
-  for (int j = 0; j <= NN; ++j) A[j] = sv[j * RS + threadIdx.x];
+  for (int j = 0; j <= NN; ++j) A[j] = sv[j * RS + col];
   {
     uint32_t c = M.one;
 #pragma unroll
@@ -164,14 +213,16 @@ __global__ void __launch_bounds__(128, fused_min_blocks(NN)) k_modres_fused(ResP
       c = madd(c, M.one, M.p);
     }
   }
-  uint32_t flag = 0u;
-  const uint32_t res = fast_euclid<NN, false>(A, B, 0u, flag, M);
+  uint32_t flag = 0u, den;
+  const uint32_t num = fast_euclid<NN, false>(A, B, 0u, flag, M, den);
+  const uint32_t inv = cta_batch_inverse(flag ? M.one : den, M);
+  if (!active) return;
   uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch;
   if (flag) {
     out[i] = kSentinel;
     push_flag(P, (static_cast<uint32_t>(b) * P.nk + kl) * P.N + i);
   } else {
-    out[i] = res;
+    out[i] = mmul(num, inv, M);
   }
 }
 
