@@ -191,3 +191,53 @@ def test_fused_k2_k3_kernel():
     assert out.returncode == 0, out.stderr[-2000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["checked"] >= 6
+
+
+def test_batch_streaming_blocks_mixed():
+    """The streaming batch path (small head / tail blocks, large middle blocks, two compute
+    streams, regions sized from the first plan): a long batch interleaving same-shape curves,
+    other shapes, zero operands and a first block smaller than the later plans, against the
+    reference's fixtures and one-shot calls."""
+    import random
+    rng = random.Random(5)
+    fixtures = [r for r in load("resultant_random.jsonl") if r["op"] == "resultant_y" and "error" not in r]
+    items, want = [], []
+    # a head of small curves (the first plan sizes the regions), then bigger ones (regrow)
+    for s in range(1, 40):
+        f = curves.make("dense", 6, 10, s)
+        items.append((f, curves.derive_y(f)))
+        want.append(None)
+    for t in range(160):
+        c = rng.random()
+        if c < 0.35:
+            r = rng.choice(fixtures)
+            items.append((dec_bipoly(r["args"][0]), dec_bipoly(r["args"][1])))
+            want.append(dec_upoly(r["result"]))
+        elif c < 0.4:
+            items.append(({}, {(0, 1): 3}))  # one zero operand -> zero polynomial
+            want.append([])
+        else:
+            f = curves.make("dense", rng.choice([8, 12, 16]), rng.choice([10, 64]), rng.randint(1, 9))
+            items.append((f, curves.derive_y(f)))
+            want.append(None)
+    got = P.resultant_batch(items)
+    assert len(got) == len(items)
+    for (p, q), g, w in zip(items, got, want):
+        assert g == (w if w is not None else P.resultant(p, q))
+    # sizes around the block boundaries
+    for n in (1, 31, 32, 33, 64, 65):
+        sub = items[:n]
+        assert P.resultant_batch(sub) == got[:n]
+
+
+def test_batch_error_in_a_late_block():
+    """Both operands zero in a late block: PreconditionError for the whole call (earlier
+    blocks already ran on the GPU; their results are released), and the library stays usable."""
+    items = []
+    for s in range(1, 80):
+        f = curves.make("dense", 6, 10, s)
+        items.append((f, curves.derive_y(f)))
+    items.append(({}, {}))
+    with pytest.raises(P.PreconditionError):
+        P.resultant_batch(items)
+    assert P.resultant_batch(items[:3]) == [P.resultant(*it) for it in items[:3]]
