@@ -983,8 +983,16 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     if (batch <= 32) {
       bounds.push_back(batch);
     } else {
-      const int s0 = std::min(32, std::max(8, batch / 8));
-      const int mid = batch - 2 * s0, nm = (mid + 127) / 128, per = (mid + nm - 1) / nm;
+      static const int kMid = [] {  // largest middle block (CTG_BLOCK_MAX, for experiments)
+        const char* e = std::getenv("CTG_BLOCK_MAX");
+        return e ? std::max(16, std::atoi(e)) : 128;
+      }();
+      static const int kHead = [] {
+        const char* e = std::getenv("CTG_BLOCK_HEAD");
+        return e ? std::max(4, std::atoi(e)) : 32;
+      }();
+      const int s0 = std::min(kHead, std::max(8, batch / 8));
+      const int mid = batch - 2 * s0, nm = (mid + kMid - 1) / kMid, per = (mid + nm - 1) / nm;
       bounds.push_back(s0);
       for (int k = 0; k < nm; ++k) bounds.push_back(std::min(s0 + mid, bounds.back() + per));
       bounds.push_back(batch);
