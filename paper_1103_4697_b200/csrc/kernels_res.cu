@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
     }
     __syncthreads();
   }
+  // C layout [curve][digit group l / 4][coefficient][4] (see the carry kernel).
   int32_t* Cb = reinterpret_cast<int32_t*>(C.cols) + static_cast<size_t>(b) * C.Jp * C.L8p;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -657,16 +658,18 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
     for (int ni = 0; ni < 4; ++ni) {
       const int r = jb + wm * 64 + mi * 16 + g;
       const int c = lb + wn * 32 + ni * 8 + tig * 2;
-      *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r) * C.L8p + c]) = make_int2(acc[mi][ni][0], acc[mi][ni][1]);
-      *reinterpret_cast<int2*>(&Cb[static_cast<size_t>(r + 8) * C.L8p + c]) = make_int2(acc[mi][ni][2], acc[mi][ni][3]);
+      int32_t* at = Cb + (static_cast<size_t>(c >> 2) * C.Jp + r) * 4 + (c & 3);
+      *reinterpret_cast<int2*>(at) = make_int2(acc[mi][ni][0], acc[mi][ni][1]);
+      *reinterpret_cast<int2*>(at + 32) = make_int2(acc[mi][ni][2], acc[mi][ni][3]);  // row r + 8
     }
 }
 
 
 
 // Carry propagation of V = sum_l C[l] 2^(8 l) - t M (K5 epilogue), one THREAD per coefficient:
-// a sequential walk over the L8 byte digits (16 per limb step, int4 loads of the GEMM
-// columns with 8 in flight per thread, M8 broadcast from L1), then, for V < 0, a two's-
+// a sequential walk over the L8 byte digits (4 per limb step: one int4 of the GEMM output,
+// whose [digit group][coefficient] layout makes every warp load 512 contiguous bytes; 8 loads
+// in flight per thread, M8 broadcast from L1), then, for V < 0, a two's-
 // complement pass over the limbs the same thread just wrote.  Each coefficient is a few
 // hundred to a few thousand digits; thousands of independent walks hide the carry-chain
 // latency.  (Measured on B200 against a warp-per-coefficient lookahead scan, SEG threads per
@@ -685,8 +688,9 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
   const double tr = rint(s);
   if (fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
   const int32_t t = static_cast<int32_t>(tr);
-  const int4* col = reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(C.cols) +
-                                                  (static_cast<size_t>(b) * C.Jp + jl) * C.L8p);
+  // GEMM output [curve][digit group][coefficient] of int4: limb w of this coefficient is
+  // col[w * Jp]; a warp's loads of one limb are consecutive coefficients (coalesced).
+  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(b) * C.Jp * (C.L8p / 4) + jl;
   const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
   uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1) + 1;
   using acc_t = typename std::conditional<WIDE, long long, int>::type;
@@ -699,7 +703,7 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
 #pragma unroll
     for (int i = 0; i < kBatch; ++i) {
       if (w0 + i < OL) {
-        cb[i] = col[w0 + i];
+        cb[i] = col[static_cast<size_t>(w0 + i) * C.Jp];
         mb[i] = __ldg(&m8[w0 + i]);
       }
     }
@@ -847,7 +851,7 @@ static bool launch_gemm_tma(const CrtParams& cp, cudaStream_t st) {
   }();
   if (!attr) return false;
   tma::k_gemm_u8_tma<BN><<<dim3(cp.L8p / BN, static_cast<unsigned>(rows / tma::kBM)), 128, tma::smem_bytes<BN>(), st>>>(
-      ta, tb, reinterpret_cast<int32_t*>(cp.cols), cp.L8p, cp.Kp);
+      ta, tb, reinterpret_cast<int4*>(cp.cols), cp.Jp, cp.L8p / 4, cp.Kp);
   return true;
 }
 

@@ -60,7 +60,7 @@ int run_tma(int M, int N, int K, unsigned seed) {
   const size_t smem = tma::smem_bytes<BN>();
   cudaFuncSetAttribute(tma::k_gemm_u8_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(N / BN, M / tma::kBM);
-  tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, C, N, K);
+  tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, N / 4, K);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("tma kernel error: %s\n", cudaGetErrorString(e));
@@ -72,16 +72,19 @@ int run_tma(int M, int N, int K, unsigned seed) {
   cudaMemcpy(hC.data(), C, 4 * hC.size(), cudaMemcpyDeviceToHost);
   cudaMemcpy(hR.data(), R, 4 * hR.size(), cudaMemcpyDeviceToHost);
   size_t bad = 0, first = 0;
-  for (size_t i = 0; i < hC.size(); ++i)
-    if (hC[i] != hR[i]) {
+  // C is laid out [n / 4][m][n % 4] (one "curve" of M rows); R is row-major [m][n].
+  for (size_t i = 0; i < hR.size(); ++i) {
+    const size_t m = i / N, n = i % N;
+    if (hC[((n / 4) * M + m) * 4 + n % 4] != hR[i]) {
       if (!bad) first = i;
       ++bad;
     }
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int r = 0; r < 5; ++r) tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, C, N, K);
+  for (int r = 0; r < 5; ++r) tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, N / 4, K);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -89,7 +92,7 @@ int run_tma(int M, int N, int K, unsigned seed) {
   ms /= 5;
   const double tops = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
   printf("TMA BN=%d M=%d N=%d K=%d: mismatches %zu", BN, M, N, K, bad);
-  if (bad) printf(" (first at m=%zu n=%zu: got %d want %d)", first / N, first % N, hC[first], hR[first]);
+  if (bad) printf(" (first at m=%zu n=%zu: want %d)", first / N, first % N, hR[first]);
   printf("  time %.3f ms  %.1f TOPS\n", ms, tops);
   cudaFree(A);
   cudaFree(B);
