@@ -241,3 +241,34 @@ def test_batch_error_in_a_late_block():
     with pytest.raises(P.PreconditionError):
         P.resultant_batch(items)
     assert P.resultant_batch(items[:3]) == [P.resultant(*it) for it in items[:3]]
+
+
+def test_concurrent_calls_from_threads():
+    """Entry points are re-entrant (SURVEY §8(b) threading row): resultants, batches, Yun and
+    gcds issued from several host threads at once (ctypes drops the GIL during the calls) give
+    the single-threaded results."""
+    import threading
+    fs = [curves.make("dense", d, 16, s) for d, s in [(8, 1), (10, 2), (12, 3), (9, 4)]]
+    pairs = [(f, curves.derive_y(f)) for f in fs]
+    want_r = [P.resultant(*pq) for pq in pairs]
+    want_y = [P.yun_squarefree(r) for r in want_r]
+    want_g = P.gcd_univariate(want_r[0], want_r[1])
+    errors = []
+
+    def work(t):
+        try:
+            for it in range(6):
+                i = (t + it) % len(pairs)
+                assert P.resultant(*pairs[i]) == want_r[i]
+                assert P.yun_squarefree(want_r[i]) == want_y[i]
+                assert P.resultant_batch(pairs) == want_r
+                assert P.gcd_univariate(want_r[0], want_r[1]) == want_g
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errors, errors[0]
