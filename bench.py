@@ -44,6 +44,21 @@ WORKLOADS = {
                   1031 * 241),
 }
 REFDRIVER = os.path.join(REPO, "oracle", "_ref", "refdriver")
+# Per-curve units (P * D with P = primes the curve ALONE needs, D = coefficients of its R) for
+# seeds 1..n of every workload (scripts/units_table.py): both arms count the same units per
+# curve, whatever prime count a batched plan happens to use.
+UNITS_FILE = os.path.join(REPO, "bench_units.json")
+
+
+def curve_units(workload, seeds):
+    try:
+        with open(UNITS_FILE) as fh:
+            table = json.load(fh)[workload]
+    except (OSError, KeyError, ValueError):
+        return None
+    if max(seeds) > len(table):
+        return None
+    return sum(table[s - 1] for s in seeds)
 CACHED_REF_SECONDS = {"d30_b128": 1700.4, "d16_b1024": 291.7, "d20_b64": 27.7, "d10_b10": 0.022}  # this container
 
 
@@ -152,22 +167,25 @@ def reference_arm(args):
     # warm-up: a tiny reference call per step (the CPU has nothing to warm beyond page-in)
     for _ in range(args.warmup):
         run_refdriver("dense", 6, 10, 1)
-    walls = []
+    walls, done_units = [], 0
     for step in range(args.steps):
+        seeds = [1 + (step * cores + c) % 64 for c in range(cores)]
         t0 = time.perf_counter()
-        procs = [subprocess.Popen([REFDRIVER, "time_res", kind, str(a), str(b), str(1 + (step * cores + c) % 64), "1"],
-                                  stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for c in range(cores)]
+        procs = [subprocess.Popen([REFDRIVER, "time_res", kind, str(a), str(b), str(s_), "1"],
+                                  stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for s_ in seeds]
         for p in procs:
             p.wait()
         walls.append(time.perf_counter() - t0)
+        done_units += curve_units(args.workload, seeds) or units * cores
     total = sum(walls)
-    value = args.steps * cores * units / total
+    value = done_units / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32 (GMP mpz)",
         "data": "synthetic", "config": {"workload": desc, "curves_per_step": cores, "seeds": "1..64 cycling",
-                                        "units_per_curve": units},
+                                        "units_per_step": done_units / args.steps,
+                                        "units": "P * D per curve, P = primes the curve alone needs (bench_units.json)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{cores} curves per step (one per core, independent processes), "
                                    f"curvetop::resultant(f, f_y, Y) from oracle/_ref/refdriver"},
@@ -214,7 +232,9 @@ def main_ours(args):
     info = plan.info
     Pn, N, D = info["n_primes"], info["n_points"], info["n_coeffs"]
     W = info["out_limbs"] + 1
-    units_step = B * Pn * D  # mod-p resultants per step (P * D per curve)
+    # mod-p resultants per step: P * D per curve with the curve's own prime count (the batched
+    # plan may use a few more primes, for the largest bound of the batch: not counted)
+    units_step = curve_units(args.workload, range(1, B + 1)) or B * Pn * D
     G = world
     k0, k1, Pb = sharding.prime_block(Pn, G, rank)  # rows per rank block (uniform for the all-gather)
     j0, j1, Jb = sharding.coeff_block(D, G, rank)
@@ -331,6 +351,7 @@ def main_ours(args):
         "dtype": "u32 (31-bit modular, Montgomery)", "data": "synthetic",
         "config": {"workload": desc, "curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N,
                    "coeffs": D, "units_per_step": units_step,
+                   "units": "P * D per curve, P = primes the curve alone needs (bench_units.json)",
                    "parallelism": f"prime-shard{G}" if G > 1 else "single",
                    "l2": "flushed (256 MB write) between timed steps",
                    "res_ms_per_curve": ms_per_step / B},
@@ -445,6 +466,7 @@ def cpu_baseline(workload, units_per_curve):
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
     secs = r["res_seconds_best"]
+    units_per_curve = curve_units(workload, [1]) or units_per_curve
     return {"value": units_per_curve / secs, "unit": UNIT, "cores": 1, "kind": "reference",
             "sample": f"1 curve {kind}({a},{b},seed=1): curvetop::resultant(f, f_y, Y), 1 thread, {secs:.2f} s",
             "seconds_per_curve": secs}
