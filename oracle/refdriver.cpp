@@ -12,6 +12,14 @@
 //   refdriver time_res KIND A B SEED REPS [yun]
 //                                       -> JSON line: wall seconds of resultant(f, f_y, Y)
 //                                          (+ yun_squarefree(R) when "yun" is given)
+//   refdriver time_ctx KIND A B SEED REPS [q]
+//                                       -> JSON line: wall seconds of the reference's own
+//                                          caller CurveContext(f) (lift.cpp:59-68: R = res(f,
+//                                          f_y) + Yun(R)) and, with "q", of resultant_q() +
+//                                          q_factorization() (lift.cpp:76-101: gcd_bivariate,
+//                                          Q, Yun(Q)).  Built twice: against the reference's
+//                                          elim.cpp (refdriver) and against the GPU drop-in TU
+//                                          (refdriver_gpu) -- the same caller, both libraries.
 //
 // Request format (text):
 //   OP <resultant_y|resultant_x|resultant_fy|yun|gcd|sqfp|gcd_bivariate|curve_q>
@@ -319,6 +327,35 @@ int cmd_time_res(const std::string& kind, int a, int b, unsigned long seed, int 
   return 0;
 }
 
+int cmd_time_ctx(const std::string& kind, int a, int b, unsigned long seed, int reps, bool q) {
+  BPoly f = make_curve(kind, a, b, seed);
+  double best = 1e300, best_q = 1e300;
+  int deg_r = -1, deg_q = -1;
+  std::string pattern;
+  for (int i = 0; i < reps; ++i) {
+    double t0 = now();
+    CurveContext ctx(f);
+    const double dt = now() - t0;
+    best = std::min(best, dt);
+    deg_r = ctx.resultant_r().degree();
+    pattern.clear();
+    for (const auto& fac : ctx.r_factorization().factors)
+      pattern += "(" + std::to_string(fac.poly.degree()) + ")^" + std::to_string(fac.multiplicity);
+    if (q) {
+      t0 = now();
+      deg_q = ctx.resultant_q().degree();
+      (void)ctx.q_factorization();
+      best_q = std::min(best_q, now() - t0);
+    }
+  }
+  std::cout << "{\"kind\":\"" << kind << "\",\"a\":" << a << ",\"b\":" << b << ",\"seed\":" << seed
+            << ",\"reps\":" << reps << ",\"ctx_seconds_best\":" << best << ",\"deg_r\":" << deg_r
+            << ",\"r_pattern\":\"" << pattern << "\"";
+  if (q) std::cout << ",\"q_seconds_best\":" << best_q << ",\"deg_q\":" << deg_q;
+  std::cout << "}" << std::endl;
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -336,7 +373,10 @@ int main(int argc, char** argv) {
     if (cmd == "time_res" && argc >= 7)
       return cmd_time_res(argv[2], std::atoi(argv[3]), std::atoi(argv[4]), std::stoul(argv[5]),
                           std::atoi(argv[6]), argc >= 8 && std::string(argv[7]) == "yun");
-    std::cerr << "usage: refdriver gen|batch|elim_cases|time_res ...\n";
+    if (cmd == "time_ctx" && argc >= 7)
+      return cmd_time_ctx(argv[2], std::atoi(argv[3]), std::atoi(argv[4]), std::stoul(argv[5]),
+                          std::atoi(argv[6]), argc >= 8 && std::string(argv[7]) == "q");
+    std::cerr << "usage: refdriver gen|batch|elim_cases|time_res|time_ctx ...\n";
     return 2;
   } catch (const std::exception& e) {
     std::cerr << "refdriver: " << e.what() << "\n";
