@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) k_eval_ntt(ResParams P, int K) {
   row_slots(P, r, off, len);
   const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S + off;
   uint32_t a[LP];
-  coset_ntt<LP, LG>(tab, len, twr, P.N, u, tw, M, a);
+  coset_ntt<LP, LG>(tab, len, u ? __ldg(&twr[P.N - u]) : M.one, tw, M, a);
   uint32_t* out = vals_row(P, b, kl, r) + u;
 #pragma unroll
   for (int j = 0; j < LP; ++j) out[static_cast<size_t>(K) * bitrev_c(j, LG)] = a[j];

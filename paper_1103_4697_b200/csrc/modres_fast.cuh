@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(128, fused_min_blocks(NN)) k_modres_fused(ResP
     const int r = threadIdx.x / TU, uu = threadIdx.x - r * TU, u = u0 + uu;
     if (r <= NN && u < K) {
       uint32_t a[LP];
-      coset_ntt<LP, LG>(tab + P.dir[r], P.dir[NN + 1 + r], twr, P.N, u, tw, M, a);
+      coset_ntt<LP, LG>(tab + P.dir[r], P.dir[NN + 1 + r], u ? __ldg(&twr[P.N - u]) : M.one, tw, M, a);
 #pragma unroll
       for (int j = 0; j < LP; ++j) sv[r * RS + bitrev_c(j, LG) * TU + uu] = a[j];
     }

@@ -25,23 +25,18 @@ constexpr int bitrev_c(int t, int lg) {
 // Decimation in frequency: natural-order input, output in bit-reversed order, i.e.
 // a[j] = value at v = bitrev(j) -- callers fold the permutation into their store addresses,
 // so every register-array index stays a compile-time constant (no local-memory arrays).
-// The twist powers omega^{t u} are read from the prime's omega^{-i} table twr (omega^j =
-// twr[N - j], L1-resident) instead of a multiplication chain: one multiplication per slot
-// on the FMA-heavy pipe that bounds the kernel, the power itself on the load pipe.
-// tw = w^e (e < LP/2, w = omega^K of order LP) in shared memory (a broadcast read per
-// butterfly, no registers held).  Shared by K2 and the fused K2+K3 kernel.
+// x = omega^u; tw = w^e (e < LP/2, w = omega^K of order LP) in shared memory (a broadcast
+// read per butterfly, no registers held).  Shared by K2 and the fused K2+K3 kernel.
 template <int LP, int LG>
-static __device__ __forceinline__ void coset_ntt(const uint32_t* __restrict__ c, int len,
-                                                 const uint32_t* __restrict__ twr, int N, int u,
+static __device__ __forceinline__ void coset_ntt(const uint32_t* __restrict__ c, int len, uint32_t x,
                                                  const uint32_t* tw, const Mod& M, uint32_t (&a)[LP]) {
-  int e = 0;  // t u mod N
+  uint32_t xp = M.one;
 #pragma unroll
-  for (int t = 0; t < LP; ++t) {  // c_t omega^{t u} (slots past the row length are zero)
+  for (int t = 0; t < LP; ++t) {  // c_t x^t (slots past the row length are zero)
     uint32_t v = 0u;
     if (t < len) {
-      v = t ? mmul(c[t], __ldg(&twr[e ? N - e : 0]), M) : c[0];
-      e += u;
-      if (e >= N) e -= N;
+      v = mmul(c[t], xp, M);
+      xp = mmul(xp, x, M);
     }
     a[t] = v;
   }
