@@ -740,6 +740,129 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
   out[-1] = static_cast<uint32_t>(sign);
 }
 
+
+// Same carry propagation with a WARP per coefficient, for calls with few coefficients (single
+// curves: 871 coefficients at d30 or 241 at d16/1024 leave the thread-per-coefficient walk
+// with 7 or 2 CTAs walking 1,000-4,000 digits each).  Lane l walks limbs [l S, (l+1) S) with
+// a local carry starting at 0 and keeps, for its segment L_l: the low 64 bits, whether the
+// limbs above them are all ones / all zeros, and its carry-out c_l (|c_l| < 2^42).  Adding a
+// carry-in to L_l can only overflow (+1) or underflow (-1) through those flags, so a 32-step
+// shuffle recurrence gives every lane its carry-in; each lane then adds it to its own limbs
+// (the ripple normally stops after two limbs) and, for V < 0, negates its limbs in parallel
+// (two's complement: zeros below the lowest nonzero limb, -limb there, ~limb above).
+template <bool WIDE>
+__global__ void __launch_bounds__(128) k_crt_carry_warp(CrtParams C) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gw >= C.J * C.B) return;  // whole warps exit together
+  const int b = gw / C.J, jl = gw - b * C.J;
+  const int OL = C.out_limbs;
+  const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+  double sp = 0;
+  for (int q = lane; q < nch; q += 32) sp += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
+#pragma unroll
+  for (int off = 16; off; off >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, off);
+  const double tr = rint(sp);
+  if (lane == 0 && fabs(sp - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  const int32_t t = static_cast<int32_t>(tr);
+  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(b) * C.Jp * (C.L8p / 4) + jl;
+  const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
+  uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1) + 1;
+  const int S = (OL + 31) / 32, w0 = lane * S, w1 = min(OL, w0 + S);
+  using acc_t = typename std::conditional<WIDE, long long, int>::type;
+  acc_t carry = 0;
+  uint32_t lo0 = 0, lo1 = 0;
+  bool ones = true, zeros = true;  // limbs w0+2 .. w1-1
+  constexpr int kBatch = 8;  // loads in flight per lane
+  for (int wb = w0; wb < w1; wb += kBatch) {
+    int4 cb[kBatch];
+    uint4 mb[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i)
+      if (wb + i < w1) {
+        cb[i] = col[static_cast<size_t>(wb + i) * C.Jp];
+        mb[i] = __ldg(&m8[wb + i]);
+      }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+    const int w = wb + i;
+    if (w >= w1) break;
+    const int4 c = cb[i];
+    const uint4 m = mb[i];
+    acc_t v = carry + c.x - static_cast<acc_t>(t) * static_cast<int>(m.x);
+    uint32_t limb = static_cast<uint32_t>(v) & 0xffu;
+    v = (v >> 8) + c.y - static_cast<acc_t>(t) * static_cast<int>(m.y);
+    limb |= (static_cast<uint32_t>(v) & 0xffu) << 8;
+    v = (v >> 8) + c.z - static_cast<acc_t>(t) * static_cast<int>(m.z);
+    limb |= (static_cast<uint32_t>(v) & 0xffu) << 16;
+    v = (v >> 8) + c.w - static_cast<acc_t>(t) * static_cast<int>(m.w);
+    limb |= static_cast<uint32_t>(v) << 24;
+    carry = v >> 8;
+    out[w] = limb;
+    if (w == w0) lo0 = limb;
+    else if (w == w0 + 1) lo1 = limb;
+    else {
+      ones &= (limb == 0xffffffffu);
+      zeros &= (limb == 0u);
+    }
+    }
+  }
+  const int nseg = w1 > w0 ? w1 - w0 : 0;  // limbs in my segment (0 for idle lanes)
+  const uint64_t lo = static_cast<uint64_t>(lo0) | (static_cast<uint64_t>(lo1) << 32);
+  const long long co = static_cast<long long>(carry);
+  // carry-in of every lane: ci_0 = 0, ci_{l+1} = c_l + ovf_l(ci_l)
+  long long c = 0, my_ci = 0;
+  for (int l = 0; l < 32; ++l) {
+    const uint64_t llo = __shfl_sync(0xffffffffu, lo, l);
+    const long long lco = __shfl_sync(0xffffffffu, co, l);
+    const int lns = __shfl_sync(0xffffffffu, nseg, l);
+    const unsigned lflags = __ballot_sync(0xffffffffu, ones) >> l & 1u;
+    const unsigned lzero = __ballot_sync(0xffffffffu, zeros) >> l & 1u;
+    if (lane == l) my_ci = c;
+    if (lns == 0) continue;  // idle lane: carries pass through
+    // ovf of L + c over the segment's 32 * lns bits (|c| < 2^42)
+    long long ovf = 0;
+    if (lns <= 2) {  // the whole segment is in llo (lns = 1: one limb)
+      const int bits = 32 * lns;
+      const unsigned __int128 full = static_cast<unsigned __int128>(llo);
+      const __int128 sum = static_cast<__int128>(full) + c;
+      const __int128 modv = static_cast<__int128>(1) << bits;
+      ovf = sum >= modv ? 1 : (sum < 0 ? -1 : 0);
+    } else {
+      const uint64_t nlo = llo + static_cast<uint64_t>(c);
+      if (c > 0 && nlo < llo && lflags) ovf = 1;
+      if (c < 0 && nlo > llo && lzero) ovf = -1;
+    }
+    c = lco + ovf;
+  }
+  // c is the carry out of the top limb: 0 (V >= 0) or -1 (V < 0); apply my carry-in
+  if (my_ci != 0 && nseg > 0) {
+    long long cc = my_ci;
+    for (int w = w0; w < w1 && cc != 0; ++w) {
+      const long long x = static_cast<long long>(out[w]) + cc;
+      out[w] = static_cast<uint32_t>(x);
+      cc = x >> 32;  // arithmetic: borrow -1, carry +1, or the carry's high part
+    }
+  }
+  __syncwarp();
+  const int sign_neg = c < 0;
+  uint32_t any = 0;
+  for (int w = w0; w < w1; ++w) any |= out[w];
+  const unsigned nz = __ballot_sync(0xffffffffu, any != 0u);
+  if (sign_neg) {
+    const int zl = __ffs(nz) - 1;  // first lane holding a nonzero limb
+    bool seen = lane > zl;
+    for (int w = w0; w < w1; ++w) {
+      const uint32_t x = out[w];
+      if (seen) {
+        out[w] = ~x;
+      } else if (x != 0u) {
+        out[w] = 0u - x;
+        seen = true;
+      }
+    }
+  }
+  if (lane == 0) out[-1] = static_cast<uint32_t>(sign_neg ? -1 : (nz ? 1 : 0));
+}
 }  // namespace
 
 size_t crt_y_words(const CrtTables& T, int B, int J) {
@@ -866,7 +989,16 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
     if (!done) k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
     // 4P * 255^2 + 2^25 < 2^31: the per-digit sum fits int32
     const bool wide = static_cast<double>(cp.P) * 4 * 255 * 255 + 33554432.0 >= 2147483648.0;
-    const unsigned blocks = static_cast<unsigned>((static_cast<long long>(cp.J) * cp.B + 127) / 128);
+    const long long coeffs = static_cast<long long>(cp.J) * cp.B;
+    if (coeffs * 64 < 148LL * 2048) {  // under half a wave of threads: a warp per coefficient
+      const unsigned blocks = static_cast<unsigned>((coeffs * 32 + 127) / 128);
+      if (wide)
+        k_crt_carry_warp<true><<<blocks, 128, 0, st>>>(cp);
+      else
+        k_crt_carry_warp<false><<<blocks, 128, 0, st>>>(cp);
+      return 3;
+    }
+    const unsigned blocks = static_cast<unsigned>((coeffs + 127) / 128);
     if (wide)
       k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
     else
