@@ -22,6 +22,7 @@
 #include "crt_gemm_tma.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.hpp"
 #include "res_common.cuh"
@@ -990,7 +991,11 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
     // 4P * 255^2 + 2^25 < 2^31: the per-digit sum fits int32
     const bool wide = static_cast<double>(cp.P) * 4 * 255 * 255 + 33554432.0 >= 2147483648.0;
     const long long coeffs = static_cast<long long>(cp.J) * cp.B;
-    if (coeffs * 64 < 148LL * 2048) {  // under half a wave of threads: a warp per coefficient
+    static const long long warp_max = [] {  // CTG_CARRY_WARP_MAX: A/B switch
+      const char* e = std::getenv("CTG_CARRY_WARP_MAX");
+      return e ? std::atoll(e) : 4736LL;
+    }();
+    if (coeffs <= warp_max) {  // few coefficients: a warp per coefficient
       const unsigned blocks = static_cast<unsigned>((coeffs * 32 + 127) / 128);
       if (wide)
         k_crt_carry_warp<true><<<blocks, 128, 0, st>>>(cp);
