@@ -272,3 +272,14 @@ def test_concurrent_calls_from_threads():
     for th in ths:
         th.join()
     assert not errors, errors[0]
+
+
+def test_crt_beyond_tensor_core_prime_count():
+    """More than kI8MaxPrimes = 8192 primes (the u8 GEMM's s32 exactness limit): dense degree 3
+    with 65,536-bit coefficients needs ~10,900 primes and takes the IMAD CRT path; exact
+    against the oracle restatement of the reference's PRS."""
+    import curvetop_oracle as O
+    f = curves.make("dense", 3, 65536, 3)
+    R = P.resultant(f, curves.derive_y(f))
+    assert P.last_call_stats()["n_primes"] > 8192
+    assert R == O.resultant(f, O.derive_y(f), "y")
