@@ -97,3 +97,29 @@ def test_gcd_conventions():
         P.gcd_univariate([], [])
     assert P.gcd_univariate([], [6, -4]) == [-3, 2]
     assert P.gcd_univariate([12], [18]) == [1]
+
+
+def test_large_gcd_and_yun_with_common_factors():
+    """Degree-700 operands sharing a degree-300 factor (40-bit coefficients): the modular gcd
+    (lucky primes, CRT of gamma-scaled images, certificate) must return pp(g) -- checked by
+    exact division on the host, independent of the GPU path -- and Yun of g^2 * u must return
+    g's and u's primitive parts with multiplicities 2 and 1."""
+    import random
+    import curvetop_oracle as O
+    rng = random.Random(77)
+
+    def rnd(deg, bits=40):
+        c = [rng.randrange(-2 ** bits, 2 ** bits) for _ in range(deg)]
+        return c + [rng.randrange(1, 2 ** bits)]
+
+    g, u, w = rnd(300), rnd(400), rnd(380)
+    A, B = O.u_mul(g, u), O.u_mul(g, w)
+    h = P.gcd_univariate(A, B)
+    assert h == O.primitive_positive(g)
+    assert O.divexact(A, h) and O.divexact(B, h)  # exact (raises otherwise)
+    g2, u2 = rnd(60, 30), rnd(90, 30)
+    F = O.u_mul(O.u_mul(g2, g2), u2)
+    unit, factors = P.yun_squarefree(F)
+    want = sorted([(O.primitive_positive(u2), 1), (O.primitive_positive(g2), 2)], key=lambda t: t[1])
+    assert [(list(f), m) for f, m in factors] == [(list(f), m) for f, m in want]
+    assert O.reconstruct(unit, factors) == F
