@@ -52,7 +52,11 @@ ZPoly parse_upoly(const ctg_upoly* p) {
     if (e < b) throw ApiError(CTG_INVALID, "upoly: limb_off not monotone");
     const int s = p->sign[i];
     if (s < -1 || s > 1) throw ApiError(CTG_INVALID, "upoly: sign must be -1, 0 or +1");
-    sbig_add_inplace(out[i], s, p->limbs + b, static_cast<int>(e - b));
+    uint32_t n = e - b;  // one coefficient per slot: take the limbs as they are (trimmed)
+    while (n > 0 && p->limbs[b + n - 1] == 0u) --n;
+    if (s == 0 || n == 0) continue;
+    out[i].sign = s;
+    out[i].mag.assign(p->limbs + b, p->limbs + b + n);
   }
   while (!out.empty() && out.back().sign == 0) out.pop_back();
   return out;
@@ -69,10 +73,23 @@ Big zcontent(const ZPoly& p) {
     if (c.sign != 0) order.push_back(&c);
   std::stable_sort(order.begin(), order.end(),
                    [](const SBig* a, const SBig* b) { return a->mag.size() < b->mag.size(); });
+  // gcd(g, c) for a one-limb g: c mod g, then a word gcd (no big-integer allocation).
+  auto small_gcd = [](uint32_t g, const Big& c) {
+    uint32_t r = big_mod_u32(c.data(), static_cast<int>(c.size()), g);
+    while (r) {
+      const uint32_t t = g % r;
+      g = r;
+      r = t;
+    }
+    return g;
+  };
+  auto step = [&](const Big& g, const Big& c) {
+    return g.size() == 1 ? Big{small_gcd(g[0], c)} : big_gcd(g, c);
+  };
   auto chain = [&](size_t i0, size_t i1) {
     Big g;
     for (size_t i = i0; i < i1; ++i) {
-      g = g.empty() ? order[i]->mag : big_gcd(g, order[i]->mag);
+      g = g.empty() ? order[i]->mag : step(g, order[i]->mag);
       if (big_is_one(g)) break;
     }
     return g;
@@ -87,17 +104,36 @@ Big zcontent(const ZPoly& p) {
   parallel_for(groups, [&](int t) {
     const size_t i0 = 2 + t * per, i1 = std::min(order.size(), i0 + per);
     Big h = g;
-    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = big_gcd(h, order[i]->mag);
+    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = step(h, order[i]->mag);
     part[t] = h;
   });
   for (const Big& h : part) g = big_gcd(g, h);
   return g;
 }
 
-// p / (s * c) for the content c and s = sign(lc p): primitive with positive leading coefficient.
+// p / (s * c) for the content c (computed unless given) and s = sign(lc p): primitive with
+// positive leading coefficient.
+ZPoly divide_content(const ZPoly& p, Big c, Big* content, int* lcsign);
+
 ZPoly zprimitive_positive(const ZPoly& p, Big* content = nullptr, int* lcsign = nullptr) {
   if (p.empty()) return p;
+  return divide_content(p, zcontent(p), content, lcsign);
+}
+
+// The same, consuming p: a primitive input (content 1, the common case) is returned in place.
+ZPoly zprimitive_positive(ZPoly&& p, Big* content = nullptr, int* lcsign = nullptr) {
+  if (p.empty()) return std::move(p);
   Big c = zcontent(p);
+  if (!big_is_one(c)) return divide_content(p, std::move(c), content, lcsign);
+  const int s = p.back().sign;
+  if (content) *content = c;
+  if (lcsign) *lcsign = s;
+  if (s < 0)
+    for (auto& x : p) x.sign = -x.sign;
+  return std::move(p);
+}
+
+ZPoly divide_content(const ZPoly& p, Big c, Big* content, int* lcsign) {
   const int s = p.back().sign;
   if (content) *content = c;
   if (lcsign) *lcsign = s;
@@ -887,7 +923,7 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
     if (a.empty()) throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial");  // elim.cpp:139
     Big content;
     int s = 0;
-    ZPoly P = zprimitive_positive(a, &content, &s);  // elim.cpp:141-144: unit = sign(lc) * content
+    ZPoly P = zprimitive_positive(std::move(a), &content, &s);  // elim.cpp:141-144: unit = sign(lc) * content
     timer.mark_setup();
     if (zdeg(P) == 0) {  // elim.cpp:145
       fill_sqf(content, s, {}, out);
@@ -913,7 +949,7 @@ ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ct
     CallTimer timer;
     ZPoly a = parse_upoly(p);
     if (a.empty()) throw ApiError(CTG_PRECONDITION, "square_free_part: zero polynomial");  // elim.cpp:205
-    ZPoly P = zprimitive_positive(a);
+    ZPoly P = zprimitive_positive(std::move(a));
     timer.mark_setup();
     if (zdeg(P) == 0) {  // elim.cpp:207
       fill_upoly(to_ucoeffs(P), out);
@@ -945,7 +981,7 @@ ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_
       timer.finish();
       return;
     }
-    ZPoly A = zprimitive_positive(a), B = zprimitive_positive(b);
+    ZPoly A = zprimitive_positive(std::move(a)), B = zprimitive_positive(std::move(b));
     timer.mark_setup();
     if (zdeg(A) == 0 || zdeg(B) == 0) {
       fill_upoly(to_ucoeffs(ZPoly{SBig{1, Big{1u}}}), out);

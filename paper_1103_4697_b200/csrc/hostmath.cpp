@@ -159,22 +159,44 @@ Big big_mul_small(const uint32_t* limbs, int n, uint32_t s) {
   return big_mul_u32(a, s);
 }
 
+// Division of a 64-bit x = r 2^32 + limb (r < d) by a 32-bit d with a precomputed
+// reciprocal mu = floor((2^64 - 1) / d): q = hi64(x mu) is at most 2 below floor(x / d), so
+// two conditional corrections give the exact quotient (no hardware 64-bit division per limb).
+namespace {
+struct Div32 {
+  uint64_t d, mu;
+  explicit Div32(uint32_t dv) : d(dv), mu(~0ull / dv) {}
+  uint64_t div(uint64_t x, uint64_t* rem) const {
+    uint64_t q = static_cast<uint64_t>((static_cast<unsigned __int128>(x) * mu) >> 64);
+    uint64_t r = x - q * d;
+    if (r >= d) {
+      r -= d;
+      ++q;
+    }
+    if (r >= d) {
+      r -= d;
+      ++q;
+    }
+    *rem = r;
+    return q;
+  }
+};
+}  // namespace
+
 Big big_div_u32(const Big& a, uint32_t b, uint32_t* rem) {
   Big q(a.size());
+  const Div32 D(b);
   uint64_t r = 0;
-  for (size_t i = a.size(); i-- > 0;) {
-    uint64_t cur = (r << 32) | a[i];
-    q[i] = static_cast<uint32_t>(cur / b);
-    r = cur % b;
-  }
+  for (size_t i = a.size(); i-- > 0;) q[i] = static_cast<uint32_t>(D.div((r << 32) | a[i], &r));
   if (rem) *rem = static_cast<uint32_t>(r);
   big_trim(q);
   return q;
 }
 
 uint32_t big_mod_u32(const uint32_t* limbs, int n, uint32_t p) {
+  const Div32 D(p);
   uint64_t r = 0;
-  for (int i = n - 1; i >= 0; --i) r = ((r << 32) | limbs[i]) % p;
+  for (int i = n - 1; i >= 0; --i) D.div((r << 32) | limbs[i], &r);
   return static_cast<uint32_t>(r);
 }
 
