@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -666,37 +667,37 @@ class ChunkPipeline {
     }
     if (t0_) cudaEventDestroy(t0_);
   }
-  // Regions for `need` (nothing may be in flight: growing synchronises and reallocates).
+  // kSlots regions of `need` each (nothing may be in flight: growing synchronises and
+  // reallocates).  Chunk i uses slot i % kSlots; before reusing a slot the pipeline finishes
+  // the chunk that held it (the oldest in flight), so memory stays bounded for any batch size.
   void reserve(const ChunkNeeds& need) {
     drain();
-    dev_ = reinterpret_cast<uint8_t*>(ctx_.scratch_u32(2, need.dev / 4 + 64));
-    dev_cap_ = need.dev + 256;
-    in_ = ctx_.pinned_input(need.in);
-    in_cap_ = need.in;
-    hout_ = ctx_.pinned_u32(need.out);
-    out_cap_ = need.out;
-    dev_used_ = in_used_ = out_used_ = 0;
+    auto up = [](size_t x, size_t a) { return (x + a - 1) / a * a; };
+    dev_cap_ = up(need.dev, 1024);  // slot bases stay aligned for vector / TMA access
+    in_cap_ = up(need.in, 256);
+    out_cap_ = up(need.out, 64);    // u32 words
+    dev_ = reinterpret_cast<uint8_t*>(ctx_.scratch_u32(2, kSlots * dev_cap_ / 4 + 64));
+    in_ = ctx_.pinned_input(kSlots * in_cap_);
+    hout_ = ctx_.pinned_u32(kSlots * out_cap_);
   }
   void enqueue(Chunk&& c) {
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     ctg_plan* pl = c.pl.get();
     const ChunkNeeds n = chunk_needs(pl);
-    if (dev_used_ + n.dev > dev_cap_ || in_used_ + n.in > in_cap_ || out_used_ + n.out > out_cap_) {
-      drain();
-      if (n.dev > dev_cap_ || n.in > in_cap_ || n.out > out_cap_)
-        reserve({std::max(n.dev, dev_cap_), std::max(n.in, in_cap_), std::max(n.out, out_cap_)});
-    }
-    pl->bump = dev_ + dev_used_;
+    if (n.dev > dev_cap_ || n.in > in_cap_ || n.out > out_cap_)
+      reserve({std::max(n.dev, dev_cap_), std::max(n.in, in_cap_), std::max(n.out, out_cap_)});
+    if (inflight_.size() >= static_cast<size_t>(kSlots)) drain_front();
+    const int slot = slot_next_;
+    slot_next_ = (slot_next_ + 1) % kSlots;
+    const size_t dev_off = static_cast<size_t>(slot) * dev_cap_;
+    pl->bump = dev_ + dev_off;
     pl->bump_off = 0;
     pl->bump_cap = n.dev;
-    dev_used_ += n.dev;
-    c.in_off = in_used_;
-    in_used_ += n.in;
+    c.in_off = static_cast<size_t>(slot) * in_cap_;
     c.per_curve = static_cast<size_t>(pl->D) * pl->out_words();
     c.out_words = c.per_curve * pl->B;
-    c.out_off = out_used_;
-    out_used_ += n.out;
+    c.out_off = static_cast<size_t>(slot) * out_cap_;
     // Chunks alternate between two compute streams, so one chunk's low-occupancy tail (K4,
     // the CRT carry) overlaps the next chunk's first kernels.
     cudaStream_t s = (n_enqueued_++ % 2 == 0) ? ctx_.stream : ctx_.aux_stream(), cp = ctx_.copy_stream();
@@ -733,11 +734,16 @@ class ChunkPipeline {
     inflight_.push_back(std::move(c));
     st_.h2d_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
   }
-  // Waits for and decodes every chunk in flight (in order), then frees the regions for reuse.
+  // Waits for and decodes every chunk in flight, in order.
   void drain() {
+    while (!inflight_.empty()) drain_front();
+  }
+  // Waits for and decodes the oldest chunk in flight (its slot becomes free).
+  void drain_front() {
     using clk = std::chrono::steady_clock;
     auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
-    for (auto& c : inflight_) {
+    Chunk& c = inflight_.front();
+    {
       auto t0 = clk::now();
       CTG_CUDA_CHECK(cudaEventSynchronize(c.copied));
       st_.device_ms += ms_since(t0);
@@ -773,8 +779,7 @@ class ChunkPipeline {
       destroy_events(c);
       st_.decode_ms += ms_since(t0);
     }
-    inflight_.clear();
-    dev_used_ = in_used_ = out_used_ = 0;
+    inflight_.pop_front();
   }
   // Drains; throws if a chunk failed its device self-check (the caller frees the results).
   void finish() {
@@ -796,12 +801,14 @@ class ChunkPipeline {
   Ctx& ctx_;
   ctg_upoly_buf* out_;
   ctg_call_stats& st_;
-  std::vector<Chunk> inflight_;
+  static constexpr int kSlots = 3;  // chunks in flight: two compute streams + one being decoded
+  std::deque<Chunk> inflight_;
+  int slot_next_ = 0;
   std::string err_;
   uint8_t* dev_ = nullptr;
   uint8_t* in_ = nullptr;
   uint32_t* hout_ = nullptr;
-  size_t dev_cap_ = 0, in_cap_ = 0, out_cap_ = 0, dev_used_ = 0, in_used_ = 0, out_used_ = 0;
+  size_t dev_cap_ = 0, in_cap_ = 0, out_cap_ = 0;  // per slot
   cudaEvent_t t0_ = nullptr;  // trace origin
   int n_enqueued_ = 0;
   std::chrono::steady_clock::time_point host0_;
@@ -1025,11 +1032,13 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
           st.n_points = static_cast<int32_t>(c.pl->N);
           st.n_coeffs = static_cast<int32_t>(c.pl->D);
           st.out_limbs = std::max(st.out_limbs, c.pl->out_limbs());
-          if (!reserved) {  // size the regions for the whole call from the first plan
+          if (!reserved) {  // size the slots for the largest block from the first plan
             const ChunkNeeds n = chunk_needs(c.pl.get());
-            const double f = 1.1 * batch / c.pl->B;
-            pl_run.reserve({static_cast<size_t>(f * n.dev) + n.dev, static_cast<size_t>(f * n.in) + n.in,
-                            static_cast<size_t>(f * n.out) + n.out});
+            int max_block = 1;
+            for (size_t q = 0; q + 1 < bounds.size(); ++q) max_block = std::max(max_block, bounds[q + 1] - bounds[q]);
+            const double f = 0.1 + std::max(1.0, static_cast<double>(max_block) / c.pl->B);
+            pl_run.reserve({static_cast<size_t>(f * n.dev), static_cast<size_t>(f * n.in),
+                            static_cast<size_t>(f * n.out)});
             reserved = true;
           }
           t_plan += std::chrono::duration<double, std::milli>(tclk::now() - t1).count();

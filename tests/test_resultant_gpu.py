@@ -283,3 +283,16 @@ def test_crt_beyond_tensor_core_prime_count():
     R = P.resultant(f, curves.derive_y(f))
     assert P.last_call_stats()["n_primes"] > 8192
     assert R == O.resultant(f, O.derive_y(f), "y")
+
+
+def test_large_batch_bounded_slots():
+    """600 curves: many more chunks than pipeline slots (each slot reused every third chunk,
+    memory bounded by the largest block), results identical to one-at-a-time calls."""
+    pairs = []
+    for s in range(1, 601):
+        f = curves.make("dense", 6 + s % 3, 12, s)
+        pairs.append((f, curves.derive_y(f)))
+    got = P.resultant_batch(pairs)
+    for i in range(0, 600, 37):
+        assert got[i] == P.resultant(*pairs[i]), i
+    assert got[:64] == P.resultant_batch(pairs[:64])
