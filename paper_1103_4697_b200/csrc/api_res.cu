@@ -558,7 +558,7 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int r
   cp.out = d_out;
   cp.out_limbs = pl->tabs->LM;
   cp.use_i8 = pl->tabs->use_i8 ? 1 : 0;
-  cp.Jp = (J + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+  cp.Rp = static_cast<int>((static_cast<long long>(pl->B) * J + kI8TileJ - 1) / kI8TileJ * kI8TileJ);
   cp.L8 = pl->tabs->L8;
   cp.L8p = pl->tabs->L8p;
   cp.Kp = pl->tabs->Kp;

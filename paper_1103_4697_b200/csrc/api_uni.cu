@@ -281,7 +281,7 @@ ZPoly crt_rows(DevArena& ar, const uint32_t* d_src, int src_pitch, const std::ve
   cp.out = d_out;
   cp.out_limbs = T->LM;
   cp.use_i8 = T->use_i8 ? 1 : 0;
-  cp.Jp = (cols + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+  cp.Rp = (cols + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
   cp.L8 = T->L8;
   cp.L8p = T->L8p;
   cp.Kp = T->Kp;

@@ -11,7 +11,7 @@
 //   warp 1 / lane 0  MMA issuer: waits full[s], issues 4 x tcgen05.mma.cta_group::1.kind::i8
 //                    (M 128, N BN, K 32) into the TMEM accumulator, tcgen05.commit -> empty[s]
 //   all warps        epilogue: tcgen05.ld.32x32b (warp w owns TMEM lanes / rows 32w..32w+31)
-//                    -> coalesced 16-byte stores, C laid out [curve][digit group][coefficient].
+//                    -> coalesced 16-byte stores, C laid out [row tile][digit group][row in tile].
 // Shared-memory descriptors: K-major SWIZZLE_128B, SBO = 1024 B (8 rows x 128 B), the K step
 // of one instruction advances the start address by 32 B inside the 1024-B-aligned atom.
 #pragma once
@@ -81,7 +81,7 @@ __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
 template <int BN>
 __global__ void __launch_bounds__(128, 1)
     k_gemm_u8_tma(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int4* __restrict__ C,
-                  int Jp, int L4, int K) {
+                  int Rp, int K) {
   extern __shared__ uint8_t smraw[];
   Smem<BN>& sm = *reinterpret_cast<Smem<BN>*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -147,12 +147,12 @@ __global__ void __launch_bounds__(128, 1)
 
   mbar_wait(&sm.final_done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-  // C layout [curve][digit group l / 4][coefficient] of int4 (4 digits): rows m = b * Jp + j;
-  // a 128-row tile lies inside one curve (Jp is a multiple of 128), so each warp's stores of
-  // one digit group are 32 consecutive int4 (512 contiguous bytes), and the carry kernel's
-  // per-coefficient walk over the digit groups reads them back coalesced.
-  const int m = m0 + warp * 32 + lane, cb = m / Jp, cj = m - cb * Jp;
-  int4* cbase = C + (static_cast<long long>(cb) * L4 + n0 / 4) * Jp + cj;
+  // C layout [row tile of 128][digit group l / 4][row in tile] of int4 (4 digits), rows = the
+  // flattened coefficients of all curves: each warp's stores of one digit group are 32
+  // consecutive int4 (512 contiguous bytes), and the carry kernel's per-coefficient walk over
+  // the digit groups reads them back coalesced with a 2 KB stride (one tile's slab).
+  const long long slab = static_cast<long long>(gridDim.x) * BN / 4;  // digit groups per row (L8p / 4)
+  int4* cbase = C + (static_cast<long long>(m0 / kBM) * slab + n0 / 4) * kBM + warp * 32 + lane;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 32) {
     uint32_t v[32];
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      cbase[static_cast<long long>(c0 / 4 + q) * Jp] =
+      cbase[static_cast<long long>(c0 / 4 + q) * kBM] =
           make_int4(static_cast<int>(v[4 * q]), static_cast<int>(v[4 * q + 1]), static_cast<int>(v[4 * q + 2]),
                     static_cast<int>(v[4 * q + 3]));
   }

@@ -110,15 +110,17 @@ struct CrtParams {
   const uint32_t* Mk16;  // [P][L16] 16-bit digits of M / p_k
   const uint32_t* M16;   // [L16] 16-bit digits of M
   int L16;
-  uint32_t* Y;           // scratch: IMAD path [B][P][J]; tensor path Yt [B][Jp][Kp/4] (k contiguous)
+  uint32_t* Y;           // scratch: IMAD path [B][P][J]; tensor path Yt [Rp][Kp/4] (k contiguous)
   double* upart;         // scratch [B][ceil(P / kCrtChunk)][J]: partial sums of y_k / p_k
-  uint64_t* cols;        // scratch: IMAD path [B][J][L16] u64; tensor path [B][Jp][L8p] s32
+  uint64_t* cols;        // scratch: IMAD path [B][J][L16] u64; tensor path [Rp/128][L8p/4][128] int4
   uint32_t* out;         // [B][J][out_limbs + 1]
   int out_limbs;
   uint32_t* counters;
-  // tensor-core path (use_i8): Jp = J rounded up to kI8TileJ
+  // tensor-core path (use_i8): the GEMM rows are the coefficients of all curves flattened,
+  // row (b, j) = b * J + j, padded to Rp = a multiple of kI8TileJ (no per-curve padding: a
+  // rank's small coefficient block of a sharded CRT fills its tiles)
   int use_i8;
-  int Jp, L8, L8p, Kp;
+  int Rp, L8, L8p, Kp;
   const uint8_t* Bt8;
   const uint32_t* M8;
   int top_digit;         // |value| < 2^(8 top_digit) (coefficient bound; L8 when unknown)

@@ -557,8 +557,8 @@ __global__ void __launch_bounds__(256) k_crt_prep_t(CrtParams C) {
   const int t = ty * 32 + tx;
   for (int e = t; e < 32 * kCrtChunk; e += 256) {
     const int jj = e / kCrtChunk, kk = e % kCrtChunk;
-    if (jb + jj < C.Jp && kbeg + kk < ppad)
-      C.Y[(static_cast<size_t>(b) * C.Jp + jb + jj) * ppad + kbeg + kk] = tile[kk][jj];
+    if (jb + jj < C.J && kbeg + kk < ppad)  // row b * J + j (the padding rows past B * J are never read back)
+      C.Y[(static_cast<size_t>(b) * C.J + jb + jj) * ppad + kbeg + kk] = tile[kk][jj];
   }
 }
 
@@ -585,7 +585,7 @@ __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* smem) 
                : "r"(a));
 }
 
-// grid (L8p / 128, Jp / 128, B), 256 threads = 8 warps (2 along j x 4 along l), warp tile
+// grid (L8p / 128, Rp / 128), 256 threads = 8 warps (2 along j x 4 along l), warp tile
 // 64 j x 32 l (4 x 4 mma tiles).  K is staged 64 bytes per step through a 2-deep cp.async
 // pipeline; fragments come from ldmatrix (row pitch 80 B: conflict-free).
 __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
@@ -595,8 +595,8 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
-  const int jb = blockIdx.y * kI8TileJ, lb = blockIdx.x * kI8TileL, b = blockIdx.z;
-  const uint8_t* Ab = reinterpret_cast<const uint8_t*>(C.Y) + (static_cast<size_t>(b) * C.Jp + jb) * C.Kp;
+  const int jb = blockIdx.y * kI8TileJ, lb = blockIdx.x * kI8TileL;  // jb: first flattened row
+  const uint8_t* Ab = reinterpret_cast<const uint8_t*>(C.Y) + static_cast<size_t>(jb) * C.Kp;
   const uint8_t* Bb = C.Bt8 + static_cast<size_t>(lb) * C.Kp;
   const int nst = C.Kp / kBK;
   auto load = [&](int stage, int buf) {
@@ -651,15 +651,15 @@ __global__ void __launch_bounds__(256) k_crt_gemm_i8(CrtParams C) {
     }
     __syncthreads();
   }
-  // C layout [curve][digit group l / 4][coefficient][4] (see the carry kernel).
-  int32_t* Cb = reinterpret_cast<int32_t*>(C.cols) + static_cast<size_t>(b) * C.Jp * C.L8p;
+  // C layout [row tile of 128][digit group l / 4][row in tile][4] (see the carry kernel).
+  int32_t* Cb = reinterpret_cast<int32_t*>(C.cols) + static_cast<size_t>(jb) * C.L8p;  // tile jb / 128
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       const int r = jb + wm * 64 + mi * 16 + g;
       const int c = lb + wn * 32 + ni * 8 + tig * 2;
-      int32_t* at = Cb + (static_cast<size_t>(c >> 2) * C.Jp + r) * 4 + (c & 3);
+      int32_t* at = Cb + (static_cast<size_t>(c >> 2) * kI8TileJ + (r - jb)) * 4 + (c & 3);
       *reinterpret_cast<int2*>(at) = make_int2(acc[mi][ni][0], acc[mi][ni][1]);
       *reinterpret_cast<int2*>(at + 32) = make_int2(acc[mi][ni][2], acc[mi][ni][3]);  // row r + 8
     }
@@ -689,9 +689,10 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
   const double tr = rint(s);
   if (fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
   const int32_t t = static_cast<int32_t>(tr);
-  // GEMM output [curve][digit group][coefficient] of int4: limb w of this coefficient is
-  // col[w * Jp]; a warp's loads of one limb are consecutive coefficients (coalesced).
-  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(b) * C.Jp * (C.L8p / 4) + jl;
+  // GEMM output [row tile of 128][digit group][row in tile] of int4, row = b * J + jl = g:
+  // limb w of this coefficient is col[w * 128]; a warp's loads of one limb are consecutive
+  // rows of one tile (coalesced), and a thread's walk strides 2 KB through its tile's slab.
+  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(g >> 7) * (C.L8p / 4) * 128 + (g & 127);
   const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
   uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1) + 1;
   using acc_t = typename std::conditional<WIDE, long long, int>::type;
@@ -704,7 +705,7 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
 #pragma unroll
     for (int i = 0; i < kBatch; ++i) {
       if (w0 + i < OL) {
-        cb[i] = col[static_cast<size_t>(w0 + i) * C.Jp];
+        cb[i] = col[static_cast<size_t>(w0 + i) * 128];
         mb[i] = __ldg(&m8[w0 + i]);
       }
     }
@@ -765,7 +766,8 @@ __global__ void __launch_bounds__(128) k_crt_carry_warp(CrtParams C) {
   const double tr = rint(sp);
   if (lane == 0 && fabs(sp - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
   const int32_t t = static_cast<int32_t>(tr);
-  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(b) * C.Jp * (C.L8p / 4) + jl;
+  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(gw >> 7) * (C.L8p / 4) * 128 +
+                    (gw & 127);  // row b * J + jl, layout as k_crt_carry_seq
   const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
   uint32_t* out = C.out + (static_cast<size_t>(b) * C.J + jl) * (OL + 1) + 1;
   const int S = (OL + 31) / 32, w0 = lane * S, w1 = min(OL, w0 + S);
@@ -780,7 +782,7 @@ __global__ void __launch_bounds__(128) k_crt_carry_warp(CrtParams C) {
 #pragma unroll
     for (int i = 0; i < kBatch; ++i)
       if (wb + i < w1) {
-        cb[i] = col[static_cast<size_t>(wb + i) * C.Jp];
+        cb[i] = col[static_cast<size_t>(wb + i) * 128];
         mb[i] = __ldg(&m8[wb + i]);
       }
 #pragma unroll
@@ -868,16 +870,16 @@ __global__ void __launch_bounds__(128) k_crt_carry_warp(CrtParams C) {
 
 size_t crt_y_words(const CrtTables& T, int B, int J) {
   if (T.use_i8) {
-    const size_t Jp = (static_cast<size_t>(J) + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
-    return static_cast<size_t>(B) * Jp * (T.Kp / 4);
+    const size_t Rp = (static_cast<size_t>(B) * J + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+    return Rp * (T.Kp / 4);
   }
   return static_cast<size_t>(B) * T.P * J;
 }
 
 size_t crt_cols_words(const CrtTables& T, int B, int J) {
   if (T.use_i8) {
-    const size_t Jp = (static_cast<size_t>(J) + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
-    return static_cast<size_t>(B) * Jp * T.L8p;
+    const size_t Rp = (static_cast<size_t>(B) * J + kI8TileJ - 1) / kI8TileJ * kI8TileJ;
+    return Rp * T.L8p;
   }
   return static_cast<size_t>(B) * J * T.L16 * 2;
 }
@@ -963,11 +965,11 @@ static bool make_u8_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_
 }
 
 // The CRT product as ONE TMA-fed tcgen05 GEMM over every curve of the batch:
-// cols[B * Jp][L8p] = Yt[B * Jp][Kp] x Bt8[L8p][Kp]^T.
+// cols[Rp/128][L8p/4][128] (int4) = Yt[Rp][Kp] x Bt8[L8p][Kp]^T.
 template <int BN>
 static bool launch_gemm_tma(const CrtParams& cp, cudaStream_t st) {
   CUtensorMap ta, tb;
-  const uint64_t rows = static_cast<uint64_t>(cp.B) * cp.Jp;
+  const uint64_t rows = static_cast<uint64_t>(cp.Rp);
   if (!make_u8_map(&ta, cp.Y, rows, cp.Kp, tma::kBM) || !make_u8_map(&tb, cp.Bt8, cp.L8p, cp.Kp, BN)) return false;
   static const bool attr = [] {
     return cudaFuncSetAttribute(tma::k_gemm_u8_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -975,7 +977,7 @@ static bool launch_gemm_tma(const CrtParams& cp, cudaStream_t st) {
   }();
   if (!attr) return false;
   tma::k_gemm_u8_tma<BN><<<dim3(cp.L8p / BN, static_cast<unsigned>(rows / tma::kBM)), 128, tma::smem_bytes<BN>(), st>>>(
-      ta, tb, reinterpret_cast<int4*>(cp.cols), cp.Jp, cp.L8p / 4, cp.Kp);
+      ta, tb, reinterpret_cast<int4*>(cp.cols), cp.Rp, cp.Kp);
   return true;
 }
 
@@ -987,7 +989,7 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
     // Long K (>= 8 stages): TMA + tcgen05; short K: the mma.sync kernel has less fixed cost.
     bool done = false;
     if (cp.Kp >= 1024) done = (cp.L8p % 256 == 0) ? launch_gemm_tma<256>(cp, st) : launch_gemm_tma<128>(cp, st);
-    if (!done) k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Jp / kI8TileJ, cp.B), 256, 0, st>>>(cp);
+    if (!done) k_crt_gemm_i8<<<dim3(cp.L8p / kI8TileL, cp.Rp / kI8TileJ, 1), 256, 0, st>>>(cp);
     // 4P * 255^2 + 2^25 < 2^31: the per-digit sum fits int32
     const bool wide = static_cast<double>(cp.P) * 4 * 255 * 255 + 33554432.0 >= 2147483648.0;
     const long long coeffs = static_cast<long long>(cp.J) * cp.B;

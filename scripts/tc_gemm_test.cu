@@ -60,7 +60,7 @@ int run_tma(int M, int N, int K, unsigned seed) {
   const size_t smem = tma::smem_bytes<BN>();
   cudaFuncSetAttribute(tma::k_gemm_u8_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(N / BN, M / tma::kBM);
-  tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, N / 4, K);
+  tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, K);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("tma kernel error: %s\n", cudaGetErrorString(e));
@@ -72,10 +72,10 @@ int run_tma(int M, int N, int K, unsigned seed) {
   cudaMemcpy(hC.data(), C, 4 * hC.size(), cudaMemcpyDeviceToHost);
   cudaMemcpy(hR.data(), R, 4 * hR.size(), cudaMemcpyDeviceToHost);
   size_t bad = 0, first = 0;
-  // C is laid out [n / 4][m][n % 4] (one "curve" of M rows); R is row-major [m][n].
+  // C is laid out [m / 128][n / 4][m % 128][n % 4]; R is row-major [m][n].
   for (size_t i = 0; i < hR.size(); ++i) {
     const size_t m = i / N, n = i % N;
-    if (hC[((n / 4) * M + m) * 4 + n % 4] != hR[i]) {
+    if (hC[(((m / 128) * (N / 4) + n / 4) * 128 + m % 128) * 4 + n % 4] != hR[i]) {
       if (!bad) first = i;
       ++bad;
     }
@@ -84,7 +84,7 @@ int run_tma(int M, int N, int K, unsigned seed) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int r = 0; r < 5; ++r) tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, N / 4, K);
+  for (int r = 0; r < 5; ++r) tma::k_gemm_u8_tma<BN><<<grid, 128, smem>>>(ta, tb, reinterpret_cast<int4*>(C), M, K);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
