@@ -327,6 +327,7 @@ struct YunResult {
 struct YunImages {
   std::vector<uint32_t> primes;
   std::vector<int32_t> deg;  // [P][n+1]
+  int32_t* d_deg = nullptr;
   uint32_t* d_fac = nullptr;
   uint32_t* d_sqf = nullptr;
 };
@@ -343,11 +344,31 @@ YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& 
   im.d_sqf = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (n + 1));
   L.n += launch_modyun(d_tab, n, T->d_pc, nk, d_deg, im.d_fac, im.d_sqf, ar.st);
   CTG_CUDA_CHECK(cudaGetLastError());
-  im.deg.resize(static_cast<size_t>(nk) * (n + 1));
-  CTG_CUDA_CHECK(cudaMemcpyAsync(im.deg.data(), d_deg, 4 * im.deg.size(), cudaMemcpyDeviceToHost, ar.st));
+  // First only columns 0..1 of every prime's pattern (status, degree of the multiplicity-1
+  // factor): enough to certify a square-free input; fetch_patterns() copies the rest.
+  im.deg.assign(static_cast<size_t>(nk) * (n + 1), 0);
+  im.d_deg = d_deg;
+  CTG_CUDA_CHECK(cudaMemcpy2DAsync(im.deg.data(), 4 * static_cast<size_t>(n + 1), d_deg, 4 * static_cast<size_t>(n + 1),
+                                   8, nk, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+  stats_tls().d2h_bytes += static_cast<int64_t>(8) * nk;
+  return im;
+}
+
+// The full degree patterns of a run_modyun result.
+void fetch_patterns(DevArena& ar, YunImages& im) {
+  CTG_CUDA_CHECK(cudaMemcpyAsync(im.deg.data(), im.d_deg, 4 * im.deg.size(), cudaMemcpyDeviceToHost, ar.st));
   CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
   stats_tls().d2h_bytes += static_cast<int64_t>(4 * im.deg.size());
-  return im;
+}
+
+// A prime with p !| lc(P) and deg gcd(P, P') = 0 mod p certifies a square-free P.
+bool certifies_squarefree(const YunImages& im, int n) {
+  for (size_t k = 0; k < im.primes.size(); ++k) {
+    const int32_t* d = im.deg.data() + k * (n + 1);
+    if (d[0] == 0 && d[1] == n) return true;
+  }
+  return false;
 }
 
 YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t st, Launches& L) {
@@ -355,26 +376,32 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
   if (n > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "yun: degree exceeds 6000");
   DevArena ar(st);
   YunResult res;
-  // Probe: a square-free P is certified by one prime p with p !| lc(P) and deg gcd(P, P') = 0 mod p.
-  {
-    std::vector<uint32_t> probe = select_uni_primes(3 * 30.0);
-    YunImages im = run_modyun(ar, P, probe, device, L);
-    for (size_t k = 0; k < probe.size(); ++k) {
-      const int32_t* d = im.deg.data() + k * (n + 1);
-      if (d[0] == 0 && d[1] == n) {
-        res.factors.push_back({P, 1});
-        res.sqfp = P;
-        return res;
-      }
-    }
-  }
+  // A prime with p !| lc(P) and deg gcd(P, P') = 0 certifies a square-free P at once (no CRT).
+  // When the full prime set fits one wave of CTAs, it is run directly (every prime's Yun runs
+  // in parallel: the latency of one prime, and a non-square-free P reuses the same images);
+  // beyond that a 3-prime probe first spares square-free inputs (every dense config) the K1
+  // and Yun work of hundreds of primes.
   const Big& lcP = P.back().mag;
   const double need = big_log2(lcP) + n + zlog2_l2(P) + 2 + 40;
+  if (select_uni_primes(need + 62).size() > 148) {
+    YunImages im = run_modyun(ar, P, select_uni_primes(3 * 30.0), device, L);
+    if (certifies_squarefree(im, n)) {
+      res.factors.push_back({P, 1});
+      res.sqfp = P;
+      return res;
+    }
+  }
   double extra = 62;
   for (int attempt = 0; attempt < 4; ++attempt, extra *= 4) {
     std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
     YunImages im = run_modyun(ar, P, primes, device, L);
+    if (certifies_squarefree(im, n)) {
+      res.factors.push_back({P, 1});
+      res.sqfp = P;
+      return res;
+    }
+    fetch_patterns(ar, im);
     // lucky pattern: maximal square-free-part degree, then the most frequent pattern
     std::map<std::vector<int32_t>, std::vector<int>> by_pattern;
     int best_sd = -1;
