@@ -67,6 +67,37 @@ __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ lim
   tab[b * tab_bstride + static_cast<size_t>(k) * S + s] = acc;
 }
 
+// K1 for few (prime, slot) pairs with long coefficients (the Yun / gcd probes on 3 primes, a
+// single big-coefficient curve): a WARP per pair, lane l summing the limbs l, l + 32, ... (the
+// weight of limb l + 32 is the weight of limb l times R^32: rpow[31] = R^33 in the table's
+// convention), then a shuffle reduction -- 32 short chains instead of one long one.
+__global__ void __launch_bounds__(128) k_reduce_warp(const uint32_t* __restrict__ limbs,
+                                                     const int8_t* __restrict__ sign, int S, int L,
+                                                     const PrimeConst* __restrict__ pc,
+                                                     const uint32_t* __restrict__ rpow, int k0, int nk,
+                                                     uint32_t* __restrict__ tab, size_t tab_bstride) {
+  const long long pair = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, b = blockIdx.y;
+  if (pair >= static_cast<long long>(nk) * S) return;  // whole warps
+  const int kl = static_cast<int>(pair / S), s_ = static_cast<int>(pair - static_cast<long long>(kl) * S);
+  const int k = k0 + kl;
+  const Mod M = load_mod(pc[k]);
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + s_;
+  const uint32_t* w = rpow + static_cast<size_t>(k) * kRedL;
+  const uint32_t r33 = __ldg(&w[31]);
+  uint32_t acc = 0, wl = __ldg(&w[lane]);
+  for (int l = lane; l < L; l += 32) {
+    if (l >= 32) wl = l < kRedL ? __ldg(&w[l]) : mmul(wl, r33, M);
+    acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], wl, M), M.p);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc = madd(acc, __shfl_xor_sync(0xffffffffu, acc, off), M.p);
+  if (lane == 0) {
+    if (sign[static_cast<size_t>(b) * S + s_] < 0) acc = mneg(acc, M.p);
+    tab[b * tab_bstride + static_cast<size_t>(k) * S + s_] = acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: evaluate every y-coefficient row at all N points omega^i (Montgomery form).
 // Row r < n+1 is p_r(x); rows n+1.. are q_r(x) when q is not dp/dy.
@@ -888,6 +919,11 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
                   const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
   if (S == 0 || nk == 0 || B == 0) return 0;
   const long long n = static_cast<long long>(nk) * S;
+  if (L >= 32 && n * B < 148LL * 256) {  // few pairs, long coefficients: a warp per pair
+    dim3 grid(static_cast<unsigned>((n * 32 + 127) / 128), B);
+    k_reduce_warp<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
+    return 1;
+  }
   dim3 grid(static_cast<unsigned>((n + 127) / 128), B);
   k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
   return 1;
