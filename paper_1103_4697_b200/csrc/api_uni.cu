@@ -207,25 +207,68 @@ struct Launches {
 };
 
 // Residues of a primitive polynomial modulo every prime of `tabs` (K1): [P][n+1] Montgomery.
+// Per-thread pinned staging for the H2D of reduce_poly (a pageable copy of R's ~1 MB of limbs
+// at d30 is staged by the driver at a fraction of the pinned rate).  Reuse waits for the
+// previous copy; never freed (process lifetime, no teardown-order hazards).
+struct PinnedStage {
+  uint8_t* buf = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  int device = -1;
+  bool pending = false;
+  uint8_t* get(size_t bytes) {
+    if (pending) CTG_CUDA_CHECK(cudaEventSynchronize(done));
+    pending = false;
+    if (bytes > cap) {
+      if (buf) cudaFreeHost(buf);
+      buf = nullptr;
+      cap = 0;
+      CTG_CUDA_CHECK(cudaMallocHost(&buf, bytes));
+      cap = bytes;
+    }
+    return buf;
+  }
+  void mark(cudaStream_t st) {
+    int dev = 0;
+    CTG_CUDA_CHECK(cudaGetDevice(&dev));
+    if (done && dev != device) {
+      cudaEventDestroy(done);
+      done = nullptr;
+    }
+    if (!done) CTG_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    device = dev;
+    CTG_CUDA_CHECK(cudaEventRecord(done, st));
+    pending = true;
+  }
+};
+thread_local PinnedStage tls_stage;
+
 uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
   const int S = static_cast<int>(p.size());
   int Lw = 1;
   for (const auto& c : p) Lw = std::max<int>(Lw, static_cast<int>(c.mag.size()));
-  std::vector<uint32_t> limbs(static_cast<size_t>(Lw) * S, 0u);
-  std::vector<int8_t> sign(S, 0);
+  const size_t nl = static_cast<size_t>(Lw) * S;
+  uint8_t* stage = tls_stage.get(4 * nl + S);
+  uint32_t* limbs = reinterpret_cast<uint32_t*>(stage);
+  int8_t* sign = reinterpret_cast<int8_t*>(stage + 4 * nl);
+  // coefficient-major [S][Lw]: one contiguous copy per coefficient (K1 reads either layout)
   for (int s = 0; s < S; ++s) {
     sign[s] = static_cast<int8_t>(p[s].sign);
-    for (size_t l = 0; l < p[s].mag.size(); ++l) limbs[l * S + s] = p[s].mag[l];
+    const size_t n = p[s].mag.size();
+    uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
+    if (n) std::memcpy(row, p[s].mag.data(), 4 * n);
+    if (n < static_cast<size_t>(Lw)) std::memset(row + n, 0, 4 * (Lw - n));
   }
-  uint32_t* d_limbs = ar.alloc<uint32_t>(limbs.size());
+  uint32_t* d_limbs = ar.alloc<uint32_t>(nl);
   int8_t* d_sign = ar.alloc<int8_t>(S);
   uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
-  CTG_CUDA_CHECK(cudaMemcpyAsync(d_limbs, limbs.data(), 4 * limbs.size(), cudaMemcpyHostToDevice, ar.st));
-  CTG_CUDA_CHECK(cudaMemcpyAsync(d_sign, sign.data(), S, cudaMemcpyHostToDevice, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_limbs, limbs, 4 * nl, cudaMemcpyHostToDevice, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_sign, sign, S, cudaMemcpyHostToDevice, ar.st));
+  tls_stage.mark(ar.st);
   L.n += launch_reduce(d_limbs, d_sign, S, Lw, tabs.d_pc, tabs.d_rpow, 0, tabs.P, d_tab, static_cast<size_t>(tabs.P) * S, 1,
-                       ar.st);
+                       ar.st, 1);
   auto& st = stats_tls();
-  st.h2d_bytes += static_cast<int64_t>(4 * limbs.size() + S);
+  st.h2d_bytes += static_cast<int64_t>(4 * nl + S);
   return d_tab;
 }
 

@@ -131,8 +131,10 @@ size_t crt_y_words(const CrtTables& T, int B, int J);
 size_t crt_cols_words(const CrtTables& T, int B, int J);  // in 32-bit words
 
 // Kernel launchers (kernels_res.cu).  Each returns the number of launches issued.
+// Limbs limb-major [B][L][S] (coef_major = 0) or coefficient-major [B][S][L] (coef_major = 1).
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc,
-                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st);
+                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st,
+                  int coef_major = 0);
 // part: 0 = K2 + K3 (+ general), 1 = K2 only, 2 = K3 (+ general) only.
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part = 0);
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,

@@ -43,24 +43,26 @@ namespace {
 __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ limbs, const int8_t* __restrict__ sign,
                                                 int S, int L, const PrimeConst* __restrict__ pc,
                                                 const uint32_t* __restrict__ rpow, int k0, int nk,
-                                                uint32_t* __restrict__ tab, size_t tab_bstride) {
+                                                uint32_t* __restrict__ tab, size_t tab_bstride, int coef_major) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (idx >= static_cast<long long>(nk) * S) return;
   const int kl = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<long long>(kl) * S);
   const int k = k0 + kl;
   const Mod M = load_mod(pc[k]);
-  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + s;
+  // limb l of slot s: limb-major [B][L][S] (plans) or coefficient-major [B][S][L] (univariate)
+  const size_t ls = coef_major ? 1 : static_cast<size_t>(S);
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + (coef_major ? static_cast<size_t>(s) * L : s);
   const uint32_t* w = rpow + static_cast<size_t>(k) * kRedL;
   uint32_t acc = 0;
   const int Lt = L < kRedL ? L : kRedL;
 #pragma unroll 4
-  for (int l = 0; l < Lt; ++l) acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], __ldg(&w[l]), M), M.p);
+  for (int l = 0; l < Lt; ++l) acc = madd(acc, mmul(lb[l * ls], __ldg(&w[l]), M), M.p);
   if (L > kRedL) {  // very long coefficients: extend the weights by R per limb
     uint32_t wl = __ldg(&w[kRedL - 1]);
     for (int l = kRedL; l < L; ++l) {
       wl = mmul(wl, M.r2, M);
-      acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], wl, M), M.p);
+      acc = madd(acc, mmul(lb[l * ls], wl, M), M.p);
     }
   }
   if (sign[static_cast<size_t>(b) * S + s] < 0) acc = mneg(acc, M.p);
@@ -75,20 +77,21 @@ __global__ void __launch_bounds__(128) k_reduce_warp(const uint32_t* __restrict_
                                                      const int8_t* __restrict__ sign, int S, int L,
                                                      const PrimeConst* __restrict__ pc,
                                                      const uint32_t* __restrict__ rpow, int k0, int nk,
-                                                     uint32_t* __restrict__ tab, size_t tab_bstride) {
+                                                     uint32_t* __restrict__ tab, size_t tab_bstride, int coef_major) {
   const long long pair = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, b = blockIdx.y;
   if (pair >= static_cast<long long>(nk) * S) return;  // whole warps
   const int kl = static_cast<int>(pair / S), s_ = static_cast<int>(pair - static_cast<long long>(kl) * S);
   const int k = k0 + kl;
   const Mod M = load_mod(pc[k]);
-  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + s_;
+  const size_t ls = coef_major ? 1 : static_cast<size_t>(S);  // coefficient-major: lanes read 128 B
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + (coef_major ? static_cast<size_t>(s_) * L : s_);
   const uint32_t* w = rpow + static_cast<size_t>(k) * kRedL;
   const uint32_t r33 = __ldg(&w[31]);
   uint32_t acc = 0, wl = __ldg(&w[lane]);
   for (int l = lane; l < L; l += 32) {
     if (l >= 32) wl = l < kRedL ? __ldg(&w[l]) : mmul(wl, r33, M);
-    acc = madd(acc, mmul(lb[static_cast<size_t>(l) * S], wl, M), M.p);
+    acc = madd(acc, mmul(lb[l * ls], wl, M), M.p);
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) acc = madd(acc, __shfl_xor_sync(0xffffffffu, acc, off), M.p);
@@ -916,16 +919,17 @@ size_t crt_cols_words(const CrtTables& T, int B, int J) {
 }
 
 int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, const PrimeConst* d_pc,
-                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st) {
+                  const uint32_t* d_rpow, int k0, int nk, uint32_t* d_tab, size_t tab_bstride, int B, cudaStream_t st,
+                  int coef_major) {
   if (S == 0 || nk == 0 || B == 0) return 0;
   const long long n = static_cast<long long>(nk) * S;
   if (L >= 32 && n * B < 148LL * 256) {  // few pairs, long coefficients: a warp per pair
     dim3 grid(static_cast<unsigned>((n * 32 + 127) / 128), B);
-    k_reduce_warp<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
+    k_reduce_warp<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride, coef_major);
     return 1;
   }
   dim3 grid(static_cast<unsigned>((n + 127) / 128), B);
-  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
+  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride, coef_major);
   return 1;
 }
 
