@@ -123,3 +123,27 @@ def test_large_gcd_and_yun_with_common_factors():
     want = sorted([(O.primitive_positive(u2), 1), (O.primitive_positive(g2), 2)], key=lambda t: t[1])
     assert [(list(f), m) for f, m in factors] == [(list(f), m) for f, m in want]
     assert O.reconstruct(unit, factors) == F
+
+
+def test_yun_probe_inconclusive_falls_through():
+    """Big coefficients push the prime set past one wave, so Yun starts with the 3-prime
+    probe; on g^2 u the probe must find no square-free certificate (gcd(P, P') != 1 mod p) and
+    the full modular Yun must still return g's and u's primitive parts."""
+    import random
+    import curvetop_oracle as O
+    rng = random.Random(91)
+
+    def rnd(deg, bits):
+        c = [rng.randrange(-2 ** bits, 2 ** bits) for _ in range(deg)]
+        return c + [rng.randrange(1, 2 ** bits)]
+
+    g, u = rnd(20, 1000), rnd(30, 1000)
+    F = O.u_mul(O.u_mul(g, g), u)
+    unit, factors = P.yun_squarefree(F)
+    assert [(list(f), m) for f, m in factors] == [(O.primitive_positive(u), 1), (O.primitive_positive(g), 2)]
+    assert O.reconstruct(unit, factors) == F
+    # and a square-free big-coefficient input is certified by the probe alone
+    S = O.u_mul(g, u)
+    unit, factors = P.yun_squarefree(S)
+    assert [(list(f), m) for f, m in factors] == [(O.primitive_positive(S), 1)]
+    assert P.last_call_stats()["kernel_launches"] == 2  # K1 + the 3-prime probe
