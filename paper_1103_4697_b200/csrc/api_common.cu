@@ -98,15 +98,15 @@ cudaStream_t Ctx::copy_stream() {
   return copy;
 }
 
-cudaStream_t Ctx::aux_stream() {
-  if (!aux) {
+cudaStream_t Ctx::aux_stream(int i) {
+  if (!aux[i]) {
     int prev = 0;
     cudaGetDevice(&prev);
     CTG_CUDA_CHECK(cudaSetDevice(device));
-    CTG_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    CTG_CUDA_CHECK(cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking));
     cudaSetDevice(prev);
   }
-  return aux;
+  return aux[i];
 }
 
 uint8_t* Ctx::pinned_input(size_t bytes) {

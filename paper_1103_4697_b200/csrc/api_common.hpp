@@ -76,8 +76,8 @@ struct Ctx {
   size_t pinned_in_bytes = 0;
   cudaStream_t copy = nullptr;            // D2H stream (overlaps the next chunk's kernels)
   cudaStream_t copy_stream();
-  cudaStream_t aux = nullptr;             // second compute stream (alternate batch chunks)
-  cudaStream_t aux_stream();
+  cudaStream_t aux[2] = {nullptr, nullptr};  // extra compute streams (batch chunks rotate)
+  cudaStream_t aux_stream(int i = 0);
   uint32_t* scratch_u32(int slot, size_t words);
   uint32_t* pinned_u32(size_t words);     // D2H staging
   uint8_t* pinned_input(size_t bytes);    // H2D staging

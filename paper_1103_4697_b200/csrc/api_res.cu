@@ -698,9 +698,14 @@ class ChunkPipeline {
     c.per_curve = static_cast<size_t>(pl->D) * pl->out_words();
     c.out_words = c.per_curve * pl->B;
     c.out_off = static_cast<size_t>(slot) * out_cap_;
-    // Chunks alternate between two compute streams, so one chunk's low-occupancy tail (K4,
-    // the CRT carry) overlaps the next chunk's first kernels.
-    cudaStream_t s = (n_enqueued_++ % 2 == 0) ? ctx_.stream : ctx_.aux_stream(), cp = ctx_.copy_stream();
+    // Chunks rotate over three compute streams, so one chunk's low-occupancy tail (K4, the CRT
+    // carry) overlaps the next chunks' kernels.
+    static const int nstreams = [] {  // CTG_CHUNK_STREAMS (1..3): A/B of the chunk rotation
+      const char* e = std::getenv("CTG_CHUNK_STREAMS");
+      return e ? std::max(1, std::min(3, std::atoi(e))) : 3;
+    }();
+    const int si = n_enqueued_++ % nstreams;
+    cudaStream_t s = si == 0 ? ctx_.stream : ctx_.aux_stream(si - 1), cp = ctx_.copy_stream();
     if (trace()) {
       for (cudaEvent_t* e : {&c.t_begin, &c.t_computed, &c.t_copied}) CTG_CUDA_CHECK(cudaEventCreate(e));
       if (!t0_) {
@@ -801,7 +806,7 @@ class ChunkPipeline {
   Ctx& ctx_;
   ctg_upoly_buf* out_;
   ctg_call_stats& st_;
-  static constexpr int kSlots = 3;  // chunks in flight: two compute streams + one being decoded
+  static constexpr int kSlots = 4;  // chunks in flight: three compute streams + one being decoded
   std::deque<Chunk> inflight_;
   int slot_next_ = 0;
   std::string err_;
@@ -992,7 +997,7 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     } else {
       static const int kMid = [] {  // largest middle block (CTG_BLOCK_MAX, for experiments)
         const char* e = std::getenv("CTG_BLOCK_MAX");
-        return e ? std::max(16, std::atoi(e)) : 128;
+        return e ? std::max(16, std::atoi(e)) : 64;
       }();
       static const int kHead = [] {
         const char* e = std::getenv("CTG_BLOCK_HEAD");
