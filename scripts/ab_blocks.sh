@@ -1,7 +1,7 @@
 #!/bin/bash
-# e2e A/B of the batch block policy (CTG_BLOCK_MAX middle blocks, CTG_BLOCK_HEAD first/last).
-# Measured on B200 (d20, 256 curves, e2e 1e9 units/s): 128/32 3.0-3.1 (default), 96/32 3.0,
-# 64/16 3.0, 128/16 2.75, 192/32 2.6, 256/16 2.4.
+# e2e A/B of the batch block policy (CTG_BLOCK_MAX middle blocks, CTG_BLOCK_HEAD first/last)
+# with two compute streams (superseded by scripts/ab_streams.sh, which also varies the stream
+# count: the default is now 3 streams and 64-curve middle blocks).
 for cfg in "128 32" "192 32" "96 32" "64 16" "128 16" "256 16"; do set -- $cfg
   export CTG_BLOCK_MAX=$1 CTG_BLOCK_HEAD=$2
   r=""
