@@ -659,7 +659,10 @@ ChunkNeeds chunk_needs(const ctg_plan* pl) {
 
 class ChunkPipeline {
  public:
-  ChunkPipeline(Ctx& ctx, ctg_upoly_buf* out) : ctx_(ctx), out_(out), st_(stats_tls()) {}
+  // nstreams: compute streams the chunks rotate over (measured: 3 for four or more blocks, as
+  // 256 d20 curves in 32 | 64 | 64 | 64 | 32; 2 for fewer, as 64 d30 curves in 8 | 48 | 8).
+  ChunkPipeline(Ctx& ctx, ctg_upoly_buf* out, int nstreams)
+      : ctx_(ctx), out_(out), st_(stats_tls()), nstreams_(std::max(1, std::min(3, nstreams))) {}
   ~ChunkPipeline() {
     for (auto& c : inflight_) {  // error path: let the copies finish before the buffers go
       if (c.copied) cudaEventSynchronize(c.copied);
@@ -700,10 +703,11 @@ class ChunkPipeline {
     c.out_off = static_cast<size_t>(slot) * out_cap_;
     // Chunks rotate over three compute streams, so one chunk's low-occupancy tail (K4, the CRT
     // carry) overlaps the next chunks' kernels.
-    static const int nstreams = [] {  // CTG_CHUNK_STREAMS (1..3): A/B of the chunk rotation
+    static const int forced = [] {  // CTG_CHUNK_STREAMS (1..3): A/B of the chunk rotation
       const char* e = std::getenv("CTG_CHUNK_STREAMS");
-      return e ? std::max(1, std::min(3, std::atoi(e))) : 3;
+      return e ? std::max(1, std::min(3, std::atoi(e))) : 0;
     }();
+    const int nstreams = forced ? forced : nstreams_;
     const int si = n_enqueued_++ % nstreams;
     cudaStream_t s = si == 0 ? ctx_.stream : ctx_.aux_stream(si - 1), cp = ctx_.copy_stream();
     if (trace()) {
@@ -816,6 +820,7 @@ class ChunkPipeline {
   size_t dev_cap_ = 0, in_cap_ = 0, out_cap_ = 0;  // per slot
   cudaEvent_t t0_ = nullptr;  // trace origin
   int n_enqueued_ = 0;
+  int nstreams_ = 2;
   std::chrono::steady_clock::time_point host0_;
 };
 
@@ -976,21 +981,11 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     std::unique_lock<std::mutex> lock;
     std::unique_ptr<ChunkPipeline> pipe;
     int dev = -1;
-    auto pipeline = [&]() -> ChunkPipeline& {
-      if (!pipe) {
-        guard = std::make_unique<DeviceGuard>(opts);
-        dev = select_device(opts);
-        Ctx& ctx = context(dev);
-        lock = std::unique_lock<std::mutex>(ctx.mu);
-        pipe = std::make_unique<ChunkPipeline>(ctx, out);
-      }
-      return *pipe;
-    };
     // Blocks of consecutive curves: parse, group by shape, plan and enqueue one block while the
     // GPU runs the previous one (each shape group of a block is one batched plan = one launch
     // set).  The first and last blocks are small (they are the exposed head -- host parsing
     // before the GPU starts -- and tail -- the last D2H and decode); the middle ones are large
-    // (fewer, fuller launches).  E.g. 256 curves -> 32 | 96 | 96 | 32.
+    // (fewer, fuller launches).  E.g. 256 curves -> 32 | 64 | 64 | 64 | 32.
     std::vector<int> bounds{0};
     if (batch <= 32) {
       bounds.push_back(batch);
@@ -1009,6 +1004,16 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
       for (int k = 0; k < nm; ++k) bounds.push_back(std::min(s0 + mid, bounds.back() + per));
       bounds.push_back(batch);
     }
+    auto pipeline = [&]() -> ChunkPipeline& {
+      if (!pipe) {
+        guard = std::make_unique<DeviceGuard>(opts);
+        dev = select_device(opts);
+        Ctx& ctx = context(dev);
+        lock = std::unique_lock<std::mutex>(ctx.mu);
+        pipe = std::make_unique<ChunkPipeline>(ctx, out, bounds.size() >= 6 ? 3 : 2);
+      }
+      return *pipe;
+    };
     bool reserved = false;
     double t_parse = 0, t_plan = 0;
     using tclk = std::chrono::steady_clock;

@@ -40,19 +40,21 @@ namespace {
 //   value R = sum_l limb_l 2^(32 l) R = sum_l mmul(limb_l, R^(l+2))
 // with the weights from a per-prime table: independent products (no Horner chain), each
 // REDC exact for any 32-bit limb (limb * w < 2^32 p), summed with a conditional subtract.
+template <bool CM>
 __global__ void __launch_bounds__(128) k_reduce(const uint32_t* __restrict__ limbs, const int8_t* __restrict__ sign,
                                                 int S, int L, const PrimeConst* __restrict__ pc,
                                                 const uint32_t* __restrict__ rpow, int k0, int nk,
-                                                uint32_t* __restrict__ tab, size_t tab_bstride, int coef_major) {
+                                                uint32_t* __restrict__ tab, size_t tab_bstride) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (idx >= static_cast<long long>(nk) * S) return;
   const int kl = static_cast<int>(idx / S), s = static_cast<int>(idx - static_cast<long long>(kl) * S);
   const int k = k0 + kl;
   const Mod M = load_mod(pc[k]);
-  // limb l of slot s: limb-major [B][L][S] (plans) or coefficient-major [B][S][L] (univariate)
-  const size_t ls = coef_major ? 1 : static_cast<size_t>(S);
-  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + (coef_major ? static_cast<size_t>(s) * L : s);
+  // limb l of slot s: limb-major [B][L][S] (plans, CM = false) or coefficient-major [B][S][L]
+  // (univariate, CM = true)
+  const size_t ls = CM ? 1 : static_cast<size_t>(S);
+  const uint32_t* lb = limbs + static_cast<size_t>(b) * L * S + (CM ? static_cast<size_t>(s) * L : s);
   const uint32_t* w = rpow + static_cast<size_t>(k) * kRedL;
   uint32_t acc = 0;
   const int Lt = L < kRedL ? L : kRedL;
@@ -929,7 +931,10 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
     return 1;
   }
   dim3 grid(static_cast<unsigned>((n + 127) / 128), B);
-  k_reduce<<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride, coef_major);
+  if (coef_major)
+    k_reduce<true><<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
+  else
+    k_reduce<false><<<grid, 128, 0, st>>>(d_limbs, d_sign, S, L, d_pc, d_rpow, k0, nk, d_tab, tab_bstride);
   return 1;
 }
 
