@@ -211,8 +211,16 @@ def main_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("CTG_BENCH_SIM_GLOO") == "1":
+            # functional test of the multi-rank path on ONE GPU (ranks share cuda:0, gloo
+            # collectives through the host; no kernel waits on another rank): timings are
+            # meaningless and not reported as measurements
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -265,7 +273,7 @@ def main_ours(args):
             if timed:
                 evs[i + 1].record(stream)
         if G > 1:
-            dist.all_gather_into_tensor(full, send)
+            dist.all_gather_into_tensor(full.view(-1, Pb, N), send)
         if timed:
             evs[5].record(stream)
         crt()
@@ -322,8 +330,11 @@ def main_ours(args):
         e2e_ms = 1e3 * sum(walls) / len(walls)
         e2e_phases = {k: st[k] for k in ("setup_ms", "h2d_ms", "device_ms", "d2h_ms", "decode_ms", "total_ms")}
     else:
-        e2e_ms, h2d, d2h = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh,
-                                       rank)
+        e2e_ms, h2d, d2h, check = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W,
+                                              N, sh, rank)
+        if rank == 0:  # the sharded pipeline's exact results against the one-shot call
+            assert check[0] == P.resultant(*pairs[0]) and check[1] == P.resultant(*pairs[B - 1]), \
+                "prime-sharded result != one-shot"
     e2e_value = units_step / (e2e_ms * 1e-3)
 
     # --- roofline of the dominant kernel: K3, the mod-p resultant (north_star: >= 50% of IMAD peak)
@@ -382,6 +393,7 @@ def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb
     G = dist.get_world_size()
     gathered = torch.zeros((G,) + tuple(out.shape), dtype=torch.int32, device=out.device)
     walls = []
+    check = None
     for it in range(args.warmup + args.steps):
         dist.barrier()
         torch.cuda.synchronize()
@@ -389,16 +401,16 @@ def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb
         plan.upload(sh)
         for s_ in (1, 2, 3):
             plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
-        dist.all_gather_into_tensor(full, send)
+        dist.all_gather_into_tensor(full.view(-1, *send.shape[1:]), send)
         plan.crt_batch(full.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N, row_block=Pb,
                        block_stride=B * Pb * N)
-        dist.all_gather_into_tensor(gathered, out)
+        dist.all_gather_into_tensor(gathered.view(-1), out)
         if rank == 0:
             from paper_1103_4697_b200 import sharding
 
             full_host = sharding.reassemble(gathered.cpu().numpy().view("uint32"), B, D, W, G)
-            for bi in range(B):
-                plan.decode(full_host[bi])
+            decoded = [plan.decode(full_host[bi]) for bi in range(B)]
+            check = (decoded[0], decoded[B - 1])
         torch.cuda.synchronize()
         if it >= args.warmup:
             walls.append(time.perf_counter() - t0)
@@ -406,7 +418,7 @@ def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb
     d2h = int(gathered.numel() * 4)
     t = torch.tensor([1e3 * sum(walls) / len(walls)], dtype=torch.float64, device=out.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item()), h2d, d2h
+    return float(t.item()), h2d, d2h, check
 
 
 def headline(P, curves):
