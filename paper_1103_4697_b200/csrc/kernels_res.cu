@@ -779,6 +779,107 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
 }
 
 
+// The same walk with coalesced output: a warp's 32 coefficients are consecutive rows, each lane
+// walks its own row's digits (as k_crt_carry_seq), the limbs go through a 32 x 33 shared-memory
+// tile per warp, and every 32 limbs the warp stores them row by row (128 contiguous bytes per
+// store instead of 32 scattered words); negative values are then negated by the whole warp,
+// one row at a time (two's complement: the +1 ripples to the lowest nonzero limb, found by a
+// ballot).  CTA = 4 warps = one 128-row tile of the GEMM output.
+template <bool WIDE>
+__global__ void __launch_bounds__(128) k_crt_carry_tile(CrtParams C) {
+  __shared__ uint32_t stage[4][32 * 33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ncoef = C.J * C.B;
+  const bool live = g < ncoef;
+  const int gc = live ? g : ncoef - 1;  // idle lanes shadow the last row (never stored)
+  const int b = gc / C.J, jl = gc - b * C.J;
+  const int OL = C.out_limbs;
+  const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+  double s = 0;
+  for (int q = 0; q < nch; ++q) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
+  const double tr = rint(s);
+  if (live && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  const int32_t t = static_cast<int32_t>(tr);
+  const int4* col = reinterpret_cast<const int4*>(C.cols) + static_cast<size_t>(gc >> 7) * (C.L8p / 4) * 128 + (gc & 127);
+  const uint4* m8 = reinterpret_cast<const uint4*>(C.M8);
+  const int row0 = blockIdx.x * blockDim.x + warp * 32;  // first row of this warp
+  uint32_t* st = stage[warp];
+  using acc_t = typename std::conditional<WIDE, long long, int>::type;
+  acc_t carry = 0;
+  uint32_t any = 0;
+  constexpr int kBatch = 8;
+  for (int w0 = 0; w0 < OL; w0 += 32) {
+#pragma unroll
+    for (int wb = 0; wb < 32; wb += kBatch) {
+      int4 cb[kBatch];
+      uint4 mb[kBatch];
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int w = w0 + wb + i;
+        if (w < OL) {
+          cb[i] = col[static_cast<size_t>(w) * 128];
+          mb[i] = __ldg(&m8[w]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int w = w0 + wb + i;
+        if (w >= OL) break;
+        const int4 c = cb[i];
+        const uint4 m = mb[i];
+        acc_t v = carry + c.x - static_cast<acc_t>(t) * static_cast<int>(m.x);
+        uint32_t limb = static_cast<uint32_t>(v) & 0xffu;
+        v = (v >> 8) + c.y - static_cast<acc_t>(t) * static_cast<int>(m.y);
+        limb |= (static_cast<uint32_t>(v) & 0xffu) << 8;
+        v = (v >> 8) + c.z - static_cast<acc_t>(t) * static_cast<int>(m.z);
+        limb |= (static_cast<uint32_t>(v) & 0xffu) << 16;
+        v = (v >> 8) + c.w - static_cast<acc_t>(t) * static_cast<int>(m.w);
+        limb |= static_cast<uint32_t>(v) << 24;
+        carry = v >> 8;
+        any |= limb;
+        st[(wb + i) * 33 + lane] = limb;
+      }
+    }
+    __syncwarp();
+    // flush limbs [w0, w0 + 32) of the warp's rows: lane l stores limb w0 + l of row c
+    const int nw = min(32, OL - w0);
+    for (int c = 0; c < 32; ++c) {
+      const int r = row0 + c;
+      if (r < ncoef && lane < nw)
+        C.out[static_cast<size_t>(r) * (OL + 1) + 1 + w0 + lane] = st[lane * 33 + c];
+    }
+    __syncwarp();
+  }
+  // |V| < M / 2 < 2^(32 OL - 1): the final carry is 0 (V >= 0) or -1 (V < 0); -V = ~V + 1.
+  const bool neg = live && carry < 0;
+  if (live) C.out[static_cast<size_t>(g) * (OL + 1)] = static_cast<uint32_t>(neg ? -1 : (any ? 1 : 0));
+  unsigned todo = __ballot_sync(0xffffffffu, neg);
+  __syncwarp();  // this warp's limb stores are visible to its own lanes
+  while (todo) {
+    const int c = __ffs(todo) - 1;
+    todo &= todo - 1;
+    uint32_t* rowp = C.out + static_cast<size_t>(row0 + c) * (OL + 1) + 1;
+    bool seen = false;  // warp-uniform: the lowest nonzero limb has been passed
+    for (int w0 = 0; w0 < OL; w0 += 32) {
+      const int w = w0 + lane;
+      const uint32_t x = w < OL ? rowp[w] : 0u;
+      uint32_t y = ~x;
+      if (!seen) {
+        const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
+        if (nz) {
+          const int z = __ffs(nz) - 1;
+          y = lane < z ? 0u : (lane == z ? 0u - x : ~x);
+          seen = true;
+        } else {
+          y = 0u;
+        }
+      }
+      if (w < OL) rowp[w] = y;
+    }
+  }
+}
+
 // Same carry propagation with a WARP per coefficient, for calls with few coefficients (single
 // curves: 871 coefficients at d30 or 241 at d16/1024 leave the thread-per-coefficient walk
 // with 7 or 2 CTAs walking 1,000-4,000 digits each).  Lane l walks limbs [l S, (l+1) S) with
@@ -1051,10 +1152,20 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
       return 3;
     }
     const unsigned blocks = static_cast<unsigned>((coeffs + 127) / 128);
-    if (wide)
-      k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
-    else
-      k_crt_carry_seq<false><<<blocks, 128, 0, st>>>(cp);
+    // Coalesced-store tile walk for short outputs (d20: 90 limbs, CRT 0.234 -> 0.201 ms per 256
+    // curves); long ones keep the per-thread walk (d16/1024's 1,000 limbs: the warp-serial
+    // negation of negative rows costs more than the scattered stores, 0.49 -> 0.84 ms).
+    static const bool seq_forced = std::getenv("CTG_CARRY_SEQ") != nullptr;  // A/B switch
+    if (seq_forced || cp.out_limbs > 128) {
+      if (wide)
+        k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
+      else
+        k_crt_carry_seq<false><<<blocks, 128, 0, st>>>(cp);
+    } else if (wide) {
+      k_crt_carry_tile<true><<<blocks, 128, 0, st>>>(cp);
+    } else {
+      k_crt_carry_tile<false><<<blocks, 128, 0, st>>>(cp);
+    }
     return 3;
   }
   k_crt_prep<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
