@@ -782,9 +782,10 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
 // The same walk with coalesced output: a warp's 32 coefficients are consecutive rows, each lane
 // walks its own row's digits (as k_crt_carry_seq), the limbs go through a 32 x 33 shared-memory
 // tile per warp, and every 32 limbs the warp stores them row by row (128 contiguous bytes per
-// store instead of 32 scattered words); negative values are then negated by the whole warp,
-// one row at a time (two's complement: the +1 ripples to the lowest nonzero limb, found by a
-// ballot).  CTA = 4 warps = one 128-row tile of the GEMM output.
+// store instead of 32 scattered words); negative values are then negated -- rows of <= 128
+// limbs by the whole warp, one row at a time (two's complement: the +1 ripples to the lowest
+// nonzero limb, found by a ballot), longer rows by their own lane (a warp-serial pass over
+// 1,000-limb rows costs more than it saves).  CTA = 4 warps = one 128-row tile of the output.
 template <bool WIDE>
 __global__ void __launch_bounds__(128) k_crt_carry_tile(CrtParams C) {
   __shared__ uint32_t stage[4][32 * 33];
@@ -854,8 +855,20 @@ __global__ void __launch_bounds__(128) k_crt_carry_tile(CrtParams C) {
   // |V| < M / 2 < 2^(32 OL - 1): the final carry is 0 (V >= 0) or -1 (V < 0); -V = ~V + 1.
   const bool neg = live && carry < 0;
   if (live) C.out[static_cast<size_t>(g) * (OL + 1)] = static_cast<uint32_t>(neg ? -1 : (any ? 1 : 0));
+  __syncwarp();  // this warp's limb stores are visible to all its lanes
+  if (OL > 128) {  // long rows: every negative lane negates its own row (rows in parallel)
+    if (neg) {
+      uint32_t* rowp = C.out + static_cast<size_t>(g) * (OL + 1) + 1;
+      uint32_t cin = 1;
+      for (int w = 0; w < OL; ++w) {
+        const uint32_t x = ~rowp[w] + cin;
+        cin = (cin && x == 0u) ? 1u : 0u;
+        rowp[w] = x;
+      }
+    }
+    return;
+  }
   unsigned todo = __ballot_sync(0xffffffffu, neg);
-  __syncwarp();  // this warp's limb stores are visible to its own lanes
   while (todo) {
     const int c = __ffs(todo) - 1;
     todo &= todo - 1;
@@ -1152,11 +1165,10 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
       return 3;
     }
     const unsigned blocks = static_cast<unsigned>((coeffs + 127) / 128);
-    // Coalesced-store tile walk for short outputs (d20: 90 limbs, CRT 0.234 -> 0.201 ms per 256
-    // curves); long ones keep the per-thread walk (d16/1024's 1,000 limbs: the warp-serial
-    // negation of negative rows costs more than the scattered stores, 0.49 -> 0.84 ms).
+    // Coalesced-store tile walk (CRT stage vs the scattered-store walk: d20 / 256 curves 0.246 ->
+    // 0.204 ms, d30 / 64 0.326 -> 0.267 ms, d16/1024 / 64 0.486 -> 0.497 ms).
     static const bool seq_forced = std::getenv("CTG_CARRY_SEQ") != nullptr;  // A/B switch
-    if (seq_forced || cp.out_limbs > 128) {
+    if (seq_forced) {
       if (wide)
         k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
       else
