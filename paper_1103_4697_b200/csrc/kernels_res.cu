@@ -321,16 +321,39 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
   }
   if (bad) atomicOr(&counters[1], kErrSentinel);
   __syncthreads();
-  // R radix-2 inverse NTTs of length Mlen (index math by shifts: every length is a power of 2)
-  const int lgh = a - 1;  // log2(Mlen / 2)
-  for (int lg = 1; lg <= a; ++lg) {
-    const int half = 1 << (lg - 1), lgstep = a - lg;
+  // R inverse NTTs of length Mlen, DIT on the bit-reversed input: stages (lg, lg + 1) fused
+  // into radix-4 passes (4 elements per thread: the same 4 twiddle products as two radix-2
+  // stages, half the shared-memory traffic, index math and barriers), then a last radix-2
+  // stage when log2(Mlen) is odd.  Index math by shifts (every length is a power of 2).
+  int lg = 1;
+  for (; lg + 1 <= a; lg += 2) {
+    const int h = 1 << (lg - 1), l4 = a - 2;  // items per NTT: Mlen / 4 = 2^l4
+    const int s1 = a - lg, s2 = a - lg - 1;   // twiddle strides of the two stages
+    for (int bb = tid; bb < (R << l4); bb += bs) {
+      const int rw = bb >> l4, q = bb & ((1 << l4) - 1);
+      const int g = q >> (lg - 1), t = q & (h - 1);
+      uint32_t* base = w + rw * Mlen + (g << (lg + 1));
+      const uint32_t x0 = base[t], x1 = base[t + h], x2 = base[t + 2 * h], x3 = base[t + 3 * h];
+      const uint32_t w1 = tw[(R * t) << s1];
+      const uint32_t v1 = mmul(x1, w1, M), v3 = mmul(x3, w1, M);
+      const uint32_t y0 = madd(x0, v1, M.p), y1 = msub(x0, v1, M.p);
+      const uint32_t y2 = madd(x2, v3, M.p), y3 = msub(x2, v3, M.p);
+      const uint32_t u2 = mmul(y2, tw[(R * t) << s2], M), u3 = mmul(y3, tw[(R * (t + h)) << s2], M);
+      base[t] = madd(y0, u2, M.p);
+      base[t + 2 * h] = msub(y0, u2, M.p);
+      base[t + h] = madd(y1, u3, M.p);
+      base[t + 3 * h] = msub(y1, u3, M.p);
+    }
+    __syncthreads();
+  }
+  if (lg == a) {  // odd log2(Mlen): one radix-2 stage
+    const int half = 1 << (lg - 1), lgh = a - 1;
     for (int bb = tid; bb < (R << lgh); bb += bs) {
       const int rw = bb >> lgh, q = bb & ((1 << lgh) - 1);
       const int g = q >> (lg - 1), t = q & (half - 1);
       uint32_t* base = w + rw * Mlen + (g << lg);
       const uint32_t u = base[t];
-      const uint32_t v = mmul(base[t + half], tw[(R * t) << lgstep], M);
+      const uint32_t v = mmul(base[t + half], tw[R * t], M);
       base[t] = madd(u, v, M.p);
       base[t + half] = msub(u, v, M.p);
     }
