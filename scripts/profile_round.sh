@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches_default.csv $DEF > $O/ncu_default.log 2>&1
 B=$(python -c "import json;print(json.load(open('$O/plain_default.json'))['config']['curves_per_step'])")
 ONE="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-headline"
-for k in k_modres_fast k_eval_ntt k_gemm_u8_tma k_crt_carry_seq k_crt_prep_t k_interp k_reduce; do
+for k in k_modres_fast k_eval_ntt k_gemm_u8_tma k_crt_carry k_crt_prep_t k_interp k_reduce; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o $O/full_$k $ONE \
       > $O/ncu_full_$k.log 2>&1 || true
 done
