@@ -520,6 +520,26 @@ class Plan:
         finally:
             lib().ctg_upoly_free(C.byref(out))
 
+    def decode_batch_raw(self, host_words: np.ndarray) -> int:
+        """Decode every curve of a [B][D][W] CRT output into library-owned sign + limb CSR
+        buffers (what ctg_resultant_batch hands a C caller) and free them; no Python ints.
+        Returns the total limb count (a use of the result)."""
+        host_words = np.ascontiguousarray(host_words, dtype=np.uint32)
+        nb = host_words.shape[0]
+        per = host_words[0].size * 4
+        bufs = (_UpolyBuf * nb)()
+        base = host_words.ctypes.data
+        dec = lib().ctg_plan_decode
+        total = 0
+        try:
+            for bi in range(nb):
+                _check(dec(self._h, C.c_void_p(base + bi * per), C.byref(bufs[bi])), "plan_decode")
+                n = bufs[bi].n_coeffs
+                total += int(bufs[bi].limb_off[n]) if n else 0
+        finally:
+            lib().ctg_upoly_free_batch(bufs, nb)
+        return total
+
     @property
     def launches(self) -> int:
         return int(lib().ctg_plan_launches(self._h))
