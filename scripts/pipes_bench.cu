@@ -323,6 +323,132 @@ __global__ void k_row_hyb(uint32_t pp, uint32_t* sink) {
   if (s == 0x12345678) sink[0] = 1;
 }
 
+// Hybrid 2: scalars pre-divided by p (t_i = c_i / p, one DMUL per scalar per step) and the
+// rounding constant folded into the first FMA at 2^-8 granularity (magic 1.5*2^44 + 0.5):
+// u = a t1 + b t2 + c t3 + magic in 3 DFMA, q = floor(S/p + 1/2) = bits [8, 40) of u (SHF),
+// r = S - q p exactly in wrapping int32 (4 IMAD), |r| <= 0.51 p.  4 FP64 ops per update.
+constexpr double kMagic8 = 26388279066624.5;  // 1.5 * 2^44 + 0.5
+__device__ __forceinline__ int32_t hyb_q(double u) {
+  return static_cast<int32_t>(__funnelshift_r(static_cast<uint32_t>(__double2loint(u)),
+                                              static_cast<uint32_t>(__double2hiint(u)), 8));
+}
+template <int CONV>
+__global__ void k_row_hyb2(uint32_t pp, uint32_t* sink) {
+  const double pd = pp, pinv = 1.0 / pd;
+  const int32_t negp = -static_cast<int32_t>(pp);
+  int32_t A[kRow], B[kRow];
+  double Ad[kRow], Bd[kRow];
+  for (int i = 0; i < kRow; ++i) {
+    A[i] = static_cast<int32_t>((threadIdx.x * 131u + i) % pp) - static_cast<int32_t>(pp / 2);
+    B[i] = static_cast<int32_t>((threadIdx.x * 17u + 3u * i + 1u) % pp) - static_cast<int32_t>(pp / 2);
+    Ad[i] = A[i];
+    Bd[i] = B[i];
+  }
+  int32_t c1 = 12345, c2 = 678, c3 = 91011;
+  double t1 = c1 * pinv, t2 = c2 * pinv, t3 = c3 * pinv;
+#pragma unroll 1
+  for (int it = 0; it < kIt / 8; ++it) {
+#pragma unroll
+    for (int t = 1; t < kRow; ++t) {
+      const double u = __fma_rn(t3, Bd[t], __fma_rn(t2, Bd[t - 1], __fma_rn(t1, Ad[t], kMagic8)));
+      const int32_t r = c1 * A[t] + c2 * B[t - 1] + c3 * B[t] + hyb_q(u) * negp;
+      A[t] = r;
+      Ad[t] = i2d<CONV>(r);
+    }
+#pragma unroll
+    for (int t = 0; t < kRow; ++t) {
+      int32_t x = A[t];
+      A[t] = B[t];
+      B[t] = x;
+      double y = Ad[t];
+      Ad[t] = Bd[t];
+      Bd[t] = y;
+    }
+    c1 ^= A[3] & 0xffff;
+    t1 = i2d<CONV>(c1) * pinv;
+  }
+  int32_t s = 0;
+  for (int i = 0; i < kRow; ++i) s ^= A[i];
+  if (s == 0x12345678) sink[0] = 1;
+}
+
+// Exactness of the hybrid update on random symmetric inputs: out[i] = r, host checks
+// r == S mod p (as integers) and |r| <= 0.51 p.
+__global__ void k_hyb_check(uint32_t pp, const int32_t* in, int32_t* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double pinv = 1.0 / static_cast<double>(pp);
+  const int32_t negp = -static_cast<int32_t>(pp);
+  const int32_t* x = in + 6 * i;  // c1 a c2 b c3 c
+  const double u = __fma_rn(x[4] * pinv, static_cast<double>(x[5]),
+                            __fma_rn(x[2] * pinv, static_cast<double>(x[3]),
+                                     __fma_rn(x[0] * pinv, static_cast<double>(x[1]), kMagic8)));
+  out[i] = x[0] * x[1] + x[2] * x[3] + x[4] * x[5] + hyb_q(u) * negp;
+}
+
+// Swap-free rows (the real K3 is fully unrolled, so the A/B role swap costs nothing there):
+// two half-iterations per loop trip, the second updating B from A.
+__global__ void k_row_mont_ns(uint32_t p, uint32_t pneg, uint32_t* sink) {
+  Mod M{p, pneg};
+  uint32_t A[kRow], B[kRow];
+  for (int i = 0; i < kRow; ++i) {
+    A[i] = (threadIdx.x * 131u + i) % p;
+    B[i] = (threadIdx.x * 17u + 3u * i + 1u) % p;
+  }
+  uint32_t c1 = 12345u, c2 = 678u, c3 = 91011u;
+#pragma unroll 1
+  for (int it = 0; it < kIt / 16; ++it) {
+#pragma unroll
+    for (int t = 1; t < kRow; ++t) A[t] = mmul3(c1, A[t], c2, B[t - 1], c3, B[t], M);
+    c1 = csub(c1 ^ A[3], p);
+#pragma unroll
+    for (int t = 1; t < kRow; ++t) B[t] = mmul3(c1, B[t], c2, A[t - 1], c3, A[t], M);
+    c1 = csub(c1 ^ B[3], p);
+  }
+  uint32_t s = 0;
+  for (int i = 0; i < kRow; ++i) s ^= A[i] ^ B[i];
+  if (s == 0x12345678u) sink[0] = s;
+}
+template <int CONV>
+__global__ void k_row_hyb2_ns(uint32_t pp, uint32_t* sink) {
+  const double pd = pp, pinv = 1.0 / pd;
+  const int32_t negp = -static_cast<int32_t>(pp);
+  int32_t A[kRow], B[kRow];
+  double Ad[kRow], Bd[kRow];
+  for (int i = 0; i < kRow; ++i) {
+    A[i] = static_cast<int32_t>((threadIdx.x * 131u + i) % pp) - static_cast<int32_t>(pp / 2);
+    B[i] = static_cast<int32_t>((threadIdx.x * 17u + 3u * i + 1u) % pp) - static_cast<int32_t>(pp / 2);
+    Ad[i] = A[i];
+    Bd[i] = B[i];
+  }
+  int32_t c1 = 12345, c2 = 678, c3 = 91011;
+  double t1 = c1 * pinv, t2 = c2 * pinv, t3 = c3 * pinv;
+#pragma unroll 1
+  for (int it = 0; it < kIt / 16; ++it) {
+#pragma unroll
+    for (int t = 1; t < kRow; ++t) {
+      const double u = __fma_rn(t3, Bd[t], __fma_rn(t2, Bd[t - 1], __fma_rn(t1, Ad[t], kMagic8)));
+      const int32_t r = c1 * A[t] + c2 * B[t - 1] + c3 * B[t] + hyb_q(u) * negp;
+      A[t] = r;
+      Ad[t] = i2d<CONV>(r);
+    }
+    c1 ^= A[3] & 0xffff;
+    t1 = i2d<CONV>(c1) * pinv;
+#pragma unroll
+    for (int t = 1; t < kRow; ++t) {
+      const double u = __fma_rn(t3, Ad[t], __fma_rn(t2, Ad[t - 1], __fma_rn(t1, Bd[t], kMagic8)));
+      const int32_t r = c1 * B[t] + c2 * A[t - 1] + c3 * A[t] + hyb_q(u) * negp;
+      B[t] = r;
+      Bd[t] = i2d<CONV>(r);
+    }
+    c1 ^= B[3] & 0xffff;
+    t1 = i2d<CONV>(c1) * pinv;
+  }
+  int32_t s = 0;
+  for (int i = 0; i < kRow; ++i) s ^= A[i] ^ B[i];
+  if (s == 0x12345678) sink[0] = 1;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -366,6 +492,41 @@ int main() {
   tm("row_both(x2)", 2.0 * (kRow - 1) * (kIt / 8), [&] { k_row_both<<<G, T>>>(p, 0u - inv, 109000001u, sink); });
   tm("row_hyb_i2f", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb<0><<<G, T>>>(1073741789u, sink); });
   tm("row_hyb_magic", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb<1><<<G, T>>>(1073741789u, sink); });
+  tm("row_hyb2_i2f", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb2<0><<<G, T>>>(1073741789u, sink); });
+  tm("row_hyb2_magic", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb2<1><<<G, T>>>(1073741789u, sink); });
+  tm("row_mont_ns", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_mont_ns<<<G, T>>>(p, 0u - inv, sink); });
+  tm("row_hyb2_ns_i2f", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb2_ns<0><<<G, T>>>(1073741789u, sink); });
+  tm("row_hyb2_ns_mag", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_hyb2_ns<1><<<G, T>>>(1073741789u, sink); });
+  tm("row_mont2", 1.0 * (kRow - 1) * (kIt / 8), [&] { k_row_mont<<<G, T>>>(p, 0u - inv, sink); });
+  {
+    const int n = 1 << 22;
+    const uint32_t pc = 1415999977u;  // near the top of the prime window (odd; primality irrelevant here)
+    int32_t *din, *dout;
+    cudaMalloc(&din, 6ull * n * 4);
+    cudaMalloc(&dout, 1ull * n * 4);
+    int32_t* hin = new int32_t[6ull * n];
+    int32_t* hout = new int32_t[n];
+    uint64_t s = 88172645463325252ull;
+    auto rnd = [&] { s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; };
+    const int64_t lim = static_cast<int64_t>(0.51 * pc);
+    for (int64_t i = 0; i < 6ll * n; ++i) {
+      int64_t v = static_cast<int64_t>(rnd() % (2 * lim + 1)) - lim;
+      if (i % 97 == 0) v = (i & 1) ? lim : -lim;  // extremes
+      hin[i] = static_cast<int32_t>(v);
+    }
+    cudaMemcpy(din, hin, 6ull * n * 4, cudaMemcpyHostToDevice);
+    k_hyb_check<<<(n + 255) / 256, 256>>>(pc, din, dout, n);
+    cudaMemcpy(hout, dout, 4ull * n, cudaMemcpyDeviceToHost);
+    long bad = 0, wide = 0;
+    for (int i = 0; i < n; ++i) {
+      const int32_t* x = hin + 6ll * i;
+      __int128 S = (__int128)x[0] * x[1] + (__int128)x[2] * x[3] + (__int128)x[4] * x[5];
+      __int128 d = S - hout[i];
+      if (d % pc != 0) ++bad;
+      if (hout[i] > lim || hout[i] < -lim) ++wide;
+    }
+    printf("hyb_check n=%d wrong=%ld out_of_range=%ld\n", n, bad, wide);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;

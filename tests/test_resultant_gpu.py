@@ -296,3 +296,40 @@ def test_large_batch_bounded_slots():
     for i in range(0, 600, 37):
         assert got[i] == P.resultant(*pairs[i]), i
     assert got[:64] == P.resultant_batch(pairs[:64])
+
+
+_HYB_EXTRA = r"""
+import hashlib, json, sys
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+import paper_1103_4697_b200 as P
+from paper_1103_4697_b200 import curves
+out = {}
+for d in (4, 9, 16, 20, 25, 32):
+    f = curves.make("dense", d, 40, d)
+    R = P.resultant(curves.derive_x(f), curves.derive_y(f))  # equal y-degrees: the EQ kernel
+    out[str(d)] = hashlib.sha256(",".join(format(c, "x") for c in R).encode()).hexdigest()
+print(json.dumps(out))
+"""
+
+
+def test_k3_hybrid_euclid():
+    """The opt-in hybrid FP64-quotient / IMAD Euclid (CTG_K3_HYB=1, read once per process):
+    every res(f, f_y) fixture, the reference digests of the big configs, and the equal-degree
+    (Teissier-shape) kernel against the default Montgomery path."""
+    import json
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CTG_K3_HYB="1")
+    out = subprocess.run([sys.executable, "-c", _FUSED_CHILD, repo], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1])["checked"] >= 6
+    out = subprocess.run([sys.executable, "-c", _HYB_EXTRA, repo], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    for d, h in got.items():
+        f = curves.make("dense", int(d), 40, int(d))
+        assert _digest(P.resultant(curves.derive_x(f), curves.derive_y(f))) == h, d
