@@ -109,6 +109,29 @@ cudaStream_t Ctx::aux_stream(int i) {
   return aux[i];
 }
 
+int Ctx::prio_levels() {
+  if (!nprio) {
+    int least = 0, greatest = 0;
+    CTG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    nprio = std::max(1, std::min(8, least - greatest + 1));
+  }
+  return nprio;
+}
+
+cudaStream_t Ctx::prio_stream(int level) {
+  level %= prio_levels();
+  if (!prio[level]) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CTG_CUDA_CHECK(cudaSetDevice(device));
+    int least = 0, greatest = 0;
+    CTG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CTG_CUDA_CHECK(cudaStreamCreateWithPriority(&prio[level], cudaStreamNonBlocking, greatest + level));
+    cudaSetDevice(prev);
+  }
+  return prio[level];
+}
+
 uint8_t* Ctx::pinned_input(size_t bytes) {
   bytes = std::max<size_t>(16, bytes);
   if (pinned_in_bytes < bytes) {

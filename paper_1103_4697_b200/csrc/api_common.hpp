@@ -78,6 +78,13 @@ struct Ctx {
   cudaStream_t copy_stream();
   cudaStream_t aux[2] = {nullptr, nullptr};  // extra compute streams (batch chunks rotate)
   cudaStream_t aux_stream(int i = 0);
+  // Compute streams of decreasing priority (level 0 = the device's greatest priority): batch
+  // chunk i runs at level i % prio_levels(), so the oldest chunk in flight wins the block
+  // scheduler and chunks complete in order while younger ones fill the idle SMs.
+  cudaStream_t prio[8] = {};
+  int nprio = 0;
+  int prio_levels();
+  cudaStream_t prio_stream(int level);
   uint32_t* scratch_u32(int slot, size_t words);
   uint32_t* pinned_u32(size_t words);     // D2H staging
   uint8_t* pinned_input(size_t bytes);    // H2D staging

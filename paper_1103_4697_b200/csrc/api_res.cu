@@ -708,8 +708,17 @@ class ChunkPipeline {
       return e ? std::max(1, std::min(3, std::atoi(e))) : 0;
     }();
     const int nstreams = forced ? forced : nstreams_;
-    const int si = n_enqueued_++ % nstreams;
-    cudaStream_t s = si == 0 ? ctx_.stream : ctx_.aux_stream(si - 1), cp = ctx_.copy_stream();
+    // CTG_CHUNK_PRIO=0: plain rotation over equal-priority streams (A/B)
+    static const bool prio = [] {
+      const char* e = std::getenv("CTG_CHUNK_PRIO");
+      return !(e && e[0] == '0');
+    }();
+    const int ci = n_enqueued_++;
+    const int si = ci % nstreams;
+    cudaStream_t s = prio && nstreams > 1 ? ctx_.prio_stream(ci)
+                     : si == 0            ? ctx_.stream
+                                          : ctx_.aux_stream(si - 1);
+    cudaStream_t cp = ctx_.copy_stream();
     if (trace()) {
       for (cudaEvent_t* e : {&c.t_begin, &c.t_computed, &c.t_copied}) CTG_CUDA_CHECK(cudaEventCreate(e));
       if (!t0_) {
