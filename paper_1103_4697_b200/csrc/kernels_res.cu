@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(128) k_crt_carry_seq(CrtParams C) {
 // limbs by the whole warp, one row at a time (two's complement: the +1 ripples to the lowest
 // nonzero limb, found by a ballot), longer rows by their own lane (a warp-serial pass over
 // 1,000-limb rows costs more than it saves).  CTA = 4 warps = one 128-row tile of the output.
-template <bool WIDE>
+template <bool WIDE, int kBatch>
 __global__ void __launch_bounds__(128) k_crt_carry_tile(CrtParams C) {
   __shared__ uint32_t stage[4][32 * 33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -832,7 +832,6 @@ __global__ void __launch_bounds__(128) k_crt_carry_tile(CrtParams C) {
   using acc_t = typename std::conditional<WIDE, long long, int>::type;
   acc_t carry = 0;
   uint32_t any = 0;
-  constexpr int kBatch = 8;
   for (int w0 = 0; w0 < OL; w0 += 32) {
 #pragma unroll
     for (int wb = 0; wb < 32; wb += kBatch) {
@@ -1196,10 +1195,24 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
         k_crt_carry_seq<true><<<blocks, 128, 0, st>>>(cp);
       else
         k_crt_carry_seq<false><<<blocks, 128, 0, st>>>(cp);
-    } else if (wide) {
-      k_crt_carry_tile<true><<<blocks, 128, 0, st>>>(cp);
     } else {
-      k_crt_carry_tile<false><<<blocks, 128, 0, st>>>(cp);
+      // limbs loaded per batch (memory-level parallelism of the walk; CTG_CARRY_KB=8 for A/B):
+      // 16 vs 8 measured d16/1024 CRT 0.498 -> 0.461 ms, d30 0.268 -> 0.262 ms, d20 equal; 32
+      // (255 registers) slower everywhere (scripts/ab_carry_kb.sh)
+      static const bool kb8 = [] {
+        const char* e = std::getenv("CTG_CARRY_KB");
+        return e && std::atoi(e) == 8;
+      }();
+      if (kb8) {
+        if (wide)
+          k_crt_carry_tile<true, 8><<<blocks, 128, 0, st>>>(cp);
+        else
+          k_crt_carry_tile<false, 8><<<blocks, 128, 0, st>>>(cp);
+      } else if (wide) {
+        k_crt_carry_tile<true, 16><<<blocks, 128, 0, st>>>(cp);
+      } else {
+        k_crt_carry_tile<false, 16><<<blocks, 128, 0, st>>>(cp);
+      }
     }
     return 3;
   }
