@@ -96,6 +96,10 @@ unsigned long __gmpz_get_ui(mpz_srcptr);
 int __gmpz_fits_slong_p(mpz_srcptr);
 void __gmpz_import(mpz_ptr, size_t, int, size_t, int, size_t, const void*);
 void* __gmpz_export(void*, size_t*, int, size_t, int, size_t, mpz_srcptr);
+size_t __gmpz_size(mpz_srcptr);
+const mp_limb_t* __gmpz_limbs_read(mpz_srcptr);
+mp_limb_t* __gmpz_limbs_write(mpz_ptr, mp_size_t);
+void __gmpz_limbs_finish(mpz_ptr, mp_size_t);
 
 /* ---- rationals ---- */
 void __gmpq_init(mpq_ptr);
@@ -157,6 +161,10 @@ char* __gmpq_get_str(char*, int, mpq_srcptr);
 #define mpz_get_si __gmpz_get_si
 #define mpz_import __gmpz_import
 #define mpz_export __gmpz_export
+#define mpz_size __gmpz_size
+#define mpz_limbs_read __gmpz_limbs_read
+#define mpz_limbs_write __gmpz_limbs_write
+#define mpz_limbs_finish __gmpz_limbs_finish
 #define mpz_sgn(z) ((z)->_mp_size < 0 ? -1 : (z)->_mp_size > 0)
 #define mpq_numref(q) (&((q)->_mp_num))
 #define mpq_denref(q) (&((q)->_mp_den))
