@@ -23,4 +23,7 @@ void __gmpz_divexact(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struc
 void __gmpz_tdiv_r(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_mul(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 size_t __gmpz_sizeinbase(const ctg_mpz_struct*, int);
+// GMP 6 limb access (64-bit little-endian limbs on x86-64: the u32 words are their bytes)
+unsigned long* __gmpz_limbs_write(ctg_mpz_struct*, long);
+void __gmpz_limbs_finish(ctg_mpz_struct*, long);
 }

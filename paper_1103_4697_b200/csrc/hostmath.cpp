@@ -1,3 +1,4 @@
+#include <cstring>
 #include "hostmath.hpp"
 
 #include "gmp_host.hpp"
@@ -260,20 +261,31 @@ double log2_sum_upper(const std::vector<double>& xs) {
 
 // Multiplication, gcd and exact division on the host go through GMP (subquadratic; the
 // reference's own dependency) -- they serve contents, primitive parts and certificates.
+static_assert(sizeof(unsigned long) == 8 && __BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__,
+              "64-bit little-endian GMP limbs expected");
 namespace {
 struct Mpz {
   ctg_mpz_struct z;
   Mpz() { __gmpz_init(&z); }
+  // u32 magnitude <-> GMP limbs by copy (mpz_import / mpz_export with 4-byte words take a
+  // generic ~0.5 GB/s path; a 1,000-limb content gcd spent most of its time converting)
   explicit Mpz(const Big& a) {
     __gmpz_init(&z);
-    if (!a.empty()) __gmpz_import(&z, a.size(), -1, 4, 0, 0, a.data());
+    size_t n = a.size();
+    while (n && a[n - 1] == 0) --n;
+    if (n) {
+      const size_t nl = (n + 1) / 2;
+      unsigned long* d = __gmpz_limbs_write(&z, static_cast<long>(nl));
+      d[nl - 1] = 0;
+      std::memcpy(d, a.data(), 4 * n);
+      __gmpz_limbs_finish(&z, static_cast<long>(nl));
+    }
   }
   ~Mpz() { __gmpz_clear(&z); }
-  Big big() const {
-    Big r((__gmpz_sizeinbase(&z, 2) + 31) / 32 + 1, 0u);
-    size_t cnt = 0;
-    __gmpz_export(r.data(), &cnt, -1, 4, 0, 0, &z);
-    r.resize(cnt);
+  Big big() const {  // magnitude
+    const size_t n = static_cast<size_t>(z._mp_size < 0 ? -z._mp_size : z._mp_size);
+    Big r(2 * n);
+    if (n) std::memcpy(r.data(), z._mp_d, 8 * n);
     big_trim(r);
     return r;
   }
