@@ -994,21 +994,27 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     // GPU runs the previous one (each shape group of a block is one batched plan = one launch
     // set).  The first and last blocks are small (they are the exposed head -- host parsing
     // before the GPU starts -- and tail -- the last D2H and decode); the middle ones are large
-    // (fewer, fuller launches).  E.g. 256 curves -> 32 | 64 | 64 | 64 | 32.
+    // (fewer, fuller launches).  E.g. 256 curves -> 32 | 64 | 64 | 64 | 32, 64 -> 8 | 16 | 16 | 16 | 8.
     std::vector<int> bounds{0};
     if (batch <= 32) {
       bounds.push_back(batch);
     } else {
-      static const int kMid = [] {  // largest middle block (CTG_BLOCK_MAX, for experiments)
+      static const int kMidForced = [] {  // largest middle block (CTG_BLOCK_MAX, for experiments)
         const char* e = std::getenv("CTG_BLOCK_MAX");
-        return e ? std::max(16, std::atoi(e)) : 64;
+        return e ? std::max(8, std::atoi(e)) : 0;
       }();
       static const int kHead = [] {
         const char* e = std::getenv("CTG_BLOCK_HEAD");
         return e ? std::max(4, std::atoi(e)) : 32;
       }();
       const int s0 = std::min(kHead, std::max(8, batch / 8));
-      const int mid = batch - 2 * s0, nm = (mid + kMid - 1) / kMid, per = (mid + nm - 1) / nm;
+      // at least three middle blocks (up to 64 curves each): with the priority streams a chunk's
+      // D2H and decode overlap the later chunks' kernels, which needs chunks to overlap
+      // (scripts/ab_blocks_big.sh, 64 curves: 8|48|8 -> 8|16|16|16|8 took d16/1024 e2e from 3.05
+      // to 4.21e9 units/s and d30 from 2.01 to 2.35e9; 256 curves keep 32|64|64|64|32)
+      const int mid = batch - 2 * s0;
+      const int kMid = kMidForced ? kMidForced : std::min(64, std::max(16, (mid + 2) / 3));
+      const int nm = (mid + kMid - 1) / kMid, per = (mid + nm - 1) / nm;
       bounds.push_back(s0);
       for (int k = 0; k < nm; ++k) bounds.push_back(std::min(s0 + mid, bounds.back() + per));
       bounds.push_back(batch);
