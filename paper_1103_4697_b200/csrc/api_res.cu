@@ -1008,12 +1008,29 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
         return e ? std::max(4, std::atoi(e)) : 32;
       }();
       const int s0 = std::min(kHead, std::max(8, batch / 8));
-      // at least three middle blocks (up to 64 curves each): with the priority streams a chunk's
+      // big results: at least three middle blocks (up to 64 curves each): with the priority streams a chunk's
       // D2H and decode overlap the later chunks' kernels, which needs chunks to overlap
       // (scripts/ab_blocks_big.sh, 64 curves: 8|48|8 -> 8|16|16|16|8 took d16/1024 e2e from 3.05
       // to 4.21e9 units/s and d30 from 2.01 to 2.35e9; 256 curves keep 32|64|64|64|32)
       const int mid = batch - 2 * s0;
-      const int kMid = kMidForced ? kMidForced : std::min(64, std::max(16, (mid + 2) / 3));
+      // Result size of the first curve, roughly deg^2 coefficients of deg * bits bits (d20/64:
+      // 64 KB, d30/128: 430 KB, d16/1024: 520 KB, d10/10: 1 KB): small results (launch-bound
+      // chunks, cheap decode: d10, 64 curves, e2e 0.21 vs 0.13e9 units/s) keep 64-curve middle blocks;
+      // d20 with 64 curves splits (e2e 1.49 -> 2.71e9).
+      double est_bytes = 0;
+      {
+        const ctg_bipoly& f = p[0];
+        int deg = 0;
+        uint32_t maxl = 0;
+        const int32_t nt = (f.dx && f.dy && f.limb_off) ? f.n_terms : 0;  // (inputs are validated later)
+        for (int32_t t = 0; t < nt; ++t) {
+          deg = std::max(deg, f.dx[t] + f.dy[t]);
+          maxl = std::max(maxl, f.limb_off[t + 1] - f.limb_off[t]);
+        }
+        est_bytes = static_cast<double>(deg) * deg * deg * 32.0 * maxl / 8.0;
+      }
+      const bool big_out = est_bytes > 20e3;
+      const int kMid = kMidForced ? kMidForced : big_out ? std::min(64, std::max(16, (mid + 2) / 3)) : 64;
       const int nm = (mid + kMid - 1) / kMid, per = (mid + nm - 1) / nm;
       bounds.push_back(s0);
       for (int k = 0; k < nm; ++k) bounds.push_back(std::min(s0 + mid, bounds.back() + per));
