@@ -252,14 +252,21 @@ __device__ uint32_t res_general(uint32_t* A, int na, uint32_t* B, int nb, const 
 
 // General path: one thread per unit, either all units (use_list = 0) or the
 // degenerate units listed by the fast path.  Unit id = (b * nk + kl) * N + i.
+// When the fast path flagged more units than the list holds (curves whose remainder sequence
+// drops degree at every point, e.g. y^n + g(x), n >= 3), the list is abandoned and every unit
+// of the launch is scanned: the ones the fast kernel left at kSentinel are recomputed.
 __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_list, uint32_t total_units) {
-  const uint32_t count = use_list ? min(P.counters[0], P.flag_cap) : total_units;
+  const uint32_t flagged = use_list ? P.counters[0] : 0u;
+  const bool scan = use_list && flagged > P.flag_cap;
+  const uint32_t all = static_cast<uint32_t>(P.B) * static_cast<uint32_t>(P.nk) * static_cast<uint32_t>(P.N);
+  const uint32_t count = scan ? all : (use_list ? flagged : total_units);
   const int nq = P.n + 1;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < count; u += gridDim.x * blockDim.x) {
-    const uint32_t unit = use_list ? P.flag_list[u] : u;
+    const uint32_t unit = (use_list && !scan) ? P.flag_list[u] : u;
     const uint32_t bk = unit / P.N;
     const int i = static_cast<int>(unit % P.N);
     const int kl = static_cast<int>(bk % P.nk), b = static_cast<int>(bk / P.nk);
+    if (scan && P.rows[b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch + i] != kSentinel) continue;
     const int k = P.k0 + kl;
     const PrimeConst pcv = P.pc[k];
     const Mod M = load_mod(pcv);
@@ -1074,12 +1081,15 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
   return 1;
 }
 
+// Enough blocks for the scan mode of k_modres_general (blocks beyond a short list exit at once).
+constexpr int kGeneralListBlocks = 148 * 4;
+
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
   if (rp.nk == 0 || rp.B == 0) return 0;
   if (fast && rp.fused) {  // K2 folded into K3: the point values never leave shared memory
     if (part == 1) return 0;
     if (dispatch_fused_any(rp.n, rp, st)) {
-      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);
+      k_modres_general<<<kGeneralListBlocks, 128, 0, st>>>(rp, 1, 0u);
       return 2;
     }
   }
@@ -1087,7 +1097,7 @@ int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
     const int launches = part == 2 ? 0 : launch_eval(rp, st);  // K2
     if (part == 1) return launches;
     if (dispatch_fast_any(rp.n, rp, st)) {                      // K3
-      k_modres_general<<<64, 128, 0, st>>>(rp, 1, 0u);          // degenerate units, exact
+      k_modres_general<<<kGeneralListBlocks, 128, 0, st>>>(rp, 1, 0u);          // degenerate units, exact
       return launches + 2;
     }
   }

@@ -77,10 +77,7 @@ constexpr int ilog2_c(int v) {
 
 static __device__ __forceinline__ void push_flag(const ResParams& P, uint32_t unit) {
   uint32_t idx = atomicAdd(&P.counters[0], 1u);
-  if (idx < P.flag_cap)
-    P.flag_list[idx] = unit;
-  else
-    atomicOr(&P.counters[1], kErrFlagOverflow);
+  if (idx < P.flag_cap) P.flag_list[idx] = unit;  // beyond the cap: k_modres_general scans for kSentinel
 }
 
 

@@ -333,3 +333,42 @@ def test_k3_hybrid_euclid():
     for d, h in got.items():
         f = curves.make("dense", int(d), 40, int(d))
         assert _digest(P.resultant(curves.derive_x(f), curves.derive_y(f))) == h, d
+
+
+def _upow_mul(g, e, c):
+    """c * g(x)^e over Z (dense low -> high)."""
+    out = [c]
+    for _ in range(e):
+        nxt = [0] * (len(out) + len(g) - 1)
+        for i, a in enumerate(out):
+            for j, b in enumerate(g):
+                nxt[i + j] += a * b
+        out = nxt
+    return out
+
+
+def test_flag_list_overflow_superelliptic():
+    """y^n + g(x): the remainder sequence drops degree at EVERY (prime, point) unit, so the fast
+    kernel flags all of them (515 primes x 256 points > the 65,536-entry flag list).
+    res(y^n + g, n y^(n-1)) = n^n g^(n-1) exactly (the reference's Sylvester convention,
+    test_elim.cpp:16: res(y^2 - x, 2y) = -4x)."""
+    import random
+    rng = random.Random(1103)
+    g = [rng.getrandbits(1024) * rng.choice((-1, 1)) for _ in range(17)]
+    f = {(i, 0): c for i, c in enumerate(g) if c}
+    f[(0, 16)] = 1
+    assert P.resultant(f, curves.derive_y(f)) == _upow_mul(g, 15, 16 ** 16)
+
+
+def test_flag_list_overflow_batch():
+    """64 curves y^20 + g_b(x) in one batched plan: ~295K flagged units in one launch."""
+    import random
+    rng = random.Random(4697)
+    pairs, want = [], []
+    for _ in range(64):
+        g = [rng.randint(-1023, 1023) or 1 for _ in range(21)]
+        f = {(i, 0): c for i, c in enumerate(g)}
+        f[(0, 20)] = 1
+        pairs.append((f, curves.derive_y(f)))
+        want.append(_upow_mul(g, 19, 20 ** 20))
+    assert P.resultant_batch(pairs) == want
