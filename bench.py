@@ -6,12 +6,14 @@ Metric (BASELINE.json): "res(f,f_y) wall ms + mod-p resultants/s at 1/2/4/8 B200
            (units = P * D per curve: primes x result coefficients, SURVEY.md §8(d));
   e2e    = the same metric through the reference-facing C ABI (ctg_resultant_batch) with HOST
            buffers: H2D of the coefficient limbs, all kernels, D2H of the exact result.
-Workload (config.workload): BASELINE.json configs[1], random dense f of total degree 20 with
-64-bit coefficients (synthetic, the §8(d) generator), a batch of curves per step processed by
-one batched plan (every kernel launch covers all curves).  The headline d=30/128-bit curve is
-measured once more on its own (key "headline").
+Workload (config.workload): BASELINE.json configs[2], the headline: random dense f of total
+degree 30 with 128-bit coefficients (synthetic, the §8(d) generator), 64 curves per step processed
+by one batched plan (every kernel launch covers all curves).  configs[1] (d=20 / 64-bit, 256
+curves per step) is measured as an extra key ("d20_b64"); one d=30 curve through ctg_resultant
+is key "headline".  Every curve whose seed has a reference digest (tests/golden/configs_big.jsonl,
+made by the reference itself) is checked against it, outside the timed regions.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--workload d20_b64|d30_b128|...]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--workload d30_b128|d20_b64|...]
   python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N     (prime sharding + NCCL)
   python bench.py --impl reference ...      (the reference CPU implementation, oracle/_ref, all host cores)
 """
@@ -59,7 +61,40 @@ def curve_units(workload, seeds):
     if max(seeds) > len(table):
         return None
     return sum(table[s - 1] for s in seeds)
-CACHED_REF_SECONDS = {"d30_b128": 1700.4, "d16_b1024": 291.7, "d20_b64": 27.7, "d10_b10": 0.022}  # this container
+DEFAULT_BATCH = {"d30_b128": 64, "d20_b64": 256, "d16_b1024": 64, "d10_b10": 64}
+GOLDEN_BIG = os.path.join(REPO, "tests", "golden", "configs_big.jsonl")
+
+
+def workload_config(workload):
+    """config of the JSON line: identical in both arms (the workload and the unit of work)."""
+    kind, a, b, desc, _ = WORKLOADS[workload]
+    return {"workload": desc, "generator": f"{kind}({a}, {b}, seed), SURVEY.md §8(d)",
+            "units": "mod-p resultants = P * D per curve, P = primes the curve alone needs (bench_units.json)"}
+
+
+def golden_digests(workload):
+    """{seed: row} of the reference's own digests of res(f, f_y) for this workload."""
+    kind, a, b, _, _ = WORKLOADS[workload]
+    out = {}
+    try:
+        with open(GOLDEN_BIG) as fh:
+            for line in fh:
+                r = json.loads(line)
+                if r["curve"][:3] == [kind, a, b]:
+                    out[r["curve"][3]] = r
+    except OSError:
+        pass
+    return out
+
+
+def digest(coeffs):
+    import hashlib
+    return hashlib.sha256(",".join(format(c, "x") for c in coeffs).encode()).hexdigest()
+
+
+def check_golden(row, R, what):
+    if not (len(R) - 1 == row["deg"] and digest(R) == row["sha256"]):
+        raise SystemExit(f"PARITY FAILURE: {what} differs from the reference digest for curve {row['curve']}")
 
 
 def parse_args():
@@ -68,11 +103,15 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="d20_b64", choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=256, help="curves per step (seeds 1..B)")
+    ap.add_argument("--workload", default="d30_b128", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="curves per step (seeds 1..B; 0 = workload default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-headline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-extra", action="store_true", help="skip the d20_b64 extra measurement")
+    a = ap.parse_args()
+    if a.batch <= 0:
+        a.batch = DEFAULT_BATCH[a.workload]
+    return a
 
 
 # ----------------------------------------------------------------------------
@@ -155,7 +194,17 @@ def run_refdriver(kind, a, b, seed, reps=1, yun=False, timeout=None):
     return json.loads(out.strip().splitlines()[-1])
 
 
+# single-core seconds per curve of the reference on the GPU box's host (r01 measured d20: 10.05 s;
+# the others scaled from the build container by the same 2.76x): only used to pick the sample shape
+EST_REF_SECONDS = {"d10_b10": 0.008, "d20_b64": 10.0, "d16_b1024": 106.0, "d30_b128": 616.0}
+
+
 def reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref/refdriver: proj/src/elim.cpp
+    compiled unmodified) on every host core, one independent process per curve (the reference is
+    single-threaded).  Cheap workloads (d10, d20): K steps of `cores` curves each.  d30/128 needs
+    ~10 min per curve, so its bounded sample is ONE wave: min(K, cores) curves (seeds 1..), one
+    per core, all started together; value = their units / the wave's wall time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -167,28 +216,45 @@ def reference_arm(args):
     # warm-up: a tiny reference call per step (the CPU has nothing to warm beyond page-in)
     for _ in range(args.warmup):
         run_refdriver("dense", 6, 10, 1)
-    walls, done_units = [], 0
-    for step in range(args.steps):
-        seeds = [1 + (step * cores + c) % 64 for c in range(cores)]
+
+    def wave(seeds):
         t0 = time.perf_counter()
         procs = [subprocess.Popen([REFDRIVER, "time_res", kind, str(a), str(b), str(s_), "1"],
                                   stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for s_ in seeds]
         for p in procs:
             p.wait()
-        walls.append(time.perf_counter() - t0)
-        done_units += curve_units(args.workload, seeds) or units * cores
-    total = sum(walls)
+            if p.returncode != 0:
+                raise SystemExit(f"reference driver failed (rc {p.returncode})")
+        return time.perf_counter() - t0
+
+    one_wave = args.steps * EST_REF_SECONDS[args.workload] > 300
+    if one_wave:
+        n = max(1, min(args.steps, cores))
+        seeds = list(range(1, n + 1))
+        total = wave(seeds)
+        done_units = curve_units(args.workload, seeds) or units * n
+        sample = (f"{n} curves {kind}({a},{b},seed) seeds 1..{n}, one independent process per core, all started "
+                  f"together (one wave, {total:.0f} s): curvetop::resultant(f, f_y, Y) from oracle/_ref/refdriver; "
+                  f"a step is one curve")
+        ms_per_step = 1e3 * total / n
+    else:
+        walls, done_units = [], 0
+        for step in range(args.steps):
+            seeds = [1 + (step * cores + c) % 64 for c in range(cores)]
+            walls.append(wave(seeds))
+            done_units += curve_units(args.workload, seeds) or units * cores
+        total = sum(walls)
+        sample = (f"{cores} curves per step (one per core, independent processes, seeds 1..64 cycling), "
+                  f"curvetop::resultant(f, f_y, Y) from oracle/_ref/refdriver")
+        ms_per_step = 1e3 * total / args.steps
     value = done_units / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32 (GMP mpz)",
-        "data": "synthetic", "config": {"workload": desc, "curves_per_step": cores, "seeds": "1..64 cycling",
-                                        "units_per_step": done_units / args.steps,
-                                        "units": "P * D per curve, P = primes the curve alone needs (bench_units.json)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{cores} curves per step (one per core, independent processes), "
-                                   f"curvetop::resultant(f, f_y, Y) from oracle/_ref/refdriver"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int (GMP mpz)",
+        "data": "synthetic", "config": workload_config(args.workload),
+        "sample": {"units_total": done_units, "wall_s": total, "cores": cores},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -203,7 +269,7 @@ def main_ours(args):
     import torch
 
     import paper_1103_4697_b200 as P
-    from paper_1103_4697_b200 import curves, sharding
+    from paper_1103_4697_b200 import curves
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -228,10 +294,53 @@ def main_ours(args):
     # the timing events.  (Handle 0 would mean "the library's own stream" to libctg.)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    G = world
+    peaks = P.microbench_int(dev)
+
+    m = measure(args, args.workload, args.batch, P, curves, torch, dist, stream, rank, G, peaks)
+    line = {
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": G, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32 (31-bit modular, Montgomery)", "data": "synthetic",
+        "config": workload_config(args.workload),
+        "sample": m["sample"],
+        "e2e": m["e2e"],
+        "gpu_launches": m["gpu_launches"],
+        "roofline": m["roofline"],
+        "clocks": m["clocks"],
+        "parity": m["parity"],
+    }
+    if rank == 0 and G == 1 and not args.no_extra and args.workload != "d20_b64":
+        x = measure(args, "d20_b64", DEFAULT_BATCH["d20_b64"], P, curves, torch, dist, stream, rank, G, peaks)
+        line["d20_b64"] = {"workload": WORKLOADS["d20_b64"][3], "value": x["value"], "unit": UNIT,
+                           "ms_per_step": x["ms_per_step"], "sample": x["sample"], "e2e": x["e2e"],
+                           "roofline_frac": x["roofline"]["frac"], "stage_ms_per_step": x["roofline"]["stage_ms_per_step"],
+                           "gpu_launches": x["gpu_launches"], "clocks": x["clocks"], "parity": x["parity"]}
+    if rank == 0 and G == 1 and not args.no_headline:
+        line["yun"] = yun_line(P, curves, args.workload)
+    if rank == 0 and G == 1:
+        cb = None if args.no_cpu_baseline else cpu_baseline(args.workload, m["units_per_curve"])
+        line["cpu_baseline"] = cb
+        if not args.no_headline:
+            line["headline"] = headline(P, curves, args.workload, cb)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks):
+    """One workload: device-resident value (staged events), e2e through the C ABI, K3 roofline,
+    and the reference-digest parity of every curve that has one."""
+    from paper_1103_4697_b200 import sharding
+
+    dev = torch.cuda.current_device()
     sh = stream.cuda_stream
     assert sh != 0
-    kind, a, b, desc, _ = WORKLOADS[args.workload]
-    B = args.batch
+    kind, a, b, desc, _ = WORKLOADS[workload]
+    gold = golden_digests(workload)
 
     # synthetic curves (seeds 1..B), one batched plan: every launch covers all B curves
     fs = [curves.make(kind, a, b, s) for s in range(1, B + 1)]
@@ -242,8 +351,7 @@ def main_ours(args):
     W = info["out_limbs"] + 1
     # mod-p resultants per step: P * D per curve with the curve's own prime count (the batched
     # plan may use a few more primes, for the largest bound of the batch: not counted)
-    units_step = curve_units(args.workload, range(1, B + 1)) or B * Pn * D
-    G = world
+    units_step = curve_units(workload, range(1, B + 1)) or B * Pn * D
     k0, k1, Pb = sharding.prime_block(Pn, G, rank)  # rows per rank block (uniform for the all-gather)
     j0, j1, Jb = sharding.coeff_block(D, G, rank)
     plan.upload(sh)
@@ -286,12 +394,6 @@ def main_ours(args):
     plan.check(sh)
     launches0 = plan.launches
 
-    # correctness spot check of the device-resident batch (curves 0 and B-1) against the one-shot call
-    if G == 1:
-        host = out.cpu().numpy().view("uint32").reshape(B, D, W)
-        for bi in {0, B - 1}:
-            assert plan.decode(host[bi]) == P.resultant(*pairs[bi]), f"batched != one-shot (curve {bi})"
-
     total_ms = 0.0
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
@@ -305,6 +407,7 @@ def main_ours(args):
             for i in range(len(STAGES)):
                 stage_ms[i] += evs[i].elapsed_time(evs[i + 1])
     gpu_launches = plan.launches - launches0
+    plan.check(sh)
     t_max = total_ms
     if dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -313,8 +416,15 @@ def main_ours(args):
     ms_per_step = t_max / args.steps
     value = units_step / (ms_per_step * 1e-3)
 
+    # parity (outside the timed region): the device-resident batch against the reference digests
+    parity = {"reference_digests": sorted(s_ for s_ in gold if s_ <= B), "source": "tests/golden/configs_big.jsonl"}
+    if G == 1:
+        host = out.cpu().numpy().view("uint32").reshape(B, D, W)
+        for s_ in parity["reference_digests"]:
+            check_golden(gold[s_], plan.decode(host[s_ - 1]), "device-resident batch")
+        parity["device_resident"] = "bit-exact"
+
     # --- e2e through the C ABI with host buffers --------------------------------------
-    e2e_ms, h2d, d2h = None, 0, 0
     e2e_phases = None
     if G == 1:
         hb = P.HostBatch(pairs)
@@ -329,16 +439,23 @@ def main_ours(args):
             h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
         e2e_ms = 1e3 * sum(walls) / len(walls)
         e2e_phases = {k: st[k] for k in ("setup_ms", "h2d_ms", "device_ms", "d2h_ms", "decode_ms", "total_ms")}
+        got = P.resultant_batch([pairs[s_ - 1] for s_ in parity["reference_digests"]]) if gold else []
+        for s_, R in zip(parity["reference_digests"], got):
+            check_golden(gold[s_], R, "ctg_resultant_batch")
+        parity["e2e"] = "bit-exact"
     else:
         e2e_ms, h2d, d2h, check = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W,
                                               N, sh, rank)
         if rank == 0:  # the sharded pipeline's exact results against the one-shot call
             assert check[0] == P.resultant(*pairs[0]) and check[1] == P.resultant(*pairs[B - 1]), \
                 "prime-sharded result != one-shot"
+            for s_ in (1, B):
+                if s_ in gold:
+                    check_golden(gold[s_], check[0 if s_ == 1 else 1], "prime-sharded pipeline")
+            parity["sharded"] = "bit-exact"
     e2e_value = units_step / (e2e_ms * 1e-3)
 
     # --- roofline of the dominant kernel: K3, the mod-p resultant (north_star: >= 50% of IMAD peak)
-    peaks = P.microbench_int(dev)
     n = info["deg_p"]
     sm = {nm: v / args.steps for nm, v in zip(STAGES, stage_ms)}
     units_launch = B * (k1 - k0) * N
@@ -346,7 +463,7 @@ def main_ours(args):
     achieved = imad_launch / (sm["modres"] * 1e-3) / 1e12
     peak = peaks["imad_per_s"] / 1e12
     roofline = {"bound": "int32-imad", "achieved": achieved, "peak": peak, "unit": "TIMAD/s",
-                "frac": achieved / peak, "traffic": traffic_for(args.workload, B),
+                "frac": achieved / peak, "traffic": traffic_for(workload, B),
                 "kernel": f"K3 = k_modres_fast<{n}> (fused division-free Euclid) + k_modres_general (flagged units)",
                 "algorithmic": f"4 IMAD x (n^2+n-2) mulmods x {units_launch} units per launch, n={n} (SURVEY §8d)",
                 "peak_source": "measured live: ctg_microbench_int (8 IMAD chains/thread, all SMs)",
@@ -355,35 +472,18 @@ def main_ours(args):
                 # K3's count over K2 + K3 time: the evaluation stage charged to the resultant
                 "stage2_frac": imad_launch / ((sm["eval"] + sm["modres"]) * 1e-3) / 1e12 / peak,
                 "stage_ms_per_step": sm}
-
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u32 (31-bit modular, Montgomery)", "data": "synthetic",
-        "config": {"workload": desc, "curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N,
-                   "coeffs": D, "units_per_step": units_step,
-                   "units": "P * D per curve, P = primes the curve alone needs (bench_units.json)",
-                   "parallelism": f"prime-shard{G}" if G > 1 else "single",
-                   "l2": "flushed (256 MB write) between timed steps",
-                   "res_ms_per_curve": ms_per_step / B},
+    plan.close()
+    del send, full, out, flush
+    return {
+        "value": value, "ms_per_step": ms_per_step, "units_per_curve": units_step / B,
+        "sample": {"curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N, "coeffs": D,
+                   "units_per_step": units_step, "parallelism": f"prime-shard{G}" if G > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps", "res_ms_per_curve": ms_per_step / B},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "res_ms_per_curve": e2e_ms / B, "path": "ctg_resultant_batch (C ABI), host CSR limbs in/out",
                 "phases_ms_last_call": e2e_phases},
-        "gpu_launches": int(gpu_launches),
-        "roofline": roofline,
-        "clocks": clk.summary(),
+        "gpu_launches": int(gpu_launches), "roofline": roofline, "clocks": clk.summary(), "parity": parity,
     }
-    if rank == 0 and G == 1 and not args.no_headline:
-        line["headline"] = headline(P, curves)
-        line["yun"] = yun_line(P, curves, args.workload)
-    if rank == 0 and G == 1:
-        line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(args.workload, Pn * D)
-    if rank == 0:
-        print(json.dumps(line))
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
 
 
 def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh, rank):
@@ -432,8 +532,9 @@ def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb
     return float(t.item()), h2d, d2h, check
 
 
-def headline(P, curves):
-    """The north-star config: one d=30 / 128-bit curve through ctg_resultant (host buffers)."""
+def headline(P, curves, workload, cb):
+    """The north-star config: one d=30 / 128-bit curve through ctg_resultant (host buffers),
+    against the reference timed live on one host core in this run (cpu_baseline)."""
     f = curves.make("dense", 30, 128, 1)
     hp, hq = P.HostBipoly(f), P.HostBipoly(curves.derive_y(f))
     for _ in range(3):
@@ -445,12 +546,13 @@ def headline(P, curves):
         ts.append(1e3 * (time.perf_counter() - t0))
         dev.append(P.last_call_stats()["device_ms"])
     ms = statistics.median(ts)
-    ref_s = CACHED_REF_SECONDS["d30_b128"]
-    return {"workload": "dense d=30, 128-bit, seed 1 (BASELINE configs[2])", "e2e_ms_median": ms,
-            "device_phase_ms_median": statistics.median(dev),
-            "reference_cpu_s": ref_s,
-            "reference_cpu_source": "oracle/_ref/refdriver, 1 core of the build container (not re-run: 28 min)",
-            "speedup_vs_reference_1gpu": ref_s * 1e3 / ms}
+    out = {"workload": "dense d=30, 128-bit, seed 1 (BASELINE configs[2]), one curve per call", "e2e_ms_median": ms,
+           "device_phase_ms_median": statistics.median(dev)}
+    if workload == "d30_b128" and cb and cb.get("seconds_per_curve"):
+        out["reference_cpu_s"] = cb["seconds_per_curve"]
+        out["reference_cpu_source"] = "cpu_baseline of this run (oracle/_ref/refdriver, 1 host core, seed 1)"
+        out["speedup_vs_reference_1gpu"] = cb["seconds_per_curve"] * 1e3 / ms
+    return out
 
 
 def yun_line(P, curves, workload):
@@ -485,7 +587,7 @@ def cpu_baseline(workload, units_per_curve):
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                 "sample": "oracle/_ref/refdriver not built", "note": "run make -C oracle"}
     try:
-        r = run_refdriver(kind, a, b, 1, timeout=300)
+        r = run_refdriver(kind, a, b, 1, timeout=1500)
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
     secs = r["res_seconds_best"]

@@ -17,6 +17,7 @@ Fixture files (JSON lines):
   configs_small.jsonl   res(f, f_y) (+ Yun) on the BASELINE configs that finish in seconds
   configs_big.jsonl     sha256 digests of res(f, f_y) at the full BASELINE sizes
   bivariate_gcd.jsonl   gcd_bivariate (elim.cpp:178-202) on coprime / content-sharing / factor-sharing pairs
+  sylvester_acceptance.jsonl  SPEC.md:632: resultant == Sylvester determinant (oracles.cpp:82-120), 500 pairs
   teissier.jsonl        CurveContext::resultant_q + q_factorization (lift.cpp:76-101): h = gcd(f_x, f_y),
                         Q = res(f_x / h, f_y / h), Yun(Q) -- SURVEY.md §8(f) rank 1
 """
@@ -34,6 +35,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
 
 from paper_1103_4697_b200 import curves  # noqa: E402
 
@@ -269,13 +271,29 @@ def digest(coeffs_hex: list) -> str:
 
 
 def configs_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
+    """Digests of the reference's R at the full BASELINE sizes, seeds 1..: outputs cached by
+    oracle/gen_big.py (parallel runs of oracle/_ref/refdriver), rows already in the committed
+    file are kept when their cache is gone."""
+    import gen_big
+    old = {}
+    path = os.path.join(GOLD, "configs_big.jsonl")
+    if os.path.exists(path):
+        for line in open(path):
+            r = json.loads(line)
+            old[tuple(r["curve"])] = r
+    todo = [("dense", 20, 64, 1, False), ("sheared", 3, 0, 1, True), ("dense", 16, 1024, 1, False),
+            ("dense", 30, 128, 1, False)] + [t[:5] for t in gen_big.PLAN]
     rows = []
-    for (kind, a, b, s) in [("dense", 20, 64, 1), ("sheared", 3, 0, 1), ("dense", 16, 1024, 1),
-                            ("dense", 30, 128, 1)]:
-        name = f"{kind}_{a}_{b}_{s}" if kind == "dense" else f"{kind}_{a}_{s}"
+    for (kind, a, b, s, with_yun) in todo:
+        name = gen_big.cache_name(kind, a, b, s)
         cached = os.path.join(cache_dir, f"out_{name}.txt")
+        lines = []
         if os.path.exists(cached) and os.path.getsize(cached) > 0:
-            r = json.loads(open(cached).read().splitlines()[0])
+            lines = open(cached).read().splitlines()
+            r = json.loads(lines[0])
+        elif (kind, a, b, s) in old:
+            rows.append(old[(kind, a, b, s)])
+            continue
         elif cached_only:
             print(f"skip {name}: no cached reference output")
             continue
@@ -286,8 +304,8 @@ def configs_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
         ints = [int(c, 16) for c in res]
         row = {"curve": [kind, a, b, s], "deg": len(res) - 1, "max_bits": max(abs(c).bit_length() for c in ints),
                "sha256": digest(res), "lc": res[-1], "c0": res[0], "ref_seconds": r["seconds"]}
-        if kind == "sheared":
-            y = run_batch([("yun", [ints])])[0]["result"]
+        if with_yun:
+            y = json.loads(lines[1])["result"] if len(lines) > 1 else run_batch([("yun", [ints])])[0]["result"]
             row["yun_unit"] = y["unit"]
             row["yun"] = [{"mult": fct["mult"], "deg": len(fct["poly"]) - 1, "sha256": digest(fct["poly"])}
                           for fct in y["factors"]]
@@ -386,8 +404,14 @@ def teissier_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
     for (kind, a, b, s) in [("dense", 20, 64, 1), ("sheared", 3, 0, 1)]:
         name = f"{kind}_{a}_{b}_{s}"
         cached = os.path.join(cache_dir, f"outq_{name}.txt")
+        prev = {}
+        if os.path.exists(os.path.join(GOLD, "teissier_big.jsonl")):
+            prev = {tuple(json.loads(l)["curve"]): json.loads(l) for l in open(os.path.join(GOLD, "teissier_big.jsonl"))}
         if os.path.exists(cached) and os.path.getsize(cached) > 0:
             r = json.loads(open(cached).read().splitlines()[0])
+        elif (kind, a, b, s) in prev:
+            rows.append(prev[(kind, a, b, s)])
+            continue
         elif cached_only:
             print(f"skip Q {name}: no cached reference output")
             continue
@@ -401,12 +425,65 @@ def teissier_big(cache_dir: str, cached_only: bool = False) -> list[dict]:
     return rows
 
 
+
+def sylvester_acceptance() -> list[dict]:
+    """SPEC.md:632 acceptance #2: resultant == Sylvester determinant on >= 500 random pairs,
+    deg <= 6, coefficients <= 2^16.  Both sides come from the reference: its resultant
+    (elim.cpp:95-136) and its own Bareiss oracle (proj/tests/oracles.cpp:82-120); the fixture
+    stores the inputs and the sha256 of the (equal) outputs."""
+    rng = random.Random(632)
+    pairs = []
+    while len(pairs) < 500:
+        def one(dmin):
+            d = rng.randint(dmin, 6)
+            dens = rng.choice((1.0, 0.7, 0.4))
+            f = {}
+            for i in range(d + 1):
+                for j in range(d + 1 - i):
+                    if rng.random() <= dens:
+                        c = rng.randint(-2**16, 2**16)
+                        if c:
+                            f[(i, j)] = c
+            return f
+        p, q = one(1), one(0)
+        if not p or not q:  # the Sylvester oracle needs two nonzero inputs (oracles.cpp:86)
+            continue
+        if rng.random() < 0.25 and p:  # share the Sylvester shape q ~ p_y more often
+            q = {(i, j - 1): j * c for (i, j), c in p.items() if j}
+            if not q:
+                continue
+        pairs.append((p, q))
+    reqs = []
+    for p, q in pairs:
+        reqs.append(("resultant_y", [p, q]))
+        reqs.append(("sylvester_y", [p, q]))
+    out = run_batch(reqs)
+    rows = []
+    for k, (p, q) in enumerate(pairs):
+        r, s_ = out[2 * k], out[2 * k + 1]
+        if "error" in r:
+            rows.append({"p": enc_bipoly(p), "q": enc_bipoly(q), "error": r["error"]})
+            continue
+        assert r["result"] == s_["result"], f"reference resultant != Sylvester oracle on pair {k}"
+        rows.append({"p": enc_bipoly(p), "q": enc_bipoly(q), "deg": len(r["result"]) - 1,
+                     "sha256": digest(r["result"])})
+    return rows
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
-    ap.add_argument("--cache", default="/tmp/gold")
+    ap.add_argument("--cache", default=os.path.join(HERE, "_gold_cache"))
     ap.add_argument("--cached-only", action="store_true", help="--big: use only cached reference outputs")
+    ap.add_argument("--big-only", action="store_true", help="only rewrite configs_big / teissier_big")
+    ap.add_argument("--only", default="", help="rewrite one small fixture (e.g. sylvester_acceptance)")
     args = ap.parse_args()
+    if args.only:
+        write(f"{args.only}.jsonl", globals()[args.only]())
+        return
+    if args.big_only:
+        write("configs_big.jsonl", configs_big(args.cache, args.cached_only))
+        write("teissier_big.jsonl", teissier_big(args.cache, args.cached_only))
+        return
     elim = subprocess.run([DRIVER, "elim_cases"], capture_output=True, text=True, check=True).stdout
     write("elim_cases.jsonl", [json.loads(l) for l in elim.splitlines() if l.strip()])
     write("worked.jsonl", worked())
@@ -415,6 +492,7 @@ def main() -> None:
     write("configs_small.jsonl", configs_small())
     write("bivariate_gcd.jsonl", bivariate_gcd())
     write("teissier.jsonl", teissier())
+    write("sylvester_acceptance.jsonl", sylvester_acceptance())
     if args.big:
         write("configs_big.jsonl", configs_big(args.cache, args.cached_only))
         write("teissier_big.jsonl", teissier_big(args.cache, args.cached_only))

@@ -22,7 +22,7 @@
 //                                          (refdriver_gpu) -- the same caller, both libraries.
 //
 // Request format (text):
-//   OP <resultant_y|resultant_x|resultant_fy|yun|gcd|sqfp|gcd_bivariate|curve_q>
+//   OP <resultant_y|resultant_x|resultant_fy|sylvester_y|yun|gcd|sqfp|gcd_bivariate|curve_q>
 //   B <nterms>  followed by nterms lines "dx dy hexcoeff"        (bivariate operand)
 //   U <ncoeffs> followed by ncoeffs lines "hexcoeff" low->high   (univariate operand)
 //   END
@@ -192,6 +192,8 @@ int cmd_batch() {
       } else if (op == "resultant_fy") {
         UPoly r = resultant(args.at(0).b, derive(args.at(0).b, Var::Y, 1), Var::Y);
         body = std::string("\"result\":") + json_upoly(r);
+      } else if (op == "sylvester_y") {  // proj/tests/oracles.cpp:82-120 (Bareiss on the Sylvester matrix)
+        body = std::string("\"result\":") + json_upoly(oracles::sylvester_resultant_y(args.at(0).b, args.at(1).b));
       } else if (op == "yun") {
         body = std::string("\"result\":") + json_sqf(yun_squarefree(args.at(0).u));
       } else if (op == "gcd") {

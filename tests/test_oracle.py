@@ -104,3 +104,13 @@ def test_restatement_curve_q():
         assert h == dec_bipoly(r["h"]), r.get("curve", r.get("name"))
         assert q == dec_upoly(r["result"])
         assert qsf == dec_sqf(r["qsf"])
+
+
+def test_restatement_sylvester_acceptance_subset():
+    """The restatement against the SPEC.md:632 acceptance fixture (every 5th of the 500 pairs)."""
+    import hashlib
+    rows = load("sylvester_acceptance.jsonl")[::5]
+    for r in rows:
+        R = O.resultant(dec_bipoly(r["p"]), dec_bipoly(r["q"]), "y")
+        assert len(R) - 1 == r["deg"]
+        assert hashlib.sha256(",".join(format(c, "x") for c in R).encode()).hexdigest() == r["sha256"]

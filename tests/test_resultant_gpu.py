@@ -372,3 +372,18 @@ def test_flag_list_overflow_batch():
         pairs.append((f, curves.derive_y(f)))
         want.append(_upow_mul(g, 19, 20 ** 20))
     assert P.resultant_batch(pairs) == want
+
+
+def test_spec_sylvester_acceptance_500_pairs():
+    """SPEC.md:632 acceptance #2 on the GPU path: resultant == Sylvester determinant on 500 random
+    pairs (deg <= 6, |c| <= 2^16), zero mismatches.  The fixture holds the reference's resultant
+    digests, which make_golden.py asserted equal to the reference's Bareiss oracle
+    (proj/tests/oracles.cpp:82-120).  Both the batched call (shapes grouped) and single calls."""
+    rows = load("sylvester_acceptance.jsonl")
+    assert len(rows) >= 500
+    pairs = [(dec_bipoly(r["p"]), dec_bipoly(r["q"])) for r in rows]
+    got = P.resultant_batch(pairs)
+    for r, R in zip(rows, got):
+        assert len(R) - 1 == r["deg"] and _digest(R) == r["sha256"], r
+    for r, pq in list(zip(rows, pairs))[::10]:
+        assert _digest(P.resultant(*pq)) == r["sha256"]

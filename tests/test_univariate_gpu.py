@@ -147,3 +147,58 @@ def test_yun_probe_inconclusive_falls_through():
     unit, factors = P.yun_squarefree(S)
     assert [(list(f), m) for f, m in factors] == [(O.primitive_positive(S), 1)]
     assert P.last_call_stats()["kernel_launches"] == 2  # K1 + the 3-prime probe
+
+
+def _squarefree_mod_p(R, p):
+    """deg gcd(R mod p, R' mod p) == 0 (pure Python Euclid over F_p).  With p not dividing
+    lc(R) this proves R square-free over Q (a mod-p gcd degree bounds the rational one)."""
+    def trim(a):
+        while a and a[-1] == 0:
+            a.pop()
+        return a
+    a = trim([c % p for c in R])
+    b = trim([(i * c) % p for i, c in enumerate(R)][1:])
+    while b:
+        inv = pow(b[-1], p - 2, p)
+        while len(a) >= len(b):
+            q = a[-1] * inv % p
+            s = len(a) - len(b)
+            for i in range(len(b)):
+                a[s + i] = (a[s + i] - q * b[i]) % p
+            trim(a)
+        a, b = b, a
+    return len(a) == 1
+
+
+def _big_config_rows():
+    rows = [r for r in load("configs_big.jsonl") if r["curve"][0] == "dense"]
+    seen, out = set(), []
+    for r in rows:  # one seed per config keeps the test at seconds (the digests cover the rest)
+        key = tuple(r["curve"][:3])
+        if key not in seen:
+            seen.add(key)
+            out.append(r)
+    return out
+
+
+@pytest.mark.parametrize("row", _big_config_rows(), ids=lambda r: "_".join(map(str, r["curve"])))
+def test_yun_of_big_config_resultants(row):
+    """Yun(R) at d20/64, d30/128, d16/1024, where the reference's CPU Yun does not finish
+    (SURVEY §8(c)): R is pinned by the reference's digest, then the GPU factorization must be
+    exactly (sgn(lc R) * content(R), [(pp(R), 1)]) -- elim.cpp:141-163 -- with the content
+    computed here in Python ints and square-freeness proven independently mod a prime."""
+    import math
+    kind, a, b, s = row["curve"]
+    f = curves.make(kind, a, b, s)
+    R = P.resultant(f, curves.derive_y(f))
+    assert hashlib.sha256(",".join(format(c, "x") for c in R).encode()).hexdigest() == row["sha256"]
+    cont = 0
+    for c in R:
+        cont = math.gcd(cont, c)
+    sgn = -1 if R[-1] < 0 else 1
+    pp = [sgn * c // cont for c in R]
+    p = 2**61 - 1
+    assert R[-1] % p and _squarefree_mod_p(R, p)
+    unit, factors = P.yun_squarefree(R)
+    assert unit == sgn * cont
+    assert factors == [(pp, 1)]
