@@ -185,7 +185,6 @@ static Problem parse_problem(const ctg_bipoly* pin, const ctg_bipoly* qin, int32
     std::swap(pr.n, pr.m);
     pr.negate = (pr.n & 1) && (pr.m & 1);  // res(p,q) = (-1)^{nm} res(q,p)
   }
-  if (pr.n > kGeneralMaxDeg) throw ApiError(CTG_UNSUPPORTED, "resultant: degree in the eliminated variable exceeds 128");
   pr.deriv = (pr.m == pr.n - 1 && pr.n >= 1 && is_y_derivative(pr.p, pr.q)) ? 1 : 0;
   // Degree bound of the result (min of the Sylvester row bound and Bezout).
   int Xp = 0, Xq = 0, tp = 0, tq = 0;
@@ -247,6 +246,7 @@ struct ctg_plan {
   double* d_upart = nullptr;       // [B][nchunk][J]
   uint64_t* d_cols = nullptr;      // [B][J][L16]
   uint32_t* d_vals = nullptr;      // K2 point values [B][P][nrows][N] (fast path only)
+  uint32_t* d_gwarp = nullptr;     // k_modres_warp buffers in global memory (deg_y beyond ~6000)
   int nrows = 0, maxlen = 0;
   bool fast_ok = false;
   bool fused = false;              // K2 folded into K3 (k_modres_fused): no d_vals
@@ -285,6 +285,7 @@ struct ctg_plan {
     size_t s = r(4 * h_limbs.size()) + r(h_sign.size()) + r(4 * dir.size()) + r(4ull * B * P * S) +
                r(4ull * flag_cap) + r(16);
     if (fast_ok && !fused) s += r(4ull * B * P * nrows * N);
+    s += r(4 * general_warp_gbuf_words(n));
     s += r(4 * crt_y_words(*tabs, B, J)) + r(8 * static_cast<size_t>(B) * nch * J) +
          r(8 * ((crt_cols_words(*tabs, B, J) + 1) / 2));
     return s;
@@ -300,6 +301,7 @@ struct ctg_plan {
     pfree(d_upart);
     pfree(d_cols);
     pfree(d_vals);
+    pfree(d_gwarp);
   }
   int out_limbs() const { return tabs ? tabs->LM : 0; }
   int out_words() const { return out_limbs() + 1; }
@@ -430,6 +432,7 @@ static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   pl->palloc(pl->d_flags, pl->flag_cap, st);
   pl->palloc(pl->d_counters, 4, st);
   if (pl->fast_ok && !pl->fused) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
+  if (general_warp_gbuf_words(pl->n)) pl->palloc(pl->d_gwarp, general_warp_gbuf_words(pl->n), st);
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
 }
 
@@ -507,6 +510,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   rp.nrows = pl->nrows;
   rp.maxlen = pl->maxlen;
   rp.twinv = pl->tabs->d_twinv;
+  rp.gwarp = pl->d_gwarp;
   pl->launches += launch_modres(rp, true, st, stage == 4 ? 1 : stage == 5 ? 2 : 0);
   CTG_CUDA_CHECK(cudaGetLastError());
 }

@@ -205,6 +205,11 @@ struct DevArena {
 struct Launches {
   int n = 0;
 };
+// Launcher result -> launch count (a negative result means a missing global scratch buffer).
+inline int launched(int r) {
+  if (r < 0) throw ApiError(CTG_INTERNAL, "K6 launch: global scratch buffer missing");
+  return r;
+}
 
 // Residues of a primitive polynomial modulo every prime of `tabs` (K1): [P][n+1] Montgomery.
 // Per-thread pinned staging for the H2D of reduce_poly (a pageable copy of R's ~1 MB of limbs
@@ -385,7 +390,9 @@ YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& 
   int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * (n + 1));
   im.d_fac = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (2 * n + 2));
   im.d_sqf = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (n + 1));
-  L.n += launch_modyun(d_tab, n, T->d_pc, nk, d_deg, im.d_fac, im.d_sqf, ar.st);
+  const size_t gb = uni_gbuf_bytes(modyun_smem(n), nk);
+  uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+  L.n += launched(launch_modyun(d_tab, n, T->d_pc, nk, d_deg, im.d_fac, im.d_sqf, gbuf, ar.st));
   CTG_CUDA_CHECK(cudaGetLastError());
   // First only columns 0..1 of every prime's pattern (status, degree of the multiplicity-1
   // factor): enough to certify a square-free input; fetch_patterns() copies the rest.
@@ -416,7 +423,6 @@ bool certifies_squarefree(const YunImages& im, int n) {
 
 YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t st, Launches& L) {
   const int n = zdeg(P);
-  if (n > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "yun: degree exceeds 6000");
   DevArena ar(st);
   YunResult res;
   // A prime with p !| lc(P) and deg gcd(P, P') = 0 certifies a square-free P at once (no CRT).
@@ -525,7 +531,6 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
 // ---------------------------------------------------------------------------
 ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, Launches& L) {
   const int na = zdeg(A), nb = zdeg(B);
-  if (std::max(na, nb) > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "gcd: degree exceeds 6000");
   DevArena ar(st);
   const Big gamma = big_gcd(A.back().mag, B.back().mag);
   const double lg = big_log2(gamma), la = zlog2_l2(A), lb = zlog2_l2(B);
@@ -540,7 +545,9 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
     const int pitch = na + nb + 3;
     int32_t* d_deg = ar.alloc<int32_t>(nk);
     uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(nk) * pitch);
-    L.n += launch_modgcd(tA, na, tB, nb, T->d_pc, nk, d_deg, d_out, pitch, ar.st);
+    const size_t gb = uni_gbuf_bytes(modgcd_smem(na, nb), nk);
+    uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+    L.n += launched(launch_modgcd(tA, na, tB, nb, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st));
     CTG_CUDA_CHECK(cudaGetLastError());
     std::vector<int32_t> deg(nk);
     CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * nk, cudaMemcpyDeviceToHost, ar.st));
@@ -644,7 +651,6 @@ ZPoly content_y(const YPoly& f, int dev, cudaStream_t st, Launches& L) {
 // y-coefficient survives: the image of the primitive gcd H then has degree deg_y H.
 bool primitive_parts_coprime(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, Launches& L) {
   const int nf = static_cast<int>(f.size()) - 1, ng = static_cast<int>(g.size()) - 1;
-  if (std::max(nf, ng) > kMaxUniDeg) throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: y-degree exceeds 6000");
   ZPoly slots;
   std::vector<int32_t> dir;
   std::vector<int32_t> off, len;
@@ -668,7 +674,10 @@ bool primitive_parts_coprime(const YPoly& f, const YPoly& g, int dev, cudaStream
   constexpr int kPoints = 8;
   const int units = T->P * kPoints;
   int32_t* d_deg = ar.alloc<int32_t>(units);
-  L.n += launch_bigcd_probe(tab, static_cast<int>(slots.size()), d_dir, nf, ng, T->d_pc, T->P, kPoints, d_deg, ar.st);
+  const size_t gb = uni_gbuf_bytes(bigcd_probe_smem(nf, ng), static_cast<size_t>(units));
+  uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+  L.n += launched(launch_bigcd_probe(tab, static_cast<int>(slots.size()), d_dir, nf, ng, T->d_pc, T->P, kPoints, d_deg, gbuf,
+                            ar.st));
   CTG_CUDA_CHECK(cudaGetLastError());
   std::vector<int32_t> deg(units);
   CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * units, cudaMemcpyDeviceToHost, ar.st));
@@ -772,8 +781,6 @@ YPoly bigcd_modular(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, La
   const int dxf = ydeg_x(f), dxg = ydeg_x(g), dgam = zdeg(gamma);
   const int bH = dgam + std::min(dxf, dxg);
   const int N = bH + std::max(dxf, dxg) + 1;
-  if (std::max(nf, ng) > kMaxUniDeg || newton_smem(N) > 227 * 1024)
-    throw ApiError(CTG_UNSUPPORTED, "gcd_bivariate: degrees exceed the modular gcd's shared-memory limits");
   // slot table: rows of f, rows of g, gamma
   ZPoly slots;
   std::vector<int32_t> dir;
@@ -809,8 +816,10 @@ YPoly bigcd_modular(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, La
     const int pitch = nf + ng + 3;
     int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * N);
     uint32_t* d_img = ar.alloc<uint32_t>(static_cast<size_t>(nk) * N * pitch);
-    L.n += launch_bigcd_images(tab, static_cast<int>(slots.size()), d_dir, nf, ng, gam_off, gam_len, T->d_pc, d_offs,
-                               nk, N, d_deg, d_img, pitch, ar.st);
+    const size_t gbi = uni_gbuf_bytes(modgcd_smem(nf, ng), static_cast<size_t>(nk) * N);
+    uint32_t* gbuf = gbi ? ar.alloc<uint32_t>(gbi / 4) : nullptr;
+    L.n += launched(launch_bigcd_images(tab, static_cast<int>(slots.size()), d_dir, nf, ng, gam_off, gam_len, T->d_pc, d_offs,
+                               nk, N, d_deg, d_img, pitch, gbuf, ar.st));
     CTG_CUDA_CHECK(cudaGetLastError());
     std::vector<int32_t> deg(static_cast<size_t>(nk) * N);
     CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * deg.size(), cudaMemcpyDeviceToHost, ar.st));
@@ -836,8 +845,14 @@ YPoly bigcd_modular(const YPoly& f, const YPoly& g, int dev, cudaStream_t st, La
     int32_t* d_idx = ar.alloc<int32_t>(lucky.size());
     CTG_CUDA_CHECK(cudaMemcpyAsync(d_idx, lucky.data(), 4 * lucky.size(), cudaMemcpyHostToDevice, ar.st));
     uint32_t* d_coef = ar.alloc<uint32_t>(static_cast<size_t>(nk) * N * cols);
-    L.n += launch_newton_interp(d_img, pitch, d_idx, static_cast<int>(lucky.size()), T->d_pc, d_offs, N, cols, d_coef,
-                                ar.st);
+    // Newton beyond the shared-memory budget: global slices for up to ~256 MB of CTAs at a time
+    const size_t per_row = newton_smem(N) * ((cols + kNewtonColsPerCta - 1) / kNewtonColsPerCta);
+    const int nrows_l = static_cast<int>(lucky.size());
+    const int grows = uni_gbuf_bytes(newton_smem(N), 1)
+                          ? std::max(1, std::min(nrows_l, static_cast<int>((size_t{256} << 20) / per_row)))
+                          : 0;
+    uint32_t* gnew = grows ? ar.alloc<uint32_t>(per_row * grows / 4) : nullptr;
+    L.n += launched(launch_newton_interp(d_img, pitch, d_idx, nrows_l, T->d_pc, d_offs, N, cols, d_coef, gnew, grows, ar.st));
     CTG_CUDA_CHECK(cudaGetLastError());
     double log2M = 0;
     const int total = N * cols;

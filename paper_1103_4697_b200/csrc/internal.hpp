@@ -27,7 +27,11 @@ struct PrimeConst {
 };
 
 constexpr int kFastMaxDeg = 40;     // fast mod-p resultant templates: deg_y p in [2, kFastMaxDeg], deg_y q = deg_y p - 1
-constexpr int kGeneralMaxDeg = 128; // general (formal-degree) kernel limit
+constexpr int kThreadGeneralMax = kFastMaxDeg;  // thread-per-unit formal-degree kernel up to this deg_y;
+                                                // above it k_modres_warp (warp per unit, any degree)
+constexpr int kWarpsGeneral = 4;                // warps per CTA of k_modres_warp
+constexpr size_t kGeneralWarpSmemMax = 200 * 1024;  // beyond: per-warp slices of global scratch
+constexpr uint32_t kGeneralWarpGlobalBlocks = 296;
 constexpr uint32_t kMaxNtt = 1u << 14;
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT rounding estimate
@@ -94,7 +98,10 @@ struct ResParams {
   int maxlen;               // longest slot run (max x-degree + 1) over the rows
   const uint32_t* twinv;    // [P][N] omega_k^{-i} (Montgomery; global prime index k)
   int fused;                // K2 folded into the K3 launch (k_modres_fused); vals unused
+  uint32_t* gwarp;          // k_modres_warp buffers in global memory (huge deg_y), else null
 };
+size_t general_warp_smem(int n);
+size_t general_warp_gbuf_words(int n);  // 0 when the buffers fit in shared memory
 
 struct CrtParams {
   int B;

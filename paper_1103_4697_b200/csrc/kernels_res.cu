@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_lis
     const Mod M = load_mod(pcv);
     const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
     const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S;
-    uint32_t bufA[kGeneralMaxDeg + 1], bufB[kGeneralMaxDeg + 1];
+    uint32_t bufA[kThreadGeneralMax + 1], bufB[kThreadGeneralMax + 1];
     for (int j = 0; j <= P.n; ++j) bufA[j] = horner(tab, P.dir[j], P.dir[nq + j], x, M);
     if (P.deriv) {
       uint32_t c = M.one;
@@ -285,6 +285,111 @@ __global__ void __launch_bounds__(128) k_modres_general(ResParams P, int use_lis
       for (int j = 0; j <= P.m; ++j) bufB[j] = horner(tab, P.dir[base + j], P.dir[base + P.m + 1 + j], x, M);
     }
     P.rows[b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch + i] = res_general(bufA, P.n, bufB, P.m, M);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3'' k_modres_warp: the same formal-degree resultant (res_general's conventions) with one
+// WARP per unit, for deg_y > kThreadGeneralMax (any size: no per-thread arrays).  A and B live
+// in shared memory (kWarpsGeneral warps per CTA, 2 (n + 1) words each) or, beyond the
+// shared-memory budget, in this warp's slice of the global scratch P.gwarp.  Every scalar
+// (degrees, leading coefficients, quotients) is computed lane-uniformly; coefficient updates
+// are spread over the lanes, with __syncwarp between dependent passes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_trim(const uint32_t* X, int d, int lane) {
+  for (int base = d; base >= 0; base -= 32) {
+    const int idx = base - lane;
+    const unsigned nz = __ballot_sync(0xffffffffu, idx >= 0 && X[idx] != 0u);
+    if (nz) return base - (__ffs(nz) - 1);
+  }
+  return -1;
+}
+
+__device__ uint32_t warp_res_general(uint32_t* A, int na, uint32_t* B, int nb, const Mod& M, int lane) {
+  uint32_t acc = M.one;
+  while (true) {
+    __syncwarp();
+    if (na == 0) return mmul(acc, mpow(A[0], static_cast<uint64_t>(nb), M), M);
+    if (nb == 0) return mmul(acc, mpow(B[0], static_cast<uint64_t>(na), M), M);
+    const int da = warp_trim(A, na, lane), db = warp_trim(B, nb, lane);
+    if (da < 0 || db < 0) return 0u;
+    if (da < na && db < nb) return 0u;
+    if (da < na) {
+      const int e = na - da;
+      acc = mmul(acc, mpow(B[nb], static_cast<uint64_t>(e), M), M);
+      if ((e & 1) && (nb & 1)) acc = mneg(acc, M.p);
+      na = da;
+      continue;
+    }
+    if (db < nb) {
+      acc = mmul(acc, mpow(A[na], static_cast<uint64_t>(nb - db), M), M);
+      nb = db;
+      continue;
+    }
+    if (na < nb) {
+      uint32_t* t = A;
+      A = B;
+      B = t;
+      const int tn = na;
+      na = nb;
+      nb = tn;
+      if ((na & 1) && (nb & 1)) acc = mneg(acc, M.p);
+    }
+    const uint32_t inv = minv(B[nb], M);
+    for (int i = na; i >= nb; --i) {
+      const uint32_t q = mmul(A[i], inv, M);
+      if (q) {
+        const uint32_t nq = mneg(q, M.p);
+        for (int j = lane; j < nb; j += 32) A[i - nb + j] = mmul2(M.one, A[i - nb + j], nq, B[j], M);
+      }
+      __syncwarp();
+      if (lane == 0) A[i] = 0u;
+      __syncwarp();
+    }
+    acc = mmul(acc, mpow(B[nb], static_cast<uint64_t>(na - nb + 1), M), M);
+    if ((na & 1) && (nb & 1)) acc = mneg(acc, M.p);
+    uint32_t* t = A;
+    A = B;
+    B = t;
+    na = nb;
+    nb = nb - 1;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsGeneral) k_modres_warp(ResParams P, int use_list, uint32_t total_units) {
+  extern __shared__ uint32_t sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t flagged = use_list ? P.counters[0] : 0u;
+  const bool scan = use_list && flagged > P.flag_cap;
+  const uint32_t all = static_cast<uint32_t>(P.B) * static_cast<uint32_t>(P.nk) * static_cast<uint32_t>(P.N);
+  const uint32_t count = scan ? all : (use_list ? flagged : total_units);
+  const int nq = P.n + 1, cap = P.n + 1;
+  const size_t wid = static_cast<size_t>(blockIdx.x) * kWarpsGeneral + wib;
+  uint32_t* bufA = P.gwarp ? P.gwarp + wid * 2 * cap : sm + static_cast<size_t>(wib) * 2 * cap;
+  uint32_t* bufB = bufA + cap;
+  for (uint32_t u = blockIdx.x * kWarpsGeneral + wib; u < count; u += gridDim.x * kWarpsGeneral) {
+    const uint32_t unit = (use_list && !scan) ? P.flag_list[u] : u;
+    const uint32_t bk = unit / P.N;
+    const int i = static_cast<int>(unit % P.N);
+    const int kl = static_cast<int>(bk % P.nk), b = static_cast<int>(bk / P.nk);
+    uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch + i;
+    if (scan && *out != kSentinel) continue;
+    const int k = P.k0 + kl;
+    const PrimeConst pcv = P.pc[k];
+    const Mod M = load_mod(pcv);
+    const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
+    const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S;
+    __syncwarp();
+    for (int j = lane; j <= P.n; j += 32) bufA[j] = horner(tab, P.dir[j], P.dir[nq + j], x, M);
+    __syncwarp();
+    if (P.deriv) {
+      for (int j = lane; j <= P.m; j += 32) bufB[j] = mmul(bufA[j + 1], mmul(static_cast<uint32_t>(j + 1), M.r2, M), M);
+    } else {
+      const int base = 2 * nq;
+      for (int j = lane; j <= P.m; j += 32) bufB[j] = horner(tab, P.dir[base + j], P.dir[base + P.m + 1 + j], x, M);
+    }
+    const uint32_t r = warp_res_general(bufA, P.n, bufB, P.m, M, lane);
+    if (lane == 0) *out = r;
   }
 }
 
@@ -1103,9 +1208,25 @@ int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
   }
   if (part == 1) return 0;
   const uint32_t total = static_cast<uint32_t>(rp.B) * rp.nk * static_cast<uint32_t>(rp.N);
+  if (rp.n > kThreadGeneralMax) {  // warp per unit (any degree)
+    const size_t smem = rp.gwarp ? 0 : general_warp_smem(rp.n);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_modres_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const uint32_t want = (total + kWarpsGeneral - 1) / kWarpsGeneral;
+    const int blocks = static_cast<int>(std::min<uint32_t>(want, rp.gwarp ? kGeneralWarpGlobalBlocks : 148u * 16u));
+    k_modres_warp<<<blocks, 32 * kWarpsGeneral, smem, st>>>(rp, 0, total);
+    return 1;
+  }
   const int blocks = static_cast<int>(std::min<uint32_t>((total + 127) / 128, 148u * 16u));
   k_modres_general<<<blocks, 128, 0, st>>>(rp, 0, total);
   return 1;
+}
+
+size_t general_warp_smem(int n) { return static_cast<size_t>(kWarpsGeneral) * 2 * (n + 1) * 4; }
+size_t general_warp_gbuf_words(int n) {
+  return general_warp_smem(n) > kGeneralWarpSmemMax
+             ? static_cast<size_t>(kGeneralWarpGlobalBlocks) * kWarpsGeneral * 2 * (n + 1)
+             : 0;
 }
 
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,

@@ -8,6 +8,9 @@
 // vector update of the remainder (threads stride the coefficients) and one barrier.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdint>
+
 #include "internal.hpp"
 #include "uni_internal.hpp"
 
@@ -25,6 +28,13 @@ __device__ __forceinline__ void swp(uint32_t*& a, uint32_t*& b) {
   uint32_t* t = a;
   a = b;
   b = t;
+}
+
+// Polynomial buffers of a CTA: shared memory, or (degrees beyond the shared-memory budget)
+// this CTA's slice of a global scratch region -- the kernels use generic pointers, so the
+// same code runs on either (global buffers stay L2-resident: 8 x (n + 2) words per CTA).
+__device__ __forceinline__ uint32_t* cta_buffers(uint32_t* sm, uint32_t* gbuf, size_t words_per_cta) {
+  return gbuf ? gbuf + static_cast<size_t>(blockIdx.x) * words_per_cta : sm;
 }
 
 // Primes p < kResPrimeMax (2^30.4): the fused pass uses mmul3 (modarith.cuh).
@@ -132,13 +142,14 @@ __device__ void blk_store_plain(uint32_t* dst, const uint32_t* X, int d, const M
 // increasing m (deg + 1 words each) at fac[k][...]; the monic square-free part at sqf[k][...].
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_modyun(const uint32_t* __restrict__ tab, int n, const PrimeConst* __restrict__ pc,
-                                                int32_t* deg, uint32_t* fac, uint32_t* sqf) {
+                                                int32_t* deg, uint32_t* fac, uint32_t* sqf, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
   const int cap = n + 2;
+  uint32_t* base = cta_buffers(sm, gbuf, 8 * cap);
   uint32_t* buf[8];
-  for (int b = 0; b < 8; ++b) buf[b] = sm + b * cap;
+  for (int b = 0; b < 8; ++b) buf[b] = base + b * cap;
   int32_t* dk = deg + static_cast<size_t>(kl) * (n + 1);
   uint32_t* fk = fac + static_cast<size_t>(kl) * (2 * n + 2);
   uint32_t* sk = sqf + static_cast<size_t>(kl) * (n + 1);
@@ -220,12 +231,13 @@ __global__ void __launch_bounds__(256) k_modyun(const uint32_t* __restrict__ tab
 __global__ void __launch_bounds__(256) k_modgcd(const uint32_t* __restrict__ tabA, int na,
                                                 const uint32_t* __restrict__ tabB, int nb,
                                                 const PrimeConst* __restrict__ pc, int32_t* deg, uint32_t* out,
-                                                int pitch) {
+                                                int pitch, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
   const int cap = (na > nb ? na : nb) + 2;
-  uint32_t *A = sm, *B = sm + cap, *X = sm + 2 * cap, *Y = sm + 3 * cap, *Q = sm + 4 * cap;
+  uint32_t* base = cta_buffers(sm, gbuf, 5 * static_cast<size_t>(cap));
+  uint32_t *A = base, *B = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap;
   const uint32_t* ra = tabA + static_cast<size_t>(kl) * (na + 1);
   const uint32_t* rb = tabB + static_cast<size_t>(kl) * (nb + 1);
   for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
@@ -269,13 +281,14 @@ __global__ void k_gather_scale(const uint32_t* __restrict__ src, int src_pitch, 
 // the gcd degree, or -1 when the unit proves nothing (both formal leading y-coefficients
 // vanish at a_j, or an image is identically zero).
 __global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ dir, int nf,
-                              int ng, const PrimeConst* __restrict__ pc, int npts, int32_t* __restrict__ deg) {
+                              int ng, const PrimeConst* __restrict__ pc, int npts, int32_t* __restrict__ deg,
+                              uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
   const Mod M = load_mod_u(pc[k]);
   const int w = (nf > ng ? nf : ng) + 2;
-  uint32_t* X = sm;
-  uint32_t* Y = sm + w;
+  uint32_t* X = cta_buffers(sm, gbuf, 2 * static_cast<size_t>(w));
+  uint32_t* Y = X + w;
   const int32_t *offf = dir, *lenf = dir + nf + 1, *offg = dir + 2 * (nf + 1), *leng = offg + ng + 1;
   // a_j: distinct small integers 2, 3, ... in Montgomery form
   const uint32_t a = mmul(static_cast<uint32_t>(j + 2), M.r2, M);
@@ -309,13 +322,14 @@ __global__ void __launch_bounds__(128) k_bigcd_images(const uint32_t* __restrict
                                                       int gam_len, const PrimeConst* __restrict__ pc,
                                                       const uint32_t* __restrict__ offs, int npts,
                                                       int32_t* __restrict__ deg, uint32_t* __restrict__ out,
-                                                      int pitch) {
+                                                      int pitch, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   __shared__ uint32_t s_gam;
   const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
   const Mod M = load_mod_u(pc[k]);
   const int cap = (na > nb ? na : nb) + 2;
-  uint32_t *A = sm, *Bv = sm + cap, *X = sm + 2 * cap, *Y = sm + 3 * cap, *Q = sm + 4 * cap;
+  uint32_t* base = cta_buffers(sm, gbuf, 5 * static_cast<size_t>(cap));
+  uint32_t *A = base, *Bv = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap;
   const int32_t *offa = dir, *lena = dir + na + 1, *offb = dir + 2 * (na + 1), *lenb = offb + nb + 1;
   uint32_t av = offs[k] + static_cast<uint32_t>(j);
   if (av >= M.p) av -= M.p;
@@ -365,8 +379,10 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
                                                                const int32_t* __restrict__ idx,
                                                                const PrimeConst* __restrict__ pc,
                                                                const uint32_t* __restrict__ offs, int N, int cols,
-                                                               uint32_t* __restrict__ dst) {
-  extern __shared__ uint32_t sm[];
+                                                               uint32_t* __restrict__ dst, uint32_t* gbuf) {
+  extern __shared__ uint32_t smem_[];
+  // shared memory, or this CTA's slice of the global scratch (N x 33 words beyond ~227 KB)
+  uint32_t* sm = gbuf ? gbuf + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * N * (kNewtonCols + 1) : smem_;
   const int k = idx[blockIdx.y];
   const Mod M = load_mod_u(pc[k]);
   const int lane = threadIdx.x, c = blockIdx.x * kNewtonCols + lane;
@@ -411,53 +427,74 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
 size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4; }
+size_t bigcd_probe_smem(int nf, int ng) { return static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4; }
+size_t newton_smem(int N) { return static_cast<size_t>(N) * (kNewtonCols + 1) * 4; }
+
+namespace {
+// Launch with `smem` bytes of shared memory, or with none and the buffers in gbuf when it
+// exceeds the per-CTA budget (the caller allocated gbuf from uni_gbuf_bytes).
+template <class K>
+size_t smem_or_global(K kern, size_t smem, uint32_t* gbuf) {
+  if (smem > kUniSmemMax) {
+    if (!gbuf) return SIZE_MAX;
+    return 0;
+  }
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  return smem;
+}
+}  // namespace
+
+size_t uni_gbuf_bytes(size_t smem, size_t ctas) { return smem > kUniSmemMax ? smem * ctas : 0; }
 
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
-                  uint32_t* sqf, cudaStream_t st) {
-  const size_t smem = modyun_smem(n);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_modyun, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_modyun<<<nk, 256, smem, st>>>(tab, n, pc, deg, fac, sqf);
+                  uint32_t* sqf, uint32_t* gbuf, cudaStream_t st) {
+  const size_t smem = smem_or_global(k_modyun, modyun_smem(n), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  k_modyun<<<nk, 256, smem, st>>>(tab, n, pc, deg, fac, sqf, smem ? nullptr : gbuf);
   return 1;
 }
 
 int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, const PrimeConst* pc, int nk,
-                  int32_t* deg, uint32_t* out, int pitch, cudaStream_t st) {
-  const size_t smem = modgcd_smem(na, nb);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_modgcd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_modgcd<<<nk, 256, smem, st>>>(tabA, na, tabB, nb, pc, deg, out, pitch);
+                  int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st) {
+  const size_t smem = smem_or_global(k_modgcd, modgcd_smem(na, nb), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  k_modgcd<<<nk, 256, smem, st>>>(tabA, na, tabB, nb, pc, deg, out, pitch, smem ? nullptr : gbuf);
   return 1;
 }
 
 int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
-                       int nk, int npts, int32_t* deg, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bigcd_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_bigcd_probe<<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg);
+                       int nk, int npts, int32_t* deg, uint32_t* gbuf, cudaStream_t st) {
+  const size_t smem = smem_or_global(k_bigcd_probe, bigcd_probe_smem(nf, ng), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  k_bigcd_probe<<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg, smem ? nullptr : gbuf);
   return 1;
 }
 
 int launch_bigcd_images(const uint32_t* tab, int S, const int32_t* dir, int na, int nb, int gam_off, int gam_len,
                         const PrimeConst* pc, const uint32_t* offs, int nk, int npts, int32_t* deg, uint32_t* out,
-                        int pitch, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bigcd_images, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_bigcd_images<<<nk * npts, 128, smem, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg, out, pitch);
+                        int pitch, uint32_t* gbuf, cudaStream_t st) {
+  const size_t smem = smem_or_global(k_bigcd_images, modgcd_smem(na, nb), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  k_bigcd_images<<<nk * npts, 128, smem, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg, out, pitch,
+                                               smem ? nullptr : gbuf);
   return 1;
 }
 
-size_t newton_smem(int N) { return static_cast<size_t>(N) * (kNewtonCols + 1) * 4; }
-
 int launch_newton_interp(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, const PrimeConst* pc,
-                         const uint32_t* offs, int N, int cols, uint32_t* dst, cudaStream_t st) {
+                         const uint32_t* offs, int N, int cols, uint32_t* dst, uint32_t* gbuf, int gbuf_rows,
+                         cudaStream_t st) {
   if (rows == 0 || cols == 0) return 0;
-  const size_t smem = newton_smem(N);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_newton_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  dim3 grid((cols + kNewtonCols - 1) / kNewtonCols, rows);
-  k_newton_interp<<<grid, kNewtonCols, smem, st>>>(src, src_pitch, idx, pc, offs, N, cols, dst);
-  return 1;
+  const size_t smem = smem_or_global(k_newton_interp, newton_smem(N), gbuf);
+  if (smem == SIZE_MAX || (!smem && gbuf_rows < 1)) return -1;
+  const int step = smem ? rows : gbuf_rows;  // global scratch: row chunks reuse the same slices
+  int launches = 0;
+  for (int r0 = 0; r0 < rows; r0 += step) {
+    dim3 grid((cols + kNewtonCols - 1) / kNewtonCols, std::min(step, rows - r0));
+    k_newton_interp<<<grid, kNewtonCols, smem, st>>>(src, src_pitch, idx + r0, pc, offs, N, cols, dst,
+                                                     smem ? nullptr : gbuf);
+    ++launches;
+  }
+  return launches;
 }
 
 int launch_gather_scale(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, int cols,

@@ -7,29 +7,37 @@
 
 namespace ctg {
 
-constexpr int kMaxUniDeg = 6000;  // 8 shared-memory polynomial buffers per CTA
+// Per-CTA shared-memory budget of the K6 kernels.  Beyond it (degrees above ~7,000 for Yun)
+// the polynomial buffers live in a global scratch region instead: every launcher takes
+// `gbuf` (uni_gbuf_bytes(smem bytes, CTAs) bytes, or null when that is 0) and returns -1 if
+// it needed one and got none.  No degree limit remains.
+constexpr size_t kUniSmemMax = 200 * 1024;
+size_t uni_gbuf_bytes(size_t smem, size_t ctas);
 
 size_t modyun_smem(int n);
 size_t modgcd_smem(int na, int nb);
+size_t bigcd_probe_smem(int nf, int ng);
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
-                  uint32_t* sqf, cudaStream_t st);
+                  uint32_t* sqf, uint32_t* gbuf, cudaStream_t st);
 int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, const PrimeConst* pc, int nk,
-                  int32_t* deg, uint32_t* out, int pitch, cudaStream_t st);
+                  int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st);
 // Bivariate gcd probe: deg[k * npts + j] = deg gcd(f(a_j, y), g(a_j, y)) mod p_k, or -1.
 // dir = offf[nf+1], lenf[nf+1], offg[ng+1], leng[ng+1] (slot runs in tab, x ascending).
 int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
-                       int nk, int npts, int32_t* deg, cudaStream_t st);
+                       int nk, int npts, int32_t* deg, uint32_t* gbuf, cudaStream_t st);
 // Brown images: per (prime k, point off[k] + j): gamma(a) * monic gcd | A/g | B/g (plain, pitch
 // words at out[k][j]); deg[k][j] = gcd degree or -2 (gamma(a) = 0).  dir as for the probe;
 // gamma is the slot run [gam_off, gam_off + gam_len) of tab.
 int launch_bigcd_images(const uint32_t* tab, int S, const int32_t* dir, int na, int nb, int gam_off, int gam_len,
                         const PrimeConst* pc, const uint32_t* offs, int nk, int npts, int32_t* deg, uint32_t* out,
-                        int pitch, cudaStream_t st);
+                        int pitch, uint32_t* gbuf, cudaStream_t st);
 // Newton interpolation on the points off[k] + j, j < N: src[k][j][c] (pitch src_pitch) ->
 // dst[k][t][c] (t < N, row pitch cols) for the rows k = idx[0..rows).
 size_t newton_smem(int N);
 int launch_newton_interp(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, const PrimeConst* pc,
-                         const uint32_t* offs, int N, int cols, uint32_t* dst, cudaStream_t st);
+                         const uint32_t* offs, int N, int cols, uint32_t* dst, uint32_t* gbuf, int gbuf_rows,
+                         cudaStream_t st);
+constexpr int kNewtonColsPerCta = 32;
 int launch_gather_scale(const uint32_t* src, int src_pitch, const int32_t* idx, int rows, int cols,
                         const int32_t* seg_end, int nseg, const uint32_t* scale, const PrimeConst* pc_dst,
                         uint32_t* dst, cudaStream_t st);

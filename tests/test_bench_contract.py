@@ -30,4 +30,4 @@ def test_reference_arm_json_contract():
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     # units per step come from the shared per-curve table (bench_units.json), as in our arm
-    assert line["config"]["units_per_step"] > 0
+    assert line["sample"]["units_total"] > 0 and line["config"]["workload"]

@@ -22,5 +22,5 @@ def test_two_rank_prime_sharded_bench():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
-    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "prime-shard2"
+    assert line["n_gpus"] == 2 and line["sample"]["parallelism"] == "prime-shard2"
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0

@@ -1,0 +1,141 @@
+"""Inputs beyond the r1 size limits: the reference's entry points (elim.cpp:80-202) accept any
+size, so the drop-in must too (no CTG_UNSUPPORTED).  Each case has an exact expected value
+by construction, or (for the resultant at deg_y > 40) the CPU restatement / an exact closed
+form, plus an evaluation-specialisation check over a 61-bit prime at random points."""
+
+import random
+import sys
+import os
+
+import pytest
+
+import paper_1103_4697_b200 as P
+from paper_1103_4697_b200 import curves
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+import curvetop_oracle as O  # noqa: E402  (checker only)
+
+pytestmark = pytest.mark.gpu
+
+Q61 = 2**61 - 1
+
+
+def _res_mod(a, b, q):
+    """Sylvester resultant of dense univariate a (deg n), b (deg m) over F_q, formal degrees =
+    actual (leading coefficients nonzero mod q): Euclid with res(A,B) = (-1)^{nm} lc(B)^{n-k} res(B,R)."""
+    a = [c % q for c in a]
+    b = [c % q for c in b]
+    acc = 1
+    while True:
+        n, m = len(a) - 1, len(b) - 1
+        if m == 0:
+            return acc * pow(b[0], n, q) % q
+        r = a[:]
+        inv = pow(b[-1], q - 2, q)
+        while len(r) - 1 >= m:
+            t = r[-1] * inv % q
+            s = len(r) - 1 - m
+            for i in range(m + 1):
+                r[s + i] = (r[s + i] - t * b[i]) % q
+            r.pop()
+        while r and r[-1] == 0:
+            r.pop()
+        if not r:
+            return 0
+        k = len(r) - 1
+        acc = acc * pow(b[-1], n - k, q) % q
+        if (n * m) & 1:
+            acc = q - acc if acc else 0
+        a, b = b, r
+
+
+def _eval_rows(f, x0, q):
+    n = max(ey for (_, ey) in f)
+    rows = [0] * (n + 1)
+    for (ex, ey), c in f.items():
+        rows[ey] = (rows[ey] + c * pow(x0, ex, q)) % q
+    return rows
+
+
+def _upoly_eval(R, x0, q):
+    acc = 0
+    for c in reversed(R):
+        acc = (acc * x0 + c) % q
+    return acc
+
+
+def _rand_curve(rng, ny, nx, bits):
+    f = {(i, j): rng.randint(-(1 << bits), 1 << bits) for j in range(ny + 1) for i in range(nx + 1)}
+    f[(0, ny)] = rng.choice((-3, -1, 1, 2, 5))  # constant leading y-coefficient: every x0 is a good point
+    for i in range(1, nx + 1):
+        f[(i, ny)] = 0
+    return {k: v for k, v in f.items() if v}
+
+
+def test_general_warp_kernel_against_restatement():
+    """deg_y 45 / 43 (not a fast-path shape, above the thread kernel's 40): k_modres_warp,
+    exact against the CPU restatement of elim.cpp:95-136."""
+    rng = random.Random(45)
+    p = _rand_curve(rng, 45, 1, 6)
+    q = _rand_curve(rng, 43, 1, 6)
+    assert P.resultant(p, q) == O.resultant(p, q, "y")
+
+
+@pytest.mark.parametrize("n", [60, 150])
+def test_superelliptic_beyond_128(n):
+    """y^n + g(x): res(f, f_y) = n^n g^(n-1) exactly; n = 150 was CTG_UNSUPPORTED in r1."""
+    rng = random.Random(n)
+    g = [rng.randint(-9, 9) or 1 for _ in range(3)]
+    f = {(i, 0): c for i, c in enumerate(g)}
+    f[(0, n)] = 1
+    want = [n ** n]
+    for _ in range(n - 1):
+        nxt = [0] * (len(want) + len(g) - 1)
+        for i, a in enumerate(want):
+            for j, b in enumerate(g):
+                nxt[i + j] += a * b
+        want = nxt
+    assert P.resultant(f, curves.derive_y(f)) == want
+
+
+def test_deg_y_150_specialisation():
+    """A random deg_y 150 curve (warp kernel, 150 x 149 Sylvester shape): R(x0) mod q equals the
+    F_q resultant of the specialised rows at random x0 (the leading y-coefficient is a constant,
+    so every x0 specialises), and deg R <= the Bezout bound."""
+    rng = random.Random(150)
+    f = _rand_curve(rng, 150, 1, 8)
+    fy = curves.derive_y(f)
+    R = P.resultant(f, fy)
+    assert 0 < len(R) - 1 <= 150 * 149
+    for _ in range(3):
+        x0 = rng.randrange(Q61)
+        want = _res_mod(_eval_rows(f, x0, Q61), _eval_rows(fy, x0, Q61), Q61)
+        assert _upoly_eval(R, x0, Q61) == want
+
+
+def test_yun_beyond_shared_memory():
+    """deg 6503 > the r1 cap of 6000 (K6 buffers in global memory):
+    Yun((x-1)^2 (x+2) (x^6500 - 3)) = [((x+2)(x^6500-3), 1), (x-1, 2)] -- x^6500 - 3 is
+    square-free and vanishes at neither 1 nor -2."""
+    h = [-3] + [0] * 6499 + [1]
+    a = O.u_mul([2, 1], h)
+    Pp = O.u_mul(O.u_mul([-1, 1], [-1, 1]), a)
+    unit, factors = P.yun_squarefree(Pp)
+    assert unit == 1
+    assert factors == [(a, 1), ([-1, 1], 2)]
+
+
+def test_gcd_beyond_shared_memory():
+    """deg 10501 (k_modgcd's five buffers exceed the shared-memory budget):
+    gcd((x+3) g, (x-5) g) = g for primitive g with positive leading coefficient."""
+    g = [1, -7] + [0] * 10498 + [1]
+    assert P.gcd_univariate(O.u_mul([3, 1], g), O.u_mul([-5, 1], g)) == g
+
+
+def test_gcd_bivariate_newton_beyond_shared_memory():
+    """x-degree 900: the Newton interpolation needs N > 1,760 points (global scratch).
+    gcd(h (y + x), h (y + x + 1)) = h for h = y + x^900 + 1 (primitive, lc_y = 1)."""
+    h = {(0, 1): 1, (900, 0): 1, (0, 0): 1}
+    f = O.b_mul(h, {(0, 1): 1, (1, 0): 1})
+    g = O.b_mul(h, {(0, 1): 1, (1, 0): 1, (0, 0): 1})
+    assert P.gcd_bivariate(f, g) == h
