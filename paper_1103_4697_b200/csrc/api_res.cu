@@ -247,6 +247,7 @@ struct ctg_plan {
   uint64_t* d_cols = nullptr;      // [B][J][L16]
   uint32_t* d_vals = nullptr;      // K2 point values [B][P][nrows][N] (fast path only)
   uint32_t* d_gwarp = nullptr;     // k_modres_warp buffers in global memory (deg_y beyond ~6000)
+  uint32_t* d_ntt = nullptr;       // K4 work array [B][P][N] when N > kMaxNttSmem
   int nrows = 0, maxlen = 0;
   bool fast_ok = false;
   bool fused = false;              // K2 folded into K3 (k_modres_fused): no d_vals
@@ -286,6 +287,7 @@ struct ctg_plan {
                r(4ull * flag_cap) + r(16);
     if (fast_ok && !fused) s += r(4ull * B * P * nrows * N);
     s += r(4 * general_warp_gbuf_words(n));
+    if (N > kMaxNttSmem) s += r(4ull * B * P * N);
     s += r(4 * crt_y_words(*tabs, B, J)) + r(8 * static_cast<size_t>(B) * nch * J) +
          r(8 * ((crt_cols_words(*tabs, B, J) + 1) / 2));
     return s;
@@ -302,6 +304,7 @@ struct ctg_plan {
     pfree(d_cols);
     pfree(d_vals);
     pfree(d_gwarp);
+    pfree(d_ntt);
   }
   int out_limbs() const { return tabs ? tabs->LM : 0; }
   int out_words() const { return out_limbs() + 1; }
@@ -395,7 +398,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   for (int v : lenq) pl->maxlen = std::max(pl->maxlen, v);
   pl->fast_ok = (m == n - 1 || m == n) && n >= 2 && n <= kFastMaxDeg;
 
-  if (degb + 1 > kMaxNtt) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 16383");
+  if (degb + 1 > (int64_t{1} << 28)) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 2^28");
   pl->D = static_cast<uint32_t>(degb + 1);
   pl->N = choose_ntt_size(pl->D, &pl->r, &pl->a);
   {
@@ -407,9 +410,19 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
     pl->fused = pl->fast_ok && pl->deriv && m == n - 1 && pl->maxlen <= lp && pl->N % lp == 0 && fuse;
   }
   pl->bound_bits = bound;
+  if (static_cast<uint64_t>(pl->B) * pl->N * static_cast<uint64_t>(std::max(1.0, (bound + 37) / 29.0)) >= (1ull << 32))
+    throw ApiError(CTG_UNSUPPORTED, "resultant: more than 2^32 evaluation units (> 16 GB of residues) in one plan");
   const double need = bound + 1 + 36;
   const auto tb2 = tclk::now();
-  std::vector<uint32_t> primes = select_primes(pl->N, need, kResPrimeMax);  // mmul3 window (modarith.cuh)
+  std::vector<uint32_t> primes;
+  try {
+    primes = select_primes(pl->N, need, kResPrimeMax);  // mmul3 window (modarith.cuh), p > 2^30
+  } catch (const std::runtime_error&) {
+    // very large N leaves too few primes p = cN + 1 above 2^30: extend the window downwards
+    // (same descending enumeration, so the first primes are unchanged; Montgomery, mmul3 and
+    // the CRT hold for any odd p < 2^30.4)
+    primes = select_primes(pl->N, need, kResPrimeMax, 1ull << 24);
+  }
   pl->P = static_cast<int>(primes.size());
   const auto tb3 = tclk::now();
   pl->tabs = get_tables(pl->device, pl->N, primes);
@@ -433,6 +446,7 @@ static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   pl->palloc(pl->d_counters, 4, st);
   if (pl->fast_ok && !pl->fused) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
   if (general_warp_gbuf_words(pl->n)) pl->palloc(pl->d_gwarp, general_warp_gbuf_words(pl->n), st);
+  if (pl->N > kMaxNttSmem) pl->palloc(pl->d_ntt, static_cast<size_t>(pl->B) * pl->P * pl->N, st);
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
 }
 
@@ -481,7 +495,8 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   if (stage == 3) {
     pl->launches += launch_interp(d_rows, rows_bstride, static_cast<int>(pl->N), nk, pl->B, pl->tabs->d_pc,
                                   pl->tabs->d_twinv, k0, static_cast<int>(pl->N), static_cast<int>(pl->r),
-                                  static_cast<int>(pl->a), static_cast<int>(pl->D), pl->negate, pl->d_counters, st);
+                                  static_cast<int>(pl->a), static_cast<int>(pl->D), pl->negate, pl->d_counters, st,
+                                  pl->d_ntt);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }

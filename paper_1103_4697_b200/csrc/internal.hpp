@@ -32,7 +32,7 @@ constexpr int kThreadGeneralMax = kFastMaxDeg;  // thread-per-unit formal-degree
 constexpr int kWarpsGeneral = 4;                // warps per CTA of k_modres_warp
 constexpr size_t kGeneralWarpSmemMax = 200 * 1024;  // beyond: per-warp slices of global scratch
 constexpr uint32_t kGeneralWarpGlobalBlocks = 296;
-constexpr uint32_t kMaxNtt = 1u << 14;
+constexpr uint32_t kMaxNttSmem = 1u << 14;  // K4 in shared memory up to this size; beyond, global passes
 constexpr uint32_t kSentinel = 0xffffffffu;
 constexpr int kCrtChunk = 64;       // primes per partial sum of the CRT rounding estimate
 constexpr int kI8TileJ = 128;       // tensor-core CRT GEMM block tile: coefficients
@@ -146,7 +146,7 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part = 0);
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
                   const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
-                  cudaStream_t st);
+                  cudaStream_t st, uint32_t* d_work = nullptr);  // d_work: B * nk * N words when N > kMaxNttSmem
 // Fills twinv[k][i] = omega_k^{-i} for all primes of a table (one launch, at table build).
 void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv);
 int launch_crt(const CrtParams& cp, cudaStream_t st);

@@ -15,6 +15,8 @@
 // Sylvester determinant at every (prime, point) determine it bit-exactly.
 #include <cuda_runtime.h>
 
+#include <stdexcept>
+
 #include <cudaTypedefs.h>
 
 #include <type_traits>
@@ -495,6 +497,66 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
       tail |= (c != 0u);
   }
   if (tail) atomicOr(&counters[1], kErrNttTail);
+}
+
+// K4 for sizes beyond shared memory (N > kMaxNttSmem): the same inverse DFT on a global
+// work array, one launch per pass -- the permutation into [R][2^a] bit-reversed rows, a
+// radix-2 DIT stages (butterfly per thread, twiddles from the [P][N] table), then the
+// r-point twiddled DFT, scaling, negation and degree-bound check of k_interp.
+__global__ void k_interp_big_permute(const uint32_t* __restrict__ rows, size_t rows_bstride, int pitch, int nk,
+                                     int N, int R, int a, uint32_t* __restrict__ w) {
+  const int kl = blockIdx.y, b = blockIdx.z;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const uint32_t* row = rows + b * rows_bstride + static_cast<size_t>(kl) * pitch;
+  uint32_t* wk = w + (static_cast<size_t>(b) * nk + kl) * N;
+  const int i1 = i % R, i2 = i / R;
+  const int br = a ? static_cast<int>(__brev(static_cast<uint32_t>(i2)) >> (32 - a)) : 0;
+  wk[(i1 << a) + br] = row[i];
+}
+
+__global__ void k_interp_big_stage(uint32_t* __restrict__ w, int nk, int N, int R, int a, int lg,
+                                   const PrimeConst* __restrict__ pc, const uint32_t* __restrict__ twinv, int k0) {
+  const int kl = blockIdx.y, b = blockIdx.z;
+  const int bb = blockIdx.x * blockDim.x + threadIdx.x;  // butterfly: R * 2^(a-1) per (curve, prime)
+  if (bb >= (R << (a - 1))) return;
+  const Mod M = load_mod(pc[k0 + kl]);
+  const uint32_t* tw = twinv + static_cast<size_t>(k0 + kl) * N;
+  uint32_t* wk = w + (static_cast<size_t>(b) * nk + kl) * N;
+  const int half = 1 << (lg - 1), lgh = a - 1;
+  const int rw = bb >> lgh, q = bb & ((1 << lgh) - 1);
+  const int g = q >> (lg - 1), t = q & (half - 1);
+  uint32_t* base = wk + (rw << a) + (g << lg);
+  const uint32_t u = base[t];
+  const uint32_t v = mmul(base[t + half], __ldg(&tw[(R * t) << (a - lg)]), M);
+  base[t] = madd(u, v, M.p);
+  base[t + half] = msub(u, v, M.p);
+}
+
+__global__ void k_interp_big_final(const uint32_t* __restrict__ w, uint32_t* rows, size_t rows_bstride, int pitch,
+                                   int nk, int N, int R, int a, int D, int negate, const PrimeConst* __restrict__ pc,
+                                   const uint32_t* __restrict__ twinv, int k0, uint32_t* counters) {
+  const int kl = blockIdx.y, b = blockIdx.z;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const PrimeConst pcv = pc[k0 + kl];
+  const Mod M = load_mod(pcv);
+  const uint32_t* tw = twinv + static_cast<size_t>(k0 + kl) * N;
+  const uint32_t* wk = w + (static_cast<size_t>(b) * nk + kl) * N;
+  const int j1 = j & ((1 << a) - 1);
+  uint32_t acc = 0;
+  long long e = 0;
+  for (int i1 = 0; i1 < R; ++i1) {
+    acc = madd(acc, mmul(wk[(i1 << a) + j1], __ldg(&tw[e]), M), M.p);
+    e += j;
+    if (e >= N) e -= N;
+  }
+  uint32_t c = mmul(acc, pcv.scale, M);
+  if (negate) c = mneg(c, M.p);
+  if (j < D)
+    rows[b * rows_bstride + static_cast<size_t>(kl) * pitch + j] = c;
+  else if (c != 0u)
+    atomicOr(&counters[1], kErrNttTail);
 }
 
 // ---------------------------------------------------------------------------
@@ -1231,8 +1293,19 @@ size_t general_warp_gbuf_words(int n) {
 
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
                   const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint32_t* d_work) {
   if (nk == 0 || B == 0) return 0;
+  if (static_cast<uint32_t>(N) > kMaxNttSmem) {  // global-memory passes (d_work: B * nk * N words)
+    if (!d_work) throw std::runtime_error("launch_interp: work array missing for N > kMaxNttSmem");
+    const dim3 gp((N + 255) / 256, nk, B);
+    k_interp_big_permute<<<gp, 256, 0, st>>>(rows, rows_bstride, pitch, nk, N, r, a, d_work);
+    const dim3 gs(((r << (a - 1)) + 255) / 256, nk, B);
+    for (int lg = 1; lg <= a; ++lg)
+      k_interp_big_stage<<<gs, 256, 0, st>>>(d_work, nk, N, r, a, lg, d_pc, d_twinv, k0);
+    k_interp_big_final<<<gp, 256, 0, st>>>(d_work, rows, rows_bstride, pitch, nk, N, r, a, D, negate, d_pc, d_twinv, k0,
+                                           counters);
+    return a + 2;
+  }
   const size_t smem = static_cast<size_t>(2) * N * 4;
   // one radix-2 butterfly per thread per stage where possible (r * 2^(a-1) of them)
   int threads = (r << a) / 2;

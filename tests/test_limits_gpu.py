@@ -139,3 +139,45 @@ def test_gcd_bivariate_newton_beyond_shared_memory():
     f = O.b_mul(h, {(0, 1): 1, (1, 0): 1})
     g = O.b_mul(h, {(0, 1): 1, (1, 0): 1, (0, 0): 1})
     assert P.gcd_bivariate(f, g) == h
+
+
+def _quad_curve(a, b):
+    """f = y^2 + a(x) y + b(x): res(f, f_y) = 4 b - a^2 (res(g, f) = lc(g)^2 f(-a/2), n m even)."""
+    f = {(0, 2): 1}
+    for i, c in enumerate(a):
+        if c:
+            f[(i, 1)] = c
+    for i, c in enumerate(b):
+        if c:
+            f[(i, 0)] = c
+    return f
+
+
+def test_result_degree_beyond_16383():
+    """deg R = 20000 (N = 20480 > the shared-memory K4's 16384: global-memory NTT passes);
+    exact: R = 4b - a^2 (numpy convolution, coefficients < 2^40)."""
+    import numpy as np
+    rng = np.random.default_rng(20000)
+    a = rng.integers(-1023, 1024, size=10001).astype(np.int64)
+    a[-1] = 7
+    b = rng.integers(-1023, 1024, size=20001).astype(np.int64)
+    want = (4 * b - np.convolve(a, a)).tolist()
+    f = _quad_curve(a.tolist(), b.tolist())
+    assert P.resultant(f, curves.derive_y(f)) == want
+
+
+def test_prime_window_extension():
+    """deg R = 80000 with ~10,000-bit coefficients: N = 81920 leaves ~200 primes p = cN + 1
+    above 2^30, fewer than the bound needs -- the window extends below 2^30.  Checked exactly
+    at the top and bottom coefficients and at random points mod a 61-bit prime."""
+    rng = random.Random(80000)
+    a = [rng.getrandbits(5000) * rng.choice((-1, 1)) for _ in range(40001)]
+    b = [rng.randint(-1023, 1023) for _ in range(80001)]
+    f = _quad_curve(a, b)
+    R = P.resultant(f, curves.derive_y(f))
+    assert len(R) == 80001
+    assert R[-1] == 4 * b[-1] - a[-1] ** 2 and R[0] == 4 * b[0] - a[0] ** 2
+    for _ in range(3):
+        x0 = rng.randrange(Q61)
+        av, bv = _upoly_eval(a, x0, Q61), _upoly_eval(b, x0, Q61)
+        assert _upoly_eval(R, x0, Q61) == (4 * bv - av * av) % Q61
