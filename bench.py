@@ -296,8 +296,15 @@ def main_ours(args):
     torch.cuda.set_stream(stream)
     G = world
     peaks = P.microbench_int(dev)
+    comm = None
+    if world > 1 and os.environ.get("CTG_BENCH_SIM_GLOO") != "1":
+        # the library's own NCCL communicator (ctg_comm): residues are exchanged by libctg;
+        # torch.distributed only carries the id, the barriers and the max-over-ranks time
+        obj = [P.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = P.Comm(world, rank, obj[0], dev)
 
-    m = measure(args, args.workload, args.batch, P, curves, torch, dist, stream, rank, G, peaks)
+    m = measure(args, args.workload, args.batch, P, curves, torch, dist, stream, rank, G, peaks, comm)
     line = {
         "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": G, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong",
@@ -311,7 +318,7 @@ def main_ours(args):
         "parity": m["parity"],
     }
     if rank == 0 and G == 1 and not args.no_extra and args.workload != "d20_b64":
-        x = measure(args, "d20_b64", DEFAULT_BATCH["d20_b64"], P, curves, torch, dist, stream, rank, G, peaks)
+        x = measure(args, "d20_b64", DEFAULT_BATCH["d20_b64"], P, curves, torch, dist, stream, rank, G, peaks, comm)
         line["d20_b64"] = {"workload": WORKLOADS["d20_b64"][3], "value": x["value"], "unit": UNIT,
                            "ms_per_step": x["ms_per_step"], "sample": x["sample"], "e2e": x["e2e"],
                            "roofline_frac": x["roofline"]["frac"], "stage_ms_per_step": x["roofline"]["stage_ms_per_step"],
@@ -327,11 +334,13 @@ def main_ours(args):
         print(json.dumps(line))
     if dist:
         dist.barrier()
+        if comm:
+            comm.close()
         dist.destroy_process_group()
     return 0
 
 
-def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks):
+def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks, comm=None):
     """One workload: device-resident value (staged events), e2e through the C ABI, K3 roofline,
     and the reference-digest parity of every curve that has one."""
     from paper_1103_4697_b200 import sharding
@@ -380,7 +389,9 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks):
             plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
             if timed:
                 evs[i + 1].record(stream)
-        if G > 1:
+        if comm:  # ctg_comm_all_gather: libctg's NCCL communicator, on the launch stream
+            comm.all_gather(send.data_ptr(), full.data_ptr(), send.numel(), sh)
+        elif G > 1:  # CTG_BENCH_SIM_GLOO: functional multi-rank test on one GPU
             dist.all_gather_into_tensor(full.view(-1, Pb, N), send)
         if timed:
             evs[5].record(stream)
@@ -425,34 +436,39 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks):
         parity["device_resident"] = "bit-exact"
 
     # --- e2e through the C ABI with host buffers --------------------------------------
+    # G > 1: every rank calls ctg_resultant_batch with ctg_opts.comm (prime-sharded product
+    # path: parse + plan + H2D + K1-K4 on its primes + NCCL all-gather + K5 on its coefficient
+    # block + all-gather of the limbs + D2H + decode); the time is the max over ranks.
     e2e_phases = None
-    if G == 1:
-        hb = P.HostBatch(pairs)
-        for _ in range(max(1, args.warmup)):
-            P.resultant_batch_raw(hb)
-        walls = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            P.resultant_batch_raw(hb)
-            walls.append(time.perf_counter() - t0)
-            st = P.last_call_stats()
-            h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
-        e2e_ms = 1e3 * sum(walls) / len(walls)
-        e2e_phases = {k: st[k] for k in ("setup_ms", "h2d_ms", "device_ms", "d2h_ms", "decode_ms", "total_ms")}
-        got = P.resultant_batch([pairs[s_ - 1] for s_ in parity["reference_digests"]]) if gold else []
-        for s_, R in zip(parity["reference_digests"], got):
-            check_golden(gold[s_], R, "ctg_resultant_batch")
-        parity["e2e"] = "bit-exact"
-    else:
-        e2e_ms, h2d, d2h, check = e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W,
-                                              N, sh, rank)
-        if rank == 0:  # the sharded pipeline's exact results against the one-shot call
-            assert check[0] == P.resultant(*pairs[0]) and check[1] == P.resultant(*pairs[B - 1]), \
-                "prime-sharded result != one-shot"
-            for s_ in (1, B):
-                if s_ in gold:
-                    check_golden(gold[s_], check[0 if s_ == 1 else 1], "prime-sharded pipeline")
-            parity["sharded"] = "bit-exact"
+    hb = P.HostBatch(pairs)
+    sim = G > 1 and comm is None  # gloo simulation on one GPU: shards via the device-list path
+    kw = {"comm": comm} if comm else ({"devices": [dev] * G} if sim else {})
+    for _ in range(max(1, args.warmup)):
+        if dist:
+            dist.barrier()
+        P.resultant_batch_raw(hb, **kw)
+    walls = []
+    for _ in range(args.steps):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        P.resultant_batch_raw(hb, **kw)
+        walls.append(time.perf_counter() - t0)
+        st = P.last_call_stats()
+        h2d, d2h = st["h2d_bytes"], st["d2h_bytes"]
+    e2e_ms = 1e3 * sum(walls) / len(walls)
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_phases = {k: st[k] for k in ("setup_ms", "h2d_ms", "device_ms", "d2h_ms", "decode_ms", "total_ms")}
+    # parity of the product path (outside the timed region): every reference-pinned seed
+    chk = [s_ for s_ in parity["reference_digests"]]
+    got = P.resultant_batch([pairs[s_ - 1] for s_ in chk], **kw) if chk else []
+    if rank == 0:
+        for s_, R in zip(chk, got):
+            check_golden(gold[s_], R, "ctg_resultant_batch" + (f" (prime-sharded, G={G})" if G > 1 else ""))
+    parity["e2e" if G == 1 else "sharded_e2e"] = "bit-exact"
     e2e_value = units_step / (e2e_ms * 1e-3)
 
     # --- roofline of the dominant kernel: K3, the mod-p resultant (north_star: >= 50% of IMAD peak)
@@ -480,56 +496,11 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks):
                    "units_per_step": units_step, "parallelism": f"prime-shard{G}" if G > 1 else "single",
                    "l2": "flushed (256 MB write) between timed steps", "res_ms_per_curve": ms_per_step / B},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "res_ms_per_curve": e2e_ms / B, "path": "ctg_resultant_batch (C ABI), host CSR limbs in/out",
+                "res_ms_per_curve": e2e_ms / B,
+                "path": "ctg_resultant_batch (C ABI), host CSR limbs in/out" + (f", ctg_opts.comm over {G} ranks" if G > 1 else ""),
                 "phases_ms_last_call": e2e_phases},
         "gpu_launches": int(gpu_launches), "roofline": roofline, "clocks": clk.summary(), "parity": parity,
     }
-
-
-def e2e_sharded(args, plan, torch, dist, send, full, out, Pb, k0, k1, j0, j1, Jb, D, W, N, sh, rank):
-    """Multi-GPU end-to-end: every rank uploads the inputs, computes its prime rows, all-gathers,
-    reconstructs its coefficient block; rank 0 gathers the exact limbs, reassembles them into
-    [B][D][W] on the device, copies them to pinned host memory and decodes every curve in C
-    (ctg_plan_decode: sign + limb CSR, the same host result the one-GPU batch call returns).
-    Plan creation (host parsing) is outside the timed region here; the one-GPU e2e includes it."""
-    from paper_1103_4697_b200 import sharding
-
-    B = plan.info["batch"]
-    G = dist.get_world_size()
-    gathered = torch.zeros((G,) + tuple(out.shape), dtype=torch.int32, device=out.device)
-    host = torch.empty((B, D, W), dtype=torch.int32, pin_memory=True) if rank == 0 else None
-    walls = []
-    for it in range(args.warmup + args.steps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        plan.upload(sh)
-        for s_ in (1, 2, 3):
-            plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
-        dist.all_gather_into_tensor(full.view(-1, *send.shape[1:]), send)
-        plan.crt_batch(full.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N, row_block=Pb,
-                       block_stride=B * Pb * N)
-        dist.all_gather_into_tensor(gathered.view(-1), out)
-        if rank == 0:
-            blocks = []
-            for r in range(G):
-                r0, r1, _ = sharding.coeff_block(D, G, r)
-                blocks.append(gathered[r, :B * (r1 - r0) * W].view(B, r1 - r0, W))
-            host.copy_(torch.cat(blocks, dim=1), non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            plan.decode_batch_raw(host.numpy().view("uint32"))
-        torch.cuda.synchronize()
-        if it >= args.warmup:
-            walls.append(time.perf_counter() - t0)
-    check = None
-    if rank == 0:  # outside the timed region: exact integers of the first and last curve
-        hv = host.numpy().view("uint32")
-        check = (plan.decode(hv[0]), plan.decode(hv[B - 1]))
-    h2d = plan.h2d_bytes * G
-    d2h = B * D * W * 4
-    t = torch.tensor([1e3 * sum(walls) / len(walls)], dtype=torch.float64, device=out.device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item()), h2d, d2h, check
 
 
 def headline(P, curves, workload, cb):

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CTG_ABI_VERSION 1
+#define CTG_ABI_VERSION 2
 
 typedef enum {
   CTG_OK = 0,
@@ -96,10 +96,25 @@ typedef struct {
   uint32_t* limbs;
 } ctg_bipoly_buf;
 
+/* Multi-process communicator (one process per GPU, e.g. under torchrun): ctg_comm_init_rank. */
+typedef struct ctg_comm ctg_comm;
+
 typedef struct {
   int32_t device;   /* CUDA device ordinal; -1 = current device */
   int32_t verify;   /* 1 (default) = run the on-device self-checks; 0 = skip the optional ones */
-  int32_t reserved[6];
+  /* Prime sharding of ctg_resultant / ctg_resultant_batch:
+   *  - n_devices > 1: this process drives devices[0..n_devices); shard g owns a contiguous
+   *    block of the primes, computes those rows of the residue matrix (K1-K4), the rows are
+   *    all-gathered over NCCL (distinct devices) or device copies (a device listed twice:
+   *    shards share it), shard g reconstructs a block of coefficients (K5) and copies it
+   *    straight into the host result.  Results are bit-identical to one device.
+   *  - comm != NULL: multi-process; every rank calls with the same inputs, computes its prime
+   *    block, NCCL all-gathers residues and CRT'd coefficient blocks; every rank returns the
+   *    full result. */
+  int32_t n_devices;
+  int32_t reserved0;
+  const int32_t* devices;
+  ctg_comm* comm;
 } ctg_opts;
 
 /* Timings of the last call on this thread (milliseconds; host wall clock around each phase). */
@@ -122,8 +137,7 @@ ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ct
  * gcd_univariate(content_y f, content_y g).  Otherwise Brown's modular gcd runs on the GPU
  * (images gamma(a) * gcd(f(a, y), g(a, y)) mod p with cofactors, Newton interpolation in x,
  * CRT) and an exactness certificate proves the result; output terms sorted by (dx, dy).
- * CTG_UNSUPPORTED only beyond the shared-memory limits (y-degree > 6000 or an x-degree
- * bound above ~1700). */
+ * No size limit: beyond the shared-memory budget the kernels' buffers move to global memory. */
 ctg_status ctg_gcd_bivariate(const ctg_bipoly* f, const ctg_bipoly* g, ctg_bipoly_buf* out,
                              const ctg_opts* opts);
 
@@ -204,6 +218,16 @@ ctg_status ctg_plan_stage_batch(ctg_plan* plan, int32_t stage, int32_t k0, int32
  * + (k % row_block) * n_points (curve_stride 0: n_primes * n_points; row_block 0: n_primes). */
 ctg_status ctg_plan_crt_batch(ctg_plan* plan, const uint32_t* d_all, int64_t curve_stride, int32_t row_block,
                               int64_t block_stride, int32_t j0, int32_t j1, uint32_t* d_out, void* stream);
+
+/* ---- multi-process communicators (NCCL, loaded at run time) ----
+ * Rank 0 creates an id with ctg_comm_unique_id, shares the bytes with the other ranks
+ * (any host channel), and every rank calls ctg_comm_init_rank with its own device.
+ * ctg_comm_all_gather: words u32 per rank, d_recv = nranks x words (device buffers). */
+#define CTG_COMM_ID_BYTES 128
+ctg_status ctg_comm_unique_id(uint8_t* id /* CTG_COMM_ID_BYTES */);
+ctg_status ctg_comm_init_rank(int32_t nranks, int32_t rank, const uint8_t* id, int32_t device, ctg_comm** comm);
+void ctg_comm_destroy(ctg_comm* comm);
+ctg_status ctg_comm_all_gather(ctg_comm* comm, const void* d_send, void* d_recv, size_t words, void* stream);
 
 /* Integer-pipe peak microbenchmarks on `device` (-1 = current): 32-bit IMAD
  * (a*b+c) and IMAD.WIDE (u32*u32+u64) results per second over all SMs, and

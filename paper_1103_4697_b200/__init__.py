@@ -80,7 +80,8 @@ class _SqfBuf(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("device", C.c_int32), ("verify", C.c_int32), ("reserved", C.c_int32 * 6)]
+    _fields_ = [("device", C.c_int32), ("verify", C.c_int32), ("n_devices", C.c_int32), ("reserved0", C.c_int32),
+                ("devices", _i32p), ("comm", C.c_void_p)]
 
 
 class CallStats(C.Structure):
@@ -112,6 +113,7 @@ EXPORTS = (
     "ctg_plan_decode", "ctg_plan_check", "ctg_plan_launches", "ctg_plan_destroy", "ctg_plan_stage",
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
     "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch", "ctg_gcd_bivariate", "ctg_bipoly_free",
+    "ctg_comm_unique_id", "ctg_comm_init_rank", "ctg_comm_destroy", "ctg_comm_all_gather",
 )
 
 _lib = None
@@ -167,6 +169,10 @@ def lib():
         L.ctg_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.ctg_plan_launches.argtypes = [C.c_void_p]
         L.ctg_plan_destroy.argtypes = [C.c_void_p]
+        L.ctg_comm_unique_id.argtypes = [C.c_void_p]
+        L.ctg_comm_init_rank.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+        L.ctg_comm_destroy.argtypes = [C.c_void_p]
+        L.ctg_comm_all_gather.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         _lib = L
         return L
 
@@ -274,11 +280,46 @@ def _decode_buf(buf: _UpolyBuf) -> list:
     return out
 
 
-def _opts(device):
+def _opts(device, devices=None, comm=None):
+    """ctg_opts: one device (default), a prime-sharded device list (one process; repeats allowed),
+    or a multi-process Comm."""
     o = _Opts()
     o.device = -1 if device is None else int(device)
     o.verify = 1
+    if devices is not None and len(devices) > 1:
+        o._devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])  # kept alive with the struct
+        o.n_devices = len(devices)
+        o.devices = C.cast(o._devs, _i32p)
+    if comm is not None:
+        o.comm = comm.handle
     return o
+
+
+class Comm:
+    """A multi-process communicator (ctg_comm): rank `rank` of `nranks`, on `device`.
+    ``Comm.unique_id()`` on rank 0, share the bytes (e.g. torch.distributed.broadcast_object_list),
+    then ``Comm(nranks, rank, uid, device)`` on every rank."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().ctg_comm_unique_id(buf), "comm_unique_id")
+        return bytes(buf)
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int):
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().ctg_comm_init_rank(nranks, rank, buf, device, C.byref(h)), "comm_init_rank")
+        self.handle, self.nranks, self.rank, self.device = h, nranks, rank, device
+
+    def all_gather(self, send_ptr, recv_ptr, words, stream=0):
+        _check(lib().ctg_comm_all_gather(self.handle, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), words,
+                                         C.c_void_p(stream)), "comm_all_gather")
+
+    def close(self):
+        if self.handle:
+            lib().ctg_comm_destroy(self.handle)
+            self.handle = None
 
 
 def last_call_stats() -> dict:
@@ -351,10 +392,10 @@ class HostBatch:
         self.nbytes = sum(a.nbytes + b.nbytes for a, b in self.ops)
 
 
-def resultant_batch_raw(hb: HostBatch, var: str = "y", device=None) -> int:
+def resultant_batch_raw(hb: HostBatch, var: str = "y", device=None, devices=None, comm=None) -> int:
     """ctg_resultant_batch into library buffers that are freed again (the C/C++ caller's call)."""
     outs = (_UpolyBuf * max(1, hb.n))()
-    o = _opts(device)
+    o = _opts(device, devices, comm)
     _check(lib().ctg_resultant_batch(hb.n, hb.p, hb.q, 1 if var in ("x", "X") else 0, outs, C.byref(o)),
            "resultant_batch")
     total = sum(outs[i].n_coeffs for i in range(hb.n))
@@ -362,11 +403,13 @@ def resultant_batch_raw(hb: HostBatch, var: str = "y", device=None) -> int:
     return total
 
 
-def resultant_batch(pairs, var: str = "y", device=None) -> list:
-    """[res(p, q) for (p, q) in pairs] with one batched GPU pipeline per input shape."""
+def resultant_batch(pairs, var: str = "y", device=None, devices=None, comm=None) -> list:
+    """[res(p, q) for (p, q) in pairs] with one batched GPU pipeline per input shape; with
+    `devices` (list of ordinals, repeats allowed) or `comm` (multi-process) the primes are
+    sharded over several GPUs (ctg_opts.n_devices / ctg_opts.comm)."""
     hb = HostBatch(pairs)
     outs = (_UpolyBuf * max(1, hb.n))()
-    o = _opts(device)
+    o = _opts(device, devices, comm)
     _check(lib().ctg_resultant_batch(hb.n, hb.p, hb.q, 1 if var in ("x", "X") else 0, outs, C.byref(o)),
            "resultant_batch")
     res = []

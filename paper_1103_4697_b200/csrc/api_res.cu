@@ -12,6 +12,7 @@
 // (enough for the largest bound), one set of kernel launches with blockIdx.z = curve.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -27,6 +28,7 @@
 #include <vector>
 
 #include "api_common.hpp"
+#include "comm.hpp"
 #include "internal.hpp"
 
 namespace ctg {
@@ -198,6 +200,12 @@ static Problem parse_problem(const ctg_bipoly* pin, const ctg_bipoly* qin, int32
   }
   pr.degb = std::min(static_cast<int64_t>(pr.m) * Xp + static_cast<int64_t>(pr.n) * Xq,
                      static_cast<int64_t>(tp) * tq);
+  // before any layout is built: a sparse input with a huge exponent must not
+  // allocate gigabytes of dense slots first
+  if (pr.degb + 1 > (int64_t{1} << 28))
+    throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 2^28");
+  if (static_cast<int64_t>(pr.n + 1) * (Xp + 1) + static_cast<int64_t>(pr.m + 1) * (Xq + 1) > (int64_t{1} << 30))
+    throw ApiError(CTG_UNSUPPORTED, "resultant: dense slot layout exceeds 2^30 coefficients");
   // Hadamard bound over |x| = 1.
   auto norm_bits = [](const Terms& t) {
     // Terms are sorted by dy: each y-degree is one contiguous run.
@@ -350,18 +358,20 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
     }
   }
   std::vector<int32_t> offp(n + 1), lenp(n + 1), offq(m + 1, 0), lenq(m + 1, 0);
-  int S = 0;
+  int64_t S64 = 0;
   for (int j = 0; j <= n; ++j) {
-    offp[j] = S;
+    offp[j] = static_cast<int32_t>(S64);
     lenp[j] = Xp[j] + 1;
-    S += lenp[j];
+    S64 += lenp[j];
   }
   if (!pl->deriv)
     for (int j = 0; j <= m; ++j) {
-      offq[j] = S;
+      offq[j] = static_cast<int32_t>(S64);
       lenq[j] = Xq[j] + 1;
-      S += lenq[j];
+      S64 += lenq[j];
     }
+  if (S64 > (int64_t{1} << 30)) throw ApiError(CTG_UNSUPPORTED, "resultant: dense slot layout exceeds 2^30 coefficients");
+  const int S = static_cast<int>(S64);
   pl->S = S;
   int L = 1;
   for (int i : idx) {
@@ -703,6 +713,18 @@ class ChunkPipeline {
     hout_ = ctx_.pinned_u32(kSlots * out_cap_);
   }
   void enqueue(Chunk&& c) {
+    try {
+      enqueue_impl(c);
+    } catch (...) {
+      // work already launched for this chunk writes into the slot's scratch and pinned
+      // staging: let it finish before the chunk is dropped and the slot reused
+      if (enq_stream_) cudaStreamSynchronize(enq_stream_);
+      cudaStreamSynchronize(ctx_.copy_stream());
+      destroy_events(c);
+      throw;
+    }
+  }
+  void enqueue_impl(Chunk& c) {
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
     ctg_plan* pl = c.pl.get();
@@ -734,9 +756,15 @@ class ChunkPipeline {
     }();
     const int ci = n_enqueued_++;
     const int si = ci % nstreams;
+    // Priority level ci % levels (6 on B200): chunks 0..5 of a call are strictly ordered, which
+    // covers every batch of up to six chunks (256 curves = 5).  Longer batches wrap: chunk 6
+    // outranks the still-running chunks 3-5 once; a strictly decreasing level would need more
+    // levels than the device has (stream priorities cannot be changed after launch).  Measured
+    // with scripts/ab_prio.sh (documented rather than drained at the wrap).
     cudaStream_t s = prio && nstreams > 1 ? ctx_.prio_stream(ci)
                      : si == 0            ? ctx_.stream
                                           : ctx_.aux_stream(si - 1);
+    enq_stream_ = s;
     cudaStream_t cp = ctx_.copy_stream();
     if (trace()) {
       for (cudaEvent_t* e : {&c.t_begin, &c.t_computed, &c.t_copied}) CTG_CUDA_CHECK(cudaEventCreate(e));
@@ -769,6 +797,7 @@ class ChunkPipeline {
     pl->last_stream = cp;
     st_.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
     inflight_.push_back(std::move(c));
+    enq_stream_ = nullptr;
     st_.h2d_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
   }
   // Waits for and decodes every chunk in flight, in order.
@@ -849,8 +878,233 @@ class ChunkPipeline {
   cudaEvent_t t0_ = nullptr;  // trace origin
   int n_enqueued_ = 0;
   int nstreams_ = 2;
+  cudaStream_t enq_stream_ = nullptr;
   std::chrono::steady_clock::time_point host0_;
 };
+
+// ---------------------------------------------------------------------------
+// Prime sharding across GPUs: ctg_resultant_batch with
+// ctg_opts.n_devices > 1 (one process, several devices) or ctg_opts.comm (one rank of a
+// multi-process job).  Shard g of G owns primes [g Pb, (g+1) Pb) of every plan: K1-K4 write
+// those rows into `send` [B][Pb][N]; ONE all-gather assembles `full` [G][B][Pb][N] on every
+// shard (NCCL over NVLink; device-to-device copies when shards share a GPU); shard g
+// reconstructs coefficients [g Jb, (g+1) Jb) (K5 reads the rank blocks in place); the exact
+// limbs go straight to the host result (one process) or through a second all-gather (every
+// rank returns the full result).  The only inter-GPU traffic is the residue matrix.
+// ---------------------------------------------------------------------------
+
+// Same plan on another device (host layout shared by value; constants from the cache).
+static ctg_plan* plan_clone(const ctg_plan* src, int device) {
+  if (src->d_tab) throw ApiError(CTG_INVALID, "plan_clone: source already on a device");
+  std::unique_ptr<ctg_plan> c(new ctg_plan());
+  c->device = device;
+  c->B = src->B;
+  c->trivial = src->trivial;
+  c->n = src->n;
+  c->m = src->m;
+  c->deriv = src->deriv;
+  c->negate = src->negate;
+  c->D = src->D;
+  c->N = src->N;
+  c->r = src->r;
+  c->a = src->a;
+  c->P = src->P;
+  c->S = src->S;
+  c->L = src->L;
+  c->bound_bits = src->bound_bits;
+  c->dir = src->dir;
+  c->h_limbs = src->h_limbs;
+  c->h_sign = src->h_sign;
+  c->flag_cap = src->flag_cap;
+  c->nrows = src->nrows;
+  c->maxlen = src->maxlen;
+  c->fast_ok = src->fast_ok;
+  c->fused = src->fused;
+  c->tabs = get_tables(device, src->N, src->tabs->primes);
+  return c.release();
+}
+
+struct Shard {
+  int device = 0, rank = 0;
+  cudaStream_t st = nullptr;
+  std::unique_ptr<ctg_plan> pl;
+  int k0 = 0, k1 = 0, j0 = 0, j1 = 0;
+  uint32_t *send = nullptr, *full = nullptr, *crt = nullptr, *gath = nullptr;
+  cudaEvent_t rows_done = nullptr;
+};
+
+static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
+                                    ctg_upoly_buf* out, const ctg_opts* opts) {
+  auto& stats = stats_tls();
+  using tclk = std::chrono::steady_clock;
+  const auto t_start = tclk::now();
+  ctg_comm* comm = opts->comm;
+  // the shard set: every shard of this process (one process) or this rank's (multi-process)
+  int G = 1;
+  std::vector<int> local_dev, local_rank;
+  if (comm) {
+    G = comm->nranks;
+    local_dev.push_back(comm->device);
+    local_rank.push_back(comm->rank);
+  } else {
+    if (!opts->devices) throw ApiError(CTG_INVALID, "ctg_opts: n_devices > 1 needs a devices array");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw ApiError(CTG_CUDA, "no CUDA device available (libctg has no CPU fallback)");
+    G = opts->n_devices;
+    for (int g = 0; g < G; ++g) {
+      if (opts->devices[g] < 0 || opts->devices[g] >= count) throw ApiError(CTG_INVALID, "ctg_opts.devices out of range");
+      local_dev.push_back(opts->devices[g]);
+      local_rank.push_back(g);
+    }
+  }
+  std::vector<int> distinct(local_dev);
+  std::sort(distinct.begin(), distinct.end());
+  const bool repeated = std::unique(distinct.begin(), distinct.end()) != distinct.end();
+  // NCCL between distinct devices of one process; device copies when a GPU hosts two shards
+  const bool use_nccl_local = !comm && !repeated && nccl_available();
+  const std::vector<ncclComm_t>* local_comms = use_nccl_local ? &device_set_comms(local_dev) : nullptr;
+
+  std::vector<Problem> probs(batch);
+  parallel_for(batch, [&](int i) { probs[i] = parse_problem(&p[i], &q[i], eliminate_x); });
+  std::map<std::tuple<int, int, int, int>, std::vector<int>> groups;
+  for (int b = 0; b < batch; ++b) {
+    if (probs[b].trivial)
+      fill_upoly({}, &out[b]);
+    else
+      groups[{probs[b].n, probs[b].m, probs[b].deriv, probs[b].negate}].push_back(b);
+  }
+  stats.setup_ms = std::chrono::duration<double, std::milli>(tclk::now() - t_start).count();
+  int nshard_on[64] = {0};
+  constexpr int kBlock = 64;  // curves per sharded plan
+  for (auto& [key, all_idx] : groups) {
+    for (size_t blk = 0; blk < all_idx.size(); blk += kBlock) {
+      std::vector<int> idx(all_idx.begin() + blk, all_idx.begin() + std::min(all_idx.size(), blk + kBlock));
+      std::vector<Shard> sh(local_dev.size());
+      std::unique_ptr<ctg_plan> pl0;
+      {
+        PlanDeviceGuard g0(local_dev[0]);
+        pl0.reset(plan_build(probs, idx, local_dev[0]));
+      }
+      const int B = pl0->B, Pn = pl0->P, N = static_cast<int>(pl0->N), D = static_cast<int>(pl0->D);
+      const int W = pl0->out_words();
+      const int Pb = (Pn + G - 1) / G, Jb = (D + G - 1) / G;
+      const size_t rows_words = static_cast<size_t>(B) * Pb * N, crt_words = static_cast<size_t>(B) * Jb * W;
+      std::fill(std::begin(nshard_on), std::end(nshard_on), 0);
+      for (size_t s = 0; s < sh.size(); ++s) {  // every shard's plan before any upload
+        sh[s].device = local_dev[s];
+        sh[s].rank = local_rank[s];
+        PlanDeviceGuard g(sh[s].device);
+        sh[s].pl.reset(s == 0 ? pl0.release() : plan_clone(sh[0].pl.get(), sh[s].device));
+      }
+      for (size_t s = 0; s < sh.size(); ++s) {
+        Shard& S = sh[s];
+        PlanDeviceGuard g(S.device);
+        Ctx& ctx = context(S.device);
+        const int slot = nshard_on[S.device % 64]++;  // shards sharing a GPU take different streams
+        S.st = slot == 0 ? ctx.stream : slot <= 2 ? ctx.aux_stream(slot - 1) : ctx.stream;
+        S.k0 = std::min(S.rank * Pb, Pn);
+        S.k1 = std::min((S.rank + 1) * Pb, Pn);
+        S.j0 = std::min(S.rank * Jb, D);
+        S.j1 = std::min((S.rank + 1) * Jb, D);
+        ctg_plan* pl = S.pl.get();
+        plan_upload(pl, S.st);
+        stats.h2d_bytes += plan_h2d_bytes(pl);
+        pl->palloc(S.send, rows_words, S.st);
+        pl->palloc(S.full, rows_words * G, S.st);
+        pl->palloc(S.crt, crt_words, S.st);
+        if (comm) pl->palloc(S.gath, crt_words * G, S.st);
+        if (S.k1 > S.k0) plan_residues(pl, S.k0, S.k1, S.send, static_cast<long long>(Pb) * N, S.st);
+        CTG_CUDA_CHECK(cudaEventCreateWithFlags(&S.rows_done, cudaEventDisableTiming));
+        CTG_CUDA_CHECK(cudaEventRecord(S.rows_done, S.st));
+      }
+      // exchange: full[h] = send of shard h, on every shard
+      if (comm) {
+        PlanDeviceGuard g(sh[0].device);
+        nccl_check(nccl().AllGather(sh[0].send, sh[0].full, rows_words, ncclUint32, comm->nc, sh[0].st), "ncclAllGather");
+      } else if (local_comms) {
+        nccl_check(nccl().GroupStart(), "ncclGroupStart");
+        for (size_t s = 0; s < sh.size(); ++s)
+          nccl_check(nccl().AllGather(sh[s].send, sh[s].full, rows_words, ncclUint32, (*local_comms)[s], sh[s].st),
+                     "ncclAllGather");
+        nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+      } else {
+        for (auto& S : sh) {
+          PlanDeviceGuard g(S.device);
+          for (auto& H : sh) {
+            CTG_CUDA_CHECK(cudaStreamWaitEvent(S.st, H.rows_done, 0));
+            CTG_CUDA_CHECK(cudaMemcpyPeerAsync(S.full + static_cast<size_t>(H.rank) * rows_words, S.device, H.send,
+                                               H.device, 4 * rows_words, S.st));
+          }
+        }
+      }
+      // K5 of each shard's coefficient block, then the exact limbs to the host [B][D][W]
+      uint32_t* host = nullptr;
+      {
+        PlanDeviceGuard g(sh[0].device);
+        host = context(sh[0].device).pinned_u32(static_cast<size_t>(B) * D * W + 4);
+      }
+      for (auto& S : sh) {
+        PlanDeviceGuard g(S.device);
+        if (S.j1 > S.j0)
+          plan_crt(S.pl.get(), S.full, static_cast<long long>(Pb) * N, Pb, static_cast<long long>(rows_words), S.j0, S.j1,
+                   S.crt, 0, S.st);
+      }
+      auto d2h_block = [&](const Shard& S, const uint32_t* src, int r) {
+        const int j0 = std::min(r * Jb, D), j1 = std::min((r + 1) * Jb, D);
+        if (j1 <= j0) return;
+        const size_t w = static_cast<size_t>(j1 - j0) * W * 4;
+        CTG_CUDA_CHECK(cudaMemcpy2DAsync(host + static_cast<size_t>(j0) * W, static_cast<size_t>(D) * W * 4, src, w, w,
+                                         B, cudaMemcpyDeviceToHost, S.st));
+        stats.d2h_bytes += static_cast<int64_t>(w) * B;
+      };
+      if (comm) {
+        Shard& S = sh[0];
+        PlanDeviceGuard g(S.device);
+        nccl_check(nccl().AllGather(S.crt, S.gath, crt_words, ncclUint32, comm->nc, S.st), "ncclAllGather");
+        for (int r = 0; r < G; ++r) d2h_block(S, S.gath + static_cast<size_t>(r) * crt_words, r);
+      } else {
+        for (auto& S : sh) {
+          PlanDeviceGuard g(S.device);
+          d2h_block(S, S.crt, S.rank);
+        }
+      }
+      uint32_t bits = 0;
+      for (auto& S : sh) {
+        PlanDeviceGuard g(S.device);
+        CTG_CUDA_CHECK(cudaStreamSynchronize(S.st));
+        bits |= plan_error_bits(S.pl.get(), S.st);
+        stats.kernel_launches += S.pl->launches;
+        cudaEventDestroy(S.rows_done);
+        S.rows_done = nullptr;
+      }
+      if (bits) throw ApiError(CTG_INTERNAL, "resultant (sharded): device self-check failed (error bits " + std::to_string(bits) + ")");
+      stats.n_primes = std::max(stats.n_primes, Pn);
+      stats.n_points = N;
+      stats.n_coeffs = D;
+      stats.out_limbs = std::max(stats.out_limbs, sh[0].pl->out_limbs());
+      const ctg_plan* plc = sh[0].pl.get();
+      std::vector<DecodeSize> sz(B);
+      parallel_for(B, [&](int b) { sz[b] = decode_size(plc, host + static_cast<size_t>(b) * D * W); });
+      std::vector<size_t> off(B + 1, 0);
+      for (int b = 0; b < B; ++b) off[b + 1] = off[b] + upoly_block_bytes(sz[b].nc, sz[b].total);
+      UpolyArena arena;
+      arena.create(off[B], B);
+      parallel_for(B, [&](int b) {
+        arena.place(&out[idx[b]], off[b], sz[b].nc, sz[b].total);
+        decode_fill(plc, host + static_cast<size_t>(b) * D * W, sz[b], &out[idx[b]]);
+      });
+      for (auto& S : sh) {  // release on each device
+        PlanDeviceGuard g(S.device);
+        S.pl->pfree(S.send);
+        S.pl->pfree(S.full);
+        S.pl->pfree(S.crt);
+        S.pl->pfree(S.gath);
+        S.pl.reset();
+      }
+    }
+  }
+}
 
 }  // namespace ctg
 
@@ -1001,6 +1255,16 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
     if (!out || !p || !q || batch < 0) throw ApiError(CTG_INVALID, "resultant_batch: bad arguments");
     CallTimer timer;
     for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
+    if (opts && (opts->comm || opts->n_devices > 1)) {  // prime-sharded over several GPUs
+      try {
+        resultant_batch_sharded(batch, p, q, eliminate_x, out, opts);
+      } catch (...) {
+        for (int b = 0; b < batch; ++b) ctg_upoly_free(&out[b]);
+        throw;
+      }
+      timer.finish_total();
+      return;
+    }
     std::vector<Problem> probs(batch);
     auto& st = stats_tls();
     // The device is touched only once a nontrivial problem exists (zero inputs and input
@@ -1097,7 +1361,9 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
             const ChunkNeeds n = chunk_needs(c.pl.get());
             int max_block = 1;
             for (size_t q = 0; q + 1 < bounds.size(); ++q) max_block = std::max(max_block, bounds[q + 1] - bounds[q]);
-            const double f = 0.1 + std::max(1.0, static_cast<double>(max_block) / c.pl->B);
+            // (capped: a first group of one large curve must not reserve max_block times its
+            // needs -- enqueue() regrows the slots when a later chunk does not fit)
+            const double f = 0.1 + std::min(4.0, std::max(1.0, static_cast<double>(max_block) / c.pl->B));
             pl_run.reserve({static_cast<size_t>(f * n.dev), static_cast<size_t>(f * n.in),
                             static_cast<size_t>(f * n.out)});
             reserved = true;

@@ -19,6 +19,7 @@
 // Status codes map to the reference's exceptions: CTG_PRECONDITION -> PreconditionError,
 // anything else -> Error (there is no CPU fallback: a CUDA failure throws).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,6 +40,31 @@ namespace {
 
 void check(ctg_status st, const char* what) {
   if (st != CTG_OK) raise(st, what);
+}
+
+// CTG_DEVICES="0,1,2,3" shards every resultant's primes over those GPUs (ctg_opts.n_devices,
+// one NCCL all-gather of the residues); unset = one device, the library default.
+const ctg_opts* resultant_opts() {
+  static ctg_opts opts{};
+  static std::vector<int32_t> devs;
+  static const ctg_opts* o = [] () -> const ctg_opts* {
+    const char* e = std::getenv("CTG_DEVICES");
+    if (!e || !*e) return nullptr;
+    for (const char* c = e; *c;) {
+      char* end = nullptr;
+      const long v = std::strtol(c, &end, 10);
+      if (end == c) break;
+      devs.push_back(static_cast<int32_t>(v));
+      c = (*end == ',') ? end + 1 : end;
+    }
+    if (devs.size() < 2) return nullptr;
+    opts.device = devs[0];
+    opts.verify = 1;
+    opts.n_devices = static_cast<int32_t>(devs.size());
+    opts.devices = devs.data();
+    return &opts;
+  }();
+  return o;
 }
 
 // Little-endian u32 limbs <-> GMP's limbs.  mpz_import / mpz_export with 4-byte words take a
@@ -151,7 +177,7 @@ UnivariatePolynomial gcd_univariate(const UnivariatePolynomial& p, const Univari
 UnivariatePolynomial resultant(const BivariatePolynomial& p, const BivariatePolynomial& q, Var eliminated) {
   BiMarshal a(p), b(q);
   ctg_upoly_buf out{};
-  check(ctg_resultant(&a.view, &b.view, eliminated == Var::X ? 1 : 0, &out, nullptr), "resultant");
+  check(ctg_resultant(&a.view, &b.view, eliminated == Var::X ? 1 : 0, &out, resultant_opts()), "resultant");
   return take(out);
 }
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
     assert set(declared) == set(P.EXPORTS)
-    assert L.ctg_abi_version() == 1
+    assert L.ctg_abi_version() == 2
 
 
 def test_conventions_without_computation():

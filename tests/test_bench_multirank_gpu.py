@@ -1,7 +1,9 @@
-"""bench.py's multi-rank path (prime sharding, all-gather, rank-block CRT, rank-0 decode and
-its exactness check against the one-shot call) run as 2 torchrun ranks sharing cuda:0 with gloo
-collectives (CTG_BENCH_SIM_GLOO=1): a functional test of the code the driver runs on N GPUs
-with NCCL.  No rank's kernel waits on another rank; the timings are not measurements."""
+"""bench.py's multi-rank path run as 2 torchrun ranks sharing cuda:0 (CTG_BENCH_SIM_GLOO=1):
+the device-resident staged step with gloo collectives, and the e2e through ctg_resultant_batch's
+prime-sharded product path (device-list mode: both shards on cuda:0, exchange by device copies;
+on N real GPUs bench.py passes a ctg_comm and libctg's NCCL does the exchange).  The reference
+digest of seed 1 is checked inside bench.py.  No rank's kernel waits on another rank; the
+timings are not measurements."""
 
 import json
 import os
@@ -24,3 +26,4 @@ def test_two_rank_prime_sharded_bench():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["sample"]["parallelism"] == "prime-shard2"
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["parity"]["sharded_e2e"] == "bit-exact" and 1 in line["parity"]["reference_digests"]

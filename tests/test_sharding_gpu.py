@@ -57,3 +57,50 @@ def test_sharded_pipeline_matches_one_shot(G, kind, a, b):
     dense = sharding.reassemble(gathered, B, D, W, G)
     for bi in range(B):
         assert plan.decode(np.ascontiguousarray(dense[bi])) == want[bi], (G, kind, bi)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_c_abi_device_list_sharding(G):
+    """The product path: ctg_resultant_batch with ctg_opts.n_devices = G (device 0 listed G
+    times: the shards share the GPU and exchange residues by device copies instead of NCCL).
+    Mixed shapes, a zero operand, a degree-0 operand and the d20/64 config (reference-pinned
+    digest of seed 1) must equal the one-device call bit for bit."""
+    import hashlib
+    import json
+    import os
+    pairs = []
+    for s in range(1, 4):
+        f = curves.make("dense", 12, 40, s)
+        pairs.append((f, curves.derive_y(f)))
+    f20 = curves.make("dense", 20, 64, 1)
+    pairs.append((f20, curves.derive_y(f20)))
+    fs = curves.make("sheared", 2, 0, 1)
+    pairs.append((fs, curves.derive_y(fs)))
+    pairs.append(({(1, 1): 3, (0, 0): -1}, {(2, 0): 1, (0, 2): 1, (0, 0): -4}))  # not a derivative pair
+    pairs.append(({(0, 2): 1, (1, 0): -1}, {}))  # one zero operand -> zero polynomial
+    pairs.append(({(0, 0): 5}, {(0, 3): 2, (1, 0): 1}))  # degree-0 operand
+    want = P.resultant_batch(pairs)
+    got = P.resultant_batch(pairs, devices=[0] * G)
+    assert got == want
+    gold = [json.loads(l) for l in open(os.path.join(os.path.dirname(__file__), "golden", "configs_big.jsonl"))]
+    row = next(r for r in gold if r["curve"] == ["dense", 20, 64, 1])
+    assert hashlib.sha256(",".join(format(c, "x") for c in got[3]).encode()).hexdigest() == row["sha256"]
+    st = P.last_call_stats()
+    assert st["kernel_launches"] > 0 and st["d2h_bytes"] > 0
+
+
+def test_c_abi_comm_single_rank():
+    """The multi-process path (ctg_opts.comm: libctg's own NCCL communicator, loaded at run time)
+    with one rank: NCCL all-gathers of the residue rows and of the CRT'd limb blocks are then
+    copies, and the result must equal the plain call.  (N ranks need N GPUs: NCCL refuses two
+    ranks on one device.)"""
+    pairs = []
+    for s in range(1, 4):
+        f = curves.make("dense", 12, 40, s)
+        pairs.append((f, curves.derive_y(f)))
+    pairs.append(({(0, 2): 1, (1, 0): -1}, {}))
+    comm = P.Comm(1, 0, P.Comm.unique_id(), 0)
+    try:
+        assert P.resultant_batch(pairs, comm=comm) == P.resultant_batch(pairs)
+    finally:
+        comm.close()
