@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -381,9 +383,14 @@ struct YunImages {
 };
 
 YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& primes, int device, Launches& L) {
+  using tclk = std::chrono::steady_clock;
+  static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
+  const auto t0 = tclk::now();
   const int n = zdeg(P);
   auto T = get_tables(device, 1, primes);
+  const auto t1 = tclk::now();
   uint32_t* d_tab = reduce_poly(ar, P, *T, L);
+  const auto t2 = tclk::now();
   const int nk = static_cast<int>(primes.size());
   YunImages im;
   im.primes = primes;
@@ -400,7 +407,13 @@ YunImages run_modyun(DevArena& ar, const ZPoly& P, const std::vector<uint32_t>& 
   im.d_deg = d_deg;
   CTG_CUDA_CHECK(cudaMemcpy2DAsync(im.deg.data(), 4 * static_cast<size_t>(n + 1), d_deg, 4 * static_cast<size_t>(n + 1),
                                    8, nk, cudaMemcpyDeviceToHost, ar.st));
+  const auto t3 = tclk::now();
   CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+  if (trace) {
+    auto us = [](tclk::time_point a, tclk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "[ctg] run_modyun n=%d P=%zu: tables %.1f us, reduce(stage+h2d+K1) %.1f us, launch %.1f us, sync %.1f us\n",
+                 n, primes.size(), us(t0, t1), us(t1, t2), us(t2, t3), us(t3, tclk::now()));
+  }
   stats_tls().d2h_bytes += static_cast<int64_t>(8) * nk;
   return im;
 }
