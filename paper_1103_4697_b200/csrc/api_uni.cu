@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <string>
@@ -42,6 +43,7 @@ using ZPoly = std::vector<SBig>;  // low -> high, trimmed
 // Primes of the univariate path: (2^30, 2^30.4), the window where the fused two-elimination
 // pass of blk_gcd (a three-product sum, mmul3) needs one Montgomery reduction.
 std::vector<uint32_t> select_uni_primes(double need_bits) { return select_primes(1, need_bits, kResPrimeMax); }
+constexpr int kProbeMinDeg = 32;  // Yun inputs from this degree get the early square-freeness probe
 
 ZPoly parse_upoly(const ctg_upoly* p) {
   ZPoly out;
@@ -178,28 +180,55 @@ double zlog2_linf(const ZPoly& p) {
   return m;
 }
 
-std::vector<UCoeff> to_ucoeffs(const ZPoly& p) {
-  std::vector<UCoeff> out(p.size());
-  for (size_t i = 0; i < p.size(); ++i) {
-    out[i].sign = static_cast<int8_t>(p[i].sign);
-    out[i].limbs = p[i].mag;
+// Device scratch owned by one call.  Small requests are bump-allocated from a per-thread,
+// per-device slab (tiny gcds -- realroots.cpp:119,136,196 -- are latency-bound and paid ~1-2 us
+// per cudaMallocAsync / cudaFreeAsync pair); arenas nest LIFO and every call of a thread runs
+// on its device's context stream, so a region released here is reused only by work that
+// stream-orders after the work that used it.  Larger requests use the stream-ordered pool.
+struct Slab {
+  uint8_t* base = nullptr;
+  size_t top = 0, cap = 0;
+};
+Slab& tls_slab(int device) {
+  thread_local std::map<int, Slab> slabs;  // process lifetime (one small region per thread and device)
+  Slab& sl = slabs[device];
+  if (!sl.base) {
+    constexpr size_t kSlabBytes = size_t{8} << 20;
+    void* p = nullptr;
+    CTG_CUDA_CHECK(cudaMalloc(&p, kSlabBytes));
+    sl.base = static_cast<uint8_t*>(p);
+    sl.cap = kSlabBytes;
   }
-  return out;
+  return sl;
 }
-
-// Device scratch owned by one call (stream-ordered allocations from the default pool).
 struct DevArena {
   cudaStream_t st;
   std::vector<void*> ptrs;
-  explicit DevArena(cudaStream_t s) : st(s) {}
+  Slab* slab = nullptr;
+  size_t mark = 0;
+  explicit DevArena(cudaStream_t s) : st(s) {
+    int dev = 0;
+    CTG_CUDA_CHECK(cudaGetDevice(&dev));
+    slab = &tls_slab(dev);
+    mark = slab->top;
+  }
+  DevArena(const DevArena&) = delete;
+  DevArena& operator=(const DevArena&) = delete;
   template <class T>
   T* alloc(size_t n) {
+    const size_t bytes = (std::max<size_t>(1, n) * sizeof(T) + 255) & ~static_cast<size_t>(255);
+    if (slab->top + bytes <= slab->cap) {
+      T* p = reinterpret_cast<T*>(slab->base + slab->top);
+      slab->top += bytes;
+      return p;
+    }
     void* p = nullptr;
-    CTG_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(T), st));
+    CTG_CUDA_CHECK(cudaMallocAsync(&p, bytes, st));
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
   ~DevArena() {
+    slab->top = mark;
     for (void* p : ptrs) cudaFreeAsync(p, st);
   }
 };
@@ -250,22 +279,29 @@ struct PinnedStage {
 };
 thread_local PinnedStage tls_stage;
 
-uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
-  const int S = static_cast<int>(p.size());
-  int Lw = 1;
-  for (const auto& c : p) Lw = std::max<int>(Lw, static_cast<int>(c.mag.size()));
+// Several polynomials reduced in ONE staging copy and ONE launch: their coefficients are
+// consecutive slots, so row k of the result holds p_0 | p_1 | ... (pitch = total slots).
+uint32_t* reduce_polys(DevArena& ar, std::initializer_list<const ZPoly*> ps, const CrtTables& tabs, Launches& L) {
+  int S = 0, Lw = 1;
+  for (const ZPoly* p : ps) {
+    S += static_cast<int>(p->size());
+    for (const auto& c : *p) Lw = std::max<int>(Lw, static_cast<int>(c.mag.size()));
+  }
   const size_t nl = static_cast<size_t>(Lw) * S;
   uint8_t* stage = tls_stage.get(4 * nl + S);
   uint32_t* limbs = reinterpret_cast<uint32_t*>(stage);
   int8_t* sign = reinterpret_cast<int8_t*>(stage + 4 * nl);
   // coefficient-major [S][Lw]: one contiguous copy per coefficient (K1 reads either layout)
-  for (int s = 0; s < S; ++s) {
-    sign[s] = static_cast<int8_t>(p[s].sign);
-    const size_t n = p[s].mag.size();
-    uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
-    if (n) std::memcpy(row, p[s].mag.data(), 4 * n);
-    if (n < static_cast<size_t>(Lw)) std::memset(row + n, 0, 4 * (Lw - n));
-  }
+  int s = 0;
+  for (const ZPoly* p : ps)
+    for (const auto& c : *p) {
+      sign[s] = static_cast<int8_t>(c.sign);
+      const size_t n = c.mag.size();
+      uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
+      if (n) std::memcpy(row, c.mag.data(), 4 * n);
+      if (n < static_cast<size_t>(Lw)) std::memset(row + n, 0, 4 * (Lw - n));
+      ++s;
+    }
   uint32_t* d_limbs = ar.alloc<uint32_t>(nl);
   int8_t* d_sign = ar.alloc<int8_t>(S);
   uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
@@ -277,6 +313,10 @@ uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launc
   auto& st = stats_tls();
   st.h2d_bytes += static_cast<int64_t>(4 * nl + S);
   return d_tab;
+}
+
+uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
+  return reduce_polys(ar, {&p}, tabs, L);
 }
 
 // Gather rows `lucky` of d_src (plain residues, pitch src_pitch), scale segment s of row r
@@ -370,6 +410,7 @@ ZPoly slice(const ZPoly& p, int a, int b) {
 // Yun over Z via per-prime Yun (K6) + CRT (K5) + certificate.
 // ---------------------------------------------------------------------------
 struct YunResult {
+  bool squarefree = false;  // certified square-free: the factorization is (P, 1) and sqfp = P (not copied)
   std::vector<std::pair<ZPoly, int>> factors;
   ZPoly sqfp;
 };
@@ -434,7 +475,57 @@ bool certifies_squarefree(const YunImages& im, int n) {
   return false;
 }
 
-YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t st, Launches& L) {
+// Square-freeness probe launched BEFORE the host computes the content (elim.cpp:141-144), so
+// the content gcd (one full-size integer gcd: ~1 ms at d16/1024) overlaps the GPU: for a
+// prime p not dividing lc(R), deg gcd(R mod p, R' mod p) is the same for R and pp(R) = R / c
+// (p | c implies p | lc(R), and such primes report status 1 and certify nothing).
+struct YunProbe {
+  std::unique_ptr<DevArena> ar;
+  std::vector<uint32_t> primes;
+  int n = -1;
+  int32_t* h = nullptr;  // pinned: (status, deg of the multiplicity-1 part) per prime
+  cudaEvent_t done = nullptr;
+  ~YunProbe() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+int32_t* probe_pinned() {
+  thread_local int32_t* buf = nullptr;
+  if (!buf) CTG_CUDA_CHECK(cudaMallocHost(&buf, 64 * sizeof(int32_t)));
+  return buf;
+}
+
+void probe_start(YunProbe& pb, const ZPoly& R, int device, cudaStream_t st, Launches& L) {
+  pb.n = zdeg(R);
+  pb.primes = select_uni_primes(3 * 30.0);
+  pb.ar = std::make_unique<DevArena>(st);
+  DevArena& ar = *pb.ar;
+  const int nk = static_cast<int>(pb.primes.size()), n = pb.n;
+  auto T = get_tables(device, 1, pb.primes);
+  uint32_t* d_tab = reduce_poly(ar, R, *T, L);
+  int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * (n + 1));
+  uint32_t* d_fac = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (2 * n + 2));
+  uint32_t* d_sqf = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (n + 1));
+  const size_t gb = uni_gbuf_bytes(modyun_smem(n), nk);
+  uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+  L.n += launched(launch_modyun(d_tab, n, T->d_pc, nk, d_deg, d_fac, d_sqf, gbuf, ar.st));
+  CTG_CUDA_CHECK(cudaGetLastError());
+  pb.h = probe_pinned();
+  CTG_CUDA_CHECK(cudaMemcpy2DAsync(pb.h, 8, d_deg, 4 * static_cast<size_t>(n + 1), 8, nk, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaEventCreateWithFlags(&pb.done, cudaEventDisableTiming));
+  CTG_CUDA_CHECK(cudaEventRecord(pb.done, ar.st));
+  stats_tls().d2h_bytes += static_cast<int64_t>(8) * nk;
+}
+
+// True if some probe prime certifies the input square-free.
+bool probe_finish(YunProbe& pb) {
+  CTG_CUDA_CHECK(cudaEventSynchronize(pb.done));
+  for (size_t k = 0; k < pb.primes.size(); ++k)
+    if (pb.h[2 * k] == 0 && pb.h[2 * k + 1] == pb.n) return true;
+  return false;
+}
+
+YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t st, Launches& L, bool probed = false) {
   const int n = zdeg(P);
   DevArena ar(st);
   YunResult res;
@@ -445,11 +536,10 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
   // and Yun work of hundreds of primes.
   const Big& lcP = P.back().mag;
   const double need = big_log2(lcP) + n + zlog2_l2(P) + 2 + 40;
-  if (select_uni_primes(need + 62).size() > 148) {
+  if (!probed && select_uni_primes(need + 62).size() > 148) {
     YunImages im = run_modyun(ar, P, select_uni_primes(3 * 30.0), device, L);
     if (certifies_squarefree(im, n)) {
-      res.factors.push_back({P, 1});
-      res.sqfp = P;
+      res.squarefree = true;
       return res;
     }
   }
@@ -459,8 +549,7 @@ YunResult yun_modular(const ZPoly& P, bool want_sqfp, int device, cudaStream_t s
     const int nk = static_cast<int>(primes.size());
     YunImages im = run_modyun(ar, P, primes, device, L);
     if (certifies_squarefree(im, n)) {
-      res.factors.push_back({P, 1});
-      res.sqfp = P;
+      res.squarefree = true;
       return res;
     }
     fetch_patterns(ar, im);
@@ -553,14 +642,16 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
     std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
     auto T = get_tables(device, 1, primes);
-    uint32_t* tA = reduce_poly(ar, A, *T, L);
-    uint32_t* tB = reduce_poly(ar, B, *T, L);
+    // one staging copy, one K1 launch for both operands (tiny gcds are latency-bound)
+    const int pitch_ab = na + nb + 2;
+    uint32_t* tA = reduce_polys(ar, {&A, &B}, *T, L);
+    uint32_t* tB = tA + (na + 1);
     const int pitch = na + nb + 3;
     int32_t* d_deg = ar.alloc<int32_t>(nk);
     uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(nk) * pitch);
     const size_t gb = uni_gbuf_bytes(modgcd_smem(na, nb), nk);
     uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
-    L.n += launched(launch_modgcd(tA, na, tB, nb, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st));
+    L.n += launched(launch_modgcd(tA, na, tB, nb, pitch_ab, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st));
     CTG_CUDA_CHECK(cudaGetLastError());
     std::vector<int32_t> deg(nk);
     CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * nk, cudaMemcpyDeviceToHost, ar.st));
@@ -990,19 +1081,43 @@ void fill_bipoly(const YPoly& f, ctg_bipoly_buf* out) {
   out->limb_off[n] = pos;
 }
 
-void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly, int>>& factors, ctg_sqf_buf* out) {
+// A ZPoly straight into a library buffer (one pass, no per-coefficient staging vectors).
+void fill_upoly_z(const ZPoly& p, ctg_upoly_buf* out) {
+  size_t n = p.size();
+  while (n > 0 && p[n - 1].sign == 0) --n;
+  size_t total = 0;
+  for (size_t i = 0; i < n; ++i) total += p[i].mag.size();
+  upoly_alloc(out, n, total);
+  uint32_t off = 0;
+  for (size_t i = 0; i < n; ++i) {
+    out->sign[i] = static_cast<int8_t>(p[i].sign);
+    out->limb_off[i] = off;
+    if (!p[i].mag.empty()) std::memcpy(out->limbs + off, p[i].mag.data(), 4 * p[i].mag.size());
+    off += static_cast<uint32_t>(p[i].mag.size());
+  }
+  out->limb_off[n] = off;
+}
+
+void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly, int>>& factors, ctg_sqf_buf* out,
+              const ZPoly* single = nullptr) {
   std::memset(out, 0, sizeof(*out));
   out->unit_sign = static_cast<int8_t>(unit.empty() ? 0 : unit_sign);
   out->unit_nlimbs = static_cast<int32_t>(unit.size());
   out->unit_limbs = static_cast<uint32_t*>(std::malloc(4 * std::max<size_t>(1, unit.size())));
   std::memcpy(out->unit_limbs, unit.data(), 4 * unit.size());
-  out->n_factors = static_cast<int32_t>(factors.size());
-  out->mult = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(1, factors.size())));
-  out->factors = static_cast<ctg_upoly_buf*>(std::calloc(std::max<size_t>(1, factors.size()), sizeof(ctg_upoly_buf)));
+  const size_t nf = single ? 1 : factors.size();
+  out->n_factors = static_cast<int32_t>(nf);
+  out->mult = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(1, nf)));
+  out->factors = static_cast<ctg_upoly_buf*>(std::calloc(std::max<size_t>(1, nf), sizeof(ctg_upoly_buf)));
   if (!out->unit_limbs || !out->mult || !out->factors) throw std::bad_alloc();
+  if (single) {  // square-free input: the one factor (multiplicity 1) is the primitive input itself
+    out->mult[0] = 1;
+    fill_upoly_z(*single, &out->factors[0]);
+    return;
+  }
   for (size_t i = 0; i < factors.size(); ++i) {
     out->mult[i] = factors[i].second;
-    fill_upoly(to_ucoeffs(factors[i].first), &out->factors[i]);
+    fill_upoly_z(factors[i].first, &out->factors[i]);
   }
 }
 
@@ -1019,6 +1134,24 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
     CallTimer timer;
     ZPoly a = parse_upoly(p);
     if (a.empty()) throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial");  // elim.cpp:139
+    Launches L;
+    std::unique_ptr<DeviceGuard> g;
+    std::unique_lock<std::mutex> lock;
+    int dev = -1;
+    Ctx* ctx = nullptr;
+    YunProbe probe;
+    // square-freeness probe on the GPU while the host takes the content -- only where
+    // yun_modular would probe too (its full prime set exceeds one wave of CTAs), so a
+    // non-square-free input never pays for it twice
+    const bool probe_first = zdeg(a) >= kProbeMinDeg &&
+                             select_uni_primes(big_log2(a.back().mag) + zdeg(a) + zlog2_l2(a) + 2 + 40 + 62).size() > 148;
+    if (probe_first) {
+      g = std::make_unique<DeviceGuard>(opts);
+      dev = select_device(opts);
+      ctx = &context(dev);
+      lock = std::unique_lock<std::mutex>(ctx->mu);
+      probe_start(probe, a, dev, ctx->stream, L);
+    }
     Big content;
     int s = 0;
     ZPoly P = zprimitive_positive(std::move(a), &content, &s);  // elim.cpp:141-144: unit = sign(lc) * content
@@ -1028,15 +1161,23 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       timer.finish();
       return;
     }
-    DeviceGuard g(opts);
-    const int dev = select_device(opts);
-    Ctx& ctx = context(dev);
-    std::lock_guard<std::mutex> lock(ctx.mu);
-    Launches L;
-    YunResult r = yun_modular(P, false, dev, ctx.stream, L);
+    if (probe.done && probe_finish(probe)) {  // square-free: the factorization is (pp(R), 1)
+      timer.mark_device();
+      stats_tls().kernel_launches = L.n;
+      fill_sqf(content, s, {}, out, &P);
+      timer.finish();
+      return;
+    }
+    if (!ctx) {
+      g = std::make_unique<DeviceGuard>(opts);
+      dev = select_device(opts);
+      ctx = &context(dev);
+      lock = std::unique_lock<std::mutex>(ctx->mu);
+    }
+    YunResult r = yun_modular(P, false, dev, ctx->stream, L, probe_first);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
-    fill_sqf(content, s, r.factors, out);
+    fill_sqf(content, s, r.factors, out, r.squarefree ? &P : nullptr);
     timer.finish();
   });
 }
@@ -1050,7 +1191,7 @@ ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ct
     ZPoly P = zprimitive_positive(std::move(a));
     timer.mark_setup();
     if (zdeg(P) == 0) {  // elim.cpp:207
-      fill_upoly(to_ucoeffs(P), out);
+      fill_upoly_z(P, out);
       timer.finish();
       return;
     }
@@ -1062,7 +1203,7 @@ ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ct
     YunResult r = yun_modular(P, true, dev, ctx.stream, L);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
-    fill_upoly(to_ucoeffs(r.sqfp), out);
+    fill_upoly_z(r.squarefree ? P : r.sqfp, out);
     timer.finish();
   });
 }
@@ -1075,14 +1216,14 @@ ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_
     // elim.cpp:81-85
     if (a.empty() && b.empty()) throw ApiError(CTG_PRECONDITION, "gcd_univariate: both inputs zero");
     if (a.empty() || b.empty()) {
-      fill_upoly(to_ucoeffs(zprimitive_positive(a.empty() ? b : a)), out);
+      fill_upoly_z(zprimitive_positive(a.empty() ? b : a), out);
       timer.finish();
       return;
     }
     ZPoly A = zprimitive_positive(std::move(a)), B = zprimitive_positive(std::move(b));
     timer.mark_setup();
     if (zdeg(A) == 0 || zdeg(B) == 0) {
-      fill_upoly(to_ucoeffs(ZPoly{SBig{1, Big{1u}}}), out);
+      fill_upoly_z(ZPoly{SBig{1, Big{1u}}}, out);
       timer.finish();
       return;
     }
@@ -1094,7 +1235,7 @@ ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_
     ZPoly r = gcd_modular(A, B, dev, ctx.stream, L);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
-    fill_upoly(to_ucoeffs(r), out);
+    fill_upoly_z(r, out);
     timer.finish();
   });
 }

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "internal.hpp"
@@ -33,8 +34,13 @@ __device__ __forceinline__ void swp(uint32_t*& a, uint32_t*& b) {
 // Polynomial buffers of a CTA: shared memory, or (degrees beyond the shared-memory budget)
 // this CTA's slice of a global scratch region -- the kernels use generic pointers, so the
 // same code runs on either (global buffers stay L2-resident: 8 x (n + 2) words per CTA).
+// (Two instantiations of each kernel, GB = false / true: derived from the extern __shared__
+// array the pointers stay in the shared window and compile to LDS / STS; a run-time select
+// between the two would make every access a generic LD / ST -- measured 1.6x slower K6.)
+template <bool GB>
 __device__ __forceinline__ uint32_t* cta_buffers(uint32_t* sm, uint32_t* gbuf, size_t words_per_cta) {
-  return gbuf ? gbuf + static_cast<size_t>(blockIdx.x) * words_per_cta : sm;
+  if constexpr (GB) return gbuf + static_cast<size_t>(blockIdx.x) * words_per_cta;
+  return sm;
 }
 
 // Primes p < kResPrimeMax (2^30.4): the fused pass uses mmul3 (modarith.cuh).
@@ -141,13 +147,14 @@ __device__ void blk_store_plain(uint32_t* dst, const uint32_t* X, int d, const M
 // deg[k][0] = status (0 ok, 1 lc(P) = 0 mod p); the monic factors concatenated in
 // increasing m (deg + 1 words each) at fac[k][...]; the monic square-free part at sqf[k][...].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_modyun(const uint32_t* __restrict__ tab, int n, const PrimeConst* __restrict__ pc,
+template <bool GB>
+__global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab, int n, const PrimeConst* __restrict__ pc,
                                                 int32_t* deg, uint32_t* fac, uint32_t* sqf, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
   const int cap = n + 2;
-  uint32_t* base = cta_buffers(sm, gbuf, 8 * cap);
+  uint32_t* base = cta_buffers<GB>(sm, gbuf, 8 * cap);
   uint32_t* buf[8];
   for (int b = 0; b < 8; ++b) buf[b] = base + b * cap;
   int32_t* dk = deg + static_cast<size_t>(kl) * (n + 1);
@@ -228,18 +235,19 @@ __global__ void __launch_bounds__(256) k_modyun(const uint32_t* __restrict__ tab
 // Row layout (plain residues): g (dg+1) | u (na-dg+1) | w (nb-dg+1).  deg[k] = dg,
 // or -2 if lc(A) or lc(B) vanishes mod p.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_modgcd(const uint32_t* __restrict__ tabA, int na,
-                                                const uint32_t* __restrict__ tabB, int nb,
+template <bool GB>
+__global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tabA, int na,
+                                                const uint32_t* __restrict__ tabB, int nb, int tab_pitch,
                                                 const PrimeConst* __restrict__ pc, int32_t* deg, uint32_t* out,
                                                 int pitch, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
   const int cap = (na > nb ? na : nb) + 2;
-  uint32_t* base = cta_buffers(sm, gbuf, 5 * static_cast<size_t>(cap));
+  uint32_t* base = cta_buffers<GB>(sm, gbuf, 5 * static_cast<size_t>(cap));
   uint32_t *A = base, *B = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap;
-  const uint32_t* ra = tabA + static_cast<size_t>(kl) * (na + 1);
-  const uint32_t* rb = tabB + static_cast<size_t>(kl) * (nb + 1);
+  const uint32_t* ra = tabA + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : na + 1);
+  const uint32_t* rb = tabB + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : nb + 1);
   for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
   for (int i = threadIdx.x; i <= nb; i += blockDim.x) B[i] = Y[i] = rb[i];
   __syncthreads();
@@ -280,6 +288,7 @@ __global__ void k_gather_scale(const uint32_t* __restrict__ src, int src_pitch, 
 // a_j by Horner, then gcd(f(a_j, y), g(a_j, y)) mod p_k runs in shared memory.  deg[unit] is
 // the gcd degree, or -1 when the unit proves nothing (both formal leading y-coefficients
 // vanish at a_j, or an image is identically zero).
+template <bool GB>
 __global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ dir, int nf,
                               int ng, const PrimeConst* __restrict__ pc, int npts, int32_t* __restrict__ deg,
                               uint32_t* gbuf) {
@@ -287,7 +296,7 @@ __global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int
   const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
   const Mod M = load_mod_u(pc[k]);
   const int w = (nf > ng ? nf : ng) + 2;
-  uint32_t* X = cta_buffers(sm, gbuf, 2 * static_cast<size_t>(w));
+  uint32_t* X = cta_buffers<GB>(sm, gbuf, 2 * static_cast<size_t>(w));
   uint32_t* Y = X + w;
   const int32_t *offf = dir, *lenf = dir + nf + 1, *offg = dir + 2 * (nf + 1), *leng = offg + ng + 1;
   // a_j: distinct small integers 2, 3, ... in Montgomery form
@@ -317,6 +326,7 @@ __global__ void k_bigcd_probe(const uint32_t* __restrict__ tab, int S, const int
 // are stored (plain) as h (dg+1) | u (na-dg+1) | w (nb-dg+1) at out[k][j][...], pitch words.
 // deg[k][j] = dg, or -2 when gamma(a) = 0 mod p (then A(a, y) or B(a, y) may drop degree).
 // ---------------------------------------------------------------------------
+template <bool GB>
 __global__ void __launch_bounds__(128) k_bigcd_images(const uint32_t* __restrict__ tab, int S,
                                                       const int32_t* __restrict__ dir, int na, int nb, int gam_off,
                                                       int gam_len, const PrimeConst* __restrict__ pc,
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(128) k_bigcd_images(const uint32_t* __restrict
   const int unit = blockIdx.x, k = unit / npts, j = unit - k * npts;
   const Mod M = load_mod_u(pc[k]);
   const int cap = (na > nb ? na : nb) + 2;
-  uint32_t* base = cta_buffers(sm, gbuf, 5 * static_cast<size_t>(cap));
+  uint32_t* base = cta_buffers<GB>(sm, gbuf, 5 * static_cast<size_t>(cap));
   uint32_t *A = base, *Bv = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap;
   const int32_t *offa = dir, *lena = dir + na + 1, *offb = dir + 2 * (na + 1), *lenb = offb + nb + 1;
   uint32_t av = offs[k] + static_cast<uint32_t>(j);
@@ -375,6 +385,7 @@ __global__ void __launch_bounds__(128) k_bigcd_images(const uint32_t* __restrict
 // spacing j - i (inverses 1..N-1 from a per-CTA table), then Horner with (x - a_i) in place,
 // the growing coefficient array stored reversed in the slots the consumed values free up.
 constexpr int kNewtonCols = 32;
+template <bool GB>
 __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* __restrict__ src, int src_pitch,
                                                                const int32_t* __restrict__ idx,
                                                                const PrimeConst* __restrict__ pc,
@@ -382,7 +393,8 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
                                                                uint32_t* __restrict__ dst, uint32_t* gbuf) {
   extern __shared__ uint32_t smem_[];
   // shared memory, or this CTA's slice of the global scratch (N x 33 words beyond ~227 KB)
-  uint32_t* sm = gbuf ? gbuf + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * N * (kNewtonCols + 1) : smem_;
+  uint32_t* sm = smem_;
+  if constexpr (GB) sm = gbuf + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * N * (kNewtonCols + 1);
   const int k = idx[blockIdx.y];
   const Mod M = load_mod_u(pc[k]);
   const int lane = threadIdx.x, c = blockIdx.x * kNewtonCols + lane;
@@ -444,39 +456,61 @@ size_t smem_or_global(K kern, size_t smem, uint32_t* gbuf) {
 }
 }  // namespace
 
+// CTA size of the per-prime kernels (CTG_UNI_THREADS overrides, for A/B).  k_modyun at n = 870
+// (3 probe primes): 256 threads 277 us, 512 threads 285 us.
+int uni_threads(int n) {
+  static const int forced = std::getenv("CTG_UNI_THREADS") ? std::atoi(std::getenv("CTG_UNI_THREADS")) : 0;
+  if (forced == 128 || forced == 256 || forced == 512) return forced;
+  return 256;  // 512 measured slower at n = 870 (285 vs 277 us)
+}
+
 size_t uni_gbuf_bytes(size_t smem, size_t ctas) { return smem > kUniSmemMax ? smem * ctas : 0; }
 
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
                   uint32_t* sqf, uint32_t* gbuf, cudaStream_t st) {
-  const size_t smem = smem_or_global(k_modyun, modyun_smem(n), gbuf);
+  const size_t smem = smem_or_global(k_modyun<false>, modyun_smem(n), gbuf);
   if (smem == SIZE_MAX) return -1;
-  k_modyun<<<nk, 256, smem, st>>>(tab, n, pc, deg, fac, sqf, smem ? nullptr : gbuf);
+  if (smem)
+    k_modyun<false><<<nk, uni_threads(n), smem, st>>>(tab, n, pc, deg, fac, sqf, nullptr);
+  else
+    k_modyun<true><<<nk, uni_threads(n), 0, st>>>(tab, n, pc, deg, fac, sqf, gbuf);
   return 1;
 }
 
-int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, const PrimeConst* pc, int nk,
-                  int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st) {
-  const size_t smem = smem_or_global(k_modgcd, modgcd_smem(na, nb), gbuf);
+int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, int tab_pitch, const PrimeConst* pc,
+                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st) {
+  const size_t smem = smem_or_global(k_modgcd<false>, modgcd_smem(na, nb), gbuf);
   if (smem == SIZE_MAX) return -1;
-  k_modgcd<<<nk, 256, smem, st>>>(tabA, na, tabB, nb, pc, deg, out, pitch, smem ? nullptr : gbuf);
+  if (smem)
+    k_modgcd<false><<<nk, uni_threads(std::max(na, nb)), smem, st>>>(tabA, na, tabB, nb, tab_pitch, pc, deg, out, pitch,
+                                                                     nullptr);
+  else
+    k_modgcd<true><<<nk, uni_threads(std::max(na, nb)), 0, st>>>(tabA, na, tabB, nb, tab_pitch, pc, deg, out, pitch, gbuf);
   return 1;
 }
 
 int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
                        int nk, int npts, int32_t* deg, uint32_t* gbuf, cudaStream_t st) {
-  const size_t smem = smem_or_global(k_bigcd_probe, bigcd_probe_smem(nf, ng), gbuf);
+  const size_t smem = smem_or_global(k_bigcd_probe<false>, bigcd_probe_smem(nf, ng), gbuf);
   if (smem == SIZE_MAX) return -1;
-  k_bigcd_probe<<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg, smem ? nullptr : gbuf);
+  if (smem)
+    k_bigcd_probe<false><<<nk * npts, 128, smem, st>>>(tab, S, dir, nf, ng, pc, npts, deg, nullptr);
+  else
+    k_bigcd_probe<true><<<nk * npts, 128, 0, st>>>(tab, S, dir, nf, ng, pc, npts, deg, gbuf);
   return 1;
 }
 
 int launch_bigcd_images(const uint32_t* tab, int S, const int32_t* dir, int na, int nb, int gam_off, int gam_len,
                         const PrimeConst* pc, const uint32_t* offs, int nk, int npts, int32_t* deg, uint32_t* out,
                         int pitch, uint32_t* gbuf, cudaStream_t st) {
-  const size_t smem = smem_or_global(k_bigcd_images, modgcd_smem(na, nb), gbuf);
+  const size_t smem = smem_or_global(k_bigcd_images<false>, modgcd_smem(na, nb), gbuf);
   if (smem == SIZE_MAX) return -1;
-  k_bigcd_images<<<nk * npts, 128, smem, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg, out, pitch,
-                                               smem ? nullptr : gbuf);
+  if (smem)
+    k_bigcd_images<false><<<nk * npts, 128, smem, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg,
+                                                        out, pitch, nullptr);
+  else
+    k_bigcd_images<true><<<nk * npts, 128, 0, st>>>(tab, S, dir, na, nb, gam_off, gam_len, pc, offs, npts, deg, out,
+                                                       pitch, gbuf);
   return 1;
 }
 
@@ -484,14 +518,16 @@ int launch_newton_interp(const uint32_t* src, int src_pitch, const int32_t* idx,
                          const uint32_t* offs, int N, int cols, uint32_t* dst, uint32_t* gbuf, int gbuf_rows,
                          cudaStream_t st) {
   if (rows == 0 || cols == 0) return 0;
-  const size_t smem = smem_or_global(k_newton_interp, newton_smem(N), gbuf);
+  const size_t smem = smem_or_global(k_newton_interp<false>, newton_smem(N), gbuf);
   if (smem == SIZE_MAX || (!smem && gbuf_rows < 1)) return -1;
   const int step = smem ? rows : gbuf_rows;  // global scratch: row chunks reuse the same slices
   int launches = 0;
   for (int r0 = 0; r0 < rows; r0 += step) {
     dim3 grid((cols + kNewtonCols - 1) / kNewtonCols, std::min(step, rows - r0));
-    k_newton_interp<<<grid, kNewtonCols, smem, st>>>(src, src_pitch, idx + r0, pc, offs, N, cols, dst,
-                                                     smem ? nullptr : gbuf);
+    if (smem)
+      k_newton_interp<false><<<grid, kNewtonCols, smem, st>>>(src, src_pitch, idx + r0, pc, offs, N, cols, dst, nullptr);
+    else
+      k_newton_interp<true><<<grid, kNewtonCols, 0, st>>>(src, src_pitch, idx + r0, pc, offs, N, cols, dst, gbuf);
     ++launches;
   }
   return launches;

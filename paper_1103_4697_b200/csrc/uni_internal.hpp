@@ -19,8 +19,9 @@ size_t modgcd_smem(int na, int nb);
 size_t bigcd_probe_smem(int nf, int ng);
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
                   uint32_t* sqf, uint32_t* gbuf, cudaStream_t st);
-int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, const PrimeConst* pc, int nk,
-                  int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st);
+// tab_pitch: words between the rows of consecutive primes for both operands (0: na + 1 / nb + 1)
+int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, int tab_pitch, const PrimeConst* pc,
+                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st);
 // Bivariate gcd probe: deg[k * npts + j] = deg gcd(f(a_j, y), g(a_j, y)) mod p_k, or -1.
 // dir = offf[nf+1], lenf[nf+1], offg[ng+1], leng[ng+1] (slot runs in tab, x ascending).
 int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
