@@ -1328,6 +1328,208 @@ void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv) {
   k_twiddles<<<static_cast<unsigned>((total + 255) / 256), 256>>>(d_pc, P, N, d_twinv);
 }
 
+// ---------------------------------------------------------------------------
+// K5 with the carry walk fused into the tcgen05 GEMM epilogue.
+//
+// The unfused CRT wrote one s32 per 8-bit digit (4x the bytes of the result limbs) from the
+// GEMM and read it back in the carry walk.  Here each epilogue thread owns one coefficient
+// (its TMEM lane) and the tile's BN digit columns: it subtracts t M (t = round(sum y_k / p_k),
+// M's byte digits), propagates the carries through its BN digits, and stores BN / 4 finished
+// u32 limbs (transposed through the freed pipeline stages: coalesced row stores straight
+// into the output records) plus a 16-byte summary of its segment: the low 64 bits, whether
+// the limbs above them are all ones / all zeros, and the signed carry out.  k_crt_fixup then
+// chains the segments of a coefficient (a carry in changes a segment only through those
+// summaries: +1 ripples through all-ones limbs, -1 through all-zeros ones), applies the rare
+// ripples, negates negative coefficients (two's complement, warp-parallel) and writes the
+// sign word.  HBM traffic of the stage: residues in, limbs out (+ the limbs of negative
+// coefficients once more), no digit matrix.
+// ---------------------------------------------------------------------------
+constexpr int kCrtMaxTiles = 64;  // segments per coefficient the fixup chains (L8p <= 64 * BN)
+
+template <int BN, int ST>
+__global__ void __launch_bounds__(128)
+    k_gemm_u8_carry(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, CrtParams C) {
+  using namespace tma;
+  extern __shared__ uint8_t smraw[];
+  using SM = Smem<BN, ST>;
+  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~static_cast<uintptr_t>(1023));
+  static_assert(sizeof(sm.a) + sizeof(sm.b) >= 128 * (BN / 4 + 1) * 4, "epilogue staging must fit the stages");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN, ti = blockIdx.x, nt = gridDim.x;
+  const uint32_t tmem = gemm_mainloop<BN, ST>(sm, ta, tb, m0, n0, C.Kp);
+
+  const int nrows = C.B * C.J, OL = C.out_limbs;
+  const int r = m0 + tid;  // this thread's coefficient (TMEM lane = row of the tile)
+  const bool live = r < nrows;
+  const int rc = live ? r : nrows - 1;
+  const int b = rc / C.J, jl = rc - b * C.J;
+  const int nch = (C.P + kCrtChunk - 1) / kCrtChunk;
+  double s = 0;
+  for (int q = 0; q < nch; ++q) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
+  const double tr = rint(s);
+  if (live && ti == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
+  const long long t = static_cast<long long>(tr);
+  constexpr int LW = BN / 4, PITCH = LW + 1;  // limbs per segment, staging pitch (conflict-free)
+  uint32_t* stg = reinterpret_cast<uint32_t*>(sm.a);  // the pipeline stages (a then b, contiguous) are free now
+  const uint4* m8 = reinterpret_cast<const uint4*>(C.M8) + n0 / 4;
+  long long carry = 0;
+  uint64_t low = 0;
+  bool ones = true, zero = true;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0), v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 m = __ldg(&m8[c0 / 4 + q]);
+      // the 4-digit group's value sum_e (C_e - t M_e) 256^e (|C_e| < 2^31: < 2^57) first, off the
+      // carry chain; then ONE dependent 64-bit add and shift per limb
+      const long long g = (static_cast<long long>(static_cast<int>(v[4 * q])) - t * static_cast<long long>(m.x)) +
+                          ((static_cast<long long>(static_cast<int>(v[4 * q + 1])) - t * static_cast<long long>(m.y)) << 8) +
+                          ((static_cast<long long>(static_cast<int>(v[4 * q + 2])) - t * static_cast<long long>(m.z)) << 16) +
+                          ((static_cast<long long>(static_cast<int>(v[4 * q + 3])) - t * static_cast<long long>(m.w)) << 24);
+      const long long x = carry + g;
+      const uint32_t limb = static_cast<uint32_t>(x);
+      carry = x >> 32;
+      const int li = c0 / 4 + q;
+      stg[tid * PITCH + li] = limb;
+      if (li < 2) {
+        low |= static_cast<uint64_t>(limb) << (32 * li);
+      } else {
+        ones = ones && limb == 0xffffffffu;
+        zero = zero && limb == 0u;
+      }
+    }
+  }
+  if (live) {
+    uint4* meta = reinterpret_cast<uint4*>(C.cols);
+    meta[static_cast<size_t>(r) * nt + ti] =
+        make_uint4(static_cast<uint32_t>(low), static_cast<uint32_t>(low >> 32), static_cast<uint32_t>(static_cast<int>(carry)),
+                   (ones ? 1u : 0u) | (zero ? 2u : 0u));
+  }
+  __syncthreads();
+  // coalesced stores: warp w writes rows 32w..32w+31 of the tile, lanes along the limbs
+  const int lim0 = n0 / 4;
+  for (int rr = warp * 32; rr < warp * 32 + 32; ++rr) {
+    const int row = m0 + rr;
+    if (row >= nrows) break;
+    uint32_t* dst = C.out + static_cast<size_t>(row) * (OL + 1) + 1 + lim0;
+    for (int li = lane; li < LW && lim0 + li < OL; li += 32) dst[li] = stg[rr * PITCH + li];
+  }
+  gemm_teardown<BN, ST>(sm, tmem);
+}
+
+// Warp per coefficient: chain the segment summaries, apply ripples, negate, sign word.  Lane i
+// loads segment i's summary; every lane walks the chain redundantly (values by shuffle), and
+// lane i keeps the fix-up of segment i.
+__global__ void __launch_bounds__(128) k_crt_fixup(CrtParams C, int nt, int LW) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= C.B * C.J) return;  // whole warps
+  const int OL = C.out_limbs;
+  const uint4* meta = reinterpret_cast<const uint4*>(C.cols) + static_cast<size_t>(row) * nt;
+  uint32_t* rowp = C.out + static_cast<size_t>(row) * (OL + 1) + 1;
+  // op: 0 none, 1 low limbs changed only, 2 +1 ripple into the upper limbs, 3 -1 ripple,
+  //     4 upper limbs all ones -> zeros, 5 all zeros -> ones
+  int my_op = 0;
+  uint64_t my_low = 0;
+  long long cin = 0;
+  int nonzero = 0;
+  for (int i0 = 0; i0 < nt; i0 += 32) {
+    const uint4 mm = i0 + lane < nt ? meta[i0 + lane] : make_uint4(0, 0, 0, 0);
+    const int nb = min(32, nt - i0);
+    for (int q = 0; q < nb; ++q) {
+      const uint32_t mx = __shfl_sync(0xffffffffu, mm.x, q), my = __shfl_sync(0xffffffffu, mm.y, q);
+      const uint32_t mz = __shfl_sync(0xffffffffu, mm.z, q), mw = __shfl_sync(0xffffffffu, mm.w, q);
+      uint64_t low = (static_cast<uint64_t>(my) << 32) | mx;
+      long long co = static_cast<int>(mz);
+      bool ones = mw & 1u, zero = (mw & 2u) != 0;
+      int op = 0;
+      if (cin != 0) {
+        const uint64_t nl = low + static_cast<uint64_t>(cin);
+        int hi = 0;  // carry out of the low 64 bits: cin > 0 overflows, cin < 0 borrows
+        if (cin > 0 && nl < low) hi = 1;
+        if (cin < 0 && nl > low) hi = -1;
+        low = nl;
+        op = 1;
+        if (hi == 1) {
+          if (ones) {
+            op = 4;
+            co += 1;
+            ones = false;
+            zero = true;
+          } else {
+            op = 2;
+            zero = false;
+          }
+        } else if (hi == -1) {
+          if (zero) {
+            op = 5;
+            co -= 1;
+            zero = false;
+            ones = true;
+          } else {
+            op = 3;
+            ones = false;
+          }
+        }
+      }
+      if (lane == q) {
+        my_op = op;
+        my_low = low;
+      }
+      // limbs >= OL are part of the two's complement chain but not of the record
+      nonzero |= (low != 0 || !zero) ? 1 : 0;
+      cin = co;
+    }
+    // apply this chunk's fix-ups (segments i0 .. i0 + nb - 1), one segment at a time
+    for (int q = 0; q < nb; ++q) {
+      const int op = __shfl_sync(0xffffffffu, my_op, q);
+      if (!op) continue;
+      const uint64_t low = __shfl_sync(0xffffffffu, my_low, q);
+      const int base = (i0 + q) * LW;
+      if (lane < 2 && base + lane < OL) rowp[base + lane] = static_cast<uint32_t>(lane ? low >> 32 : low);
+      if (op == 4 || op == 5) {
+        for (int li = 2 + lane; li < LW && base + li < OL; li += 32) rowp[base + li] = op == 4 ? 0u : 0xffffffffu;
+      } else if (op == 2 || op == 3) {
+        // +1: the lowest upper limb != all-ones gets +1, the ones below it become 0 (-1: mirrored)
+        const uint32_t stop = op == 2 ? 0xffffffffu : 0u;
+        for (int l0 = 2; l0 < LW; l0 += 32) {
+          const int li = l0 + lane;
+          const bool in = li < LW && base + li < OL;
+          const uint32_t x = in ? rowp[base + li] : stop;
+          const unsigned hit = __ballot_sync(0xffffffffu, in && x != stop);
+          const int z = hit ? __ffs(hit) - 1 : 32;
+          if (in && lane <= z) rowp[base + li] = lane == z ? (op == 2 ? x + 1u : x - 1u) : ~stop;
+          if (hit) break;
+        }
+      }
+    }
+  }
+  const int neg = cin < 0 ? 1 : 0;  // |V| < M / 2 fits the record: the final carry is 0 or -1
+  __syncwarp();
+  if (neg) {  // two's complement: zeros below the lowest nonzero limb, -limb there, ~limb above
+    bool seen = false;
+    for (int w0 = 0; w0 < OL; w0 += 32) {
+      const int w = w0 + lane;
+      const uint32_t x = w < OL ? rowp[w] : 0u;
+      uint32_t y = ~x;
+      if (!seen) {
+        const unsigned nz = __ballot_sync(0xffffffffu, x != 0u);
+        if (nz) {
+          const int z = __ffs(nz) - 1;
+          y = lane < z ? 0u : (lane == z ? 0u - x : ~x);
+          seen = true;
+        } else {
+          y = 0u;
+        }
+      }
+      if (w < OL) rowp[w] = y;
+    }
+  }
+  if (lane == 0) rowp[-1] = static_cast<uint32_t>(neg ? -1 : (nonzero ? 1 : 0));
+}
+
 // 2D u8 tensor map (K-major rows of `kbytes` bytes), SWIZZLE_128B boxes of 128 B x box_rows.
 static bool make_u8_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kbytes, uint32_t box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -1366,11 +1568,49 @@ static bool launch_gemm_tma(const CrtParams& cp, cudaStream_t st) {
   return true;
 }
 
+// prep_t -> tcgen05 GEMM with the carry in its epilogue -> k_crt_fixup (false: not applicable).
+// Two pipeline stages (96 / 64 KB of shared memory: 2 / 3 CTAs per SM, so one CTA's serial
+// carry epilogue overlaps another's TMA + MMA) unless CTG_CRT_STAGES=4.
+template <int BN, int ST>
+static bool launch_crt_fused_st(const CrtParams& cp, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb,
+                                int nt) {
+  static const bool attr = [] {
+    return cudaFuncSetAttribute(k_gemm_u8_carry<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(tma::smem_bytes<BN, ST>())) == cudaSuccess;
+  }();
+  if (!attr) return false;
+  k_gemm_u8_carry<BN, ST><<<dim3(nt, static_cast<unsigned>(cp.Rp / tma::kBM)), 128, tma::smem_bytes<BN, ST>(), st>>>(
+      ta, tb, cp);
+  return true;
+}
+
+template <int BN>
+static bool launch_crt_fused(const CrtParams& cp, cudaStream_t st) {
+  const int nt = cp.L8p / BN;
+  if (cp.L8p % BN || nt > kCrtMaxTiles) return false;
+  CUtensorMap ta, tb;
+  const uint64_t rows = static_cast<uint64_t>(cp.Rp);
+  if (!make_u8_map(&ta, cp.Y, rows, cp.Kp, tma::kBM) || !make_u8_map(&tb, cp.Bt8, cp.L8p, cp.Kp, BN)) return false;
+  static const int stages = std::getenv("CTG_CRT_STAGES") ? std::atoi(std::getenv("CTG_CRT_STAGES")) : 2;
+  const bool ok = stages == 4 ? launch_crt_fused_st<BN, 4>(cp, st, ta, tb, nt) : launch_crt_fused_st<BN, 2>(cp, st, ta, tb, nt);
+  if (!ok) return false;
+  const long long coeffs = static_cast<long long>(cp.J) * cp.B;
+  k_crt_fixup<<<static_cast<unsigned>((coeffs * 32 + 127) / 128), 128, 0, st>>>(cp, nt, BN / 4);
+  return true;
+}
+
 int launch_crt(const CrtParams& cp, cudaStream_t st) {
   if (cp.J == 0 || cp.B == 0) return 0;
   const int nch = (cp.P + kCrtChunk - 1) / kCrtChunk;
   if (cp.use_i8) {
     k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
+    // Default: the carry fused into the tcgen05 GEMM's epilogue (any K).  CTG_CRT_UNFUSED=1:
+    // the r1 path (digit matrix to HBM, then the carry walk) for A/B.
+    static const bool unfused = std::getenv("CTG_CRT_UNFUSED") && std::getenv("CTG_CRT_UNFUSED")[0] == '1';
+    static const int bn_forced = std::getenv("CTG_CRT_BN") ? std::atoi(std::getenv("CTG_CRT_BN")) : 0;  // A/B
+    const bool bn256 = bn_forced ? bn_forced == 256 && cp.L8p % 256 == 0 : (cp.L8p % 256 == 0 && cp.L8p / 256 >= 2);
+    if (!unfused && (bn256 ? launch_crt_fused<256>(cp, st) : launch_crt_fused<128>(cp, st)))
+      return 3;
     // Long K (>= 8 stages): TMA + tcgen05; short K: the mma.sync kernel has less fixed cost.
     bool done = false;
     if (cp.Kp >= 1024) done = (cp.L8p % 256 == 0) ? launch_gemm_tma<256>(cp, st) : launch_gemm_tma<128>(cp, st);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Prime tables: Montgomery constants, roots of unity (for the NTT size N) and the
 // fixed-point CRT constants: (M/p_k)^{-1} mod p_k, 1/p_k and the digits of M/p_k in two
 // layouts -- 16-bit digits for the IMAD GEMM, and the byte-sliced, shift-expanded
@@ -46,7 +47,8 @@ std::shared_ptr<CrtTables> build_tables(int device, const std::vector<uint32_t>&
   T->use_i8 = P <= kI8MaxPrimes;
   std::vector<PrimeConst> pc(P);
   std::vector<double> minv(P);
-  std::vector<uint32_t> Mk16(static_cast<size_t>(P) * T->L16, 0u), M16(T->L16, 0u), M8(T->L8, 0u);
+  std::vector<uint32_t> Mk16(static_cast<size_t>(P) * T->L16, 0u), M16(T->L16, 0u),
+      M8(std::max(T->L8, T->L8p), 0u);  // zero-padded to L8p: the fused CRT epilogue reads whole tiles
   std::vector<uint8_t> Bt8;
   if (T->use_i8) Bt8.assign(static_cast<size_t>(T->L8p) * T->Kp, 0u);
   for (int l = 0; l < T->LM; ++l) {

@@ -181,3 +181,36 @@ def test_prime_window_extension():
         x0 = rng.randrange(Q61)
         av, bv = _upoly_eval(a, x0, Q61), _upoly_eval(b, x0, Q61)
         assert _upoly_eval(R, x0, Q61) == (4 * bv - av * av) % Q61
+
+
+def test_crt_carry_chain_patterns():
+    """Coefficients whose two's complement has long runs of zeros / ones across the fused CRT
+    epilogue's segments (K5: tcgen05 GEMM + carry in the epilogue + k_crt_fixup): powers of two,
+    2^k - 1, small values and zeros make the segment carries ripple (+1 through all-ones
+    limbs, -1 through all-zeros limbs).  R = 4 b exactly for f = y^2 + b(x)."""
+    vals = []
+    for k in (31, 32, 63, 64, 65, 1000, 2047, 2048, 2049, 4000, 6143, 6144):
+        vals += [2**k, -(2**k), 2**k - 1, -(2**k - 1), 2**k + 1, 3 * 2**k]
+    vals += [0, 1, -1, 2, -5, 2**6000 - 2**3000, -(2**6000) + 2**64]
+    b = vals + [1]
+    f = {(0, 2): 1}
+    for i, c in enumerate(b):
+        if c:
+            f[(i, 0)] = c
+    R = P.resultant(f, curves.derive_y(f))
+    want = [4 * c for c in b]
+    while want and want[-1] == 0:
+        want.pop()
+    assert R == want
+    # the same coefficients in a 16-curve batch (multi-tile rows of many curves)
+    rng = random.Random(6144)
+    pairs, wants = [], []
+    for _ in range(16):
+        bb = vals[:]
+        rng.shuffle(bb)
+        bb.append(7)
+        g = {(0, 2): 1}
+        g.update({(i, 0): c for i, c in enumerate(bb) if c})
+        pairs.append((g, curves.derive_y(g)))
+        wants.append([4 * c for c in bb])
+    assert P.resultant_batch(pairs) == wants
