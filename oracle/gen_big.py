@@ -29,7 +29,7 @@ import make_golden as mg  # noqa: E402
 from paper_1103_4697_b200 import curves  # noqa: E402
 
 # (kind, a, b, seed, with_yun, est_seconds)   est = build-container seconds per curve
-PLAN = ([("dense", 30, 128, s, False, 1700) for s in range(2, 17)]
+PLAN = ([("dense", 30, 128, s, False, 1700) for s in range(2, 65)]
         + [("dense", 16, 1024, s, False, 290) for s in range(2, 9)]
         + [("dense", 20, 64, s, False, 28) for s in range(2, 65)]
         + [("sheared", 3, 0, s, True, 35) for s in range(2, 6)]

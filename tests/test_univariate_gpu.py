@@ -65,13 +65,14 @@ def _digest(coeffs):
     return hashlib.sha256(",".join(format(c, "x") for c in coeffs).encode()).hexdigest()
 
 
-def test_yun_sheared_k3_digest():
-    rows = [r for r in load("configs_big.jsonl") if r["curve"][0] == "sheared"]
-    if not rows:
-        pytest.skip("no sheared fixture")
-    row = rows[0]
+@pytest.mark.parametrize("row", [r for r in load("configs_big.jsonl") if r["curve"][0] == "sheared"],
+                         ids=lambda r: "_".join(map(str, r["curve"])))
+def test_yun_sheared_digest(row):
+    """The singular family (BASELINE configs[3], sheared K = 3 seeds 1-5 and K = 2 seeds 3-5):
+    R and its Yun factors (many high-multiplicity roots) against the reference's digests."""
     f = curves.make(*row["curve"])
     R = P.resultant(f, curves.derive_y(f))
+    assert _digest(R) == row["sha256"]
     unit, factors = P.yun_squarefree(R)
     assert format(unit, "x") == row["yun_unit"]
     got = [{"mult": m, "deg": len(p) - 1, "sha256": _digest(p)} for p, m in factors]
