@@ -1606,7 +1606,15 @@ int launch_crt(const CrtParams& cp, cudaStream_t st) {
     k_crt_prep_t<<<dim3((cp.J + 31) / 32, nch, cp.B), dim3(32, 8), 0, st>>>(cp);
     // Default: the carry fused into the tcgen05 GEMM's epilogue (any K).  CTG_CRT_UNFUSED=1:
     // the r1 path (digit matrix to HBM, then the carry walk) for A/B.
-    static const bool unfused = std::getenv("CTG_CRT_UNFUSED") && std::getenv("CTG_CRT_UNFUSED")[0] == '1';
+    static const bool unfused_forced = std::getenv("CTG_CRT_UNFUSED") && std::getenv("CTG_CRT_UNFUSED")[0] == '1';
+    // Few coefficients (single-curve calls: 871 at d30): the fused GEMM has only ~30 CTAs for
+    // its serial epilogues, where the unfused GEMM + warp-per-coefficient carry is faster
+    // (d30, one curve: 38 vs 30 us); batches take the fused path.
+    static const long long fused_min = [] {
+      const char* e = std::getenv("CTG_CRT_FUSED_MIN");
+      return e ? std::atoll(e) : 4737LL;
+    }();
+    const bool unfused = unfused_forced || static_cast<long long>(cp.J) * cp.B < fused_min;
     static const int bn_forced = std::getenv("CTG_CRT_BN") ? std::atoi(std::getenv("CTG_CRT_BN")) : 0;  // A/B
     const bool bn256 = bn_forced ? bn_forced == 256 && cp.L8p % 256 == 0 : (cp.L8p % 256 == 0 && cp.L8p / 256 >= 2);
     if (!unfused && (bn256 ? launch_crt_fused<256>(cp, st) : launch_crt_fused<128>(cp, st)))
