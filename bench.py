@@ -325,6 +325,7 @@ def main_ours(args):
                            "gpu_launches": x["gpu_launches"], "clocks": x["clocks"], "parity": x["parity"]}
     if rank == 0 and G == 1 and not args.no_headline:
         line["yun"] = yun_line(P, curves, args.workload)
+        line["yun"]["batch"] = yun_batch_line(P, curves, args.workload, args.batch)
     if rank == 0 and G == 1:
         cb = None if args.no_cpu_baseline else cpu_baseline(args.workload, m["units_per_curve"])
         line["cpu_baseline"] = cb
@@ -550,6 +551,24 @@ def yun_line(P, curves, workload):
                      "kernel_launches": P.last_call_stats()["kernel_launches"]}
     out["sheared_k3"]["reference_cpu_s"] = 29.2  # SURVEY §6.2, oracle/_ref in the build container
     return out
+
+
+def yun_batch_line(P, curves, workload, B):
+    """Yun of every R of the workload's batch through ctg_yun_squarefree_batch (CurveContext
+    over many curves: one probe launch for all, contents on the host meanwhile)."""
+    kind, a, b, _, _ = WORKLOADS[workload]
+    pairs = [(f, curves.derive_y(f)) for f in (curves.make(kind, a, b, s) for s in range(1, B + 1))]
+    hb = P.HostUpolyBatch(P.resultant_batch(pairs))
+    P.yun_squarefree_batch(hb, raw=True)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        pats = P.yun_squarefree_batch(hb, raw=True)
+        ts.append(1e3 * (time.perf_counter() - t0))
+    ms = statistics.median(ts)
+    return {"curves": B, "ms_median": ms, "ms_per_curve": ms / B,
+            "path": "ctg_yun_squarefree_batch (C ABI), host CSR limbs in/out",
+            "square_free": sum(1 for p in pats if len(p) == 1 and p[0][1] == 1)}
 
 
 def cpu_baseline(workload, units_per_curve):

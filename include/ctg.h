@@ -130,6 +130,10 @@ ctg_status ctg_resultant(const ctg_bipoly* p, const ctg_bipoly* q, int32_t elimi
 ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_opts* opts);
 ctg_status ctg_gcd_univariate(const ctg_upoly* p, const ctg_upoly* q, ctg_upoly_buf* out,
                               const ctg_opts* opts);
+/* yun_squarefree over a batch (CurveContext over many curves, lift.cpp:67): one K1 launch and
+ * one square-freeness probe launch for all inputs, contents on the host meanwhile; inputs the
+ * probe does not certify go through ctg_yun_squarefree's path.  out[b] = Yun(p[b]) exactly. */
+ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_buf* out, const ctg_opts* opts);
 ctg_status ctg_square_free_part(const ctg_upoly* p, ctg_upoly_buf* out, const ctg_opts* opts);
 /* gcd_bivariate (elim.cpp:178-202): y-contents by GPU univariate gcds, then a GPU probe of
  * gcd(f(a, y), g(a, y)) mod p at several (p, a) with lc_y(f)(a) or lc_y(g)(a) nonzero mod p.

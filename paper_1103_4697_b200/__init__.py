@@ -114,6 +114,7 @@ EXPORTS = (
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
     "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch", "ctg_gcd_bivariate", "ctg_bipoly_free",
     "ctg_comm_unique_id", "ctg_comm_init_rank", "ctg_comm_destroy", "ctg_comm_all_gather",
+    "ctg_yun_squarefree_batch",
 )
 
 _lib = None
@@ -169,6 +170,7 @@ def lib():
         L.ctg_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.ctg_plan_launches.argtypes = [C.c_void_p]
         L.ctg_plan_destroy.argtypes = [C.c_void_p]
+        L.ctg_yun_squarefree_batch.argtypes = [C.c_int32, C.POINTER(_Upoly), C.POINTER(_SqfBuf), C.POINTER(_Opts)]
         L.ctg_comm_unique_id.argtypes = [C.c_void_p]
         L.ctg_comm_init_rank.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
         L.ctg_comm_destroy.argtypes = [C.c_void_p]
@@ -471,6 +473,43 @@ def yun_squarefree(p: list, device=None):
         return unit, factors
     finally:
         lib().ctg_sqf_free(C.byref(out))
+
+
+def _decode_sqf(out):
+    unit = 0
+    if out.unit_nlimbs:
+        limbs = np.ctypeslib.as_array(out.unit_limbs, shape=(out.unit_nlimbs,))
+        unit = int.from_bytes(limbs.tobytes(), "little")
+    unit = -unit if out.unit_sign < 0 else unit
+    return unit, [(_decode_buf(out.factors[i]), int(out.mult[i])) for i in range(out.n_factors)]
+
+
+class HostUpolyBatch:
+    """Caller-owned host operands of a batch of univariate inputs (array of ctg_upoly)."""
+
+    def __init__(self, polys):
+        self.hs = [HostUpoly(p) for p in polys]
+        self.n = len(self.hs)
+        self.arr = (_Upoly * max(1, self.n))(*[h.struct for h in self.hs])
+
+
+def yun_squarefree_batch(polys, device=None, raw=False):
+    """[yun_squarefree(p) for p in polys] through ctg_yun_squarefree_batch (one probe launch for
+    all inputs).  `polys` may be a HostUpolyBatch (pre-marshaled).  raw=True: (degree,
+    multiplicity) patterns only, without decoding the factors."""
+    hb = polys if isinstance(polys, HostUpolyBatch) else HostUpolyBatch(polys)
+    n, arr = hb.n, hb.arr
+    outs = (_SqfBuf * max(1, n))()
+    o = _opts(device)
+    _check(lib().ctg_yun_squarefree_batch(n, arr, outs, C.byref(o)), "yun_squarefree_batch")
+    try:
+        if raw:
+            return [[(int(outs[b].factors[i].n_coeffs) - 1, int(outs[b].mult[i])) for i in range(outs[b].n_factors)]
+                    for b in range(n)]
+        return [_decode_sqf(outs[b]) for b in range(n)]
+    finally:
+        for b in range(n):
+            lib().ctg_sqf_free(C.byref(outs[b]))
 
 
 def gcd_univariate(p: list, q: list, device=None) -> list:

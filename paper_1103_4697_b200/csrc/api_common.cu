@@ -270,20 +270,28 @@ class Pool {
 };
 }  // namespace
 
+// Set while a thread runs items of a parallel_for: a nested parallel_for (e.g. a content gcd
+// inside a batch's per-input work) runs inline instead of re-entering the pool (whose one-job-
+// at-a-time lock would deadlock).
+static thread_local bool tls_in_parallel_for = false;
+
 void parallel_for(int n, const std::function<void(int)>& fn) {
-  if (n <= 1) {
-    if (n == 1) fn(0);
+  if (n <= 1 || tls_in_parallel_for) {
+    for (int i = 0; i < n; ++i) fn(i);
     return;
   }
   static Pool pool;
   // Exceptions are captured per index and the first one rethrown on the caller's thread.
   std::vector<std::exception_ptr> errs(n);
   pool.run(n, [&](int i) {
+    const bool outer = tls_in_parallel_for;
+    tls_in_parallel_for = true;
     try {
       fn(i);
     } catch (...) {
       errs[i] = std::current_exception();
     }
+    tls_in_parallel_for = outer;
   });
   for (auto& e : errs)
     if (e) std::rethrow_exception(e);

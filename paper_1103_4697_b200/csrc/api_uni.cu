@@ -281,7 +281,8 @@ thread_local PinnedStage tls_stage;
 
 // Several polynomials reduced in ONE staging copy and ONE launch: their coefficients are
 // consecutive slots, so row k of the result holds p_0 | p_1 | ... (pitch = total slots).
-uint32_t* reduce_polys(DevArena& ar, std::initializer_list<const ZPoly*> ps, const CrtTables& tabs, Launches& L) {
+template <class List>
+uint32_t* reduce_polys(DevArena& ar, const List& ps, const CrtTables& tabs, Launches& L) {
   int S = 0, Lw = 1;
   for (const ZPoly* p : ps) {
     S += static_cast<int>(p->size());
@@ -291,17 +292,22 @@ uint32_t* reduce_polys(DevArena& ar, std::initializer_list<const ZPoly*> ps, con
   uint8_t* stage = tls_stage.get(4 * nl + S);
   uint32_t* limbs = reinterpret_cast<uint32_t*>(stage);
   int8_t* sign = reinterpret_cast<int8_t*>(stage + 4 * nl);
-  // coefficient-major [S][Lw]: one contiguous copy per coefficient (K1 reads either layout)
-  int s = 0;
+  // coefficient-major [S][Lw]: one contiguous copy per coefficient (K1 reads either layout),
+  // filled in parallel over blocks of 64 slots (a batch stages tens of MB)
+  std::vector<const SBig*> slot;
+  slot.reserve(S);
   for (const ZPoly* p : ps)
-    for (const auto& c : *p) {
+    for (const auto& c : *p) slot.push_back(&c);
+  parallel_for((S + 63) / 64, [&](int blk) {
+    for (int s = blk * 64; s < std::min(S, blk * 64 + 64); ++s) {
+      const SBig& c = *slot[s];
       sign[s] = static_cast<int8_t>(c.sign);
       const size_t n = c.mag.size();
       uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
       if (n) std::memcpy(row, c.mag.data(), 4 * n);
       if (n < static_cast<size_t>(Lw)) std::memset(row + n, 0, 4 * (Lw - n));
-      ++s;
     }
+  });
   uint32_t* d_limbs = ar.alloc<uint32_t>(nl);
   int8_t* d_sign = ar.alloc<int8_t>(S);
   uint32_t* d_tab = ar.alloc<uint32_t>(static_cast<size_t>(tabs.P) * S);
@@ -316,7 +322,7 @@ uint32_t* reduce_polys(DevArena& ar, std::initializer_list<const ZPoly*> ps, con
 }
 
 uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
-  return reduce_polys(ar, {&p}, tabs, L);
+  return reduce_polys(ar, std::initializer_list<const ZPoly*>{&p}, tabs, L);
 }
 
 // Gather rows `lucky` of d_src (plain residues, pitch src_pitch), scale segment s of row r
@@ -644,7 +650,7 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
     auto T = get_tables(device, 1, primes);
     // one staging copy, one K1 launch for both operands (tiny gcds are latency-bound)
     const int pitch_ab = na + nb + 2;
-    uint32_t* tA = reduce_polys(ar, {&A, &B}, *T, L);
+    uint32_t* tA = reduce_polys(ar, std::initializer_list<const ZPoly*>{&A, &B}, *T, L);
     uint32_t* tB = tA + (na + 1);
     const int pitch = na + nb + 3;
     int32_t* d_deg = ar.alloc<int32_t>(nk);
@@ -1178,6 +1184,113 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
     fill_sqf(content, s, r.factors, out, r.squarefree ? &P : nullptr);
+    timer.finish();
+  });
+}
+
+// Throughput form of yun_squarefree (CurveContext over many curves): ONE K1 launch reduces every
+// input modulo the 3 probe primes, ONE k_sqf_probe launch runs gcd(P, P') mod p for every
+// (input, prime) pair in parallel, and the host takes the contents meanwhile (parallel_for).
+// Inputs certified square-free return (sgn * content, [(pp, 1)]); the rest go through the
+// single-input path.  Results are identical to calling ctg_yun_squarefree on each input.
+ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_buf* out, const ctg_opts* opts) {
+  return guarded([&] {
+    if (!out || !p || batch < 0) throw ApiError(CTG_INVALID, "yun_squarefree_batch: bad arguments");
+    CallTimer timer;
+    for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
+    std::vector<ZPoly> a(batch);
+    parallel_for(batch, [&](int b) { a[b] = parse_upoly(&p[b]); });
+    for (int b = 0; b < batch; ++b)
+      if (a[b].empty())
+        throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial (batch entry " + std::to_string(b) + ")");
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    Launches L;
+    // probe every input of degree >= 2 (one table, one launch)
+    std::vector<int> idx;
+    std::vector<int32_t> off, degs;
+    std::vector<const ZPoly*> polys;
+    int S = 0, maxd = 0;
+    for (int b = 0; b < batch; ++b)
+      if (zdeg(a[b]) >= 2) {
+        idx.push_back(b);
+        off.push_back(S);
+        degs.push_back(zdeg(a[b]));
+        polys.push_back(&a[b]);
+        S += static_cast<int>(a[b].size());
+        maxd = std::max(maxd, zdeg(a[b]));
+      }
+    const int np = static_cast<int>(idx.size());
+    const std::vector<uint32_t> primes = select_uni_primes(3 * 30.0);
+    const int nk = static_cast<int>(primes.size());
+    DevArena ar(ctx.stream);
+    thread_local int32_t* h_out = nullptr;
+    thread_local size_t h_cap = 0;
+    cudaEvent_t done = nullptr;
+    if (np) {
+      auto T = get_tables(dev, 1, primes);
+      uint32_t* d_tab = reduce_polys(ar, polys, *T, L);
+      int32_t* d_meta = ar.alloc<int32_t>(2 * static_cast<size_t>(np));
+      int32_t* d_out = ar.alloc<int32_t>(2 * static_cast<size_t>(np) * nk);
+      std::vector<int32_t> meta(off);
+      meta.insert(meta.end(), degs.begin(), degs.end());
+      CTG_CUDA_CHECK(cudaMemcpyAsync(d_meta, meta.data(), 4 * meta.size(), cudaMemcpyHostToDevice, ar.st));
+      const size_t gb = uni_gbuf_bytes(sqf_probe_smem(maxd), static_cast<size_t>(np) * nk);
+      uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+      L.n += launched(launch_sqf_probe(d_tab, S, d_meta, d_meta + np, np, nk, T->d_pc, maxd, d_out, gbuf, ar.st));
+      CTG_CUDA_CHECK(cudaGetLastError());
+      const size_t need = 2 * static_cast<size_t>(np) * nk;
+      if (h_cap < need) {
+        if (h_out) cudaFreeHost(h_out);
+        h_out = nullptr;
+        CTG_CUDA_CHECK(cudaMallocHost(&h_out, 4 * need));
+        h_cap = need;
+      }
+      CTG_CUDA_CHECK(cudaMemcpyAsync(h_out, d_out, 4 * need, cudaMemcpyDeviceToHost, ar.st));
+      CTG_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      CTG_CUDA_CHECK(cudaEventRecord(done, ar.st));
+      stats_tls().d2h_bytes += static_cast<int64_t>(4 * need);
+    }
+    // contents on the host while the GPU probes (elim.cpp:141-144)
+    std::vector<Big> content(batch);
+    std::vector<int> sgn(batch, 0);
+    std::vector<ZPoly> P(batch);
+    parallel_for(batch, [&](int b) { P[b] = zprimitive_positive(std::move(a[b]), &content[b], &sgn[b]); });
+    timer.mark_setup();
+    std::vector<char> sqfree(batch, 0);
+    if (done) {
+      CTG_CUDA_CHECK(cudaEventSynchronize(done));
+      cudaEventDestroy(done);
+      for (int q = 0; q < np; ++q)
+        for (int k = 0; k < nk; ++k) {
+          const int32_t* o = h_out + 2 * (static_cast<size_t>(q) * nk + k);
+          if (o[0] == 0 && o[1] == 0) sqfree[idx[q]] = 1;
+        }
+    }
+    timer.mark_device();
+    try {
+      // certified / constant inputs: fill the outputs in parallel; the rest one by one
+      parallel_for(batch, [&](int b) {
+        if (zdeg(P[b]) == 0)  // elim.cpp:145
+          fill_sqf(content[b], sgn[b], {}, &out[b]);
+        else if (sqfree[b])
+          fill_sqf(content[b], sgn[b], {}, &out[b], &P[b]);
+      });
+      for (int b = 0; b < batch; ++b) {
+        if (zdeg(P[b]) == 0 || sqfree[b]) {
+          continue;
+        } else {
+          YunResult r = yun_modular(P[b], false, dev, ctx.stream, L);
+          fill_sqf(content[b], sgn[b], r.factors, &out[b], r.squarefree ? &P[b] : nullptr);
+        }
+      }
+    } catch (...) {
+      for (int b = 0; b < batch; ++b) ctg_sqf_free(&out[b]);
+      throw;
+    }
+    stats_tls().kernel_launches = L.n;
     timer.finish();
   });
 }

@@ -231,6 +231,42 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
 }
 
 // ---------------------------------------------------------------------------
+// Batched square-freeness probe (ctg_yun_squarefree_batch): CTA per (problem i, prime k);
+// problem i's residues mod p_k are slots [off[i], off[i] + n_i] of row k (pitch S) of one K1
+// table.  out[2 (i nk + k)] = status (0 ok, 1 lc(P) = 0 mod p), out[+1] = deg gcd(P, P') mod p.
+// Two polynomial buffers of cap words (the largest degree + 2).
+// ---------------------------------------------------------------------------
+template <bool GB>
+__global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ off,
+                                                   const int32_t* __restrict__ degs, int nk,
+                                                   const PrimeConst* __restrict__ pc, int cap, int32_t* out,
+                                                   uint32_t* gbuf) {
+  extern __shared__ uint32_t sm[];
+  const int i = blockIdx.x / nk, k = blockIdx.x % nk;
+  const int n = degs[i];
+  const Mod M = load_mod_u(pc[k]);
+  uint32_t* X = cta_buffers<GB>(sm, gbuf, 2 * static_cast<size_t>(cap));
+  uint32_t* Y = X + cap;
+  const uint32_t* row = tab + static_cast<size_t>(k) * S + off[i];
+  for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = row[t];
+  __syncthreads();
+  int32_t* o = out + 2 * (static_cast<size_t>(i) * nk + k);
+  if (X[n] == 0u) {
+    if (threadIdx.x == 0) {
+      o[0] = 1;
+      o[1] = -1;
+    }
+    return;
+  }
+  blk_derivative(Y, X, n, M);  // deg n - 1 exactly (p > n, lc != 0)
+  const int dg = blk_gcd(X, n, Y, n - 1, M);
+  if (threadIdx.x == 0) {
+    o[0] = 0;
+    o[1] = dg;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // gcd modulo p with cofactors: g = monic gcd(A, B), u = A / g, w = B / g.
 // Row layout (plain residues): g (dg+1) | u (na-dg+1) | w (nb-dg+1).  deg[k] = dg,
 // or -2 if lc(A) or lc(B) vanishes mod p.
@@ -439,6 +475,7 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
 size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4; }
+size_t sqf_probe_smem(int max_deg) { return static_cast<size_t>(2) * (max_deg + 2) * 4; }
 size_t bigcd_probe_smem(int nf, int ng) { return static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4; }
 size_t newton_smem(int N) { return static_cast<size_t>(N) * (kNewtonCols + 1) * 4; }
 
@@ -462,6 +499,19 @@ int uni_threads(int n) {
   static const int forced = std::getenv("CTG_UNI_THREADS") ? std::atoi(std::getenv("CTG_UNI_THREADS")) : 0;
   if (forced == 128 || forced == 256 || forced == 512) return forced;
   return 256;  // 512 measured slower at n = 870 (285 vs 277 us)
+}
+
+int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
+                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st) {
+  if (nprob == 0) return 0;
+  const int cap = max_deg + 2;
+  const size_t smem = smem_or_global(k_sqf_probe<false>, sqf_probe_smem(max_deg), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  if (smem)
+    k_sqf_probe<false><<<nprob * nk, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr);
+  else
+    k_sqf_probe<true><<<nprob * nk, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf);
+  return 1;
 }
 
 size_t uni_gbuf_bytes(size_t smem, size_t ctas) { return smem > kUniSmemMax ? smem * ctas : 0; }

@@ -203,3 +203,23 @@ def test_yun_of_big_config_resultants(row):
     unit, factors = P.yun_squarefree(R)
     assert unit == sgn * cont
     assert factors == [(pp, 1)]
+
+
+def test_yun_squarefree_batch_matches_single_calls():
+    """ctg_yun_squarefree_batch (one probe launch for all inputs, contents on the host meanwhile)
+    returns exactly what ctg_yun_squarefree returns input by input: square-free config
+    resultants, the singular sheared family, the reference test_elim Yun inputs (seed 23:
+    multiplicities), constants and linear inputs, negative leading coefficients and contents."""
+    polys = []
+    for s in range(1, 6):
+        f = curves.make("dense", 12, 40, s)
+        polys.append(P.resultant(f, curves.derive_y(f)))
+    fs = curves.make("sheared", 2, 0, 1)
+    polys.append(P.resultant(fs, curves.derive_y(fs)))
+    polys += [dec_upoly(r["u"]) for r in load("elim_cases.jsonl") if r["case"].startswith("yun")][:40]
+    polys += [[7], [-12], [3, 6], [-4, 0, -4], [0, 0, 0, 5]]
+    polys += [[-3 * c for c in polys[0]]]
+    got = P.yun_squarefree_batch(polys)
+    assert got == [P.yun_squarefree(p) for p in polys]
+    with pytest.raises(P.PreconditionError):
+        P.yun_squarefree_batch([[1, 1], []])
