@@ -358,6 +358,35 @@ __device__ uint32_t warp_res_general(uint32_t* A, int na, uint32_t* B, int nb, c
   }
 }
 
+// K3's fused division-free Euclid (fast_euclid, modres_fast.cuh) with the coefficients spread
+// over the lanes of a warp (A, B in shared memory): r'_i = b_k^2 a_i - b_k a_{k+1} b_{i-1} - A1_k b_i,
+// one three-product reduction per coefficient per step, no inversion until the end
+// (res = r'_0 / (prod b_k^{k-1})^2).  A (deg n) and B (deg n - 1) are consumed.  flag != 0: a
+// leading coefficient vanished (degree drop) -- the caller recomputes with warp_res_general.
+__device__ uint32_t warp_fast_euclid(uint32_t* A, uint32_t* B, int n, const Mod& M, int lane, uint32_t& flag) {
+  __syncwarp();
+  flag = (A[n] == 0u) | (B[n - 1] == 0u);
+  uint32_t U = M.one, E = M.one;
+  for (int kk = n - 1; kk >= 1 && !flag; --kk) {
+    const uint32_t bk = B[kk];
+    const uint32_t na = mneg(A[kk + 1], M.p);
+    const uint32_t c1 = mmul(bk, bk, M);
+    const uint32_t c2 = mmul(bk, na, M);
+    const uint32_t c3 = mneg(mmul2(bk, A[kk], na, B[kk - 1], M), M.p);
+    __syncwarp();  // every lane has read the step's leading coefficients
+    for (int t = lane; t < kk; t += 32) A[t] = t ? mmul3(c1, A[t], c2, B[t - 1], c3, B[t], M) : mmul2(c1, A[0], c3, B[0], M);
+    __syncwarp();
+    flag |= (A[kk - 1] == 0u);
+    U = mmul(U, bk, M);
+    if (kk >= 2) E = mmul(E, U, M);
+    uint32_t* t = A;  // (A, B) <- (B, r')
+    A = B;
+    B = t;
+  }
+  if (flag) return 0u;
+  return mmul(B[0], minv(mmul(E, E, M), M), M);
+}
+
 __global__ void __launch_bounds__(32 * kWarpsGeneral) k_modres_warp(ResParams P, int use_list, uint32_t total_units) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -390,7 +419,21 @@ __global__ void __launch_bounds__(32 * kWarpsGeneral) k_modres_warp(ResParams P,
       const int base = 2 * nq;
       for (int j = lane; j <= P.m; j += 32) bufB[j] = horner(tab, P.dir[base + j], P.dir[base + P.m + 1 + j], x, M);
     }
-    const uint32_t r = warp_res_general(bufA, P.n, bufB, P.m, M, lane);
+    uint32_t r;
+    uint32_t flag = 1u;
+    if (P.m == P.n - 1) r = warp_fast_euclid(bufA, bufB, P.n, M, lane, flag);
+    if (flag) {  // not the normal shape, or a degree drop mod p: the exact formal-degree path
+      __syncwarp();
+      for (int j = lane; j <= P.n; j += 32) bufA[j] = horner(tab, P.dir[j], P.dir[nq + j], x, M);
+      __syncwarp();
+      if (P.deriv) {
+        for (int j = lane; j <= P.m; j += 32) bufB[j] = mmul(bufA[j + 1], mmul(static_cast<uint32_t>(j + 1), M.r2, M), M);
+      } else {
+        const int base = 2 * nq;
+        for (int j = lane; j <= P.m; j += 32) bufB[j] = horner(tab, P.dir[base + j], P.dir[base + P.m + 1 + j], x, M);
+      }
+      r = warp_res_general(bufA, P.n, bufB, P.m, M, lane);
+    }
     if (lane == 0) *out = r;
   }
 }

@@ -7,7 +7,7 @@
 ``sheared(K, seed)``   f = g * prod_{k=1}^{K-1} g(x, y + k x + k), g = dense(6, 10, seed).
 
 The generator is the workload definition used by ``bench.py`` and the tests;
-``tests/test_curves.py`` checks it against ``oracle/_ref/refdriver gen``.
+``tests/test_curves.py`` checks it against ``oracle/_ref/refdriver gen`` (the reference side).
 Polynomials are dicts ``{(deg_x, deg_y): int}``.
 """
 
