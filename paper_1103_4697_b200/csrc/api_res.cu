@@ -258,6 +258,7 @@ struct ctg_plan {
   uint32_t* d_ntt = nullptr;       // K4 work array [B][P][N] when N > kMaxNttSmem
   int nrows = 0, maxlen = 0;
   bool fast_ok = false;
+  bool mw_ok = false;              // 40 < n <= 127, m = n - 1: K2 point values + k_modres_mw
   bool fused = false;              // K2 folded into K3 (k_modres_fused): no d_vals
   int crt_cap = 0;
   int launches = 0;
@@ -293,7 +294,7 @@ struct ctg_plan {
     const size_t nch = static_cast<size_t>((P + kCrtChunk - 1) / kCrtChunk);
     size_t s = r(4 * h_limbs.size()) + r(h_sign.size()) + r(4 * dir.size()) + r(4ull * B * P * S) +
                r(4ull * flag_cap) + r(16);
-    if (fast_ok && !fused) s += r(4ull * B * P * nrows * N);
+    if ((fast_ok && !fused) || mw_ok) s += r(4ull * B * P * nrows * N);
     s += r(4 * general_warp_gbuf_words(n));
     if (N > kMaxNttSmem) s += r(4ull * B * P * N);
     s += r(4 * crt_y_words(*tabs, B, J)) + r(8 * static_cast<size_t>(B) * nch * J) +
@@ -407,6 +408,7 @@ ctg_plan* plan_build(const std::vector<Problem>& probs, const std::vector<int>& 
   for (int v : lenp) pl->maxlen = std::max(pl->maxlen, v);
   for (int v : lenq) pl->maxlen = std::max(pl->maxlen, v);
   pl->fast_ok = (m == n - 1 || m == n) && n >= 2 && n <= kFastMaxDeg;
+  pl->mw_ok = m == n - 1 && n > kFastMaxDeg && n <= 127;
 
   if (degb + 1 > (int64_t{1} << 28)) throw ApiError(CTG_UNSUPPORTED, "resultant: degree bound of the result exceeds 2^28");
   pl->D = static_cast<uint32_t>(degb + 1);
@@ -454,7 +456,8 @@ static void plan_alloc(ctg_plan* pl, cudaStream_t st) {
   pl->palloc(pl->d_tab, static_cast<size_t>(pl->B) * pl->P * pl->S, st);
   pl->palloc(pl->d_flags, pl->flag_cap, st);
   pl->palloc(pl->d_counters, 4, st);
-  if (pl->fast_ok && !pl->fused) pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
+  if ((pl->fast_ok && !pl->fused) || pl->mw_ok)
+    pl->palloc(pl->d_vals, static_cast<size_t>(pl->B) * pl->P * pl->nrows * pl->N, st);
   if (general_warp_gbuf_words(pl->n)) pl->palloc(pl->d_gwarp, general_warp_gbuf_words(pl->n), st);
   if (pl->N > kMaxNttSmem) pl->palloc(pl->d_ntt, static_cast<size_t>(pl->B) * pl->P * pl->N, st);
   CTG_CUDA_CHECK(cudaMemsetAsync(pl->d_counters, 0, sizeof(uint32_t) * 4, st));
@@ -530,7 +533,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   rp.flag_list = pl->d_flags;
   rp.counters = pl->d_counters;
   rp.flag_cap = pl->flag_cap;
-  rp.vals = pl->fast_ok && !pl->fused ? pl->d_vals : nullptr;
+  rp.vals = (pl->fast_ok && !pl->fused) || pl->mw_ok ? pl->d_vals : nullptr;
   rp.fused = pl->fused ? 1 : 0;
   rp.nrows = pl->nrows;
   rp.maxlen = pl->maxlen;
@@ -919,6 +922,7 @@ static ctg_plan* plan_clone(const ctg_plan* src, int device) {
   c->nrows = src->nrows;
   c->maxlen = src->maxlen;
   c->fast_ok = src->fast_ok;
+  c->mw_ok = src->mw_ok;
   c->fused = src->fused;
   c->tabs = get_tables(device, src->N, src->tabs->primes);
   return c.release();

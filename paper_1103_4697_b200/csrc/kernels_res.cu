@@ -387,11 +387,113 @@ __device__ uint32_t warp_fast_euclid(uint32_t* A, uint32_t* B, int n, const Mod&
   return mmul(B[0], minv(mmul(E, E, M), M), M);
 }
 
+// ---------------------------------------------------------------------------
+// K3 for 40 < deg_y <= 127 with the derivative / n, n-1 shape: FOUR units per warp, 8 lanes per
+// unit, each lane holding C consecutive coefficients of A and B in registers (n + 1 <= 8 C).
+// Same fused division-free step as fast_euclid; the two new leading remainder coefficients of
+// a step come from their owner lanes by shuffle (the other two step inputs carry over from the
+// previous step), y_{i-1} across a lane boundary by shfl_up.  A unit whose leading coefficient
+// vanishes mod p (degree drop) is marked kSentinel and recomputed by k_modres_warp's exact
+// path.  (k_modres_warp alone -- one unit per warp, coefficients in shared memory -- ran deg_y
+// 41 / 50 / 64 at 1.0e8 / 8.7e7 / 6.9e7 units/s.)
+// ---------------------------------------------------------------------------
+template <int C>
+__global__ void __launch_bounds__(128) k_modres_mw(ResParams P, uint32_t total_units) {
+  constexpr int G = 8;  // lanes per unit
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
+  const unsigned gmask = 0xffu << gbase;
+  const int nq = P.n + 1, n = P.n;
+  const uint32_t units_per_block = (blockDim.x / G);
+  for (uint32_t u0 = blockIdx.x * units_per_block; u0 < total_units; u0 += gridDim.x * units_per_block) {
+    const uint32_t unit = u0 + threadIdx.x / G;
+    const bool live = unit < total_units;
+    const uint32_t uu = live ? unit : total_units - 1;
+    const uint32_t bk_ = uu / P.N;
+    const int i = static_cast<int>(uu % P.N);
+    const int kl = static_cast<int>(bk_ % P.nk), b = static_cast<int>(bk_ / P.nk);
+    const int k = P.k0 + kl;
+    const PrimeConst pcv = P.pc[k];
+    const Mod M = load_mod(pcv);
+    const uint32_t x = mpow(pcv.omega, static_cast<uint64_t>(i), M);
+    const uint32_t* tab = P.tab + b * P.tab_bstride + static_cast<size_t>(k) * P.S;
+    uint32_t A[C], B[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {  // K2's point values when present, else Horner
+      const int j = gl * C + c;
+      A[c] = j > n ? 0u : (P.vals ? vals_row(P, b, kl, j)[i] : horner(tab, P.dir[j], P.dir[nq + j], x, M));
+    }
+    // B = A' (deriv) or the second operand's rows
+    {
+      const uint32_t up = __shfl_down_sync(0xffffffffu, A[0], 1);  // A[j + 1] across the lane boundary
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int j = gl * C + c;
+        if (P.deriv) {
+          const uint32_t an = c + 1 < C ? A[c + 1 < C ? c + 1 : c] : (gl + 1 < G ? up : 0u);
+          B[c] = j <= n - 1 ? mmul(an, mmul(static_cast<uint32_t>(j + 1), M.r2, M), M) : 0u;
+        } else {
+          B[c] = j > n - 1 ? 0u
+                           : (P.vals ? vals_row(P, b, kl, nq + j)[i]
+                                     : horner(tab, P.dir[2 * nq + j], P.dir[2 * nq + n + j], x, M));
+        }
+      }
+    }
+    // owner lane of coefficient j within the group, and the value there
+    auto fetch = [&](const uint32_t (&V)[C], int j) -> uint32_t {
+      uint32_t v = 0u;
+      const int oc = j % C;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (c == oc) v = V[c];
+      return __shfl_sync(0xffffffffu, v, gbase + j / C);
+    };
+    uint32_t a1 = fetch(A, n), a0 = fetch(A, n - 1), b1 = fetch(B, n - 1), b0 = fetch(B, n - 2);
+    uint32_t flag = (a1 == 0u) | (b1 == 0u);
+    uint32_t U = M.one, E = M.one;
+    for (int kk = n - 1; kk >= 1; --kk) {
+      // step on (A deg kk + 1, B deg kk): a1 = A[kk+1], a0 = A[kk], b1 = B[kk], b0 = B[kk-1]
+      const uint32_t na = mneg(a1, M.p);
+      const uint32_t c1 = mmul(b1, b1, M), c2 = mmul(b1, na, M);
+      const uint32_t c3 = mneg(mmul2(b1, a0, na, b0, M), M.p);
+      const uint32_t bprev = __shfl_up_sync(0xffffffffu, B[C - 1], 1);  // B[gl C - 1]
+      uint32_t R[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int j = gl * C + c;
+        const uint32_t bm1 = c ? B[c ? c - 1 : 0] : (gl ? bprev : 0u);
+        R[c] = j < kk ? mmul3(c1, A[c], c2, bm1, c3, B[c], M) : 0u;
+      }
+      U = mmul(U, b1, M);
+      if (kk >= 2) E = mmul(E, U, M);
+      // (A, B) <- (B, R): the next step's a1, a0 are this step's b1, b0
+      const uint32_t r1 = fetch(R, kk - 1), r0 = kk >= 2 ? fetch(R, kk - 2) : 0u;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        A[c] = B[c];
+        B[c] = R[c];
+      }
+      a1 = b1;
+      a0 = b0;
+      b1 = r1;
+      b0 = r0;
+      flag |= (r1 == 0u);
+    }
+    // after the last step B[0] is the numerator (fast_euclid: num = B[0])
+    const uint32_t num = __shfl_sync(0xffffffffu, B[0], gbase);
+    if (live && gl == 0) {
+      uint32_t* out = P.rows + b * P.rows_bstride + static_cast<size_t>(kl) * P.pitch + i;
+      *out = flag ? kSentinel : mmul(num, minv(mmul(E, E, M), M), M);
+    }
+  }
+  (void)gmask;
+}
+
 __global__ void __launch_bounds__(32 * kWarpsGeneral) k_modres_warp(ResParams P, int use_list, uint32_t total_units) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t flagged = use_list ? P.counters[0] : 0u;
-  const bool scan = use_list && flagged > P.flag_cap;
+  // use_list: 0 every unit, 1 the flag list (or a scan when it overflowed), 2 scan for kSentinel
+  const uint32_t flagged = use_list == 1 ? P.counters[0] : 0u;
+  const bool scan = use_list == 2 || (use_list == 1 && flagged > P.flag_cap);
   const uint32_t all = static_cast<uint32_t>(P.B) * static_cast<uint32_t>(P.nk) * static_cast<uint32_t>(P.N);
   const uint32_t count = scan ? all : (use_list ? flagged : total_units);
   const int nq = P.n + 1, cap = P.n + 1;
@@ -1294,6 +1396,13 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
 // Enough blocks for the scan mode of k_modres_general (blocks beyond a short list exit at once).
 constexpr int kGeneralListBlocks = 148 * 4;
 
+// k_modres_warp over the units a previous kernel left at kSentinel (scan mode).
+static int launch_sentinel_scan(const ResParams& rp, size_t smem, cudaStream_t st) {
+  const int blocks = rp.gwarp ? static_cast<int>(kGeneralWarpGlobalBlocks) : 148 * 16;
+  k_modres_warp<<<blocks, 32 * kWarpsGeneral, smem, st>>>(rp, 2, 0u);
+  return 1;
+}
+
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
   if (rp.nk == 0 || rp.B == 0) return 0;
   if (fast && rp.fused) {  // K2 folded into K3: the point values never leave shared memory
@@ -1311,8 +1420,28 @@ int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part) {
       return launches + 2;
     }
   }
-  if (part == 1) return 0;
   const uint32_t total = static_cast<uint32_t>(rp.B) * rp.nk * static_cast<uint32_t>(rp.N);
+  if (rp.n > kThreadGeneralMax && rp.n <= 127 && rp.m == rp.n - 1) {
+    // K2 (point values by coset NTT, when the plan holds the buffer), then four units per warp in
+    // registers, then the exact path for the units it marked
+    const int ev = rp.vals && part != 2 ? launch_eval(rp, st) : 0;
+    if (part == 1) return ev;
+    const uint32_t blocks_mw = std::min<uint32_t>((total + 15) / 16, 148u * 32u);
+    const int C = (rp.n + 1 + 7) / 8;
+    if (C <= 6)
+      k_modres_mw<6><<<blocks_mw, 128, 0, st>>>(rp, total);
+    else if (C <= 8)
+      k_modres_mw<8><<<blocks_mw, 128, 0, st>>>(rp, total);
+    else if (C <= 12)
+      k_modres_mw<12><<<blocks_mw, 128, 0, st>>>(rp, total);
+    else
+      k_modres_mw<16><<<blocks_mw, 128, 0, st>>>(rp, total);
+    const size_t smem = rp.gwarp ? 0 : general_warp_smem(rp.n);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_modres_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    return ev + 1 + launch_sentinel_scan(rp, smem, st);
+  }
+  if (part == 1) return 0;
   if (rp.n > kThreadGeneralMax) {  // warp per unit (any degree)
     const size_t smem = rp.gwarp ? 0 : general_warp_smem(rp.n);
     if (smem > 48 * 1024)

@@ -1,5 +1,5 @@
 """The formal-degree path beyond the fast kernel's deg_y 40 (k_modres_warp, warp per unit):
-throughput of dense curves of total degree 40 (fast kernel) vs 41, 50, 64 (warp kernel),
+throughput of dense curves of total degree 40 (fast kernel) vs 41, 50, 64 (k_modres_mw: four units per warp),
 16-bit coefficients, 8 curves per call through ctg_resultant_batch (host buffers)."""
 import json
 import os
@@ -23,6 +23,6 @@ for d in (40, 41, 50, 64):
     st = P.last_call_stats()
     units = st["n_primes"] * st["n_coeffs"] * len(pairs)
     ms = 1e3 * statistics.median(ts)
-    print(json.dumps({"deg": d, "kernel": "k_modres_fast" if d <= 40 else "k_modres_warp", "curves": len(pairs),
+    print(json.dumps({"deg": d, "kernel": "k_modres_fast" if d <= 40 else "k_eval_ntt + k_modres_mw", "curves": len(pairs),
                       "primes": st["n_primes"], "coeffs": st["n_coeffs"], "ms_per_call": ms,
                       "units_per_s": units / (ms * 1e-3)}))

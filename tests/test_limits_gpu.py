@@ -214,3 +214,42 @@ def test_crt_carry_chain_patterns():
         pairs.append((g, curves.derive_y(g)))
         wants.append([4 * c for c in bb])
     assert P.resultant_batch(pairs) == wants
+
+
+@pytest.mark.parametrize("d", [41, 47, 48, 63, 64, 95, 100])
+def test_multi_unit_warp_kernel_specialisation(d):
+    """deg_y in (40, 127] with the derivative shape runs k_modres_mw (four units per warp, 8 lanes
+    per unit, C = 6 / 8 / 12 / 16 coefficients per lane): R(x0) mod q == the F_q resultant of the
+    specialised rows at random points, deg R <= d (d - 1), R(0) against the same check."""
+    rng = random.Random(d)
+    f = curves.dense(d, 8, 1000 + d)
+    fy = curves.derive_y(f)
+    R = P.resultant(f, fy)
+    assert 0 < len(R) - 1 <= d * (d - 1)
+    for x0 in [0, 1] + [rng.randrange(Q61) for _ in range(2)]:
+        want = _res_mod(_eval_rows(f, x0, Q61), _eval_rows(fy, x0, Q61), Q61)
+        assert _upoly_eval(R, x0, Q61) == want
+
+
+def test_multi_unit_warp_kernel_staged_plan():
+    """The staged plan API (K2 and K3 as separate stages, as bench.py times them) on a deg_y 50
+    batch equals the one-call result: k_modres_mw reads K2's point values."""
+    import torch
+    pairs = [(f, curves.derive_y(f)) for f in (curves.dense(50, 8, s) for s in (1, 2, 3))]
+    want = P.resultant_batch(pairs)
+    plan = P.Plan(pairs)
+    info = plan.info
+    Pn, N, D, W = info["n_primes"], info["n_points"], info["n_coeffs"], info["out_limbs"] + 1
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    B = len(pairs)
+    rows = torch.zeros((B, Pn, N), dtype=torch.int32, device="cuda")
+    out = torch.zeros((B * D * W,), dtype=torch.int32, device="cuda")
+    plan.upload(sh)
+    for st_ in (1, 4, 5, 3):
+        plan.stage(st_, 0, Pn, rows.data_ptr(), sh, curve_stride=Pn * N)
+    plan.crt_batch(rows.data_ptr(), 0, D, out.data_ptr(), sh, curve_stride=Pn * N)
+    torch.cuda.synchronize()
+    plan.check(sh)
+    host = out.cpu().numpy().view("uint32").reshape(B, D, W)
+    assert [plan.decode(host[b]) for b in range(B)] == want
