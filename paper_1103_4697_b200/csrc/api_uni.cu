@@ -40,6 +40,14 @@ namespace {
 
 using ZPoly = std::vector<SBig>;  // low -> high, trimmed
 
+// One coefficient to reduce: sign and trimmed little-endian u32 magnitude (not owned).
+struct Slot {
+  int8_t sign;
+  const uint32_t* mag;
+  int n;
+};
+
+
 // Primes of the univariate path: (2^30, 2^30.4), the window where the fused two-elimination
 // pass of blk_gcd (a three-product sum, mmul3) needs one Montgomery reduction.
 std::vector<uint32_t> select_uni_primes(double need_bits) { return select_primes(1, need_bits, kResPrimeMax); }
@@ -67,6 +75,27 @@ ZPoly parse_upoly(const ctg_upoly* p) {
 }
 
 int zdeg(const ZPoly& p) { return static_cast<int>(p.size()) - 1; }
+// The caller's CSR polynomial as trimmed slots (pointers into its limbs; validated like
+// parse_upoly; trailing zero coefficients dropped).
+std::vector<Slot> view_upoly(const ctg_upoly* p) {
+  std::vector<Slot> out;
+  if (!p || p->n_coeffs == 0) return out;
+  if (p->n_coeffs < 0 || !p->sign || !p->limb_off || (!p->limbs && p->limb_off[p->n_coeffs] > 0))
+    throw ApiError(CTG_INVALID, "upoly: null pointer or negative coefficient count");
+  out.resize(p->n_coeffs);
+  for (int i = 0; i < p->n_coeffs; ++i) {
+    const uint32_t b = p->limb_off[i], e = p->limb_off[i + 1];
+    if (e < b) throw ApiError(CTG_INVALID, "upoly: limb_off not monotone");
+    const int sg = p->sign[i];
+    if (sg < -1 || sg > 1) throw ApiError(CTG_INVALID, "upoly: sign must be -1, 0 or +1");
+    uint32_t n = e - b;
+    while (n > 0 && p->limbs[b + n - 1] == 0u) --n;
+    out[i] = (sg == 0 || n == 0) ? Slot{0, nullptr, 0} : Slot{static_cast<int8_t>(sg), p->limbs + b, static_cast<int>(n)};
+  }
+  while (!out.empty() && out.back().n == 0) out.pop_back();
+  return out;
+}
+
 
 // Positive gcd of all coefficients, stopping at 1 (upoly.cpp:59-66).  The coefficients are
 // visited shortest first, so the one full-size gcd is between the two smallest and every
@@ -109,6 +138,40 @@ Big zcontent(const ZPoly& p) {
     const size_t i0 = 2 + t * per, i1 = std::min(order.size(), i0 + per);
     Big h = g;
     for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = step(h, order[i]->mag);
+    part[t] = h;
+  });
+  for (const Big& h : part) g = big_gcd(g, h);
+  return g;
+}
+
+// zcontent over slots (the same visiting order and early exit).
+Big slots_content(const std::vector<Slot>& p) {
+  std::vector<const Slot*> order;
+  for (const auto& c : p)
+    if (c.n) order.push_back(&c);
+  std::stable_sort(order.begin(), order.end(), [](const Slot* a, const Slot* b) { return a->n < b->n; });
+  auto big = [](const Slot* c) { return Big(c->mag, c->mag + c->n); };
+  auto small_gcd = [](uint32_t g, const Slot* c) {
+    uint32_t r = big_mod_u32(c->mag, c->n, g);
+    while (r) {
+      const uint32_t t = g % r;
+      g = r;
+      r = t;
+    }
+    return g;
+  };
+  auto step = [&](const Big& g, const Slot* c) { return g.size() == 1 ? Big{small_gcd(g[0], c)} : big_gcd(g, big(c)); };
+  if (order.empty()) return Big();
+  Big g = big(order[0]);
+  if (order.size() > 1) g = step(g, order[1]);
+  if (big_is_one(g) || order.size() <= 2) return g;
+  const int groups = 16;
+  std::vector<Big> part(groups);
+  const size_t rest = order.size() - 2, per = (rest + groups - 1) / groups;
+  parallel_for(groups, [&](int t) {
+    const size_t i0 = 2 + t * per, i1 = std::min(order.size(), i0 + per);
+    Big h = g;
+    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = step(h, order[i]);
     part[t] = h;
   });
   for (const Big& h : part) g = big_gcd(g, h);
@@ -279,33 +342,25 @@ struct PinnedStage {
 };
 thread_local PinnedStage tls_stage;
 
-// Several polynomials reduced in ONE staging copy and ONE launch: their coefficients are
-// consecutive slots, so row k of the result holds p_0 | p_1 | ... (pitch = total slots).
-template <class List>
-uint32_t* reduce_polys(DevArena& ar, const List& ps, const CrtTables& tabs, Launches& L) {
-  int S = 0, Lw = 1;
-  for (const ZPoly* p : ps) {
-    S += static_cast<int>(p->size());
-    for (const auto& c : *p) Lw = std::max<int>(Lw, static_cast<int>(c.mag.size()));
-  }
+// Coefficients reduced modulo every prime of `tabs` (K1) in ONE staging copy and ONE launch:
+// row k of the result holds the slots in order (pitch = slots.size()), Montgomery form.
+uint32_t* reduce_slots(DevArena& ar, const std::vector<Slot>& slot, const CrtTables& tabs, Launches& L) {
+  const int S = static_cast<int>(slot.size());
+  int Lw = 1;
+  for (const Slot& c : slot) Lw = std::max(Lw, c.n);
   const size_t nl = static_cast<size_t>(Lw) * S;
   uint8_t* stage = tls_stage.get(4 * nl + S);
   uint32_t* limbs = reinterpret_cast<uint32_t*>(stage);
   int8_t* sign = reinterpret_cast<int8_t*>(stage + 4 * nl);
   // coefficient-major [S][Lw]: one contiguous copy per coefficient (K1 reads either layout),
   // filled in parallel over blocks of 64 slots (a batch stages tens of MB)
-  std::vector<const SBig*> slot;
-  slot.reserve(S);
-  for (const ZPoly* p : ps)
-    for (const auto& c : *p) slot.push_back(&c);
   parallel_for((S + 63) / 64, [&](int blk) {
     for (int s = blk * 64; s < std::min(S, blk * 64 + 64); ++s) {
-      const SBig& c = *slot[s];
-      sign[s] = static_cast<int8_t>(c.sign);
-      const size_t n = c.mag.size();
+      const Slot& c = slot[s];
+      sign[s] = c.sign;
       uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
-      if (n) std::memcpy(row, c.mag.data(), 4 * n);
-      if (n < static_cast<size_t>(Lw)) std::memset(row + n, 0, 4 * (Lw - n));
+      if (c.n) std::memcpy(row, c.mag, 4 * static_cast<size_t>(c.n));
+      if (c.n < Lw) std::memset(row + c.n, 0, 4 * static_cast<size_t>(Lw - c.n));
     }
   });
   uint32_t* d_limbs = ar.alloc<uint32_t>(nl);
@@ -319,6 +374,15 @@ uint32_t* reduce_polys(DevArena& ar, const List& ps, const CrtTables& tabs, Laun
   auto& st = stats_tls();
   st.h2d_bytes += static_cast<int64_t>(4 * nl + S);
   return d_tab;
+}
+
+// Several polynomials as consecutive slots of one table (row k = p_0 | p_1 | ...).
+template <class List>
+uint32_t* reduce_polys(DevArena& ar, const List& ps, const CrtTables& tabs, Launches& L) {
+  std::vector<Slot> slot;
+  for (const ZPoly* p : ps)
+    for (const auto& c : *p) slot.push_back({static_cast<int8_t>(c.sign), c.mag.data(), static_cast<int>(c.mag.size())});
+  return reduce_slots(ar, slot, tabs, L);
 }
 
 uint32_t* reduce_poly(DevArena& ar, const ZPoly& p, const CrtTables& tabs, Launches& L) {
@@ -501,23 +565,27 @@ int32_t* probe_pinned() {
   return buf;
 }
 
-void probe_start(YunProbe& pb, const ZPoly& R, int device, cudaStream_t st, Launches& L) {
-  pb.n = zdeg(R);
+// Launches the probe on the coefficient slots of R (deg n): K1 modulo 3 primes and one
+// k_sqf_probe CTA per prime (gcd(R, R') mod p only -- the rest of Yun runs only if needed).
+void probe_start(YunProbe& pb, const std::vector<Slot>& slots, int n, int device, cudaStream_t st, Launches& L) {
+  pb.n = n;
   pb.primes = select_uni_primes(3 * 30.0);
   pb.ar = std::make_unique<DevArena>(st);
   DevArena& ar = *pb.ar;
-  const int nk = static_cast<int>(pb.primes.size()), n = pb.n;
+  const int nk = static_cast<int>(pb.primes.size());
   auto T = get_tables(device, 1, pb.primes);
-  uint32_t* d_tab = reduce_poly(ar, R, *T, L);
-  int32_t* d_deg = ar.alloc<int32_t>(static_cast<size_t>(nk) * (n + 1));
-  uint32_t* d_fac = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (2 * n + 2));
-  uint32_t* d_sqf = ar.alloc<uint32_t>(static_cast<size_t>(nk) * (n + 1));
-  const size_t gb = uni_gbuf_bytes(modyun_smem(n), nk);
+  uint32_t* d_tab = reduce_slots(ar, slots, *T, L);
+  const int32_t meta_h[2] = {0, n};
+  int32_t* d_meta = ar.alloc<int32_t>(2);
+  int32_t* d_out = ar.alloc<int32_t>(2 * static_cast<size_t>(nk));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d_meta, meta_h, sizeof(meta_h), cudaMemcpyHostToDevice, ar.st));
+  const size_t gb = uni_gbuf_bytes(sqf_probe_smem(n), nk);
   uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
-  L.n += launched(launch_modyun(d_tab, n, T->d_pc, nk, d_deg, d_fac, d_sqf, gbuf, ar.st));
+  L.n += launched(launch_sqf_probe(d_tab, static_cast<int>(slots.size()), d_meta, d_meta + 1, 1, nk, T->d_pc, n, d_out,
+                                   gbuf, ar.st));
   CTG_CUDA_CHECK(cudaGetLastError());
   pb.h = probe_pinned();
-  CTG_CUDA_CHECK(cudaMemcpy2DAsync(pb.h, 8, d_deg, 4 * static_cast<size_t>(n + 1), 8, nk, cudaMemcpyDeviceToHost, ar.st));
+  CTG_CUDA_CHECK(cudaMemcpyAsync(pb.h, d_out, 8 * static_cast<size_t>(nk), cudaMemcpyDeviceToHost, ar.st));
   CTG_CUDA_CHECK(cudaEventCreateWithFlags(&pb.done, cudaEventDisableTiming));
   CTG_CUDA_CHECK(cudaEventRecord(pb.done, ar.st));
   stats_tls().d2h_bytes += static_cast<int64_t>(8) * nk;
@@ -527,7 +595,7 @@ void probe_start(YunProbe& pb, const ZPoly& R, int device, cudaStream_t st, Laun
 bool probe_finish(YunProbe& pb) {
   CTG_CUDA_CHECK(cudaEventSynchronize(pb.done));
   for (size_t k = 0; k < pb.primes.size(); ++k)
-    if (pb.h[2 * k] == 0 && pb.h[2 * k + 1] == pb.n) return true;
+    if (pb.h[2 * k] == 0 && pb.h[2 * k + 1] == 0) return true;  // lc != 0 mod p, deg gcd(R, R') = 0
   return false;
 }
 
@@ -1104,14 +1172,30 @@ void fill_upoly_z(const ZPoly& p, ctg_upoly_buf* out) {
   out->limb_off[n] = off;
 }
 
+// A primitive polynomial given as slots, divided by sgn(lc), into a library buffer.
+void fill_upoly_slots(const std::vector<Slot>& p, int lcsign, ctg_upoly_buf* out) {
+  const size_t n = p.size();
+  size_t total = 0;
+  for (const Slot& c : p) total += static_cast<size_t>(c.n);
+  upoly_alloc(out, n, total);
+  uint32_t off = 0;
+  for (size_t i = 0; i < n; ++i) {
+    out->sign[i] = static_cast<int8_t>(p[i].sign * lcsign);
+    out->limb_off[i] = off;
+    if (p[i].n) std::memcpy(out->limbs + off, p[i].mag, 4 * static_cast<size_t>(p[i].n));
+    off += static_cast<uint32_t>(p[i].n);
+  }
+  out->limb_off[n] = off;
+}
+
 void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly, int>>& factors, ctg_sqf_buf* out,
-              const ZPoly* single = nullptr) {
+              const ZPoly* single = nullptr, const std::vector<Slot>* single_slots = nullptr) {
   std::memset(out, 0, sizeof(*out));
   out->unit_sign = static_cast<int8_t>(unit.empty() ? 0 : unit_sign);
   out->unit_nlimbs = static_cast<int32_t>(unit.size());
   out->unit_limbs = static_cast<uint32_t*>(std::malloc(4 * std::max<size_t>(1, unit.size())));
   std::memcpy(out->unit_limbs, unit.data(), 4 * unit.size());
-  const size_t nf = single ? 1 : factors.size();
+  const size_t nf = (single || single_slots) ? 1 : factors.size();
   out->n_factors = static_cast<int32_t>(nf);
   out->mult = static_cast<int32_t*>(std::malloc(4 * std::max<size_t>(1, nf)));
   out->factors = static_cast<ctg_upoly_buf*>(std::calloc(std::max<size_t>(1, nf), sizeof(ctg_upoly_buf)));
@@ -1119,6 +1203,11 @@ void fill_sqf(const Big& unit, int unit_sign, const std::vector<std::pair<ZPoly,
   if (single) {  // square-free input: the one factor (multiplicity 1) is the primitive input itself
     out->mult[0] = 1;
     fill_upoly_z(*single, &out->factors[0]);
+    return;
+  }
+  if (single_slots) {  // the same from the caller's limbs (content 1): R / sgn(lc R)
+    out->mult[0] = 1;
+    fill_upoly_slots(*single_slots, unit_sign, &out->factors[0]);
     return;
   }
   for (size_t i = 0; i < factors.size(); ++i) {
@@ -1138,48 +1227,64 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
   return guarded([&] {
     if (!out) throw ApiError(CTG_INVALID, "yun_squarefree: null output");
     CallTimer timer;
-    ZPoly a = parse_upoly(p);
-    if (a.empty()) throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial");  // elim.cpp:139
+    // The input as slots over the caller's CSR (no copies): the common case -- a primitive,
+    // square-free R (every dense config) -- is answered from them directly.
+    std::vector<Slot> slots = view_upoly(p);
+    if (slots.empty()) throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial");  // elim.cpp:139
+    const int n = static_cast<int>(slots.size()) - 1;
     Launches L;
     std::unique_ptr<DeviceGuard> g;
     std::unique_lock<std::mutex> lock;
     int dev = -1;
     Ctx* ctx = nullptr;
-    YunProbe probe;
-    // square-freeness probe on the GPU while the host takes the content -- only where
-    // yun_modular would probe too (its full prime set exceeds one wave of CTAs), so a
-    // non-square-free input never pays for it twice
-    const bool probe_first = zdeg(a) >= kProbeMinDeg &&
-                             select_uni_primes(big_log2(a.back().mag) + zdeg(a) + zlog2_l2(a) + 2 + 40 + 62).size() > 148;
-    if (probe_first) {
+    auto device = [&] {
+      if (ctx) return;
       g = std::make_unique<DeviceGuard>(opts);
       dev = select_device(opts);
       ctx = &context(dev);
       lock = std::unique_lock<std::mutex>(ctx->mu);
-      probe_start(probe, a, dev, ctx->stream, L);
+    };
+    YunProbe probe;
+    // square-freeness probe on the GPU while the host takes the content -- only where
+    // yun_modular would probe too (its full prime set exceeds one wave of CTAs), so a
+    // non-square-free input never pays for it twice
+    bool probe_first = false;
+    if (n >= kProbeMinDeg) {
+      std::vector<double> sq;
+      for (const Slot& c : slots)
+        if (c.n) sq.push_back(2 * log2_upper(c.mag, c.n));
+      const double need = log2_upper(slots.back().mag, slots.back().n) + n + 0.5 * log2_sum_upper(sq) + 2 + 40;
+      probe_first = select_uni_primes(need + 62).size() > 148;
     }
-    Big content;
-    int s = 0;
-    ZPoly P = zprimitive_positive(std::move(a), &content, &s);  // elim.cpp:141-144: unit = sign(lc) * content
+    if (probe_first) {
+      device();
+      probe_start(probe, slots, n, dev, ctx->stream, L);
+    }
+    const int s = slots.back().sign;
+    Big content = slots_content(slots);  // elim.cpp:141-144: unit = sign(lc) * content
     timer.mark_setup();
-    if (zdeg(P) == 0) {  // elim.cpp:145
+    if (n == 0) {  // elim.cpp:145
       fill_sqf(content, s, {}, out);
       timer.finish();
       return;
     }
-    if (probe.done && probe_finish(probe)) {  // square-free: the factorization is (pp(R), 1)
+    const bool certified = probe.done && probe_finish(probe);
+    if (certified && big_is_one(content)) {  // (R / sgn(lc), 1): straight from the caller's limbs
+      timer.mark_device();
+      stats_tls().kernel_launches = L.n;
+      fill_sqf(content, s, {}, out, nullptr, &slots);
+      timer.finish();
+      return;
+    }
+    ZPoly P = divide_content(parse_upoly(p), content, nullptr, nullptr);
+    if (certified) {  // square-free: the factorization is (pp(R), 1)
       timer.mark_device();
       stats_tls().kernel_launches = L.n;
       fill_sqf(content, s, {}, out, &P);
       timer.finish();
       return;
     }
-    if (!ctx) {
-      g = std::make_unique<DeviceGuard>(opts);
-      dev = select_device(opts);
-      ctx = &context(dev);
-      lock = std::unique_lock<std::mutex>(ctx->mu);
-    }
+    device();
     YunResult r = yun_modular(P, false, dev, ctx->stream, L, probe_first);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
