@@ -935,6 +935,23 @@ struct Shard {
   int k0 = 0, k1 = 0, j0 = 0, j1 = 0;
   uint32_t *send = nullptr, *full = nullptr, *crt = nullptr, *gath = nullptr;
   cudaEvent_t rows_done = nullptr;
+  Shard() = default;
+  Shard(const Shard&) = delete;
+  Shard& operator=(const Shard&) = delete;
+  ~Shard() {  // error paths: let the shard's work finish before its buffers go back to the pool
+    if (!pl) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (st) cudaStreamSynchronize(st);
+    pl->pfree(send);
+    pl->pfree(full);
+    pl->pfree(crt);
+    pl->pfree(gath);
+    if (rows_done) cudaEventDestroy(rows_done);
+    pl.reset();
+    cudaSetDevice(prev);
+  }
 };
 
 static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
@@ -964,7 +981,9 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
   }
   std::vector<int> distinct(local_dev);
   std::sort(distinct.begin(), distinct.end());
-  const bool repeated = std::unique(distinct.begin(), distinct.end()) != distinct.end();
+  const auto uend = std::unique(distinct.begin(), distinct.end());
+  const bool repeated = uend != distinct.end();
+  distinct.erase(uend, distinct.end());
   // NCCL between distinct devices of one process; device copies when a GPU hosts two shards
   const bool use_nccl_local = !comm && !repeated && nccl_available();
   const std::vector<ncclComm_t>* local_comms = use_nccl_local ? &device_set_comms(local_dev) : nullptr;
@@ -978,6 +997,11 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
     else
       groups[{probs[b].n, probs[b].m, probs[b].deriv, probs[b].negate}].push_back(b);
   }
+  // the device contexts' streams, scratch and pinned staging are this call's: lock every
+  // involved device's context, in device order (no lock-order inversion between calls)
+  std::vector<std::unique_lock<std::mutex>> locks;
+  if (!groups.empty())
+    for (int d : distinct) locks.emplace_back(context(d).mu);
   stats.setup_ms = std::chrono::duration<double, std::milli>(tclk::now() - t_start).count();
   int nshard_on[64] = {0};
   constexpr int kBlock = 64;  // curves per sharded plan
@@ -1079,8 +1103,6 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
         CTG_CUDA_CHECK(cudaStreamSynchronize(S.st));
         bits |= plan_error_bits(S.pl.get(), S.st);
         stats.kernel_launches += S.pl->launches;
-        cudaEventDestroy(S.rows_done);
-        S.rows_done = nullptr;
       }
       if (bits) throw ApiError(CTG_INTERNAL, "resultant (sharded): device self-check failed (error bits " + std::to_string(bits) + ")");
       stats.n_primes = std::max(stats.n_primes, Pn);
@@ -1098,14 +1120,7 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
         arena.place(&out[idx[b]], off[b], sz[b].nc, sz[b].total);
         decode_fill(plc, host + static_cast<size_t>(b) * D * W, sz[b], &out[idx[b]]);
       });
-      for (auto& S : sh) {  // release on each device
-        PlanDeviceGuard g(S.device);
-        S.pl->pfree(S.send);
-        S.pl->pfree(S.full);
-        S.pl->pfree(S.crt);
-        S.pl->pfree(S.gath);
-        S.pl.reset();
-      }
+      sh.clear();  // ~Shard releases every buffer on its device
     }
   }
 }
