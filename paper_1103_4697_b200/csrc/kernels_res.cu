@@ -401,7 +401,6 @@ template <int C>
 __global__ void __launch_bounds__(128) k_modres_mw(ResParams P, uint32_t total_units) {
   constexpr int G = 8;  // lanes per unit
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
-  const unsigned gmask = 0xffu << gbase;
   const int nq = P.n + 1, n = P.n;
   const uint32_t units_per_block = (blockDim.x / G);
   for (uint32_t u0 = blockIdx.x * units_per_block; u0 < total_units; u0 += gridDim.x * units_per_block) {
@@ -485,7 +484,6 @@ __global__ void __launch_bounds__(128) k_modres_mw(ResParams P, uint32_t total_u
       *out = flag ? kSentinel : mmul(num, minv(mmul(E, E, M), M), M);
     }
   }
-  (void)gmask;
 }
 
 __global__ void __launch_bounds__(32 * kWarpsGeneral) k_modres_warp(ResParams P, int use_list, uint32_t total_units) {
