@@ -314,10 +314,11 @@ size_t pad16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 struct ArenaHdr {
   BufHdr h;         // magic, live members
   uint64_t cap;     // usable bytes after the header
-  uint64_t pad;
+  uint64_t pinned;  // 1: page-locked (cudaMallocHost), the D2H target of device-packed results
 };
 class ArenaCache {
  public:
+  explicit ArenaCache(bool pinned) : pinned_(pinned) {}
   uint8_t* take(size_t bytes) {
     {
       std::lock_guard<std::mutex> l(mu_);
@@ -336,9 +337,17 @@ class ArenaCache {
       }
     }
     const size_t cap = (bytes + 65535) & ~static_cast<size_t>(65535);
-    auto* b = static_cast<uint8_t*>(std::malloc(sizeof(ArenaHdr) + cap));
+    uint8_t* b = nullptr;
+    if (pinned_) {
+      void* p = nullptr;
+      if (cudaMallocHost(&p, sizeof(ArenaHdr) + cap) != cudaSuccess) throw std::bad_alloc();
+      b = static_cast<uint8_t*>(p);
+    } else {
+      b = static_cast<uint8_t*>(std::malloc(sizeof(ArenaHdr) + cap));
+    }
     if (!b) throw std::bad_alloc();
     reinterpret_cast<ArenaHdr*>(b)->cap = cap;
+    reinterpret_cast<ArenaHdr*>(b)->pinned = pinned_ ? 1u : 0u;
     return b;
   }
   void give(uint8_t* b) {
@@ -351,22 +360,30 @@ class ArenaCache {
         return;
       }
     }
-    std::free(b);
+    release(b);
   }
   ~ArenaCache() {
-    for (uint8_t* b : blocks_) std::free(b);
+    for (uint8_t* b : blocks_) release(b);
   }
 
  private:
+  void release(uint8_t* b) const {
+    if (pinned_)
+      cudaFreeHost(b);
+    else
+      std::free(b);
+  }
+  bool pinned_;
   static constexpr size_t kMaxBlocks = 32;
   static constexpr uint64_t kMaxHeld = 1ull << 30;
   std::mutex mu_;
   std::vector<uint8_t*> blocks_;
   uint64_t held_ = 0;
 };
-ArenaCache& arena_cache() {
-  static ArenaCache* c = new ArenaCache();  // never destroyed: results may be freed at exit
-  return *c;
+ArenaCache& arena_cache(bool pinned = false) {
+  static ArenaCache* c = new ArenaCache(false);  // never destroyed: results may be freed at exit
+  static ArenaCache* cp = new ArenaCache(true);
+  return pinned ? *cp : *c;
 }
 
 void place_block(uint8_t* block, uint64_t magic, uint64_t aux, ctg_upoly_buf* out, size_t n, size_t total) {
@@ -388,11 +405,20 @@ void upoly_alloc(ctg_upoly_buf* out, size_t n, size_t total) {
   place_block(block, kSingleMagic, 0, out, n, total);
 }
 
-void UpolyArena::create(size_t bytes, int64_t members) {
-  base = arena_cache().take(bytes);
+void UpolyArena::create(size_t bytes, int64_t members, bool pinned) {
+  base = arena_cache(pinned).take(bytes);
   auto* h = reinterpret_cast<BufHdr*>(base);
   h->magic = kArenaMagic;
   h->aux = static_cast<uint64_t>(members);
+}
+
+uint8_t* UpolyArena::members() const { return base + sizeof(ArenaHdr); }
+
+void UpolyArena::discard() {
+  if (!base) return;
+  reinterpret_cast<BufHdr*>(base)->magic = 0;
+  arena_cache(reinterpret_cast<ArenaHdr*>(base)->pinned != 0).give(base);
+  base = nullptr;
 }
 
 void UpolyArena::place(ctg_upoly_buf* out, size_t off, size_t n, size_t total) const {
@@ -435,7 +461,7 @@ void ctg_upoly_free(ctg_upoly_buf* buf) {
       auto* ah = reinterpret_cast<BufHdr*>(base);
       if (__atomic_sub_fetch(&ah->aux, 1, __ATOMIC_ACQ_REL) == 0) {
         ah->magic = 0;
-        arena_cache().give(base);
+        arena_cache(reinterpret_cast<ArenaHdr*>(base)->pinned != 0).give(base);
       }
     }
   }

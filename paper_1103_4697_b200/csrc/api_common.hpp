@@ -124,10 +124,24 @@ size_t upoly_block_bytes(size_t n_coeffs, size_t total_limbs);
 void upoly_alloc(ctg_upoly_buf* out, size_t n_coeffs, size_t total_limbs);  // single block
 struct UpolyArena {
   uint8_t* base = nullptr;
-  // Creates an arena for `members` blocks totalling `bytes` (sum of upoly_block_bytes).
-  void create(size_t bytes, int64_t members);
+  UpolyArena() = default;
+  UpolyArena(const UpolyArena&) = delete;
+  UpolyArena& operator=(const UpolyArena&) = delete;
+  UpolyArena(UpolyArena&& o) noexcept : base(o.base) { o.base = nullptr; }
+  UpolyArena& operator=(UpolyArena&& o) noexcept {
+    base = o.base;
+    o.base = nullptr;
+    return *this;
+  }
+  // Creates an arena for `members` blocks totalling `bytes` (sum of upoly_block_bytes);
+  // pinned: page-locked host memory (a D2H target), from its own recycled cache.
+  void create(size_t bytes, int64_t members, bool pinned = false);
+  // First byte of the member area (block offsets are relative to it).
+  uint8_t* members() const;
   // Places a block at byte offset `off` (from the first block) into out.
   void place(ctg_upoly_buf* out, size_t off, size_t n_coeffs, size_t total_limbs) const;
+  // Returns an arena that never got its members (error paths) to its cache.
+  void discard();
 };
 
 }  // namespace ctg

@@ -670,6 +670,11 @@ struct Chunk {
   size_t in_off = 0, out_off = 0, out_words = 0, per_curve = 0;
   uint32_t* d_rows = nullptr;
   uint32_t* d_out = nullptr;
+  // device-packed results: the D2H target is the page-locked result arena itself
+  uint32_t *d_nl = nullptr, *d_meta = nullptr;
+  uint8_t* d_pk = nullptr;
+  size_t pk_bytes = 0;
+  UpolyArena arena;
   cudaEvent_t computed = nullptr, copied = nullptr;
   cudaEvent_t t_begin = nullptr, t_computed = nullptr, t_copied = nullptr;  // CTG_TRACE_HOST only
   double host_enqueued_ms = 0;
@@ -681,11 +686,14 @@ struct ChunkNeeds {
 
 ChunkNeeds chunk_needs(const ctg_plan* pl) {
   ChunkNeeds n;
-  const size_t rows = (4ull * pl->B * pl->P * pl->N + 255) & ~static_cast<size_t>(255);
+  auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  const size_t rows = r(4ull * pl->B * pl->P * pl->N);
   const size_t outw = static_cast<size_t>(pl->D) * pl->out_words() * pl->B;
-  n.dev = pl->scratch_bytes(static_cast<int>(pl->D)) + rows + ((4 * outw + 255) & ~static_cast<size_t>(255));
-  n.in = (static_cast<size_t>(plan_h2d_bytes(pl)) + 255) & ~static_cast<size_t>(255);
-  n.out = outw + 4;
+  const size_t pack = r(4ull * pl->B * pl->D) + r(4 * pack_meta_words(pl->B, static_cast<int>(pl->D))) +
+                      r(pack_bytes_bound(pl->B, static_cast<int>(pl->D), pl->out_words()));
+  n.dev = pl->scratch_bytes(static_cast<int>(pl->D)) + rows + r(4 * outw) + pack;
+  n.in = r(static_cast<size_t>(plan_h2d_bytes(pl)));
+  n.out = 4 * (static_cast<size_t>(pl->B) + 1) + 4;  // packing meta + the two counters
   return n;
 }
 
@@ -699,6 +707,7 @@ class ChunkPipeline {
     for (auto& c : inflight_) {  // error path: let the copies finish before the buffers go
       if (c.copied) cudaEventSynchronize(c.copied);
       destroy_events(c);
+      c.arena.discard();
     }
     if (t0_) cudaEventDestroy(t0_);
   }
@@ -724,6 +733,7 @@ class ChunkPipeline {
       if (enq_stream_) cudaStreamSynchronize(enq_stream_);
       cudaStreamSynchronize(ctx_.copy_stream());
       destroy_events(c);
+      c.arena.discard();
       throw;
     }
   }
@@ -784,21 +794,31 @@ class ChunkPipeline {
     pl->palloc(c.d_out, c.out_words, s);
     plan_residues(pl, 0, pl->P, c.d_rows, 0, s);
     plan_crt(pl, c.d_rows, 0, 0, 0, 0, static_cast<int>(pl->D), c.d_out, 0, s);
+    // results packed on the device into the library's block layout (no host decode)
+    const int B = pl->B, D = static_cast<int>(pl->D), W = pl->out_words();
+    c.pk_bytes = pack_bytes_bound(B, D, W);
+    pl->palloc(c.d_nl, static_cast<size_t>(B) * D, s);
+    pl->palloc(c.d_meta, pack_meta_words(B, D), s);
+    pl->palloc(c.d_pk, c.pk_bytes, s);
+    pl->launches += launch_pack(c.d_out, B, D, W, c.d_nl, c.d_meta, c.d_pk, s);
+    c.arena.create(c.pk_bytes, B, /*pinned=*/true);
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.copied, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventRecord(c.computed, s));
     if (trace()) CTG_CUDA_CHECK(cudaEventRecord(c.t_computed, s));
     CTG_CUDA_CHECK(cudaStreamWaitEvent(cp, c.computed, 0));
     uint32_t* ho = hout_ + c.out_off;
-    CTG_CUDA_CHECK(cudaMemcpyAsync(ho + c.out_words, pl->d_counters, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
-    CTG_CUDA_CHECK(cudaMemcpyAsync(ho, c.d_out, sizeof(uint32_t) * c.out_words, cudaMemcpyDeviceToHost, cp));
+    const size_t mw = 4 * (static_cast<size_t>(B) + 1);
+    CTG_CUDA_CHECK(cudaMemcpyAsync(ho + mw, pl->d_counters, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp));
+    CTG_CUDA_CHECK(cudaMemcpyAsync(ho, c.d_meta, 4 * mw, cudaMemcpyDeviceToHost, cp));
+    CTG_CUDA_CHECK(cudaMemcpyAsync(c.arena.members(), c.d_pk, c.pk_bytes, cudaMemcpyDeviceToHost, cp));
     CTG_CUDA_CHECK(cudaEventRecord(c.copied, cp));
     if (trace()) {
       CTG_CUDA_CHECK(cudaEventRecord(c.t_copied, cp));
       c.host_enqueued_ms = std::chrono::duration<double, std::milli>(clk::now() - host0_).count();
     }
     pl->last_stream = cp;
-    st_.d2h_bytes += static_cast<int64_t>(sizeof(uint32_t) * (c.out_words + 2));
+    st_.d2h_bytes += static_cast<int64_t>(c.pk_bytes + 4 * (mw + 2));
     inflight_.push_back(std::move(c));
     enq_stream_ = nullptr;
     st_.h2d_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
@@ -819,23 +839,17 @@ class ChunkPipeline {
       t0 = clk::now();
       ctg_plan* pl = c.pl.get();
       const uint32_t* ho = hout_ + c.out_off;
+      const size_t mw = 4 * (static_cast<size_t>(pl->B) + 1);
       st_.kernel_launches += pl->launches;
-      st_.flagged_units += static_cast<int32_t>(ho[c.out_words]);
-      const uint32_t bits = ho[c.out_words + 1];
+      st_.flagged_units += static_cast<int32_t>(ho[mw]);
+      const uint32_t bits = ho[mw + 1];
       if (bits && err_.empty()) err_ = "resultant: device self-check failed (error bits " + std::to_string(bits) + ")";
       if (err_.empty()) {
-        // Decode the chunk into one refcounted arena (one allocation for its curves).
-        std::vector<DecodeSize> sz(pl->B);
-        parallel_for(pl->B, [&](int b) { sz[b] = decode_size(pl, ho + c.per_curve * b); });
-        std::vector<size_t> off(pl->B + 1, 0);
-        for (int b = 0; b < pl->B; ++b) off[b + 1] = off[b] + upoly_block_bytes(sz[b].nc, sz[b].total);
-        UpolyArena arena;
-        arena.create(off[pl->B], pl->B);
-        parallel_for(pl->B, [&](int b) {
-          ctg_upoly_buf* o = &out_[c.idx[b]];
-          arena.place(o, off[b], sz[b].nc, sz[b].total);
-          decode_fill(pl, ho + c.per_curve * b, sz[b], o);
-        });
+        // the packed blocks are already in the arena: set the result pointers
+        for (int b = 0; b < pl->B; ++b) c.arena.place(&out_[c.idx[b]], ho[4 * b + 2], ho[4 * b], ho[4 * b + 1]);
+        c.arena.base = nullptr;  // owned by the results now
+      } else {
+        c.arena.discard();
       }
       if (trace()) {
         float a = 0, b = 0, d = 0;

@@ -150,5 +150,12 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
 // Fills twinv[k][i] = omega_k^{-i} for all primes of a table (one launch, at table build).
 void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv);
 int launch_crt(const CrtParams& cp, cudaStream_t st);
+// Device packing of B CRT outputs [B][D][W] into result blocks (api_common layout, back to back):
+// meta [B + 1][4] u32 = (n_coeffs, total limbs, byte offset, -) per curve, meta[4 B] = bytes;
+// nl scratch [B][D].  pack_bytes_bound = the image size for any result of the plan.
+int launch_pack(const uint32_t* d_out, int B, int D, int W, uint32_t* d_nl, uint32_t* d_meta, uint8_t* d_pk,
+                cudaStream_t st);
+size_t pack_bytes_bound(int B, int D, int W);
+size_t pack_meta_words(int B, int D);  // meta + the per-block partial sums (device words)
 
 }  // namespace ctg

@@ -1700,6 +1700,144 @@ __global__ void __launch_bounds__(128) k_crt_fixup(CrtParams C, int nt, int LW) 
   if (lane == 0) rowp[-1] = static_cast<uint32_t>(neg ? -1 : (nonzero ? 1 : 0));
 }
 
+// ---------------------------------------------------------------------------
+// Result packing on the device (ctg_resultant_batch): the CRT records [B][D][W] (sign word +
+// LM limbs per coefficient) become the library's result blocks exactly as the host would build
+// them (api_common: [16-byte header][limb_off n+1][limbs total][sign n], padded to 16 bytes,
+// blocks of consecutive curves back to back), so the D2H lands straight in the page-locked
+// result arena and the host only sets pointers.  meta[b] = (n_coeffs, total limbs, byte offset).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pack_block_bytes(uint32_t n, uint32_t total) {
+  return (16u + 4u * (n + 1u) + 4u * total + n + 15u) & ~15u;
+}
+
+// (1) limb counts: CTA (256 coefficients, curve); partial (max nonzero index + 1, limb sum)
+__global__ void __launch_bounds__(256) k_pack_size(const uint32_t* __restrict__ out, int D, int W,
+                                                   uint32_t* __restrict__ nl, uint32_t* __restrict__ part) {
+  __shared__ int s_max[8];
+  __shared__ unsigned long long s_sum[8];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  const int j = blockIdx.x * blockDim.x + tid;
+  int jmax = -1;
+  unsigned long long sum = 0;
+  if (j < D) {
+    const uint32_t* rec = out + (static_cast<size_t>(b) * D + j) * W;
+    int n = W - 1;
+    while (n > 0 && rec[n] == 0u) --n;
+    const int v = rec[0] != 0u ? n : 0;
+    nl[static_cast<size_t>(b) * D + j] = static_cast<uint32_t>(v);
+    if (v) jmax = j;
+    sum = static_cast<unsigned long long>(v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((tid & 31) == 0) {
+    s_max[tid >> 5] = jmax;
+    s_sum[tid >> 5] = sum;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) {
+      jmax = max(jmax, s_max[w]);
+      sum += s_sum[w];
+    }
+    uint32_t* pp = part + 2 * (static_cast<size_t>(b) * gridDim.x + blockIdx.x);
+    pp[0] = static_cast<uint32_t>(jmax + 1);
+    pp[1] = static_cast<uint32_t>(sum);
+  }
+}
+
+// (2) per curve: n_coeffs, total limbs (limbs beyond the last nonzero coefficient are 0) and the
+//     block's byte offset (blocks back to back in curve order)
+__global__ void k_pack_offsets(int B, int nblk, const uint32_t* __restrict__ part, uint32_t* __restrict__ meta) {
+  uint32_t off = 0;
+  for (int b = 0; b < B; ++b) {
+    uint32_t n = 0, total = 0;
+    for (int q = 0; q < nblk; ++q) {
+      n = max(n, part[2 * (b * nblk + q)]);
+      total += part[2 * (b * nblk + q) + 1];
+    }
+    meta[4 * b] = n;
+    meta[4 * b + 1] = total;
+    meta[4 * b + 2] = off;
+    off += pack_block_bytes(n, total);
+  }
+  meta[4 * B] = off;
+}
+
+// (3) per curve: header, limb_off (exclusive scan of the counts) and the sign bytes
+__global__ void __launch_bounds__(256) k_pack_index(const uint32_t* __restrict__ out, int D, int W,
+                                                    const uint32_t* __restrict__ nl, const uint32_t* __restrict__ meta,
+                                                    uint8_t* __restrict__ pk) {
+  __shared__ uint32_t s_wsum[8];
+  __shared__ uint32_t s_carry;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = meta[4 * b], total = meta[4 * b + 1];
+  uint8_t* base = pk + meta[4 * b + 2];
+  uint32_t* loff = reinterpret_cast<uint32_t*>(base + 16);
+  int8_t* sg = reinterpret_cast<int8_t*>(loff + n + 1 + total);
+  const uint32_t* nlb = nl + static_cast<size_t>(b) * D;
+  if (tid < 4) reinterpret_cast<uint32_t*>(base)[tid] = 0u;
+  if (tid == 0) s_carry = 0u;
+  __syncthreads();
+  for (uint32_t j0 = 0; j0 < n; j0 += blockDim.x) {
+    const uint32_t j = j0 + tid;
+    const uint32_t v = j < n ? nlb[j] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = s_carry;
+    for (int w = 0; w < warp; ++w) before += s_wsum[w];
+    if (j < n) {
+      loff[j] = before + x - v;
+      sg[j] = v ? static_cast<int8_t>(static_cast<int32_t>(out[(static_cast<size_t>(b) * D + j) * W])) : static_cast<int8_t>(0);
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_carry = before + x;
+    __syncthreads();
+  }
+  if (tid == 0) loff[n] = total;
+}
+
+// (4) limbs: a warp per coefficient over the whole grid, lanes along the limbs (coalesced)
+__global__ void __launch_bounds__(256) k_pack_copy(const uint32_t* __restrict__ out, int D, int W,
+                                                   const uint32_t* __restrict__ nl, const uint32_t* __restrict__ meta,
+                                                   uint8_t* __restrict__ pk) {
+  const int b = blockIdx.y, lane = threadIdx.x & 31;
+  const uint32_t j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t n = meta[4 * b];
+  if (j >= n) return;
+  const uint32_t* loff = reinterpret_cast<const uint32_t*>(pk + meta[4 * b + 2] + 16);
+  uint32_t* limbs = reinterpret_cast<uint32_t*>(pk + meta[4 * b + 2] + 16) + n + 1;
+  const uint32_t o = loff[j], c = nl[static_cast<size_t>(b) * D + j];
+  const uint32_t* rec = out + (static_cast<size_t>(b) * D + j) * W + 1;
+  for (uint32_t l = lane; l < c; l += 32) limbs[o + l] = rec[l];
+}
+
+int launch_pack(const uint32_t* d_out, int B, int D, int W, uint32_t* d_nl, uint32_t* d_meta, uint8_t* d_pk,
+                cudaStream_t st) {
+  if (B == 0) return 0;
+  const int nblk = (D + 255) / 256;
+  uint32_t* part = d_meta + 4 * (static_cast<size_t>(B) + 1);  // [B][nblk][2] after the meta
+  k_pack_size<<<dim3(nblk, B), 256, 0, st>>>(d_out, D, W, d_nl, part);
+  k_pack_offsets<<<1, 1, 0, st>>>(B, nblk, part, d_meta);
+  k_pack_index<<<B, 256, 0, st>>>(d_out, D, W, d_nl, d_meta, d_pk);
+  k_pack_copy<<<dim3((D + 7) / 8, B), 256, 0, st>>>(d_out, D, W, d_nl, d_meta, d_pk);
+  return 4;
+}
+
+size_t pack_meta_words(int B, int D) { return 4 * (static_cast<size_t>(B) + 1) + 2 * static_cast<size_t>(B) * ((D + 255) / 256); }
+
+size_t pack_bytes_bound(int B, int D, int W) {
+  return static_cast<size_t>(B) * ((16u + 4u * (static_cast<size_t>(D) + 1) + 4u * static_cast<size_t>(D) * (W - 1) + D + 15u) & ~static_cast<size_t>(15));
+}
+
 // 2D u8 tensor map (K-major rows of `kbytes` bytes), SWIZZLE_128B boxes of 128 B x box_rows.
 static bool make_u8_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t kbytes, uint32_t box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
