@@ -36,3 +36,28 @@ def test_conventions_without_computation():
 def test_no_cpu_fallback():
     with pytest.raises(P.CudaError):
         P.resultant({(0, 2): 1, (1, 0): -1}, {(0, 1): 2})
+
+
+@pytest.mark.skipif(P.device_count() > 0, reason="GPU present")
+def test_no_cpu_fallback_any_entry_point():
+    """Every compute entry point -- including the r2 batch, device-list and communicator paths --
+    raises CudaError on a machine without a GPU instead of computing on the CPU."""
+    f = {(0, 2): 1, (1, 0): -1}
+    fy = {(0, 1): 2}
+    for call in (lambda: P.yun_squarefree([1, 0, -2, 0, 1]),
+                 lambda: P.yun_squarefree_batch([[1, 0, -2, 0, 1], [-2, 0, 1]]),
+                 lambda: P.gcd_univariate([-1, 0, 1], [-1, 1]),
+                 lambda: P.square_free_part([1, 2, 1]),
+                 lambda: P.gcd_bivariate(f, fy),
+                 lambda: P.resultant_batch([(f, fy)] * 3),
+                 lambda: P.resultant_batch([(f, fy)] * 3, devices=[0, 0])):
+        with pytest.raises(P.CudaError):
+            call()
+
+
+def test_opts_layout_matches_header():
+    """ctg_opts is 32 bytes in both the header (int32 device, verify, n_devices, reserved0,
+    pointer devices, pointer comm) and the ctypes mirror."""
+    import ctypes
+    assert ctypes.sizeof(P._Opts) == 32
+    assert P._Opts.devices.offset == 16 and P._Opts.comm.offset == 24
