@@ -63,9 +63,26 @@ struct PlanDeviceGuard {
   ~PlanDeviceGuard();
 };
 
+// The square-freeness probe a single-curve ctg_resultant leaves behind (lift.cpp:64-67 calls
+// yun_squarefree(R) right after resultant): gcd(R, R') modulo three of the resultant's own
+// primes, run on its interpolated residues while the host decodes R.  ctg_yun_squarefree
+// uses it when its input equals R exactly (compared limb by limb with the copy kept here).
+struct SqfProbeCache {
+  bool valid = false;
+  int n = -1;                        // deg R
+  std::vector<int8_t> sign;          // R itself (trimmed CSR)
+  std::vector<uint32_t> off, limbs;
+  uint32_t* d_rows = nullptr;        // 3 rows of plain residues
+  size_t d_cap = 0;                  // words
+  int32_t* d_io = nullptr;           // [2] meta (offset, degree) + [2 * 3] results
+  int32_t* h_out = nullptr;          // pinned copy of the results
+  cudaEvent_t done = nullptr;
+};
+
 // Per-device context: one non-blocking stream, grow-only device scratch and pinned staging.
 struct Ctx {
   std::mutex mu;
+  SqfProbeCache probe;
   int device = -1;
   cudaStream_t stream = nullptr;
   std::vector<void*> scratch;

@@ -30,6 +30,7 @@
 #include "api_common.hpp"
 #include "comm.hpp"
 #include "internal.hpp"
+#include "uni_internal.hpp"
 
 namespace ctg {
 
@@ -675,6 +676,7 @@ struct Chunk {
   uint8_t* d_pk = nullptr;
   size_t pk_bytes = 0;
   UpolyArena arena;
+  bool probed = false;  // a square-freeness probe of this (single-curve) result was launched
   cudaEvent_t computed = nullptr, copied = nullptr;
   cudaEvent_t t_begin = nullptr, t_computed = nullptr, t_copied = nullptr;  // CTG_TRACE_HOST only
   double host_enqueued_ms = 0;
@@ -701,8 +703,9 @@ class ChunkPipeline {
  public:
   // nstreams: compute streams the chunks rotate over (measured: 3 for four or more blocks, as
   // 256 d20 curves in 32 | 64 | 64 | 64 | 32; 2 for fewer, as 64 d30 curves in 8 | 48 | 8).
-  ChunkPipeline(Ctx& ctx, ctg_upoly_buf* out, int nstreams)
-      : ctx_(ctx), out_(out), st_(stats_tls()), nstreams_(std::max(1, std::min(3, nstreams))) {}
+  // probe_r: a single-curve call -- leave the square-freeness probe of R behind (SqfProbeCache)
+  ChunkPipeline(Ctx& ctx, ctg_upoly_buf* out, int nstreams, bool probe_r = false)
+      : ctx_(ctx), out_(out), st_(stats_tls()), nstreams_(std::max(1, std::min(3, nstreams))), probe_r_(probe_r) {}
   ~ChunkPipeline() {
     for (auto& c : inflight_) {  // error path: let the copies finish before the buffers go
       if (c.copied) cudaEventSynchronize(c.copied);
@@ -802,9 +805,42 @@ class ChunkPipeline {
     pl->palloc(c.d_pk, c.pk_bytes, s);
     pl->launches += launch_pack(c.d_out, B, D, W, c.d_nl, c.d_meta, c.d_pk, s);
     c.arena.create(c.pk_bytes, B, /*pinned=*/true);
+    // single-curve call: copy three residue rows of R for the probe (before `computed`, so the
+    // slot's rows are not reused under the copy), then launch it behind the result
+    const int rdeg = D - 1;
+    c.probed = probe_r_ && B == 1 && rdeg >= 32 && pl->P >= 3 && sqf_probe_smem(rdeg) <= kUniSmemMax;
+    SqfProbeCache& pc = ctx_.probe;
+    if (c.probed) {
+      pc.valid = false;
+      if (pc.done) CTG_CUDA_CHECK(cudaStreamWaitEvent(s, pc.done, 0));  // a previous probe reads d_rows
+      const size_t words = 3 * static_cast<size_t>(pl->N);
+      if (pc.d_cap < words) {
+        if (pc.d_rows) {
+          CTG_CUDA_CHECK(cudaStreamSynchronize(s));
+          cudaFree(pc.d_rows);
+          pc.d_rows = nullptr;
+        }
+        CTG_CUDA_CHECK(cudaMalloc(&pc.d_rows, 4 * words));
+        pc.d_cap = words;
+      }
+      if (!pc.d_io) CTG_CUDA_CHECK(cudaMalloc(&pc.d_io, 8 * sizeof(int32_t)));
+      if (!pc.h_out) CTG_CUDA_CHECK(cudaMallocHost(&pc.h_out, 8 * sizeof(int32_t)));
+      if (!pc.done) CTG_CUDA_CHECK(cudaEventCreateWithFlags(&pc.done, cudaEventDisableTiming));
+      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.d_rows, c.d_rows, 4 * words, cudaMemcpyDeviceToDevice, s));
+    }
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.copied, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventRecord(c.computed, s));
+    if (c.probed) {
+      pc.h_out[6] = 0;  // (offset, degree) of the one problem, staged through the pinned words
+      pc.h_out[7] = rdeg;
+      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.d_io, pc.h_out + 6, 2 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      pl->launches += launch_sqf_probe(pc.d_rows, static_cast<int>(pl->N), pc.d_io, pc.d_io + 1, 1, 3, pl->tabs->d_pc,
+                                       rdeg, pc.d_io + 2, nullptr, s, /*plain=*/1);
+      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.h_out, pc.d_io + 2, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CTG_CUDA_CHECK(cudaEventRecord(pc.done, s));
+      pc.n = rdeg;
+    }
     if (trace()) CTG_CUDA_CHECK(cudaEventRecord(c.t_computed, s));
     CTG_CUDA_CHECK(cudaStreamWaitEvent(cp, c.computed, 0));
     uint32_t* ho = hout_ + c.out_off;
@@ -848,6 +884,16 @@ class ChunkPipeline {
         // the packed blocks are already in the arena: set the result pointers
         for (int b = 0; b < pl->B; ++b) c.arena.place(&out_[c.idx[b]], ho[4 * b + 2], ho[4 * b], ho[4 * b + 1]);
         c.arena.base = nullptr;  // owned by the results now
+        if (c.probed) {  // remember exactly which polynomial the probe is about
+          const ctg_upoly_buf& r = out_[c.idx[0]];
+          SqfProbeCache& pc = ctx_.probe;
+          if (r.n_coeffs - 1 == pc.n) {
+            pc.sign.assign(r.sign, r.sign + r.n_coeffs);
+            pc.off.assign(r.limb_off, r.limb_off + r.n_coeffs + 1);
+            pc.limbs.assign(r.limbs, r.limbs + r.limb_off[r.n_coeffs]);
+            pc.valid = true;
+          }
+        }
       } else {
         c.arena.discard();
       }
@@ -896,6 +942,7 @@ class ChunkPipeline {
   int n_enqueued_ = 0;
   int nstreams_ = 2;
   cudaStream_t enq_stream_ = nullptr;
+  bool probe_r_ = false;
   std::chrono::steady_clock::time_point host0_;
 };
 
@@ -1358,7 +1405,7 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
         dev = select_device(opts);
         Ctx& ctx = context(dev);
         lock = std::unique_lock<std::mutex>(ctx.mu);
-        pipe = std::make_unique<ChunkPipeline>(ctx, out, bounds.size() >= 6 ? 3 : 2);
+        pipe = std::make_unique<ChunkPipeline>(ctx, out, bounds.size() >= 6 ? 3 : 2, /*probe_r=*/batch == 1);
       }
       return *pipe;
     };

@@ -75,6 +75,18 @@ ZPoly parse_upoly(const ctg_upoly* p) {
 }
 
 int zdeg(const ZPoly& p) { return static_cast<int>(p.size()) - 1; }
+// The input equals the polynomial the resultant's probe ran on (signs and limbs, exactly).
+bool probe_matches(const SqfProbeCache& pc, const std::vector<Slot>& slots) {
+  if (static_cast<int>(slots.size()) != pc.n + 1 || pc.sign.size() != slots.size()) return false;
+  for (size_t i = 0; i < slots.size(); ++i) {
+    const Slot& c = slots[i];
+    const uint32_t len = pc.off[i + 1] - pc.off[i];
+    if (c.sign != pc.sign[i] || static_cast<uint32_t>(c.n) != len) return false;
+    if (len && std::memcmp(c.mag, pc.limbs.data() + pc.off[i], 4 * static_cast<size_t>(len)) != 0) return false;
+  }
+  return true;
+}
+
 // The caller's CSR polynomial as trimmed slots (pointers into its limbs; validated like
 // parse_upoly; trailing zero coefficients dropped).
 std::vector<Slot> view_upoly(const ctg_upoly* p) {
@@ -1245,6 +1257,14 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       lock = std::unique_lock<std::mutex>(ctx->mu);
     };
     YunProbe probe;
+    // R straight from a single-curve ctg_resultant (CurveContext, lift.cpp:64-67): its probe ran
+    // on the GPU behind the resultant -- use it when the input is exactly that R
+    int cached = -1;  // -1 no, 0 probed and not certified, 1 certified square-free
+    if (n >= kProbeMinDeg) {
+      device();
+      const SqfProbeCache& pc = ctx->probe;
+      if (pc.valid && pc.n == n && probe_matches(pc, slots)) cached = 0;  // read after the content
+    }
     // square-freeness probe on the GPU while the host takes the content -- only where
     // yun_modular would probe too (its full prime set exceeds one wave of CTAs), so a
     // non-square-free input never pays for it twice
@@ -1256,7 +1276,7 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       const double need = log2_upper(slots.back().mag, slots.back().n) + n + 0.5 * log2_sum_upper(sq) + 2 + 40;
       probe_first = select_uni_primes(need + 62).size() > 148;
     }
-    if (probe_first) {
+    if (probe_first && cached < 0) {
       device();
       probe_start(probe, slots, n, dev, ctx->stream, L);
     }
@@ -1268,7 +1288,13 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       timer.finish();
       return;
     }
-    const bool certified = probe.done && probe_finish(probe);
+    if (cached == 0) {  // the resultant's probe has had the content computation to finish
+      const SqfProbeCache& pc = ctx->probe;
+      CTG_CUDA_CHECK(cudaEventSynchronize(pc.done));
+      for (int k = 0; k < 3; ++k)
+        if (pc.h_out[2 * k] == 0 && pc.h_out[2 * k + 1] == 0) cached = 1;
+    }
+    const bool certified = cached >= 0 ? cached == 1 : (probe.done && probe_finish(probe));
     if (certified && big_is_one(content)) {  // (R / sgn(lc), 1): straight from the caller's limbs
       timer.mark_device();
       stats_tls().kernel_launches = L.n;
@@ -1285,7 +1311,7 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       return;
     }
     device();
-    YunResult r = yun_modular(P, false, dev, ctx->stream, L, probe_first);
+    YunResult r = yun_modular(P, false, dev, ctx->stream, L, probe_first || cached >= 0);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
     fill_sqf(content, s, r.factors, out, r.squarefree ? &P : nullptr);

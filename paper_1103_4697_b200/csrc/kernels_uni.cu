@@ -240,7 +240,7 @@ template <bool GB>
 __global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ off,
                                                    const int32_t* __restrict__ degs, int nk,
                                                    const PrimeConst* __restrict__ pc, int cap, int32_t* out,
-                                                   uint32_t* gbuf) {
+                                                   uint32_t* gbuf, int plain) {
   extern __shared__ uint32_t sm[];
   const int i = blockIdx.x / nk, k = blockIdx.x % nk;
   const int n = degs[i];
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ 
   uint32_t* X = cta_buffers<GB>(sm, gbuf, 2 * static_cast<size_t>(cap));
   uint32_t* Y = X + cap;
   const uint32_t* row = tab + static_cast<size_t>(k) * S + off[i];
-  for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = row[t];
+  for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = plain ? mmul(row[t], M.r2, M) : row[t];
   __syncthreads();
   int32_t* o = out + 2 * (static_cast<size_t>(i) * nk + k);
   if (X[n] == 0u) {
@@ -502,15 +502,15 @@ int uni_threads(int n) {
 }
 
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
-                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st) {
+                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain) {
   if (nprob == 0) return 0;
   const int cap = max_deg + 2;
   const size_t smem = smem_or_global(k_sqf_probe<false>, sqf_probe_smem(max_deg), gbuf);
   if (smem == SIZE_MAX) return -1;
   if (smem)
-    k_sqf_probe<false><<<nprob * nk, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr);
+    k_sqf_probe<false><<<nprob * nk, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
   else
-    k_sqf_probe<true><<<nprob * nk, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf);
+    k_sqf_probe<true><<<nprob * nk, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
   return 1;
 }
 

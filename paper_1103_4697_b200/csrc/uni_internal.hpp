@@ -19,8 +19,9 @@ size_t modgcd_smem(int na, int nb);
 size_t bigcd_probe_smem(int nf, int ng);
 size_t sqf_probe_smem(int max_deg);
 // Batched square-freeness probe: CTA per (problem, prime); out[2 (i nk + k)] = (status, deg gcd(P, P')).
+// plain = 1: the table holds plain residues (e.g. a resultant's interpolated rows), else Montgomery.
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
-                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st);
+                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain = 0);
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
                   uint32_t* sqf, uint32_t* gbuf, cudaStream_t st);
 // tab_pitch: words between the rows of consecutive primes for both operands (0: na + 1 / nb + 1)
