@@ -223,3 +223,24 @@ def test_yun_squarefree_batch_matches_single_calls():
     assert got == [P.yun_squarefree(p) for p in polys]
     with pytest.raises(P.PreconditionError):
         P.yun_squarefree_batch([[1, 1], []])
+
+
+def test_resultant_probe_reuse_exact_match_only():
+    """A single-curve resultant leaves a square-freeness probe of R behind; yun_squarefree uses it
+    only for exactly that R.  A different input of the same degree right after it -- here
+    (x + 1)^2 (x^(d-2) + 3), not square-free -- must get its own factorization."""
+    import math
+    f = curves.make("dense", 20, 64, 3)
+    R = P.resultant(f, curves.derive_y(f))
+    d = len(R) - 1
+    cont = 0
+    for c in R:
+        cont = math.gcd(cont, c)
+    sgn = -1 if R[-1] < 0 else 1
+    assert P.yun_squarefree(R) == (sgn * cont, [([sgn * c // cont for c in R], 1)])
+    P.resultant(f, curves.derive_y(f))  # the probe of R again
+    import curvetop_oracle as O  # checker only
+    h = [3] + [0] * (d - 3) + [1]
+    Q = O.u_mul(O.u_mul([1, 1], [1, 1]), h)
+    assert len(Q) - 1 == d
+    assert P.yun_squarefree(Q) == (1, [(h, 1), ([1, 1], 2)])
