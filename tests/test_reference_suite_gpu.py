@@ -40,3 +40,20 @@ def test_reference_suite_on_gpu_elim(binary, args, cases, checks):
     assert m and a, summary[-2000:]
     assert (int(m.group(1)), int(m.group(3))) == (cases, 0)
     assert (int(a.group(1)), int(a.group(3))) == (checks, 0)
+
+
+@pytest.mark.parametrize("binary,args,cases,checks", [c for c in CASES if c[0] in ("test_elim_gpu", "test_bisolve_gpu")],
+                         ids=["test_elim_gpu", "test_bisolve_gpu"])
+def test_reference_suite_prime_sharded(binary, args, cases, checks):
+    """The same reference tests with CTG_DEVICES=0,0,0: every curvetop::resultant the reference's
+    callers make runs prime-sharded over three shards (here all on cuda:0: the device-copy
+    exchange) through ctg_opts.n_devices -- the multi-GPU product path behind the unchanged API."""
+    path = os.path.join(REF, binary)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (make -C oracle gpu_tests in the build container)")
+    env = dict(os.environ, CTG_DEVICES="0,0,0")
+    r = subprocess.run([path, *args], capture_output=True, text=True, timeout=600, env=env)
+    summary = r.stdout + r.stderr
+    assert r.returncode == 0, summary[-3000:]
+    a = re.search(r"assertions: (\d+) \| (\d+) passed \| (\d+) failed", summary)
+    assert a and (int(a.group(1)), int(a.group(3))) == (checks, 0), summary[-2000:]
