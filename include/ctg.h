@@ -238,6 +238,14 @@ ctg_status ctg_comm_all_gather(ctg_comm* comm, const void* d_send, void* d_recv,
  * Montgomery two-product reductions (modarith.cuh mmul2) per second. */
 ctg_status ctg_microbench_int(int32_t device, double* imad_per_s, double* imad_wide_per_s, double* mmul2_per_s);
 
+/* Test and A/B hook of K6's remainder-sequence kernels (no reference counterpart): deg gcd(a, b)
+ * over F_p for p = the prime_index-th (0..15) univariate prime, a[0..na] and b[0..nb] plain
+ * residues < p; method 0 = the blocked (Lehmer-style) kernel the square-freeness probe runs,
+ * 1 = one CTA pass per Euclid step.  *deg = -1 when both vanish; *prime = p, *ms = kernel time
+ * (either may be NULL). */
+ctg_status ctg_modp_gcd_degree(const uint32_t* a, int32_t na, const uint32_t* b, int32_t nb, int32_t prime_index,
+                               int32_t method, int32_t* deg, uint32_t* prime, float* ms, const ctg_opts* opts);
+
 #ifdef __cplusplus
 }
 #endif

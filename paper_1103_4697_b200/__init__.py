@@ -114,7 +114,7 @@ EXPORTS = (
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
     "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch", "ctg_gcd_bivariate", "ctg_bipoly_free",
     "ctg_comm_unique_id", "ctg_comm_init_rank", "ctg_comm_destroy", "ctg_comm_all_gather",
-    "ctg_yun_squarefree_batch",
+    "ctg_yun_squarefree_batch", "ctg_modp_gcd_degree",
 )
 
 _lib = None
@@ -155,6 +155,9 @@ def lib():
         L.ctg_plan_stage.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         L.ctg_microbench_int.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
+        L.ctg_modp_gcd_degree.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.POINTER(C.c_float),
+                                          C.POINTER(_Opts)]
         L.ctg_plan_crt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         L.ctg_plan_crt_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                            C.c_void_p, C.c_void_p]
@@ -336,6 +339,30 @@ def microbench_int(device=None) -> dict:
     _check(lib().ctg_microbench_int(-1 if device is None else int(device), C.byref(a), C.byref(b), C.byref(c)),
            "microbench")
     return {"imad_per_s": a.value, "imad_wide_per_s": b.value, "mmul2_per_s": c.value}
+
+
+def uni_prime(prime_index: int = 0, device=None, method: int = 0) -> int:
+    """The prime_index-th univariate (K6) prime, or with method=2 the prime_index-th (0..2)
+    square-freeness probe prime (< 2^15)."""
+    z = (C.c_uint32 * 1)(0)
+    p, d = C.c_uint32(), C.c_int32()
+    _check(lib().ctg_modp_gcd_degree(z, 0, z, 0, int(prime_index), int(method), C.byref(d), C.byref(p), None,
+                                     _opts(device)), "modp_gcd_degree")
+    return p.value
+
+
+def modp_gcd_degree(a, b, prime_index: int = 0, method: int = 0, device=None) -> dict:
+    """deg gcd(a mod p, b mod p) over F_p for p = uni_prime(prime_index) (K6 test / A-B hook,
+    ``ctg_modp_gcd_degree``); a, b: integer coefficients, ascending.  method 0 = the blocked
+    Lehmer kernel, 1 = one pass per Euclid step, 2 = the blocked kernel in the probe's 32-bit
+    arithmetic modulo the prime_index-th probe prime (< 2^15).  Returns {"deg", "prime", "ms"}."""
+    p = uni_prime(prime_index, device, method if method == 2 else 0)
+    A = (C.c_uint32 * len(a))(*[int(v) % p for v in a])
+    B = (C.c_uint32 * len(b))(*[int(v) % p for v in b])
+    d, pp, ms = C.c_int32(), C.c_uint32(), C.c_float()
+    _check(lib().ctg_modp_gcd_degree(A, len(a) - 1, B, len(b) - 1, int(prime_index), int(method), C.byref(d),
+                                     C.byref(pp), C.byref(ms), _opts(device)), "modp_gcd_degree")
+    return {"deg": d.value, "prime": pp.value, "ms": ms.value}
 
 
 def device_count() -> int:

@@ -51,6 +51,18 @@ struct Slot {
 // Primes of the univariate path: (2^30, 2^30.4), the window where the fused two-elimination
 // pass of blk_gcd (a three-product sum, mmul3) needs one Montgomery reduction.
 std::vector<uint32_t> select_uni_primes(double need_bits) { return select_primes(1, need_bits, kResPrimeMax); }
+
+// Square-freeness probe primes: the three largest primes below 2^15 above max(n, 2^14) (a prime
+// p not dividing lc(P) with deg gcd(P, P') = 0 mod p certifies P square-free; p > n keeps the
+// derivative's degree).  Small primes run the probe in 32-bit arithmetic (lehmer::SmallA).
+std::vector<uint32_t> select_probe_primes(int n) {
+  std::vector<uint32_t> out;
+  const uint32_t lo = std::max<uint32_t>(static_cast<uint32_t>(std::max(n, 0)), 1u << 14);
+  for (uint32_t p = (1u << 15) - 1; p > lo && out.size() < 3; p -= 2)
+    if (is_prime_u32(p)) out.push_back(p);
+  if (out.size() < 3) out.clear();
+  return out;
+}
 constexpr int kProbeMinDeg = 32;  // Yun inputs from this degree get the early square-freeness probe
 
 ZPoly parse_upoly(const ctg_upoly* p) {
@@ -581,7 +593,9 @@ int32_t* probe_pinned() {
 // k_sqf_probe CTA per prime (gcd(R, R') mod p only -- the rest of Yun runs only if needed).
 void probe_start(YunProbe& pb, const std::vector<Slot>& slots, int n, int device, cudaStream_t st, Launches& L) {
   pb.n = n;
-  pb.primes = select_uni_primes(3 * 30.0);
+  pb.primes = select_probe_primes(n);
+  const bool small = !pb.primes.empty();
+  if (!small) pb.primes = select_uni_primes(3 * 30.0);
   pb.ar = std::make_unique<DevArena>(st);
   DevArena& ar = *pb.ar;
   const int nk = static_cast<int>(pb.primes.size());
@@ -594,7 +608,7 @@ void probe_start(YunProbe& pb, const std::vector<Slot>& slots, int n, int device
   const size_t gb = uni_gbuf_bytes(sqf_probe_smem(n), nk);
   uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
   L.n += launched(launch_sqf_probe(d_tab, static_cast<int>(slots.size()), d_meta, d_meta + 1, 1, nk, T->d_pc, n, d_out,
-                                   gbuf, ar.st));
+                                   gbuf, ar.st, 0, small));
   CTG_CUDA_CHECK(cudaGetLastError());
   pb.h = probe_pinned();
   CTG_CUDA_CHECK(cudaMemcpyAsync(pb.h, d_out, 8 * static_cast<size_t>(nk), cudaMemcpyDeviceToHost, ar.st));
@@ -1354,7 +1368,9 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
         maxd = std::max(maxd, zdeg(a[b]));
       }
     const int np = static_cast<int>(idx.size());
-    const std::vector<uint32_t> primes = select_uni_primes(3 * 30.0);
+    std::vector<uint32_t> primes = select_probe_primes(maxd);
+    const bool small = !primes.empty();
+    if (!small) primes = select_uni_primes(3 * 30.0);
     const int nk = static_cast<int>(primes.size());
     DevArena ar(ctx.stream);
     thread_local int32_t* h_out = nullptr;
@@ -1370,7 +1386,8 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
       CTG_CUDA_CHECK(cudaMemcpyAsync(d_meta, meta.data(), 4 * meta.size(), cudaMemcpyHostToDevice, ar.st));
       const size_t gb = uni_gbuf_bytes(sqf_probe_smem(maxd), static_cast<size_t>(np) * nk);
       uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
-      L.n += launched(launch_sqf_probe(d_tab, S, d_meta, d_meta + np, np, nk, T->d_pc, maxd, d_out, gbuf, ar.st));
+      L.n += launched(launch_sqf_probe(d_tab, S, d_meta, d_meta + np, np, nk, T->d_pc, maxd, d_out, gbuf, ar.st, 0,
+                                       small));
       CTG_CUDA_CHECK(cudaGetLastError());
       const size_t need = 2 * static_cast<size_t>(np) * nk;
       if (h_cap < need) {
@@ -1530,3 +1547,65 @@ void ctg_bipoly_free(ctg_bipoly_buf* buf) {
 }
 
 }  // extern "C"
+
+ctg_status ctg_modp_gcd_degree(const uint32_t* a, int32_t na, const uint32_t* b, int32_t nb, int32_t prime_index,
+                               int32_t method, int32_t* deg, uint32_t* prime, float* ms, const ctg_opts* opts) {
+  using namespace ctg;
+  return guarded([&] {
+    if (!a || !b || !deg || na < 0 || nb < 0 || prime_index < 0 || prime_index > 15 || method < 0 || method > 2 ||
+        (method == 2 && prime_index > 2))
+      throw ApiError(CTG_INVALID, "modp_gcd_degree: bad arguments");
+    DeviceGuard g(opts);
+    const int dev = select_device(opts);
+    Ctx& ctx = context(dev);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    const std::vector<uint32_t> all = method == 2 ? select_probe_primes(0) : select_uni_primes(30.0 * (prime_index + 1));
+    if (static_cast<int>(all.size()) <= prime_index) throw ApiError(CTG_INTERNAL, "modp_gcd_degree: prime table");
+    const std::vector<uint32_t> one{all[prime_index]};
+    for (int32_t i = 0; i <= na; ++i)
+      if (a[i] >= one[0]) throw ApiError(CTG_INVALID, "modp_gcd_degree: residue >= p");
+    for (int32_t i = 0; i <= nb; ++i)
+      if (b[i] >= one[0]) throw ApiError(CTG_INVALID, "modp_gcd_degree: residue >= p");
+    auto T = get_tables(dev, 1, one);
+    DevArena ar(ctx.stream);
+    uint32_t* d_a = ar.alloc<uint32_t>(na + 1);
+    uint32_t* d_b = ar.alloc<uint32_t>(nb + 1);
+    int32_t* d_out = ar.alloc<int32_t>(1);
+    CTG_CUDA_CHECK(cudaMemcpyAsync(d_a, a, 4 * static_cast<size_t>(na + 1), cudaMemcpyHostToDevice, ar.st));
+    CTG_CUDA_CHECK(cudaMemcpyAsync(d_b, b, 4 * static_cast<size_t>(nb + 1), cudaMemcpyHostToDevice, ar.st));
+    const size_t gb = uni_gbuf_bytes(gcd_degree_smem(na, nb), 1);
+    uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
+    cudaEvent_t e0, e1;
+    CTG_CUDA_CHECK(cudaEventCreate(&e0));
+    CTG_CUDA_CHECK(cudaEventCreate(&e1));
+    CTG_CUDA_CHECK(cudaEventRecord(e0, ar.st));
+    // CTG_LEHMER_PROF=1: phase cycles of the blocked kernel (printed to stderr; A/B only)
+    static const bool prof_on = std::getenv("CTG_LEHMER_PROF") != nullptr;
+    unsigned long long* d_prof = nullptr;
+    if (prof_on) {
+      d_prof = ar.alloc<unsigned long long>(8);
+      CTG_CUDA_CHECK(cudaMemsetAsync(d_prof, 0, 64, ar.st));
+    }
+    const int rc = launch_gcd_degree(d_a, na, d_b, nb, T->d_pc, method, d_out, gbuf, ar.st, d_prof);
+    CTG_CUDA_CHECK(cudaEventRecord(e1, ar.st));
+    CTG_CUDA_CHECK(cudaGetLastError());
+    int32_t h = 0;
+    CTG_CUDA_CHECK(cudaMemcpyAsync(&h, d_out, 4, cudaMemcpyDeviceToHost, ar.st));
+    CTG_CUDA_CHECK(cudaStreamSynchronize(ar.st));
+    float t = 0.f;
+    CTG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc < 0) throw ApiError(CTG_INTERNAL, "modp_gcd_degree: no scratch");
+    if (d_prof) {
+      unsigned long long hp[8];
+      CTG_CUDA_CHECK(cudaMemcpy(hp, d_prof, 64, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "lehmer prof n=%d: leaf %llu, bottom %llu, top %llu cycles; blocks %llu, gap passes %llu\n",
+                   na, hp[0], hp[1], hp[2], hp[3], hp[4]);
+    }
+    *deg = h;
+    if (prime) *prime = one[0];
+    if (ms) *ms = t;
+    stats_tls().kernel_launches = 1;
+  });
+}

@@ -14,6 +14,7 @@
 
 #include "internal.hpp"
 #include "uni_internal.hpp"
+#include "lehmer.cuh"
 
 namespace ctg {
 namespace {
@@ -234,21 +235,25 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
 // Batched square-freeness probe (ctg_yun_squarefree_batch): CTA per (problem i, prime k);
 // problem i's residues mod p_k are slots [off[i], off[i] + n_i] of row k (pitch S) of one K1
 // table.  out[2 (i nk + k)] = status (0 ok, 1 lc(P) = 0 mod p), out[+1] = deg gcd(P, P') mod p.
-// Two polynomial buffers of cap words (the largest degree + 2).
+// Four polynomial buffers of cap words (the largest degree + 2): lehmer::blk_gcd_degree.
 // ---------------------------------------------------------------------------
-template <bool GB>
+template <bool GB, bool SMALL>
 __global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ off,
                                                    const int32_t* __restrict__ degs, int nk,
                                                    const PrimeConst* __restrict__ pc, int cap, int32_t* out,
                                                    uint32_t* gbuf, int plain) {
   extern __shared__ uint32_t sm[];
+  __shared__ __align__(16) uint32_t Ms[2 * 128];
+  __shared__ int ctl[4];
   const int i = blockIdx.x / nk, k = blockIdx.x % nk;
   const int n = degs[i];
   const Mod M = load_mod_u(pc[k]);
-  uint32_t* X = cta_buffers<GB>(sm, gbuf, 2 * static_cast<size_t>(cap));
-  uint32_t* Y = X + cap;
+  uint32_t* X = cta_buffers<GB>(sm, gbuf, 4 * static_cast<size_t>(cap));
+  uint32_t *Y = X + cap, *X2 = X + 2 * cap, *Y2 = X + 3 * cap;
   const uint32_t* row = tab + static_cast<size_t>(k) * S + off[i];
-  for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = plain ? mmul(row[t], M.r2, M) : row[t];
+  // SMALL: K1 residues (Montgomery form, i.e. 2^32 R mod p: a constant multiple of R, the same
+  // gcd degree) read as plain residues modulo a prime < 2^15.
+  for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = (plain && !SMALL) ? mmul(row[t], M.r2, M) : row[t];
   __syncthreads();
   int32_t* o = out + 2 * (static_cast<size_t>(i) * nk + k);
   if (X[n] == 0u) {
@@ -258,12 +263,51 @@ __global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ 
     }
     return;
   }
-  blk_derivative(Y, X, n, M);  // deg n - 1 exactly (p > n, lc != 0)
-  const int dg = blk_gcd(X, n, Y, n - 1, M);
+  int dg;
+  if constexpr (SMALL) {
+    const lehmer::SmallA A = lehmer::make_small(M.p);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) Y[t] = A.mul(static_cast<uint32_t>(t + 1) % M.p, X[t + 1]);
+    __syncthreads();
+    dg = lehmer::blk_gcd_degree(X, n, Y, n - 1, X2, Y2, Ms, ctl, A);
+  } else {
+    blk_derivative(Y, X, n, M);  // deg n - 1 exactly (p > n, lc != 0)
+    dg = lehmer::blk_gcd_degree(X, n, Y, n - 1, X2, Y2, Ms, ctl, lehmer::MontA{M});
+  }
   if (threadIdx.x == 0) {
     o[0] = 0;
     o[1] = dg;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Test / A-B hook (ctg_modp_gcd_degree): deg gcd(a, b) mod one prime, plain residues in,
+// by the blocked kernel (method 0: lehmer::blk_gcd_degree) or one pass per step (1: blk_gcd).
+// ---------------------------------------------------------------------------
+template <bool GB>
+__global__ void __launch_bounds__(256) k_gcd_degree(const uint32_t* __restrict__ a, int na, const uint32_t* __restrict__ b,
+                                                    int nb, const PrimeConst* __restrict__ pc, int cap, int method,
+                                                    int32_t* out, uint32_t* gbuf, unsigned long long* prof) {
+  extern __shared__ uint32_t sm[];
+  __shared__ __align__(16) uint32_t Ms[2 * 128];
+  __shared__ int ctl[4];
+  const Mod M = load_mod_u(pc[0]);
+  uint32_t* X = cta_buffers<GB>(sm, gbuf, 4 * static_cast<size_t>(cap));
+  uint32_t *Y = X + cap, *X2 = X + 2 * cap, *Y2 = X + 3 * cap;
+  for (int t = threadIdx.x; t < cap; t += blockDim.x) {  // method 2: plain residues mod a small prime
+    X[t] = t <= na ? (method == 2 ? a[t] : mmul(a[t], M.r2, M)) : 0u;
+    Y[t] = t <= nb ? (method == 2 ? b[t] : mmul(b[t], M.r2, M)) : 0u;
+  }
+  __syncthreads();
+  const int dx = blk_trim(X, na), dy = blk_trim(Y, nb);
+  int dg;
+  if (method == 0) {
+    dg = lehmer::blk_gcd_degree(X, dx, Y, dy, X2, Y2, Ms, ctl, lehmer::MontA{M}, prof);
+  } else if (method == 2) {
+    dg = lehmer::blk_gcd_degree(X, dx, Y, dy, X2, Y2, Ms, ctl, lehmer::make_small(M.p), prof);
+  } else {
+    dg = blk_gcd(X, dx, Y, dy, M);
+  }
+  if (threadIdx.x == 0) out[0] = dg;
 }
 
 // ---------------------------------------------------------------------------
@@ -475,7 +519,8 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
 size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4; }
-size_t sqf_probe_smem(int max_deg) { return static_cast<size_t>(2) * (max_deg + 2) * 4; }
+size_t gcd_degree_smem(int na, int nb) { return static_cast<size_t>(4) * ((na > nb ? na : nb) + 2) * 4; }
+size_t sqf_probe_smem(int max_deg) { return static_cast<size_t>(4) * (max_deg + 2) * 4; }
 size_t bigcd_probe_smem(int nf, int ng) { return static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4; }
 size_t newton_smem(int N) { return static_cast<size_t>(N) * (kNewtonCols + 1) * 4; }
 
@@ -502,15 +547,37 @@ int uni_threads(int n) {
 }
 
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
-                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain) {
+                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain,
+                     bool small) {
   if (nprob == 0) return 0;
   const int cap = max_deg + 2;
-  const size_t smem = smem_or_global(k_sqf_probe<false>, sqf_probe_smem(max_deg), gbuf);
+  const size_t smem = smem_or_global(small ? k_sqf_probe<false, true> : k_sqf_probe<false, false>,
+                                     sqf_probe_smem(max_deg), gbuf);
+  if (smem == SIZE_MAX) return -1;
+  const int g = nprob * nk;
+  if (smem) {
+    if (small)
+      k_sqf_probe<false, true><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
+    else
+      k_sqf_probe<false, false><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
+  } else {
+    if (small)
+      k_sqf_probe<true, true><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
+    else
+      k_sqf_probe<true, false><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
+  }
+  return 1;
+}
+
+int launch_gcd_degree(const uint32_t* a, int na, const uint32_t* b, int nb, const PrimeConst* pc, int method,
+                      int32_t* out, uint32_t* gbuf, cudaStream_t st, unsigned long long* prof) {
+  const int cap = (na > nb ? na : nb) + 2;
+  const size_t smem = smem_or_global(k_gcd_degree<false>, gcd_degree_smem(na, nb), gbuf);
   if (smem == SIZE_MAX) return -1;
   if (smem)
-    k_sqf_probe<false><<<nprob * nk, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
+    k_gcd_degree<false><<<1, 256, smem, st>>>(a, na, b, nb, pc, cap, method, out, nullptr, prof);
   else
-    k_sqf_probe<true><<<nprob * nk, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
+    k_gcd_degree<true><<<1, 256, 0, st>>>(a, na, b, nb, pc, cap, method, out, gbuf, prof);
   return 1;
 }
 

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "internal.hpp"
 
 namespace ctg {
@@ -20,8 +22,16 @@ size_t bigcd_probe_smem(int nf, int ng);
 size_t sqf_probe_smem(int max_deg);
 // Batched square-freeness probe: CTA per (problem, prime); out[2 (i nk + k)] = (status, deg gcd(P, P')).
 // plain = 1: the table holds plain residues (e.g. a resultant's interpolated rows), else Montgomery.
+// small: the primes are probe primes < 2^15 (api_uni.cu select_probe_primes; K1 residues), run with the
+// 32-bit Barrett arithmetic of lehmer::SmallA.
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
-                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain = 0);
+                     const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain = 0,
+                     bool small = false);
+
+// deg gcd(a, b) mod pc[0] (plain residues; method 0 blocked Lehmer, 1 one pass per step) -> out[0].
+size_t gcd_degree_smem(int na, int nb);
+int launch_gcd_degree(const uint32_t* a, int na, const uint32_t* b, int nb, const PrimeConst* pc, int method,
+                      int32_t* out, uint32_t* gbuf, cudaStream_t st, unsigned long long* prof = nullptr);
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
                   uint32_t* sqf, uint32_t* gbuf, cudaStream_t st);
 // tab_pitch: words between the rows of consecutive primes for both operands (0: na + 1 / nb + 1)
