@@ -20,6 +20,7 @@ void __gmpz_import(ctg_mpz_struct*, size_t, int, size_t, int, size_t, const void
 void* __gmpz_export(void*, size_t*, int, size_t, int, size_t, const ctg_mpz_struct*);
 void __gmpz_gcd(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_divexact(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
+void __gmpz_set(ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_tdiv_r(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_mul(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 size_t __gmpz_sizeinbase(const ctg_mpz_struct*, int);

@@ -318,6 +318,30 @@ Big big_divexact(const Big& a, const Big& b) {
   return q.big();
 }
 
+size_t big_divexact_to(const uint32_t* a, int na, const Big& c, uint32_t* q) {
+  // per-thread scratch (no allocation once warm): x = a, y = c (re-read only when c changes)
+  thread_local Mpz x, y, r;
+  thread_local Big yc;
+  if (c.empty()) throw std::runtime_error("big_divexact_to: zero divisor");
+  while (na && a[na - 1] == 0) --na;
+  if (!na) return 0;
+  if (yc != c) {
+    Mpz t(c);
+    __gmpz_set(&y.z, &t.z);
+    yc = c;
+  }
+  const size_t nl = (static_cast<size_t>(na) + 1) / 2;
+  unsigned long* d = __gmpz_limbs_write(&x.z, static_cast<long>(nl));
+  d[nl - 1] = 0;
+  std::memcpy(d, a, 4 * static_cast<size_t>(na));
+  __gmpz_limbs_finish(&x.z, static_cast<long>(nl));
+  __gmpz_divexact(&r.z, &x.z, &y.z);
+  size_t n = 2 * static_cast<size_t>(r.z._mp_size < 0 ? -r.z._mp_size : r.z._mp_size);
+  if (n) std::memcpy(q, r.z._mp_d, 4 * n);
+  while (n && q[n - 1] == 0) --n;
+  return n;
+}
+
 void sbig_add_inplace(SBig& acc, int sign, const uint32_t* limbs, int n) {
   Big b(limbs, limbs + n);
   big_trim(b);

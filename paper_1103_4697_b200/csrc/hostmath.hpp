@@ -48,6 +48,9 @@ Big big_mul(const Big& a, const Big& b);
 Big big_gcd(const Big& a, const Big& b);
 // a / b for an exact divisor b != 0 (throws if the remainder is nonzero).
 Big big_divexact(const Big& a, const Big& b);
+// a / c for c dividing a (not checked): writes the quotient's limbs to q (room for na - |c| + 4
+// limbs) and returns their count.  Thread-local GMP scratch: no allocation per call.
+size_t big_divexact_to(const uint32_t* a, int na, const Big& c, uint32_t* q);
 // a mod p for a u32 modulus.
 inline uint32_t big_mod(const Big& a, uint32_t p) { return big_mod_u32(a.data(), static_cast<int>(a.size()), p); }
 inline bool big_is_one(const Big& a) { return a.size() == 1 && a[0] == 1; }
