@@ -132,6 +132,19 @@ cudaStream_t Ctx::prio_stream(int level) {
   return prio[level];
 }
 
+cudaStream_t Ctx::probe_stream() {
+  if (!probe) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CTG_CUDA_CHECK(cudaSetDevice(device));
+    int least = 0, greatest = 0;
+    CTG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CTG_CUDA_CHECK(cudaStreamCreateWithPriority(&probe, cudaStreamNonBlocking, least));
+    cudaSetDevice(prev);
+  }
+  return probe;
+}
+
 uint8_t* Ctx::pinned_input(size_t bytes) {
   bytes = std::max<size_t>(16, bytes);
   if (pinned_in_bytes < bytes) {

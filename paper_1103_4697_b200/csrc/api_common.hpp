@@ -70,19 +70,26 @@ struct PlanDeviceGuard {
 struct SqfProbeCache {
   bool valid = false;
   int n = -1;                        // deg R
-  std::vector<int8_t> sign;          // R itself (trimmed CSR)
-  std::vector<uint32_t> off, limbs;
-  uint32_t* d_rows = nullptr;        // 3 rows of plain residues
-  size_t d_cap = 0;                  // words
-  int32_t* d_io = nullptr;           // [2] meta (offset, degree) + [2 * 3] results
-  int32_t* h_out = nullptr;          // pinned copy of the results
-  cudaEvent_t done = nullptr;
+  // Two slots, alternating per call, so a probe still running never holds up the next result
+  // (its inputs are copied on the compute stream; the probe runs on a low-priority stream).
+  struct Slot {
+    uint32_t* d_rows = nullptr;      // 3 rows of plain residues
+    size_t d_cap = 0;                // words
+    int32_t* d_out = nullptr;        // [2 * 3] results
+    int32_t* h_out = nullptr;        // pinned copy of the results
+    uint8_t* d_blk = nullptr;        // R in the library's block layout (device copy of the packed result)
+    uint8_t* h_blk = nullptr;        // ... and its pinned host copy (DMA behind the probe: no host time)
+    size_t blk_cap = 0;
+    cudaEvent_t done = nullptr;      // probe results and h_blk are ready
+  };
+  Slot slot[2];
+  int cur = 0;                       // slot of the latest probe
+  size_t blk_off = 0, blk_total = 0; // R's block in h_blk: byte offset, limbs (n + 1 coefficients)
 };
-
 // Per-device context: one non-blocking stream, grow-only device scratch and pinned staging.
 struct Ctx {
   std::mutex mu;
-  SqfProbeCache probe;
+  SqfProbeCache sqf;
   int device = -1;
   cudaStream_t stream = nullptr;
   std::vector<void*> scratch;
@@ -102,6 +109,8 @@ struct Ctx {
   int nprio = 0;
   int prio_levels();
   cudaStream_t prio_stream(int level);
+  cudaStream_t probe = nullptr;           // lowest priority: the square-freeness probe left behind results
+  cudaStream_t probe_stream();
   uint32_t* scratch_u32(int slot, size_t words);
   uint32_t* pinned_u32(size_t words);     // D2H staging
   uint8_t* pinned_input(size_t bytes);    // H2D staging

@@ -809,36 +809,52 @@ class ChunkPipeline {
     // slot's rows are not reused under the copy), then launch it behind the result
     const int rdeg = D - 1;
     c.probed = probe_r_ && B == 1 && rdeg >= 32 && pl->P >= 3 && sqf_probe_smem(rdeg) <= kUniSmemMax;
-    SqfProbeCache& pc = ctx_.probe;
+    SqfProbeCache& pc = ctx_.sqf;
+    const int pj = pc.cur ^ 1;
+    SqfProbeCache::Slot& sl = pc.slot[pj];
     if (c.probed) {
       pc.valid = false;
-      if (pc.done) CTG_CUDA_CHECK(cudaStreamWaitEvent(s, pc.done, 0));  // a previous probe reads d_rows
+      if (sl.done) CTG_CUDA_CHECK(cudaStreamWaitEvent(s, sl.done, 0));  // the probe two calls back reads sl's rows
       const size_t words = 3 * static_cast<size_t>(pl->N);
-      if (pc.d_cap < words) {
-        if (pc.d_rows) {
-          CTG_CUDA_CHECK(cudaStreamSynchronize(s));
-          cudaFree(pc.d_rows);
-          pc.d_rows = nullptr;
+      if (sl.d_cap < words) {
+        if (sl.d_rows) {
+          CTG_CUDA_CHECK(cudaStreamSynchronize(ctx_.probe_stream()));
+          cudaFree(sl.d_rows);
+          sl.d_rows = nullptr;
         }
-        CTG_CUDA_CHECK(cudaMalloc(&pc.d_rows, 4 * words));
-        pc.d_cap = words;
+        CTG_CUDA_CHECK(cudaMalloc(&sl.d_rows, 4 * words));
+        sl.d_cap = words;
       }
-      if (!pc.d_io) CTG_CUDA_CHECK(cudaMalloc(&pc.d_io, 8 * sizeof(int32_t)));
-      if (!pc.h_out) CTG_CUDA_CHECK(cudaMallocHost(&pc.h_out, 8 * sizeof(int32_t)));
-      if (!pc.done) CTG_CUDA_CHECK(cudaEventCreateWithFlags(&pc.done, cudaEventDisableTiming));
-      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.d_rows, c.d_rows, 4 * words, cudaMemcpyDeviceToDevice, s));
+      if (!sl.d_out) CTG_CUDA_CHECK(cudaMalloc(&sl.d_out, 8 * sizeof(int32_t)));
+      if (!sl.h_out) CTG_CUDA_CHECK(cudaMallocHost(&sl.h_out, 8 * sizeof(int32_t)));
+      if (!sl.done) CTG_CUDA_CHECK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+      if (sl.blk_cap < c.pk_bytes) {
+        if (sl.d_blk) {
+          CTG_CUDA_CHECK(cudaStreamSynchronize(ctx_.probe_stream()));
+          cudaFree(sl.d_blk);
+          cudaFreeHost(sl.h_blk);
+          sl.d_blk = sl.h_blk = nullptr;
+        }
+        CTG_CUDA_CHECK(cudaMalloc(&sl.d_blk, c.pk_bytes));
+        CTG_CUDA_CHECK(cudaMallocHost(&sl.h_blk, c.pk_bytes));
+        sl.blk_cap = c.pk_bytes;
+      }
+      CTG_CUDA_CHECK(cudaMemcpyAsync(sl.d_rows, c.d_rows, 4 * words, cudaMemcpyDeviceToDevice, s));
+      CTG_CUDA_CHECK(cudaMemcpyAsync(sl.d_blk, c.d_pk, c.pk_bytes, cudaMemcpyDeviceToDevice, s));
     }
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.computed, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventCreateWithFlags(&c.copied, cudaEventDisableTiming));
     CTG_CUDA_CHECK(cudaEventRecord(c.computed, s));
-    if (c.probed) {
-      pc.h_out[6] = 0;  // (offset, degree) of the one problem, staged through the pinned words
-      pc.h_out[7] = rdeg;
-      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.d_io, pc.h_out + 6, 2 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      pl->launches += launch_sqf_probe(pc.d_rows, static_cast<int>(pl->N), pc.d_io, pc.d_io + 1, 1, 3, pl->tabs->d_pc,
-                                       rdeg, pc.d_io + 2, nullptr, s, /*plain=*/1);
-      CTG_CUDA_CHECK(cudaMemcpyAsync(pc.h_out, pc.d_io + 2, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      CTG_CUDA_CHECK(cudaEventRecord(pc.done, s));
+    if (c.probed) {  // behind the result, on its own low-priority stream: the result never waits for it
+      cudaStream_t ps = ctx_.probe_stream();
+      CTG_CUDA_CHECK(cudaStreamWaitEvent(ps, c.computed, 0));
+      pl->launches += launch_sqf_probe(sl.d_rows, static_cast<int>(pl->N), nullptr, nullptr, 1, 3, pl->tabs->d_pc,
+                                       rdeg, sl.d_out, nullptr, ps, /*plain=*/1, /*small=*/false, /*single_deg=*/rdeg);
+      CTG_CUDA_CHECK(cudaMemcpyAsync(sl.h_out, sl.d_out, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, ps));
+      // R itself for the exact input check of the Yun call (probe_matches), by DMA
+      CTG_CUDA_CHECK(cudaMemcpyAsync(sl.h_blk, sl.d_blk, c.pk_bytes, cudaMemcpyDeviceToHost, ps));
+      CTG_CUDA_CHECK(cudaEventRecord(sl.done, ps));
+      pc.cur = pj;
       pc.n = rdeg;
     }
     if (trace()) CTG_CUDA_CHECK(cudaEventRecord(c.t_computed, s));
@@ -884,13 +900,11 @@ class ChunkPipeline {
         // the packed blocks are already in the arena: set the result pointers
         for (int b = 0; b < pl->B; ++b) c.arena.place(&out_[c.idx[b]], ho[4 * b + 2], ho[4 * b], ho[4 * b + 1]);
         c.arena.base = nullptr;  // owned by the results now
-        if (c.probed) {  // remember exactly which polynomial the probe is about
-          const ctg_upoly_buf& r = out_[c.idx[0]];
-          SqfProbeCache& pc = ctx_.probe;
-          if (r.n_coeffs - 1 == pc.n) {
-            pc.sign.assign(r.sign, r.sign + r.n_coeffs);
-            pc.off.assign(r.limb_off, r.limb_off + r.n_coeffs + 1);
-            pc.limbs.assign(r.limbs, r.limbs + r.limb_off[r.n_coeffs]);
+        if (c.probed) {  // where R sits in the probe slot's copy of the packed block
+          SqfProbeCache& pc = ctx_.sqf;
+          if (ho[0] - 1 == static_cast<uint32_t>(pc.n)) {
+            pc.blk_off = ho[2];
+            pc.blk_total = ho[1];
             pc.valid = true;
           }
         }
@@ -1405,7 +1419,10 @@ ctg_status ctg_resultant_batch(int32_t batch, const ctg_bipoly* p, const ctg_bip
         dev = select_device(opts);
         Ctx& ctx = context(dev);
         lock = std::unique_lock<std::mutex>(ctx.mu);
-        pipe = std::make_unique<ChunkPipeline>(ctx, out, bounds.size() >= 6 ? 3 : 2, /*probe_r=*/batch == 1);
+        // CTG_NO_R_PROBE=1 drops the probe left behind single-curve results (A/B only)
+        static const bool no_probe = std::getenv("CTG_NO_R_PROBE") != nullptr;
+        pipe = std::make_unique<ChunkPipeline>(ctx, out, bounds.size() >= 6 ? 3 : 2,
+                                               /*probe_r=*/batch == 1 && !no_probe);
       }
       return *pipe;
     };

@@ -87,14 +87,22 @@ ZPoly parse_upoly(const ctg_upoly* p) {
 }
 
 int zdeg(const ZPoly& p) { return static_cast<int>(p.size()) - 1; }
-// The input equals the polynomial the resultant's probe ran on (signs and limbs, exactly).
+// The input equals the polynomial the resultant's probe ran on (signs and limbs, exactly),
+// compared with the slot's pinned copy of R's block (the caller has synchronised on its event).
 bool probe_matches(const SqfProbeCache& pc, const std::vector<Slot>& slots) {
-  if (static_cast<int>(slots.size()) != pc.n + 1 || pc.sign.size() != slots.size()) return false;
-  for (size_t i = 0; i < slots.size(); ++i) {
+  const SqfProbeCache::Slot& sl = pc.slot[pc.cur];
+  const size_t n = static_cast<size_t>(pc.n) + 1;
+  if (!pc.valid || slots.size() != n || !sl.h_blk) return false;
+  const uint8_t* block = sl.h_blk + pc.blk_off;
+  const uint32_t* off = reinterpret_cast<const uint32_t*>(block + 16);  // after the 16-byte block header
+  const uint32_t* limbs = off + (n + 1);
+  const int8_t* sign = reinterpret_cast<const int8_t*>(limbs + pc.blk_total);
+  if (off[n] != pc.blk_total) return false;
+  for (size_t i = 0; i < n; ++i) {
     const Slot& c = slots[i];
-    const uint32_t len = pc.off[i + 1] - pc.off[i];
-    if (c.sign != pc.sign[i] || static_cast<uint32_t>(c.n) != len) return false;
-    if (len && std::memcmp(c.mag, pc.limbs.data() + pc.off[i], 4 * static_cast<size_t>(len)) != 0) return false;
+    const uint32_t len = off[i + 1] - off[i];
+    if (c.sign != sign[i] || static_cast<uint32_t>(c.n) != len) return false;
+    if (len && std::memcmp(c.mag, limbs + off[i], 4 * static_cast<size_t>(len)) != 0) return false;
   }
   return true;
 }
@@ -1314,10 +1322,11 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
     // R straight from a single-curve ctg_resultant (CurveContext, lift.cpp:64-67): its probe ran
     // on the GPU behind the resultant -- use it when the input is exactly that R
     int cached = -1;  // -1 no, 0 probed and not certified, 1 certified square-free
+    bool candidate = false;  // the latest resultant's R has this degree: compare after the content
     if (n >= kProbeMinDeg) {
       device();
-      const SqfProbeCache& pc = ctx->probe;
-      if (pc.valid && pc.n == n && probe_matches(pc, slots)) cached = 0;  // read after the content
+      const SqfProbeCache& pc = ctx->sqf;
+      candidate = pc.valid && pc.n == n;
     }
     // square-freeness probe on the GPU while the host takes the content -- only where
     // yun_modular would probe too (its full prime set exceeds one wave of CTAs), so a
@@ -1330,7 +1339,7 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       const double need = log2_upper(slots.back().mag, slots.back().n) + n + 0.5 * log2_sum_upper(sq) + 2 + 40;
       probe_first = select_uni_primes(need + 62).size() > 148;
     }
-    if (probe_first && cached < 0) {
+    if (probe_first && !candidate) {
       device();
       probe_start(probe, slots, n, dev, ctx->stream, L);
     }
@@ -1342,11 +1351,15 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
       timer.finish();
       return;
     }
-    if (cached == 0) {  // the resultant's probe has had the content computation to finish
-      const SqfProbeCache& pc = ctx->probe;
-      CTG_CUDA_CHECK(cudaEventSynchronize(pc.done));
-      for (int k = 0; k < 3; ++k)
-        if (pc.h_out[2 * k] == 0 && pc.h_out[2 * k + 1] == 0) cached = 1;
+    if (candidate) {  // the resultant's probe has had the content computation to finish
+      const SqfProbeCache& pc = ctx->sqf;
+      const SqfProbeCache::Slot& sl = pc.slot[pc.cur];
+      CTG_CUDA_CHECK(cudaEventSynchronize(sl.done));
+      if (probe_matches(pc, slots)) {
+        cached = 0;
+        for (int k = 0; k < 3; ++k)
+          if (sl.h_out[2 * k] == 0 && sl.h_out[2 * k + 1] == 0) cached = 1;
+      }
     }
     const bool certified = cached >= 0 ? cached == 1 : (probe.done && probe_finish(probe));
     if (certified) {  // (R / (sgn(lc) content), 1): straight from the caller's limbs
@@ -1358,7 +1371,7 @@ ctg_status ctg_yun_squarefree(const ctg_upoly* p, ctg_sqf_buf* out, const ctg_op
     }
     ZPoly P = divide_content(parse_upoly(p), content, nullptr, nullptr);
     device();
-    YunResult r = yun_modular(P, false, dev, ctx->stream, L, probe_first || cached >= 0);
+    YunResult r = yun_modular(P, false, dev, ctx->stream, L, (probe_first && !candidate) || cached >= 0);
     timer.mark_device();
     stats_tls().kernel_launches = L.n;
     fill_sqf(content, s, r.factors, out, r.squarefree ? &P : nullptr);

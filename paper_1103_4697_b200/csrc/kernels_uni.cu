@@ -241,16 +241,16 @@ template <bool GB, bool SMALL>
 __global__ void __launch_bounds__(256) k_sqf_probe(const uint32_t* __restrict__ tab, int S, const int32_t* __restrict__ off,
                                                    const int32_t* __restrict__ degs, int nk,
                                                    const PrimeConst* __restrict__ pc, int cap, int32_t* out,
-                                                   uint32_t* gbuf, int plain) {
+                                                   uint32_t* gbuf, int plain, int single_deg) {
   extern __shared__ uint32_t sm[];
   __shared__ __align__(16) uint32_t Ms[2 * 128];
   __shared__ int ctl[4];
   const int i = blockIdx.x / nk, k = blockIdx.x % nk;
-  const int n = degs[i];
+  const int n = degs ? degs[i] : single_deg;  // one problem at offset 0 when degs is null
   const Mod M = load_mod_u(pc[k]);
   uint32_t* X = cta_buffers<GB>(sm, gbuf, 4 * static_cast<size_t>(cap));
   uint32_t *Y = X + cap, *X2 = X + 2 * cap, *Y2 = X + 3 * cap;
-  const uint32_t* row = tab + static_cast<size_t>(k) * S + off[i];
+  const uint32_t* row = tab + static_cast<size_t>(k) * S + (off ? off[i] : 0);
   // SMALL: K1 residues (Montgomery form, i.e. 2^32 R mod p: a constant multiple of R, the same
   // gcd degree) read as plain residues modulo a prime < 2^15.
   for (int t = threadIdx.x; t <= n; t += blockDim.x) X[t] = (plain && !SMALL) ? mmul(row[t], M.r2, M) : row[t];
@@ -548,7 +548,7 @@ int uni_threads(int n) {
 
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
                      const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain,
-                     bool small) {
+                     bool small, int single_deg) {
   if (nprob == 0) return 0;
   const int cap = max_deg + 2;
   const size_t smem = smem_or_global(small ? k_sqf_probe<false, true> : k_sqf_probe<false, false>,
@@ -557,14 +557,14 @@ int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32
   const int g = nprob * nk;
   if (smem) {
     if (small)
-      k_sqf_probe<false, true><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
+      k_sqf_probe<false, true><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain, single_deg);
     else
-      k_sqf_probe<false, false><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain);
+      k_sqf_probe<false, false><<<g, 256, smem, st>>>(tab, S, off, degs, nk, pc, cap, out, nullptr, plain, single_deg);
   } else {
     if (small)
-      k_sqf_probe<true, true><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
+      k_sqf_probe<true, true><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain, single_deg);
     else
-      k_sqf_probe<true, false><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain);
+      k_sqf_probe<true, false><<<g, 256, 0, st>>>(tab, S, off, degs, nk, pc, cap, out, gbuf, plain, single_deg);
   }
   return 1;
 }

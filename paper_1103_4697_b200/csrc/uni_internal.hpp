@@ -26,7 +26,7 @@ size_t sqf_probe_smem(int max_deg);
 // 32-bit Barrett arithmetic of lehmer::SmallA.
 int launch_sqf_probe(const uint32_t* tab, int S, const int32_t* off, const int32_t* degs, int nprob, int nk,
                      const PrimeConst* pc, int max_deg, int32_t* out, uint32_t* gbuf, cudaStream_t st, int plain = 0,
-                     bool small = false);
+                     bool small = false, int single_deg = 0);  // off = degs = null: one problem at 0
 
 // deg gcd(a, b) mod pc[0] (plain residues; method 0 blocked Lehmer, 1 one pass per step) -> out[0].
 size_t gcd_degree_smem(int na, int nb);
