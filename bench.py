@@ -529,26 +529,39 @@ def headline(P, curves, workload, cb):
 
 def yun_line(P, curves, workload):
     """Second §8 row: yun_squarefree(R) through the C ABI for the workload's seed-1 curve
-    (and the singular sheared K=3 family, the Yun stress config), GPU wall ms (median of 5)."""
+    (and the singular sheared K=3 family, the Yun stress config), GPU wall ms (median of 5).
+    "standalone": R from an earlier call (its own K1 + square-freeness probe on the GPU while
+    the host takes the content); "after_resultant": right behind ctg_resultant(f, f_y) of the
+    same curve, as CurveContext calls it (lift.cpp:64-67: the probe the resultant left behind)."""
     out = {}
     kind, a, b, _, _ = WORKLOADS[workload]
+    tiny = curves.make("dense", 8, 10, 1)  # deg R = 56: its call leaves its own probe behind
     for name, (k_, a_, b_) in ((workload, (kind, a, b)), ("sheared_k3", ("sheared", 3, 0))):
         f = curves.make(k_, a_, b_, 1)
+        hf, hq = P.HostBipoly(f), P.HostBipoly(curves.derive_y(f))
         R = P.resultant(f, curves.derive_y(f))
         hp = P.HostUpoly(R)
-        for _ in range(2):
-            P.yun_squarefree_raw(hp)
-        ts, dev = [], []
-        for _ in range(5):
-            t0 = time.perf_counter()
-            fac = P.yun_squarefree_raw(hp)
-            ts.append(1e3 * (time.perf_counter() - t0))
-            dev.append(P.last_call_stats()["device_ms"])
-        out[name] = {"deg_R": len(R) - 1, "gpu_ms_median": statistics.median(ts),
-                     "device_phase_ms_median": statistics.median(dev),
-                     "path": "ctg_yun_squarefree (C ABI), host CSR limbs in/out",
-                     "pattern": "".join(f"({d})^{m}" for d, m in fac),
-                     "kernel_launches": P.last_call_stats()["kernel_launches"]}
+        row = {"deg_R": len(R) - 1, "path": "ctg_yun_squarefree (C ABI), host CSR limbs in/out"}
+        for mode in ("standalone", "after_resultant"):
+            ts, dev, launches = [], [], []
+            for it in range(7):
+                if mode == "standalone":
+                    P.resultant(tiny, curves.derive_y(tiny))  # the probe cache now holds another R
+                else:
+                    P.resultant_raw(hf, hq)
+                t0 = time.perf_counter()
+                fac = P.yun_squarefree_raw(hp)
+                if it >= 2:
+                    ts.append(1e3 * (time.perf_counter() - t0))
+                    st = P.last_call_stats()
+                    dev.append(st["device_ms"])
+                    launches.append(st["kernel_launches"])
+            row[mode] = {"gpu_ms_median": statistics.median(ts), "device_phase_ms_median": statistics.median(dev),
+                         "kernel_launches": launches[-1]}
+        row["pattern"] = "".join(f"({d})^{m}" for d, m in fac)
+        # the standalone call is the headline (no state carried over from the resultant)
+        row["gpu_ms_median"] = row["standalone"]["gpu_ms_median"]
+        out[name] = row
     out["sheared_k3"]["reference_cpu_s"] = 29.2  # SURVEY §6.2, oracle/_ref in the build container
     return out
 
