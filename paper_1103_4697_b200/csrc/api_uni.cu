@@ -192,10 +192,16 @@ Big slots_content(const std::vector<Slot>& p) {
     }
     return g;
   };
-  auto step = [&](const Big& g, const Slot* c) { return g.size() == 1 ? Big{small_gcd(g[0], c)} : big_gcd(g, big(c)); };
+  // g <- gcd(g, c): a word gcd after c mod g for a one-limb g, else GMP on thread-local scratch
+  auto step = [&](Big& g, const Slot* c) {
+    if (g.size() == 1)
+      g = Big{small_gcd(g[0], c)};
+    else
+      big_gcd_update(g, c->mag, c->n);
+  };
   if (order.empty()) return Big();
   Big g = big(order[0]);
-  if (order.size() > 1) g = step(g, order[1]);
+  if (order.size() > 1) g = big_gcd(g, big(order[1]));
   if (big_is_one(g) || order.size() <= 2) return g;
   const int groups = 16;
   std::vector<Big> part(groups);
@@ -203,7 +209,7 @@ Big slots_content(const std::vector<Slot>& p) {
   parallel_for(groups, [&](int t) {
     const size_t i0 = 2 + t * per, i1 = std::min(order.size(), i0 + per);
     Big h = g;
-    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) h = step(h, order[i]);
+    for (size_t i = i0; i < i1 && !big_is_one(h); ++i) step(h, order[i]);
     part[t] = h;
   });
   for (const Big& h : part) g = big_gcd(g, h);
@@ -1389,31 +1395,41 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
     if (!out || !p || batch < 0) throw ApiError(CTG_INVALID, "yun_squarefree_batch: bad arguments");
     CallTimer timer;
     for (int b = 0; b < batch; ++b) std::memset(&out[b], 0, sizeof(out[b]));
-    std::vector<ZPoly> a(batch);
-    parallel_for(batch, [&](int b) { a[b] = parse_upoly(&p[b]); });
-    for (int b = 0; b < batch; ++b)
-      if (a[b].empty())
+    // every input as slots over the caller's CSR (no copies, as ctg_yun_squarefree)
+    std::vector<std::vector<Slot>> sl(batch);
+    for (int b = 0; b < batch; ++b) {
+      sl[b] = view_upoly(&p[b]);
+      if (sl[b].empty())
         throw ApiError(CTG_PRECONDITION, "yun_squarefree: zero polynomial (batch entry " + std::to_string(b) + ")");
+    }
     DeviceGuard g(opts);
     const int dev = select_device(opts);
     Ctx& ctx = context(dev);
     std::lock_guard<std::mutex> lock(ctx.mu);
     Launches L;
-    // probe every input of degree >= 2 (one table, one launch)
+    // probe every input of degree >= 2 (one K1 over all their slots, one launch)
     std::vector<int> idx;
     std::vector<int32_t> off, degs;
-    std::vector<const ZPoly*> polys;
-    int S = 0, maxd = 0;
-    for (int b = 0; b < batch; ++b)
-      if (zdeg(a[b]) >= 2) {
+    std::vector<Slot> all;
+    int maxd = 0;
+    for (int b = 0; b < batch; ++b) {
+      const int d = static_cast<int>(sl[b].size()) - 1;
+      if (d >= 2) {
         idx.push_back(b);
-        off.push_back(S);
-        degs.push_back(zdeg(a[b]));
-        polys.push_back(&a[b]);
-        S += static_cast<int>(a[b].size());
-        maxd = std::max(maxd, zdeg(a[b]));
+        off.push_back(static_cast<int32_t>(all.size()));
+        degs.push_back(d);
+        all.insert(all.end(), sl[b].begin(), sl[b].end());
+        maxd = std::max(maxd, d);
       }
+    }
     const int np = static_cast<int>(idx.size());
+    const int S = static_cast<int>(all.size());
+    static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto tms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t_a = tnow();
     std::vector<uint32_t> primes = select_probe_primes(maxd);
     const bool small = !primes.empty();
     if (!small) primes = select_uni_primes(3 * 30.0);
@@ -1424,7 +1440,7 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
     cudaEvent_t done = nullptr;
     if (np) {
       auto T = get_tables(dev, 1, primes);
-      uint32_t* d_tab = reduce_polys(ar, polys, *T, L);
+      uint32_t* d_tab = reduce_slots(ar, all, *T, L);
       int32_t* d_meta = ar.alloc<int32_t>(2 * static_cast<size_t>(np));
       int32_t* d_out = ar.alloc<int32_t>(2 * static_cast<size_t>(np) * nk);
       std::vector<int32_t> meta(off);
@@ -1448,10 +1464,15 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
       stats_tls().d2h_bytes += static_cast<int64_t>(4 * need);
     }
     // contents on the host while the GPU probes (elim.cpp:141-144)
+    const auto t_b = tnow();
     std::vector<Big> content(batch);
     std::vector<int> sgn(batch, 0);
-    std::vector<ZPoly> P(batch);
-    parallel_for(batch, [&](int b) { P[b] = zprimitive_positive(std::move(a[b]), &content[b], &sgn[b]); });
+    parallel_for(batch, [&](int b) {
+      content[b] = slots_content(sl[b]);
+      sgn[b] = sl[b].back().sign;
+    });
+    if (trace) std::fprintf(stderr, "[ctg] yun batch %d: probe enqueue (K1 staging) %.3f ms, contents %.3f ms\n", batch,
+                            tms(t_a, t_b), tms(t_b, tnow()));
     timer.mark_setup();
     std::vector<char> sqfree(batch, 0);
     if (done) {
@@ -1465,20 +1486,19 @@ ctg_status ctg_yun_squarefree_batch(int32_t batch, const ctg_upoly* p, ctg_sqf_b
     }
     timer.mark_device();
     try {
-      // certified / constant inputs: fill the outputs in parallel; the rest one by one
+      // constants and certified square-free inputs: (R / (sgn content), 1) straight from the
+      // caller's limbs, in parallel; the rest through the full modular Yun one by one
       parallel_for(batch, [&](int b) {
-        if (zdeg(P[b]) == 0)  // elim.cpp:145
+        if (sl[b].size() == 1)  // elim.cpp:145
           fill_sqf(content[b], sgn[b], {}, &out[b]);
         else if (sqfree[b])
-          fill_sqf(content[b], sgn[b], {}, &out[b], &P[b]);
+          fill_sqf(content[b], sgn[b], {}, &out[b], nullptr, &sl[b], big_is_one(content[b]) ? nullptr : &content[b]);
       });
       for (int b = 0; b < batch; ++b) {
-        if (zdeg(P[b]) == 0 || sqfree[b]) {
-          continue;
-        } else {
-          YunResult r = yun_modular(P[b], false, dev, ctx.stream, L);
-          fill_sqf(content[b], sgn[b], r.factors, &out[b], r.squarefree ? &P[b] : nullptr);
-        }
+        if (sl[b].size() == 1 || sqfree[b]) continue;
+        ZPoly Pb = divide_content(parse_upoly(&p[b]), content[b], nullptr, nullptr);
+        YunResult r = yun_modular(Pb, false, dev, ctx.stream, L);
+        fill_sqf(content[b], sgn[b], r.factors, &out[b], r.squarefree ? &Pb : nullptr);
       }
     } catch (...) {
       for (int b = 0; b < batch; ++b) ctg_sqf_free(&out[b]);

@@ -318,6 +318,31 @@ Big big_divexact(const Big& a, const Big& b) {
   return q.big();
 }
 
+bool big_gcd_update(Big& g, const uint32_t* c, int n) {
+  thread_local Mpz x, y, r;
+  thread_local Big yc;
+  while (n && c[n - 1] == 0) --n;
+  if (!n) return false;  // gcd(g, 0) = g
+  if (yc != g) {
+    Mpz t(g);
+    __gmpz_set(&y.z, &t.z);
+    yc = g;
+  }
+  const size_t nl = (static_cast<size_t>(n) + 1) / 2;
+  unsigned long* d = __gmpz_limbs_write(&x.z, static_cast<long>(nl));
+  d[nl - 1] = 0;
+  std::memcpy(d, c, 4 * static_cast<size_t>(n));
+  __gmpz_limbs_finish(&x.z, static_cast<long>(nl));
+  __gmpz_gcd(&r.z, &y.z, &x.z);
+  if (r.z._mp_size == y.z._mp_size &&
+      std::memcmp(r.z._mp_d, y.z._mp_d, 8 * static_cast<size_t>(r.z._mp_size < 0 ? -r.z._mp_size : r.z._mp_size)) == 0)
+    return false;
+  g = r.big();
+  yc = g;
+  __gmpz_set(&y.z, &r.z);
+  return true;
+}
+
 size_t big_divexact_to(const uint32_t* a, int na, const Big& c, uint32_t* q) {
   // per-thread scratch (no allocation once warm): x = a, y = c (re-read only when c changes)
   thread_local Mpz x, y, r;

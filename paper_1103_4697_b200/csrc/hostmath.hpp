@@ -48,6 +48,9 @@ Big big_mul(const Big& a, const Big& b);
 Big big_gcd(const Big& a, const Big& b);
 // a / b for an exact divisor b != 0 (throws if the remainder is nonzero).
 Big big_divexact(const Big& a, const Big& b);
+// g <- gcd(g, c) for u32 limbs c[0..n) (g nonzero); thread-local GMP scratch, no allocation
+// unless g changes.  Returns true if it changed.
+bool big_gcd_update(Big& g, const uint32_t* c, int n);
 // a / c for c dividing a (not checked): writes the quotient's limbs to q (room for na - |c| + 4
 // limbs) and returns their count.  Thread-local GMP scratch: no allocation per call.
 size_t big_divexact_to(const uint32_t* a, int na, const Big& c, uint32_t* q);
