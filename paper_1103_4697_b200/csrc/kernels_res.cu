@@ -1538,7 +1538,7 @@ __global__ void __launch_bounds__(128)
   for (int q = 0; q < nch; ++q) s += C.upart[(static_cast<size_t>(b) * nch + q) * C.J + jl];
   const double tr = rint(s);
   if (live && ti == 0 && fabs(s - tr) > 1e-6) atomicOr(&C.counters[1], kErrCrtRound);
-  const long long t = static_cast<long long>(tr);
+  const int t32 = static_cast<int>(tr);  // t < P
   constexpr int LW = BN / 4, PITCH = LW + 1;  // limbs per segment, staging pitch (conflict-free)
   uint32_t* stg = reinterpret_cast<uint32_t*>(sm.a);  // the pipeline stages (a then b, contiguous) are free now
   const uint4* m8 = reinterpret_cast<const uint4*>(C.M8) + n0 / 4;
@@ -1554,10 +1554,11 @@ __global__ void __launch_bounds__(128)
       const uint4 m = __ldg(&m8[c0 / 4 + q]);
       // the 4-digit group's value sum_e (C_e - t M_e) 256^e (|C_e| < 2^31: < 2^57) first, off the
       // carry chain; then ONE dependent 64-bit add and shift per limb
-      const long long g = (static_cast<long long>(static_cast<int>(v[4 * q])) - t * static_cast<long long>(m.x)) +
-                          ((static_cast<long long>(static_cast<int>(v[4 * q + 1])) - t * static_cast<long long>(m.y)) << 8) +
-                          ((static_cast<long long>(static_cast<int>(v[4 * q + 2])) - t * static_cast<long long>(m.z)) << 16) +
-                          ((static_cast<long long>(static_cast<int>(v[4 * q + 3])) - t * static_cast<long long>(m.w)) << 24);
+      // C_e - t M_e in int32 (C_e < 4 P 255^2 < 2^31, t M_e < P 255), then widened
+      const long long g = static_cast<long long>(static_cast<int>(v[4 * q]) - t32 * static_cast<int>(m.x)) +
+                          (static_cast<long long>(static_cast<int>(v[4 * q + 1]) - t32 * static_cast<int>(m.y)) << 8) +
+                          (static_cast<long long>(static_cast<int>(v[4 * q + 2]) - t32 * static_cast<int>(m.z)) << 16) +
+                          (static_cast<long long>(static_cast<int>(v[4 * q + 3]) - t32 * static_cast<int>(m.w)) << 24);
       const long long x = carry + g;
       const uint32_t limb = static_cast<uint32_t>(x);
       carry = x >> 32;
