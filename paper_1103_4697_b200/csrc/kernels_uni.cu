@@ -152,8 +152,11 @@ template <bool GB>
 __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab, int n, const PrimeConst* __restrict__ pc,
                                                 int32_t* deg, uint32_t* fac, uint32_t* sqf, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
+  __shared__ __align__(16) uint32_t Ms[2 * 128];  // lehmer::blk_gcd_core's matrices and control
+  __shared__ int ctl[4];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
+  const lehmer::MontA MA{M};
   const int cap = n + 2;
   uint32_t* base = cta_buffers<GB>(sm, gbuf, 8 * cap);
   uint32_t* buf[8];
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
   blk_derivative(A1, A0, n, M);  // deg n-1 exactly (p > n, lc != 0)
   blk_copy(X, A0, n);
   blk_copy(Y, A1, n - 1);
-  const int dg = blk_gcd(X, n, Y, n - 1, M);  // monic gcd in X
+  const int dg = lehmer::blk_gcd_core<true>(X, n, Y, n - 1, V, W, Ms, ctl, MA);  // monic gcd in X (V, W: scratch)
   if (dg == 0) {
     blk_monic(A0, n, M);
     blk_store_plain(fk, A0, n, M);
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
     } else {
       blk_copy(X, V, dv);
       blk_copy(Y, W, dz);
-      dh = blk_gcd(X, dv, Y, dz, M);
+      dh = lehmer::blk_gcd_core<true>(X, dv, Y, dz, A0, A1, Ms, ctl, MA);  // A0, A1 are free by now
       H = X;
     }
     if (dh > 0) {
@@ -321,11 +324,14 @@ __global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tab
                                                 const PrimeConst* __restrict__ pc, int32_t* deg, uint32_t* out,
                                                 int pitch, uint32_t* gbuf) {
   extern __shared__ uint32_t sm[];
+  __shared__ __align__(16) uint32_t Ms[2 * 128];  // lehmer::blk_gcd_core's matrices and control
+  __shared__ int ctl[4];
   const int kl = blockIdx.x;
   const Mod M = load_mod_u(pc[kl]);
   const int cap = (na > nb ? na : nb) + 2;
-  uint32_t* base = cta_buffers<GB>(sm, gbuf, 5 * static_cast<size_t>(cap));
-  uint32_t *A = base, *B = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap;
+  uint32_t* base = cta_buffers<GB>(sm, gbuf, 6 * static_cast<size_t>(cap));
+  uint32_t *A = base, *B = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap,
+           *Z = base + 5 * cap;
   const uint32_t* ra = tabA + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : na + 1);
   const uint32_t* rb = tabB + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : nb + 1);
   for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tab
     if (threadIdx.x == 0) deg[kl] = -2;
     return;
   }
-  const int dg = blk_gcd(X, na, Y, nb, M);
+  const int dg = lehmer::blk_gcd_core<true>(X, na, Y, nb, Q, Z, Ms, ctl, lehmer::MontA{M});  // monic gcd in X
   uint32_t* o = out + static_cast<size_t>(kl) * pitch;
   blk_store_plain(o, X, dg, M);
   const int du = blk_divexact_monic(A, na, X, dg, Q, M);
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(kNewtonCols) k_newton_interp(const uint32_t* _
 }  // namespace
 
 size_t modyun_smem(int n) { return static_cast<size_t>(8) * (n + 2) * 4; }
-size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(5) * ((na > nb ? na : nb) + 2) * 4; }
+size_t modgcd_smem(int na, int nb) { return static_cast<size_t>(6) * ((na > nb ? na : nb) + 2) * 4; }
 size_t gcd_degree_smem(int na, int nb) { return static_cast<size_t>(4) * ((na > nb ? na : nb) + 2) * 4; }
 size_t sqf_probe_smem(int max_deg) { return static_cast<size_t>(4) * (max_deg + 2) * 4; }
 size_t bigcd_probe_smem(int nf, int ng) { return static_cast<size_t>(2) * ((nf > ng ? nf : ng) + 2) * 4; }

@@ -63,6 +63,7 @@ struct MontA {
     return static_cast<uint64_t>(static_cast<uint32_t>(t >> 32)) * M.one + static_cast<uint32_t>(t);
   }
   __device__ __forceinline__ uint32_t finish(Acc t) const { return redc(fold(t), M.p, M.pneg); }
+  __device__ __forceinline__ uint32_t inv(uint32_t a) const { return minv(a, M); }
 };
 struct SmallA {
   uint32_t p, m, np;  // m = floor(2^32 / p), np = 2^32 - p (opaque: see make_small)
@@ -87,6 +88,14 @@ struct SmallA {
   __device__ __forceinline__ Acc mac(Acc t, uint32_t a, uint32_t b) const { return t + a * b; }
   __device__ __forceinline__ Acc fold(Acc t) const { return red(t); }
   __device__ __forceinline__ uint32_t finish(Acc t) const { return red(t); }
+  __device__ __forceinline__ uint32_t inv(uint32_t a) const {  // a^(p-2)
+    uint32_t r = 1u, b = a;
+    for (uint32_t e = p - 2; e; e >>= 1) {
+      if (e & 1u) r = mul(r, b);
+      b = mul(b, b);
+    }
+    return r;
+  }
 };
 __device__ __forceinline__ SmallA make_small(uint32_t p) {
   uint32_t np;
@@ -404,15 +413,27 @@ __device__ __forceinline__ void apply_bottom(const uint32_t* Ms, const uint32_t*
   }
 }
 
-// deg gcd(X, Y) over F_p (-1 if both vanish).  X, Y: exact degrees dx, dy, written and
-// synchronised by the caller; X2, Y2: two more buffers of the same capacity (all four are
-// clobbered).  Ms: 2 x 128 words of shared memory, ctl: 4 ints of shared memory.  Every thread
-// of the CTA calls it (blockDim.x a multiple of 128); returns the degree on every thread.
+// Scale X[0..d] to monic in place (lc nonzero); every thread calls it.
+template <class Ar>
+__device__ __forceinline__ void blk_make_monic(uint32_t* X, int d, const Ar& A) {
+  const uint32_t inv = A.inv(X[d]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) X[i] = A.mul(X[i], inv);
+  if (threadIdx.x == 0) X[d] = A.one();
+  __syncthreads();
+}
+
+// gcd(X, Y) over F_p by the blocked remainder sequence.  X, Y: exact degrees dx, dy, written and
+// synchronised by the caller; X2, Y2: two more buffers of the same capacity.  The four buffer
+// pointers are permuted (the caller's set of four stays the same; all are clobbered).
+// FULL = false: returns deg gcd (-1 if both vanish).  FULL = true: also leaves the monic gcd in
+// X (its degree returned).  Ms: 2 x 128 words of shared memory, ctl: 4 ints of shared memory.
+// Every thread of the CTA calls it (blockDim.x a multiple of 128); returns on every thread.
 // prof (A/B hook only, null otherwise): cycles of [0] leaf, [1] bottom rows (warp 1), [2] top rows +
 // barriers (thread 0), [3] blocks, [4] gap passes.
-template <class Ar>
-__device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t* X2, uint32_t* Y2, uint32_t* Ms,
-                              int* ctl, const Ar& A, unsigned long long* prof = nullptr) {
+template <bool FULL, class Ar>
+__device__ int blk_gcd_core(uint32_t*& X, int dx, uint32_t*& Y, int dy, uint32_t*& X2, uint32_t*& Y2, uint32_t* Ms,
+                            int* ctl, const Ar& A, unsigned long long* prof = nullptr) {
   const int tid = threadIdx.x, bs = blockDim.x, warp = tid >> 5;
   // warps off the leaf's sub-partition (warp % 4 != 0) apply the bottom rows during the leaf
   const int napp = (bs >> 5) - ((bs >> 5) + 3) / 4;
@@ -420,6 +441,13 @@ __device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t
   bool pend = false;
   const uint32_t *Xp = nullptr, *Yp = nullptr, *Mp = nullptr;
   int pdx = 0, pdy = 0, cur = 0;
+  auto constant_gcd = [&]() {  // gcd is a nonzero constant: monic 1
+    if constexpr (FULL) {
+      if (tid == 0) X[0] = A.one();
+      __syncthreads();
+    }
+    return 0;
+  };
   for (;;) {
     if (dx < dy) {  // (never with a pending bottom: the leaf hands back dx >= dy when it is exact)
       uint32_t* s = X;
@@ -432,8 +460,13 @@ __device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t
       dx = dy;
       dy = q;
     }
-    if (dy < 0) return dx;
-    if (dy == 0) return 0;
+    if (dy < 0) {  // (X is complete here: no pending bottom)
+      if constexpr (FULL) {
+        if (dx >= 0) blk_make_monic(X, dx, A);
+      }
+      return dx;
+    }
+    if (dy == 0) return constant_gcd();
     if (dx - dy > kMD) {
       // gap beyond M: complete the full polynomials, then one direct elimination pass
       if (pend) {
@@ -474,8 +507,21 @@ __device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t
     const int ndx = ctl[0], st = ctl[2];
     int ndy = ctl[1];
     pend = false;
-    if (st == kConst) return 0;
-    if (st == kDone) return ndx;
+    if (st == kConst) {
+      __syncthreads();  // everyone has read ctl
+      return constant_gcd();
+    }
+    if (st == kDone) {
+      if constexpr (FULL) {  // the gcd is the new X: its full product, then monic
+        apply_bottom(Mc, X, dx, Y, dy, X2, ndx, Y2, -1, tid, bs, A);
+        __syncthreads();
+        uint32_t* s = X;
+        X = X2;
+        X2 = s;
+        blk_make_monic(X, ndx, A);
+      }
+      return ndx;
+    }
     if (st == kUnknown) {
       // full product, then the degree of Y2 from its upper bound
       apply_bottom(Mc, X, dx, Y, dy, X2, ndx, Y2, ndy, tid, bs, A);
@@ -508,6 +554,13 @@ __device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t
     dx = ndx;
     dy = ndy;
   }
+}
+
+// deg gcd(X, Y) over F_p (-1 if both vanish); the four buffers are clobbered.
+template <class Ar>
+__device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t* X2, uint32_t* Y2, uint32_t* Ms,
+                              int* ctl, const Ar& A, unsigned long long* prof = nullptr) {
+  return blk_gcd_core<false>(X, dx, Y, dy, X2, Y2, Ms, ctl, A, prof);
 }
 
 }  // namespace lehmer
