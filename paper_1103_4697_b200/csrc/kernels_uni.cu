@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
     if (threadIdx.x == 0) dk[1] = n;
     return;
   }
-  int dv = blk_divexact_monic(A0, n, X, dg, V, M);      // v = P / g
-  int dw = blk_divexact_monic(A1, n - 1, X, dg, W, M);  // w = P' / g
+  int dv = lehmer::blk_divexact_blocked(A0, n, X, dg, V, MA);      // v = P / g
+  int dw = lehmer::blk_divexact_blocked(A1, n - 1, X, dg, W, MA);  // w = P' / g
   {
     blk_copy(F1, V, dv);
     blk_monic(F1, dv, M);
@@ -222,10 +222,10 @@ __global__ void __launch_bounds__(512) k_modyun(const uint32_t* __restrict__ tab
       off += dh + 1;
       if (threadIdx.x == 0) dk[k] = dh;
     }
-    dv = blk_divexact_monic(V, dv, H, dh, F1, M);
+    dv = lehmer::blk_divexact_blocked(V, dv, H, dh, F1, MA);
     swp(V, F1);
     if (dz >= 0) {
-      dw = blk_divexact_monic(W, dz, H, dh, F2, M);
+      dw = lehmer::blk_divexact_blocked(W, dz, H, dh, F2, MA);
       swp(W, F2);
     } else {
       dw = -1;
@@ -341,13 +341,14 @@ __global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tab
     if (threadIdx.x == 0) deg[kl] = -2;
     return;
   }
-  const int dg = lehmer::blk_gcd_core<true>(X, na, Y, nb, Q, Z, Ms, ctl, lehmer::MontA{M});  // monic gcd in X
+  const lehmer::MontA MA{M};
+  const int dg = lehmer::blk_gcd_core<true>(X, na, Y, nb, Q, Z, Ms, ctl, MA);  // monic gcd in X
   uint32_t* o = out + static_cast<size_t>(kl) * pitch;
   blk_store_plain(o, X, dg, M);
-  const int du = blk_divexact_monic(A, na, X, dg, Q, M);
+  const int du = lehmer::blk_divexact_blocked(A, na, X, dg, Q, MA);
   blk_store_plain(o + dg + 1, Q, du, M);
   __syncthreads();
-  const int dw = blk_divexact_monic(B, nb, X, dg, Q, M);
+  const int dw = lehmer::blk_divexact_blocked(B, nb, X, dg, Q, MA);
   blk_store_plain(o + dg + 1 + du + 1, Q, dw, M);
   if (threadIdx.x == 0) deg[kl] = dg;
 }

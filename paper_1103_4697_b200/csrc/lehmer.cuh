@@ -64,6 +64,7 @@ struct MontA {
   }
   __device__ __forceinline__ uint32_t finish(Acc t) const { return redc(fold(t), M.p, M.pneg); }
   __device__ __forceinline__ uint32_t inv(uint32_t a) const { return minv(a, M); }
+  __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return msub(a, b, M.p); }
 };
 struct SmallA {
   uint32_t p, m, np;  // m = floor(2^32 / p), np = 2^32 - p (opaque: see make_small)
@@ -88,6 +89,7 @@ struct SmallA {
   __device__ __forceinline__ Acc mac(Acc t, uint32_t a, uint32_t b) const { return t + a * b; }
   __device__ __forceinline__ Acc fold(Acc t) const { return red(t); }
   __device__ __forceinline__ uint32_t finish(Acc t) const { return red(t); }
+  __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return a >= b ? a - b : a + p - b; }
   __device__ __forceinline__ uint32_t inv(uint32_t a) const {  // a^(p-2)
     uint32_t r = 1u, b = a;
     for (uint32_t e = p - 2; e; e >>= 1) {
@@ -561,6 +563,57 @@ template <class Ar>
 __device__ int blk_gcd_degree(uint32_t* X, int dx, uint32_t* Y, int dy, uint32_t* X2, uint32_t* Y2, uint32_t* Ms,
                               int* ctl, const Ar& A, unsigned long long* prof = nullptr) {
   return blk_gcd_core<false>(X, dx, Y, dy, X2, Y2, Ms, ctl, A, prof);
+}
+
+// Exact division by a monic divisor, blocked the same way: Q = X / D (deg dq = dx - dd; X
+// destroyed).  Per block of 32 quotient coefficients one warp runs the long division on the top
+// 32 coefficients of X in registers (one broadcast + one product per coefficient and step: the
+// chain is a shuffle and a multiply, not a CTA pass), then the CTA subtracts the block's
+// Q_blk * D from the coefficients below (dot products of length <= 32) and synchronises once.
+// One CTA pass per 32 quotient coefficients instead of one per coefficient (blk_divexact_monic).
+template <class Ar>
+__device__ int blk_divexact_blocked(uint32_t* X, int dx, const uint32_t* D, int dd, uint32_t* Q, const Ar& A) {
+  const int tid = threadIdx.x, bs = blockDim.x, lane = tid & 31;
+  if (dd == 0) {
+    for (int i = tid; i <= dx; i += bs) Q[i] = X[i];
+    __syncthreads();
+    return dx;
+  }
+  const int dq = dx - dd;
+  for (int top = dq; top >= 0; top -= 32) {  // quotient coefficients top .. top - K + 1
+    const int K = top + 1 < 32 ? top + 1 : 32;
+    if (tid < 32) {
+      uint32_t w = lane < K ? X[dd + top - lane] : 0u;  // X's window, top coefficient in lane 0
+      uint32_t sd = lane <= dd ? D[dd - lane] : 0u;     // at step t: lane l holds D[dd - (l - t)]
+      for (int t = 0; t < K; ++t) {
+        const uint32_t q = __shfl_sync(0xffffffffu, w, t);
+        if (lane == t) Q[top - t] = q;
+        if (lane > t) w = A.sub(w, A.mul(q, sd));
+        sd = __shfl_up_sync(0xffffffffu, sd, 1);
+        if (lane == 0) sd = 0u;
+      }
+    }
+    __syncthreads();
+    // the coefficients below the window: X[i] -= sum_t q_t D[i - (top - t)]
+    const int lo = top - K + 1, hi = dd + top - K;
+    for (int i = lo + tid; i <= hi; i += bs) {
+      typename Ar::Acc acc = 0;
+      int n = 0;
+      for (int t = 0; t < K; ++t) {
+        const int j = i - top + t;
+        if (j < 0) continue;
+        if (j > dd) break;
+        acc = A.mac(acc, Q[top - t], D[j]);
+        if (++n == 2 * Ar::kFoldA) {
+          acc = A.fold(acc);
+          n = 0;
+        }
+      }
+      X[i] = A.sub(X[i], A.finish(acc));
+    }
+    __syncthreads();
+  }
+  return dq;
 }
 
 }  // namespace lehmer

@@ -244,3 +244,34 @@ def test_resultant_probe_reuse_exact_match_only():
     Q = O.u_mul(O.u_mul([1, 1], [1, 1]), h)
     assert len(Q) - 1 == d
     assert P.yun_squarefree(Q) == (1, [(h, 1), ([1, 1], 2)])
+
+
+def test_resultant_probe_slots_alternate():
+    """The probe slots alternate per single-curve call: after resultant(f1), resultant(f2), Yun of
+    R1 must run on its own (the cache holds R2) and Yun of R2 must take the cached probe -- both
+    equal to (sgn content, [(pp R, 1)]), and a different non-square-free input of R2's degree
+    right after must get its own factorization."""
+    import math
+
+    import curvetop_oracle as O  # checker only
+
+    def expect(R):
+        cont = 0
+        for c in R:
+            cont = math.gcd(cont, c)
+        sgn = -1 if R[-1] < 0 else 1
+        return (sgn * cont, [([sgn * c // cont for c in R], 1)])
+
+    f1, f2 = curves.make("dense", 16, 64, 5), curves.make("dense", 16, 64, 6)
+    R1 = P.resultant(f1, curves.derive_y(f1))
+    R2 = P.resultant(f2, curves.derive_y(f2))
+    assert P.yun_squarefree(R1) == expect(R1)
+    assert P.last_call_stats()["kernel_launches"] > 0  # its own K1 + probe
+    P.resultant(f1, curves.derive_y(f1))
+    P.resultant(f2, curves.derive_y(f2))
+    assert P.yun_squarefree(R2) == expect(R2)
+    assert P.last_call_stats()["kernel_launches"] == 0  # the probe left behind by resultant(f2)
+    d = len(R2) - 1
+    h = [3] + [0] * (d - 3) + [1]
+    Q = O.u_mul(O.u_mul([1, 1], [1, 1]), h)
+    assert P.yun_squarefree(Q) == (1, [(h, 1), ([1, 1], 2)])
