@@ -1821,9 +1821,75 @@ __global__ void __launch_bounds__(256) k_pack_copy(const uint32_t* __restrict__ 
   for (uint32_t l = lane; l < c; l += 32) limbs[o + l] = rec[l];
 }
 
+// (1-3) in one CTA for a single curve (the latency path: one launch instead of three small
+// ones): limb counts, n_coeffs / total / offset, header, limb_off (block scan) and sign bytes.
+__global__ void __launch_bounds__(1024) k_pack_one(const uint32_t* __restrict__ out, int D, int W,
+                                                   uint32_t* __restrict__ nl, uint32_t* __restrict__ meta,
+                                                   uint8_t* __restrict__ pk) {
+  __shared__ uint32_t s_w[32];
+  __shared__ int s_max[32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // pass 1: counts and the last nonzero coefficient
+  int jmax = -1;
+  for (int j = tid; j < D; j += blockDim.x) {
+    const uint32_t* rec = out + static_cast<size_t>(j) * W;
+    int n = W - 1;
+    while (n > 0 && rec[n] == 0u) --n;
+    const int v = rec[0] != 0u ? n : 0;
+    nl[j] = static_cast<uint32_t>(v);
+    if (v) jmax = j;
+  }
+  for (int o = 16; o; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+  if (lane == 0) s_max[warp] = jmax;
+  if (tid == 0) s_carry = 0u;
+  __syncthreads();
+  if (tid == 0)
+    for (int w = 1; w < nw; ++w) s_max[0] = max(s_max[0], s_max[w]);
+  __syncthreads();
+  const uint32_t n = static_cast<uint32_t>(s_max[0] + 1);
+  uint32_t* loff = reinterpret_cast<uint32_t*>(pk + 16);
+  if (tid < 4) reinterpret_cast<uint32_t*>(pk)[tid] = 0u;
+  // pass 2: exclusive scan of the counts -> limb_off; the sign bytes go after the limbs, so
+  // they are written once the total is known (pass 3)
+  for (uint32_t j0 = 0; j0 < n; j0 += blockDim.x) {
+    const uint32_t j = j0 + tid;
+    const uint32_t v = j < n ? nl[j] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t before = s_carry;
+    for (int w = 0; w < warp; ++w) before += s_w[w];
+    if (j < n) loff[j] = before + x - v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_carry = before + x;
+    __syncthreads();
+  }
+  const uint32_t total = s_carry;
+  if (tid == 0) {
+    loff[n] = total;
+    meta[0] = n;
+    meta[1] = total;
+    meta[2] = 0u;
+    meta[4] = pack_block_bytes(n, total);
+  }
+  int8_t* sg = reinterpret_cast<int8_t*>(loff + n + 1 + total);
+  for (uint32_t j = tid; j < n; j += blockDim.x)
+    sg[j] = nl[j] ? static_cast<int8_t>(static_cast<int32_t>(out[static_cast<size_t>(j) * W])) : static_cast<int8_t>(0);
+}
+
 int launch_pack(const uint32_t* d_out, int B, int D, int W, uint32_t* d_nl, uint32_t* d_meta, uint8_t* d_pk,
                 cudaStream_t st) {
   if (B == 0) return 0;
+  if (B == 1) {  // single curve: counts, offsets and index in one CTA, then the copy
+    k_pack_one<<<1, 1024, 0, st>>>(d_out, D, W, d_nl, d_meta, d_pk);
+    k_pack_copy<<<dim3((D + 7) / 8, 1), 256, 0, st>>>(d_out, D, W, d_nl, d_meta, d_pk);
+    return 2;
+  }
   const int nblk = (D + 255) / 256;
   uint32_t* part = d_meta + 4 * (static_cast<size_t>(B) + 1);  // [B][nblk][2] after the meta
   k_pack_size<<<dim3(nblk, B), 256, 0, st>>>(d_out, D, W, d_nl, part);
