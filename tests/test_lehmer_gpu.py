@@ -6,6 +6,7 @@ squares and common factors (nonzero gcd degree), sparse inputs with large degree
 beyond the matrix's reach, constants, and degrees past the shared-memory budget (global buffers).
 """
 
+import os
 import random
 
 import pytest
@@ -145,3 +146,27 @@ def test_gcd_degree_other_primes():
         G = rand_poly(rng, 12, p)
         f = mul(mul(G, G, p), rand_poly(rng, 200, p), p)
         assert P.modp_gcd_degree(f, derivative(f, p), k, 0, device=0)["deg"] == gcd_deg(f, derivative(f, p), p)
+
+
+def test_gcd_degree_random_stress():
+    """Randomised mix of the structures above (planted common factors, sparse supports with long
+    zero runs, equal and far-apart degrees) in both arithmetics, against Python's Euclid."""
+    rng = random.Random(2024)
+    q = P.uni_prime(1, device=0, method=2)
+    p = P.uni_prime(0, device=0)
+    for it in range(int(os.environ.get("CTG_STRESS_N", "120"))):
+        mod, method, k = (p, 0, 0) if it % 2 == 0 else (q, 2, 1)
+        g = rng.choice([0, 0, 1, 3, 17, 40, 75])
+        G = rand_poly(rng, g, mod)
+
+        def cofactor(n):
+            if rng.random() < 0.3:  # sparse: a few nonzero coefficients, long zero runs
+                c = [0] * n + [rng.randrange(1, mod)]
+                for _ in range(rng.randrange(1, 5)):
+                    c[rng.randrange(0, n + 1)] = rng.randrange(1, mod)
+                return c
+            return rand_poly(rng, n, mod)
+        a = mul(G, cofactor(rng.randrange(1, 300)), mod)
+        b = mul(G, cofactor(rng.randrange(0, 300)), mod) if rng.random() < 0.8 else derivative(a, mod)
+        got = P.modp_gcd_degree(a, b, k, method, device=0)
+        assert got["deg"] == gcd_deg(a, b, mod), (it, method, len(a) - 1, len(b) - 1, got)
