@@ -491,7 +491,9 @@ int64_t plan_h2d_bytes(const ctg_plan* pl) {
 }
 
 // Rows of curve b, prime k in [k0, k1): d_rows + b * curve_stride + (k - k0) * N  (curve_stride 0 = dense).
-void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st) {
+// scatter (stage 3 only): K4 writes the coefficients to the shards' receive blocks instead of d_rows.
+void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st,
+                const RowScatter* scatter = nullptr) {
   if (pl->trivial) return;
   if (!pl->uploaded) throw ApiError(CTG_INVALID, "plan: inputs not uploaded");
   if (k0 < 0 || k1 > pl->P || k0 > k1) throw ApiError(CTG_INVALID, "plan: prime range out of bounds");
@@ -510,7 +512,7 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
     pl->launches += launch_interp(d_rows, rows_bstride, static_cast<int>(pl->N), nk, pl->B, pl->tabs->d_pc,
                                   pl->tabs->d_twinv, k0, static_cast<int>(pl->N), static_cast<int>(pl->r),
                                   static_cast<int>(pl->a), static_cast<int>(pl->D), pl->negate, pl->d_counters, st,
-                                  pl->d_ntt);
+                                  pl->d_ntt, scatter);
     CTG_CUDA_CHECK(cudaGetLastError());
     return;
   }
@@ -544,14 +546,17 @@ void plan_stage(ctg_plan* pl, int stage, int k0, int k1, uint32_t* d_rows, long 
   CTG_CUDA_CHECK(cudaGetLastError());
 }
 
-void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st) {
-  for (int stage = 1; stage <= 3; ++stage) plan_stage(pl, stage, k0, k1, d_rows, curve_stride, st);
+void plan_residues(ctg_plan* pl, int k0, int k1, uint32_t* d_rows, long long curve_stride, cudaStream_t st,
+                   const RowScatter* scatter = nullptr) {
+  for (int stage = 1; stage <= 3; ++stage) plan_stage(pl, stage, k0, k1, d_rows, curve_stride, st, scatter);
 }
 
 // Coefficients [j0, j1) of every curve.  Residues of curve b, prime k at d_all + b * curve_stride
 // + (k / row_block) * block_stride + (k % row_block) * N; output curve b at d_out + b * out_stride.
+// pitch / col0 (a shard's receive block of a fused exchange): rows of `pitch` words holding
+// coefficients [col0, col0 + pitch) (defaults: N words, coefficient 0 first).
 void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int row_block, long long block_stride,
-              int j0, int j1, uint32_t* d_out, long long out_stride, cudaStream_t st) {
+              int j0, int j1, uint32_t* d_out, long long out_stride, cudaStream_t st, int pitch = 0, int col0 = 0) {
   if (pl->trivial) return;
   if (j0 < 0 || j1 > static_cast<int>(pl->D) || j0 > j1) throw ApiError(CTG_INVALID, "plan: coefficient range out of bounds");
   const int J = j1 - j0;
@@ -574,7 +579,8 @@ void plan_crt(ctg_plan* pl, const uint32_t* d_all, long long curve_stride, int r
   cp.B = pl->B;
   cp.rows = d_all;
   cp.curve_stride = curve_stride > 0 ? curve_stride : static_cast<long long>(pl->P) * pl->N;
-  cp.pitch = static_cast<int>(pl->N);
+  cp.pitch = pitch > 0 ? pitch : static_cast<int>(pl->N);
+  cp.col0 = col0;
   cp.P = pl->P;
   cp.row_block = row_block > 0 ? row_block : pl->P;
   cp.block_stride = row_block > 0 ? block_stride : 0;
@@ -1009,6 +1015,7 @@ struct Shard {
   std::unique_ptr<ctg_plan> pl;
   int k0 = 0, k1 = 0, j0 = 0, j1 = 0;
   uint32_t *send = nullptr, *full = nullptr, *crt = nullptr, *gath = nullptr;
+  bool full_pooled = true;  // false: `full` is the device context's receive scratch (fused exchange)
   cudaEvent_t rows_done = nullptr;
   Shard() = default;
   Shard(const Shard&) = delete;
@@ -1020,7 +1027,7 @@ struct Shard {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
     pl->pfree(send);
-    pl->pfree(full);
+    if (full_pooled) pl->pfree(full);
     pl->pfree(crt);
     pl->pfree(gath);
     if (rows_done) cudaEventDestroy(rows_done);
@@ -1028,6 +1035,38 @@ struct Shard {
     cudaSetDevice(prev);
   }
 };
+
+// Peer access between every pair of the distinct devices (enabled once per pair, cached); false
+// if some pair cannot reach the other's memory (then the exchange goes through copies / NCCL).
+static bool enable_peer_access(const std::vector<int>& devs) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  bool ok = true;
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      auto it = done.find({a, b});
+      if (it != done.end()) {
+        ok = ok && it->second;
+        continue;
+      }
+      int can = 0;
+      bool pair_ok = cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can;
+      if (pair_ok) {
+        cudaSetDevice(a);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        pair_ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+      }
+      done[{a, b}] = pair_ok;
+      ok = ok && pair_ok;
+    }
+  cudaSetDevice(prev);
+  return ok;
+}
 
 static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bipoly* q, int32_t eliminate_x,
                                     ctg_upoly_buf* out, const ctg_opts* opts) {
@@ -1059,8 +1098,15 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
   const auto uend = std::unique(distinct.begin(), distinct.end());
   const bool repeated = uend != distinct.end();
   distinct.erase(uend, distinct.end());
+  // Exchange of one process's shards: by default fused into K4 (its epilogue stores every
+  // coefficient straight into the owning shard's receive block: NVLink peer stores, local stores
+  // when shards share a GPU; each shard receives only its coefficient columns -- 1/G of an
+  // all-gather's bytes).  CTG_SHARD_EXCHANGE=copy / nccl: the all-gather of whole rows (NCCL
+  // between distinct devices, device copies otherwise), for A/B and as the fallback.
+  const std::string xmode = std::getenv("CTG_SHARD_EXCHANGE") ? std::getenv("CTG_SHARD_EXCHANGE") : "fused";
+  const bool fused_x = !comm && xmode == "fused" && G <= kMaxScatter && enable_peer_access(distinct);
   // NCCL between distinct devices of one process; device copies when a GPU hosts two shards
-  const bool use_nccl_local = !comm && !repeated && nccl_available();
+  const bool use_nccl_local = !comm && !fused_x && !repeated && xmode != "copy" && nccl_available();
   const std::vector<ncclComm_t>* local_comms = use_nccl_local ? &device_set_comms(local_dev) : nullptr;
 
   std::vector<Problem> probs(batch);
@@ -1083,6 +1129,15 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
   for (auto& [key, all_idx] : groups) {
     for (size_t blk = 0; blk < all_idx.size(); blk += kBlock) {
       std::vector<int> idx(all_idx.begin() + blk, all_idx.begin() + std::min(all_idx.size(), blk + kBlock));
+      static const bool trace = std::getenv("CTG_TRACE_HOST") != nullptr;
+      auto tp = tclk::now();
+      auto lap = [&](const char* what) {
+        if (!trace) return;
+        const auto t = tclk::now();
+        std::fprintf(stderr, "[ctg] sharded G=%d block %zu: %s %.3f ms\n", G, blk, what,
+                     std::chrono::duration<double, std::milli>(t - tp).count());
+        tp = t;
+      };
       std::vector<Shard> sh(local_dev.size());
       std::unique_ptr<ctg_plan> pl0;
       {
@@ -1093,6 +1148,9 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
       const int W = pl0->out_words();
       const int Pb = (Pn + G - 1) / G, Jb = (D + G - 1) / G;
       const size_t rows_words = static_cast<size_t>(B) * Pb * N, crt_words = static_cast<size_t>(B) * Jb * W;
+      // fused exchange: shard r's receive block holds coefficients [r Jb, (r + 1) Jb) of every
+      // prime, [G blocks of primes][B][Pb][Jb]
+      const size_t recv_words = static_cast<size_t>(G) * B * Pb * Jb;
       std::fill(std::begin(nshard_on), std::end(nshard_on), 0);
       for (size_t s = 0; s < sh.size(); ++s) {  // every shard's plan before any upload
         sh[s].device = local_dev[s];
@@ -1114,15 +1172,40 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
         plan_upload(pl, S.st);
         stats.h2d_bytes += plan_h2d_bytes(pl);
         pl->palloc(S.send, rows_words, S.st);
-        pl->palloc(S.full, rows_words * G, S.st);
+        if (fused_x) {  // other GPUs store into it: plain device memory (peer access covers
+                        // cudaMalloc'd memory; stream-ordered pool memory would need pool access)
+          S.full = ctx.scratch_u32(8 + slot, recv_words);
+          S.full_pooled = false;
+        } else {
+          pl->palloc(S.full, rows_words * G, S.st);
+        }
         pl->palloc(S.crt, crt_words, S.st);
         if (comm) pl->palloc(S.gath, crt_words * G, S.st);
-        if (S.k1 > S.k0) plan_residues(pl, S.k0, S.k1, S.send, static_cast<long long>(Pb) * N, S.st);
+      }
+      for (size_t s = 0; s < sh.size(); ++s) {  // every receive block exists before any K4 stores into it
+        Shard& S = sh[s];
+        PlanDeviceGuard g(S.device);
+        RowScatter sc{};
+        if (fused_x) {
+          sc.G = G;
+          sc.Jb = Jb;
+          for (size_t r = 0; r < sh.size(); ++r) sc.dst[sh[r].rank] = sh[r].full;
+          sc.shard_off = static_cast<long long>(S.rank) * B * Pb * Jb;
+          sc.curve_stride = static_cast<long long>(Pb) * Jb;
+        }
+        if (S.k1 > S.k0)
+          plan_residues(S.pl.get(), S.k0, S.k1, S.send, static_cast<long long>(Pb) * N, S.st, fused_x ? &sc : nullptr);
         CTG_CUDA_CHECK(cudaEventCreateWithFlags(&S.rows_done, cudaEventDisableTiming));
         CTG_CUDA_CHECK(cudaEventRecord(S.rows_done, S.st));
       }
-      // exchange: full[h] = send of shard h, on every shard
-      if (comm) {
+      lap("plans + uploads + K1-K4 enqueued");
+      // exchange: full[h] = send of shard h, on every shard (fused: K4 already stored it)
+      if (fused_x) {
+        for (auto& S : sh) {
+          PlanDeviceGuard g(S.device);
+          for (auto& H : sh) CTG_CUDA_CHECK(cudaStreamWaitEvent(S.st, H.rows_done, 0));
+        }
+      } else if (comm) {
         PlanDeviceGuard g(sh[0].device);
         nccl_check(nccl().AllGather(sh[0].send, sh[0].full, rows_words, ncclUint32, comm->nc, sh[0].st), "ncclAllGather");
       } else if (local_comms) {
@@ -1149,9 +1232,14 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
       }
       for (auto& S : sh) {
         PlanDeviceGuard g(S.device);
-        if (S.j1 > S.j0)
-          plan_crt(S.pl.get(), S.full, static_cast<long long>(Pb) * N, Pb, static_cast<long long>(rows_words), S.j0, S.j1,
-                   S.crt, 0, S.st);
+        if (S.j1 > S.j0) {
+          if (fused_x)
+            plan_crt(S.pl.get(), S.full, static_cast<long long>(Pb) * Jb, Pb, static_cast<long long>(B) * Pb * Jb, S.j0,
+                     S.j1, S.crt, 0, S.st, /*pitch=*/Jb, /*col0=*/S.j0);
+          else
+            plan_crt(S.pl.get(), S.full, static_cast<long long>(Pb) * N, Pb, static_cast<long long>(rows_words), S.j0,
+                     S.j1, S.crt, 0, S.st);
+        }
       }
       auto d2h_block = [&](const Shard& S, const uint32_t* src, int r) {
         const int j0 = std::min(r * Jb, D), j1 = std::min((r + 1) * Jb, D);
@@ -1172,6 +1260,7 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
           d2h_block(S, S.crt, S.rank);
         }
       }
+      lap("exchange + K5 + D2H enqueued");
       uint32_t bits = 0;
       for (auto& S : sh) {
         PlanDeviceGuard g(S.device);
@@ -1184,6 +1273,7 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
       stats.n_points = N;
       stats.n_coeffs = D;
       stats.out_limbs = std::max(stats.out_limbs, sh[0].pl->out_limbs());
+      lap("device work done");
       const ctg_plan* plc = sh[0].pl.get();
       std::vector<DecodeSize> sz(B);
       parallel_for(B, [&](int b) { sz[b] = decode_size(plc, host + static_cast<size_t>(b) * D * W); });
@@ -1195,7 +1285,9 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
         arena.place(&out[idx[b]], off[b], sz[b].nc, sz[b].total);
         decode_fill(plc, host + static_cast<size_t>(b) * D * W, sz[b], &out[idx[b]]);
       });
+      lap("host decode");
       sh.clear();  // ~Shard releases every buffer on its device
+      lap("release");
     }
   }
 }

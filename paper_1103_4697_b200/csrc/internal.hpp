@@ -112,6 +112,7 @@ struct CrtParams {
   int row_block;
   long long block_stride;
   int j0, J;             // coefficient range
+  int col0;              // column of coefficient col0 is 0 in each row (a shard's receive block), else 0
   const PrimeConst* pc;
   const double* minv;    // 1/p_k
   const uint32_t* Mk16;  // [P][L16] 16-bit digits of M / p_k
@@ -144,9 +145,20 @@ int launch_reduce(const uint32_t* d_limbs, const int8_t* d_sign, int S, int L, c
                   int coef_major = 0);
 // part: 0 = K2 + K3 (+ general), 1 = K2 only, 2 = K3 (+ general) only.
 int launch_modres(const ResParams& rp, bool fast, cudaStream_t st, int part = 0);
+// K4's epilogue as the prime-sharded exchange: coefficient j of curve b, local
+// prime kl goes straight to shard r = j / Jb's receive buffer,
+//   dst[r][shard_off + b * curve_stride + kl * Jb + (j - r * Jb)],
+// by (NVLink peer) stores from the kernel -- no all-gather of whole rows.  G = 0: in place.
+constexpr int kMaxScatter = 8;
+struct RowScatter {
+  uint32_t* dst[kMaxScatter];
+  int G, Jb;
+  long long shard_off, curve_stride;
+};
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
                   const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
-                  cudaStream_t st, uint32_t* d_work = nullptr);  // d_work: B * nk * N words when N > kMaxNttSmem
+                  cudaStream_t st, uint32_t* d_work = nullptr,  // d_work: B * nk * N words when N > kMaxNttSmem
+                  const RowScatter* scatter = nullptr);
 // Fills twinv[k][i] = omega_k^{-i} for all primes of a table (one launch, at table build).
 void launch_twiddles(const PrimeConst* d_pc, int P, int N, uint32_t* d_twinv);
 int launch_crt(const CrtParams& cp, cudaStream_t st);

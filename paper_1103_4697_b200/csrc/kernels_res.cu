@@ -556,7 +556,7 @@ template <int R>
 __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstride, int pitch,
                                                 const PrimeConst* __restrict__ pc,
                                                 const uint32_t* __restrict__ twinv, int k0, int N, int a,
-                                                int D, int negate, uint32_t* counters) {
+                                                int D, int negate, uint32_t* counters, RowScatter sc) {
   extern __shared__ uint32_t sm[];
   uint32_t* tw = sm;      // omega^{-i}, i < N
   uint32_t* w = sm + N;   // work array
@@ -634,10 +634,16 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
     }
     uint32_t c = mmul(acc, pcv.scale, M);  // Montgomery x plain -> plain
     if (negate) c = mneg(c, M.p);
-    if (j < D)
-      row[j] = c;
-    else
+    if (j < D) {
+      if (sc.G) {  // straight into the owning shard's receive block (peer store over NVLink)
+        const int r = j / sc.Jb;
+        sc.dst[r][sc.shard_off + b * sc.curve_stride + static_cast<long long>(kl) * sc.Jb + (j - r * sc.Jb)] = c;
+      } else {
+        row[j] = c;
+      }
+    } else {
       tail |= (c != 0u);
+    }
   }
   if (tail) atomicOr(&counters[1], kErrNttTail);
 }
@@ -678,7 +684,7 @@ __global__ void k_interp_big_stage(uint32_t* __restrict__ w, int nk, int N, int 
 
 __global__ void k_interp_big_final(const uint32_t* __restrict__ w, uint32_t* rows, size_t rows_bstride, int pitch,
                                    int nk, int N, int R, int a, int D, int negate, const PrimeConst* __restrict__ pc,
-                                   const uint32_t* __restrict__ twinv, int k0, uint32_t* counters) {
+                                   const uint32_t* __restrict__ twinv, int k0, uint32_t* counters, RowScatter sc) {
   const int kl = blockIdx.y, b = blockIdx.z;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
@@ -696,10 +702,16 @@ __global__ void k_interp_big_final(const uint32_t* __restrict__ w, uint32_t* row
   }
   uint32_t c = mmul(acc, pcv.scale, M);
   if (negate) c = mneg(c, M.p);
-  if (j < D)
-    rows[b * rows_bstride + static_cast<size_t>(kl) * pitch + j] = c;
-  else if (c != 0u)
+  if (j < D) {
+    if (sc.G) {
+      const int r = j / sc.Jb;
+      sc.dst[r][sc.shard_off + b * sc.curve_stride + static_cast<long long>(kl) * sc.Jb + (j - r * sc.Jb)] = c;
+    } else {
+      rows[b * rows_bstride + static_cast<size_t>(kl) * pitch + j] = c;
+    }
+  } else if (c != 0u) {
     atomicOr(&counters[1], kErrNttTail);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -726,7 +738,7 @@ __global__ void __launch_bounds__(256) k_crt_prep(CrtParams C) {
     for (int k = kbeg + ty; k < kend; k += 8) {
       const PrimeConst& pcv = C.pc[k];
       const Mod M = load_mod(pcv);
-      const uint32_t v = crt_row(C, b, k)[C.j0 + jl];
+      const uint32_t v = crt_row(C, b, k)[C.j0 - C.col0 + jl];
       const uint32_t y = mmul(v, pcv.crt_c, M);
       C.Y[(static_cast<size_t>(b) * C.P + k) * C.J + jl] = y;
       u += static_cast<double>(y) * C.minv[k];
@@ -916,7 +928,7 @@ __global__ void __launch_bounds__(256) k_crt_prep_t(CrtParams C) {
     if (k < kend && jl < C.J) {
       const PrimeConst& pcv = C.pc[k];
       const Mod M = load_mod(pcv);
-      y = mmul(crt_row(C, b, k)[C.j0 + jl], pcv.crt_c, M);
+      y = mmul(crt_row(C, b, k)[C.j0 - C.col0 + jl], pcv.crt_c, M);
       u += static_cast<double>(y) * C.minv[k];
     }
     tile[k - kbeg][tx] = y;
@@ -1463,8 +1475,10 @@ size_t general_warp_gbuf_words(int n) {
 
 int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B, const PrimeConst* d_pc,
                   const uint32_t* d_twinv, int k0, int N, int r, int a, int D, int negate, uint32_t* counters,
-                  cudaStream_t st, uint32_t* d_work) {
+                  cudaStream_t st, uint32_t* d_work, const RowScatter* scatter) {
   if (nk == 0 || B == 0) return 0;
+  RowScatter sc{};
+  if (scatter) sc = *scatter;
   if (static_cast<uint32_t>(N) > kMaxNttSmem) {  // global-memory passes (d_work: B * nk * N words)
     if (!d_work) throw std::runtime_error("launch_interp: work array missing for N > kMaxNttSmem");
     const dim3 gp((N + 255) / 256, nk, B);
@@ -1473,7 +1487,7 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
     for (int lg = 1; lg <= a; ++lg)
       k_interp_big_stage<<<gs, 256, 0, st>>>(d_work, nk, N, r, a, lg, d_pc, d_twinv, k0);
     k_interp_big_final<<<gp, 256, 0, st>>>(d_work, rows, rows_bstride, pitch, nk, N, r, a, D, negate, d_pc, d_twinv, k0,
-                                           counters);
+                                           counters, sc);
     return a + 2;
   }
   const size_t smem = static_cast<size_t>(2) * N * 4;
@@ -1482,7 +1496,7 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
   threads = threads < 32 ? 32 : (threads > 256 ? 256 : (threads + 31) / 32 * 32);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<dim3(nk, B), threads, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, a, D, negate, counters);
+    kern<<<dim3(nk, B), threads, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, a, D, negate, counters, sc);
   };
   switch (r) {
     case 1: go(k_interp<1>); break;

@@ -59,15 +59,19 @@ def test_sharded_pipeline_matches_one_shot(G, kind, a, b):
         assert plan.decode(np.ascontiguousarray(dense[bi])) == want[bi], (G, kind, bi)
 
 
-@pytest.mark.parametrize("G", [2, 3, 8])
-def test_c_abi_device_list_sharding(G):
+@pytest.mark.parametrize("G,mode", [(2, "fused"), (3, "fused"), (8, "fused"), (9, "fused"), (2, "copy"),
+                                    (3, "copy")])
+def test_c_abi_device_list_sharding(G, mode, monkeypatch):
     """The product path: ctg_resultant_batch with ctg_opts.n_devices = G (device 0 listed G
-    times: the shards share the GPU and exchange residues by device copies instead of NCCL).
+    times: the shards share the GPU).  Exchange "fused" (default, G <= 8): K4's epilogue stores
+    each coefficient straight into the owning shard's receive block (peer stores across GPUs,
+    local stores here); G = 9 and "copy": the all-gather of whole residue rows by device copies.
     Mixed shapes, a zero operand, a degree-0 operand and the d20/64 config (reference-pinned
     digest of seed 1) must equal the one-device call bit for bit."""
     import hashlib
     import json
     import os
+    monkeypatch.setenv("CTG_SHARD_EXCHANGE", mode)
     pairs = []
     for s in range(1, 4):
         f = curves.make("dense", 12, 40, s)
