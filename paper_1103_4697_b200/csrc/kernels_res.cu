@@ -552,7 +552,7 @@ __global__ void k_twiddles(const PrimeConst* __restrict__ pc, int P, int N, uint
   twinv[idx] = mpow(pcv.omega_inv, static_cast<uint64_t>(i), load_mod(pcv));
 }
 
-template <int R>
+template <int R, bool SCATTER>
 __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstride, int pitch,
                                                 const PrimeConst* __restrict__ pc,
                                                 const uint32_t* __restrict__ twinv, int k0, int N, int a,
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(256) k_interp(uint32_t* rows, size_t rows_bstr
     uint32_t c = mmul(acc, pcv.scale, M);  // Montgomery x plain -> plain
     if (negate) c = mneg(c, M.p);
     if (j < D) {
-      if (sc.G) {  // straight into the owning shard's receive block (peer store over NVLink)
+      if constexpr (SCATTER) {  // straight into the owning shard's receive block (peer store over NVLink)
         const int r = j / sc.Jb;
         sc.dst[r][sc.shard_off + b * sc.curve_stride + static_cast<long long>(kl) * sc.Jb + (j - r * sc.Jb)] = c;
       } else {
@@ -682,6 +682,7 @@ __global__ void k_interp_big_stage(uint32_t* __restrict__ w, int nk, int N, int 
   base[t + half] = msub(u, v, M.p);
 }
 
+template <bool SCATTER>
 __global__ void k_interp_big_final(const uint32_t* __restrict__ w, uint32_t* rows, size_t rows_bstride, int pitch,
                                    int nk, int N, int R, int a, int D, int negate, const PrimeConst* __restrict__ pc,
                                    const uint32_t* __restrict__ twinv, int k0, uint32_t* counters, RowScatter sc) {
@@ -703,7 +704,7 @@ __global__ void k_interp_big_final(const uint32_t* __restrict__ w, uint32_t* row
   uint32_t c = mmul(acc, pcv.scale, M);
   if (negate) c = mneg(c, M.p);
   if (j < D) {
-    if (sc.G) {
+    if constexpr (SCATTER) {
       const int r = j / sc.Jb;
       sc.dst[r][sc.shard_off + b * sc.curve_stride + static_cast<long long>(kl) * sc.Jb + (j - r * sc.Jb)] = c;
     } else {
@@ -1486,8 +1487,12 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
     const dim3 gs(((r << (a - 1)) + 255) / 256, nk, B);
     for (int lg = 1; lg <= a; ++lg)
       k_interp_big_stage<<<gs, 256, 0, st>>>(d_work, nk, N, r, a, lg, d_pc, d_twinv, k0);
-    k_interp_big_final<<<gp, 256, 0, st>>>(d_work, rows, rows_bstride, pitch, nk, N, r, a, D, negate, d_pc, d_twinv, k0,
-                                           counters, sc);
+    if (sc.G)
+      k_interp_big_final<true><<<gp, 256, 0, st>>>(d_work, rows, rows_bstride, pitch, nk, N, r, a, D, negate, d_pc,
+                                                   d_twinv, k0, counters, sc);
+    else
+      k_interp_big_final<false><<<gp, 256, 0, st>>>(d_work, rows, rows_bstride, pitch, nk, N, r, a, D, negate, d_pc,
+                                                    d_twinv, k0, counters, sc);
     return a + 2;
   }
   const size_t smem = static_cast<size_t>(2) * N * 4;
@@ -1498,11 +1503,20 @@ int launch_interp(uint32_t* rows, size_t rows_bstride, int pitch, int nk, int B,
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<dim3(nk, B), threads, smem, st>>>(rows, rows_bstride, pitch, d_pc, d_twinv, k0, N, a, D, negate, counters, sc);
   };
-  switch (r) {
-    case 1: go(k_interp<1>); break;
-    case 3: go(k_interp<3>); break;
-    case 5: go(k_interp<5>); break;
-    default: go(k_interp<7>); break;
+  if (sc.G) {
+    switch (r) {
+      case 1: go(k_interp<1, true>); break;
+      case 3: go(k_interp<3, true>); break;
+      case 5: go(k_interp<5, true>); break;
+      default: go(k_interp<7, true>); break;
+    }
+  } else {
+    switch (r) {
+      case 1: go(k_interp<1, false>); break;
+      case 3: go(k_interp<3, false>); break;
+      case 5: go(k_interp<5, false>); break;
+      default: go(k_interp<7, false>); break;
+    }
   }
   return 1;
 }
