@@ -1014,7 +1014,7 @@ struct Shard {
   cudaStream_t st = nullptr;
   std::unique_ptr<ctg_plan> pl;
   int k0 = 0, k1 = 0, j0 = 0, j1 = 0;
-  uint32_t *send = nullptr, *full = nullptr, *crt = nullptr, *gath = nullptr;
+  uint32_t *send = nullptr, *full = nullptr, *crt = nullptr, *gath = nullptr, *xsend = nullptr;
   bool full_pooled = true;  // false: `full` is the device context's receive scratch (fused exchange)
   cudaEvent_t rows_done = nullptr;
   Shard() = default;
@@ -1030,6 +1030,7 @@ struct Shard {
     if (full_pooled) pl->pfree(full);
     pl->pfree(crt);
     pl->pfree(gath);
+    pl->pfree(xsend);
     if (rows_done) cudaEventDestroy(rows_done);
     pl.reset();
     cudaSetDevice(prev);
@@ -1105,6 +1106,10 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
   // between distinct devices, device copies otherwise), for A/B and as the fallback.
   const std::string xmode = std::getenv("CTG_SHARD_EXCHANGE") ? std::getenv("CTG_SHARD_EXCHANGE") : "fused";
   const bool fused_x = !comm && xmode == "fused" && G <= kMaxScatter && enable_peer_access(distinct);
+  // multi-process (one rank per GPU): K4 stores by destination into a local send block and the
+  // ranks swap column blocks with grouped ncclSend / ncclRecv (an all-to-all: each rank receives
+  // only its coefficient columns, 1/G of an all-gather of whole rows)
+  const bool a2a_x = comm && xmode != "copy" && xmode != "nccl" && G <= kMaxScatter;
   // NCCL between distinct devices of one process; device copies when a GPU hosts two shards
   const bool use_nccl_local = !comm && !fused_x && !repeated && xmode != "copy" && nccl_available();
   const std::vector<ncclComm_t>* local_comms = use_nccl_local ? &device_set_comms(local_dev) : nullptr;
@@ -1176,11 +1181,15 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
                         // cudaMalloc'd memory; stream-ordered pool memory would need pool access)
           S.full = ctx.scratch_u32(8 + slot, recv_words);
           S.full_pooled = false;
+        } else if (a2a_x) {
+          pl->palloc(S.full, recv_words, S.st);
+          pl->palloc(S.gath, crt_words * G, S.st);
+          pl->palloc(S.xsend, recv_words, S.st);
         } else {
           pl->palloc(S.full, rows_words * G, S.st);
         }
         pl->palloc(S.crt, crt_words, S.st);
-        if (comm) pl->palloc(S.gath, crt_words * G, S.st);
+        if (comm && !a2a_x) pl->palloc(S.gath, crt_words * G, S.st);
       }
       for (size_t s = 0; s < sh.size(); ++s) {  // every receive block exists before any K4 stores into it
         Shard& S = sh[s];
@@ -1192,9 +1201,16 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
           for (size_t r = 0; r < sh.size(); ++r) sc.dst[sh[r].rank] = sh[r].full;
           sc.shard_off = static_cast<long long>(S.rank) * B * Pb * Jb;
           sc.curve_stride = static_cast<long long>(Pb) * Jb;
+        } else if (a2a_x) {  // by destination rank: xsend[r] = [B][Pb][Jb] block for rank r
+          sc.G = G;
+          sc.Jb = Jb;
+          for (int r = 0; r < G; ++r) sc.dst[r] = S.xsend + static_cast<size_t>(r) * B * Pb * Jb;
+          sc.shard_off = 0;
+          sc.curve_stride = static_cast<long long>(Pb) * Jb;
         }
+        const bool scatter = fused_x || a2a_x;
         if (S.k1 > S.k0)
-          plan_residues(S.pl.get(), S.k0, S.k1, S.send, static_cast<long long>(Pb) * N, S.st, fused_x ? &sc : nullptr);
+          plan_residues(S.pl.get(), S.k0, S.k1, S.send, static_cast<long long>(Pb) * N, S.st, scatter ? &sc : nullptr);
         CTG_CUDA_CHECK(cudaEventCreateWithFlags(&S.rows_done, cudaEventDisableTiming));
         CTG_CUDA_CHECK(cudaEventRecord(S.rows_done, S.st));
       }
@@ -1205,6 +1221,16 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
           PlanDeviceGuard g(S.device);
           for (auto& H : sh) CTG_CUDA_CHECK(cudaStreamWaitEvent(S.st, H.rows_done, 0));
         }
+      } else if (a2a_x) {
+        Shard& S = sh[0];
+        PlanDeviceGuard g(S.device);
+        const size_t blk_words = static_cast<size_t>(B) * Pb * Jb;
+        nccl_check(nccl().GroupStart(), "ncclGroupStart");
+        for (int r = 0; r < G; ++r) {
+          nccl_check(nccl().Send(S.xsend + r * blk_words, blk_words, ncclUint32, r, comm->nc, S.st), "ncclSend");
+          nccl_check(nccl().Recv(S.full + r * blk_words, blk_words, ncclUint32, r, comm->nc, S.st), "ncclRecv");
+        }
+        nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
       } else if (comm) {
         PlanDeviceGuard g(sh[0].device);
         nccl_check(nccl().AllGather(sh[0].send, sh[0].full, rows_words, ncclUint32, comm->nc, sh[0].st), "ncclAllGather");
@@ -1233,7 +1259,7 @@ static void resultant_batch_sharded(int batch, const ctg_bipoly* p, const ctg_bi
       for (auto& S : sh) {
         PlanDeviceGuard g(S.device);
         if (S.j1 > S.j0) {
-          if (fused_x)
+          if (fused_x || a2a_x)
             plan_crt(S.pl.get(), S.full, static_cast<long long>(Pb) * Jb, Pb, static_cast<long long>(B) * Pb * Jb, S.j0,
                      S.j1, S.crt, 0, S.st, /*pitch=*/Jb, /*col0=*/S.j0);
           else

@@ -28,7 +28,8 @@ const NcclApi& nccl() {
     };
     a.ok = sym(a.GetUniqueId, "ncclGetUniqueId") && sym(a.CommInitRank, "ncclCommInitRank") &&
            sym(a.CommInitAll, "ncclCommInitAll") && sym(a.CommDestroy, "ncclCommDestroy") &&
-           sym(a.AllGather, "ncclAllGather") && sym(a.GroupStart, "ncclGroupStart") &&
+           sym(a.AllGather, "ncclAllGather") && sym(a.Send, "ncclSend") && sym(a.Recv, "ncclRecv") &&
+           sym(a.GroupStart, "ncclGroupStart") &&
            sym(a.GroupEnd, "ncclGroupEnd") && sym(a.GetErrorString, "ncclGetErrorString");
     if (!a.ok) a.why = "libnccl.so.2 lacks an expected entry point";
     return a;

@@ -95,9 +95,10 @@ def test_c_abi_device_list_sharding(G, mode, monkeypatch):
 
 def test_c_abi_comm_single_rank():
     """The multi-process path (ctg_opts.comm: libctg's own NCCL communicator, loaded at run time)
-    with one rank: NCCL all-gathers of the residue rows and of the CRT'd limb blocks are then
-    copies, and the result must equal the plain call.  (N ranks need N GPUs: NCCL refuses two
-    ranks on one device.)"""
+    with one rank: K4's by-destination send block, the grouped ncclSend / ncclRecv column swap
+    and the all-gather of the CRT'd limb blocks are then copies to itself, and the result must
+    equal the plain call (CTG_SHARD_EXCHANGE=nccl: the row all-gather instead).  (N ranks need
+    N GPUs: NCCL refuses two ranks on one device.)"""
     pairs = []
     for s in range(1, 4):
         f = curves.make("dense", 12, 40, s)
