@@ -1628,82 +1628,52 @@ __global__ void __launch_bounds__(128) k_crt_fixup(CrtParams C, int nt, int LW) 
   const int OL = C.out_limbs;
   const uint4* meta = reinterpret_cast<const uint4*>(C.cols) + static_cast<size_t>(row) * nt;
   uint32_t* rowp = C.out + static_cast<size_t>(row) * (OL + 1) + 1;
-  // op: 0 none, 1 low limbs changed only, 2 +1 ripple into the upper limbs, 3 -1 ripple,
-  //     4 upper limbs all ones -> zeros, 5 all zeros -> ones
-  int my_op = 0;
-  uint64_t my_low = 0;
+  // every lane walks the chain (the summaries are broadcast loads: one LDG per segment, no
+  // shuffles) and the warp applies a segment's fix-up as soon as it is known
   long long cin = 0;
   int nonzero = 0;
-  for (int i0 = 0; i0 < nt; i0 += 32) {
-    const uint4 mm = i0 + lane < nt ? meta[i0 + lane] : make_uint4(0, 0, 0, 0);
-    const int nb = min(32, nt - i0);
-    for (int q = 0; q < nb; ++q) {
-      const uint32_t mx = __shfl_sync(0xffffffffu, mm.x, q), my = __shfl_sync(0xffffffffu, mm.y, q);
-      const uint32_t mz = __shfl_sync(0xffffffffu, mm.z, q), mw = __shfl_sync(0xffffffffu, mm.w, q);
-      uint64_t low = (static_cast<uint64_t>(my) << 32) | mx;
-      long long co = static_cast<int>(mz);
-      bool ones = mw & 1u, zero = (mw & 2u) != 0;
-      int op = 0;
-      if (cin != 0) {
-        const uint64_t nl = low + static_cast<uint64_t>(cin);
-        int hi = 0;  // carry out of the low 64 bits: cin > 0 overflows, cin < 0 borrows
-        if (cin > 0 && nl < low) hi = 1;
-        if (cin < 0 && nl > low) hi = -1;
-        low = nl;
-        op = 1;
-        if (hi == 1) {
-          if (ones) {
-            op = 4;
-            co += 1;
-            ones = false;
-            zero = true;
-          } else {
-            op = 2;
-            zero = false;
-          }
-        } else if (hi == -1) {
-          if (zero) {
-            op = 5;
-            co -= 1;
-            zero = false;
-            ones = true;
-          } else {
-            op = 3;
-            ones = false;
-          }
-        }
-      }
-      if (lane == q) {
-        my_op = op;
-        my_low = low;
-      }
-      // limbs >= OL are part of the two's complement chain but not of the record
-      nonzero |= (low != 0 || !zero) ? 1 : 0;
-      cin = co;
-    }
-    // apply this chunk's fix-ups (segments i0 .. i0 + nb - 1), one segment at a time
-    for (int q = 0; q < nb; ++q) {
-      const int op = __shfl_sync(0xffffffffu, my_op, q);
-      if (!op) continue;
-      const uint64_t low = __shfl_sync(0xffffffffu, my_low, q);
-      const int base = (i0 + q) * LW;
+  for (int i = 0; i < nt; ++i) {
+    const uint4 mm = meta[i];
+    uint64_t low = (static_cast<uint64_t>(mm.y) << 32) | mm.x;
+    long long co = static_cast<int>(mm.z);
+    bool ones = mm.w & 1u, zero = (mm.w & 2u) != 0;
+    if (cin != 0) {
+      const uint64_t nl = low + static_cast<uint64_t>(cin);
+      int hi = 0;  // carry out of the low 64 bits: cin > 0 overflows, cin < 0 borrows
+      if (cin > 0 && nl < low) hi = 1;
+      if (cin < 0 && nl > low) hi = -1;
+      low = nl;
+      const int base = i * LW;
       if (lane < 2 && base + lane < OL) rowp[base + lane] = static_cast<uint32_t>(lane ? low >> 32 : low);
-      if (op == 4 || op == 5) {
-        for (int li = 2 + lane; li < LW && base + li < OL; li += 32) rowp[base + li] = op == 4 ? 0u : 0xffffffffu;
-      } else if (op == 2 || op == 3) {
-        // +1: the lowest upper limb != all-ones gets +1, the ones below it become 0 (-1: mirrored)
-        const uint32_t stop = op == 2 ? 0xffffffffu : 0u;
-        for (int l0 = 2; l0 < LW; l0 += 32) {
-          const int li = l0 + lane;
-          const bool in = li < LW && base + li < OL;
-          const uint32_t x = in ? rowp[base + li] : stop;
-          const unsigned hit = __ballot_sync(0xffffffffu, in && x != stop);
-          const int z = hit ? __ffs(hit) - 1 : 32;
-          if (in && lane <= z) rowp[base + li] = lane == z ? (op == 2 ? x + 1u : x - 1u) : ~stop;
-          if (hit) break;
+      if (hi != 0) {
+        const bool flip = hi == 1 ? ones : zero;  // every upper limb ripples: all ones -> zeros / zeros -> ones
+        if (flip) {
+          for (int li = 2 + lane; li < LW && base + li < OL; li += 32) rowp[base + li] = hi == 1 ? 0u : 0xffffffffu;
+          co += hi;
+          ones = hi == -1;
+          zero = hi == 1;
+        } else {
+          // +1: the lowest upper limb != all-ones gets +1, the ones below it become 0 (-1: mirrored)
+          const uint32_t stop = hi == 1 ? 0xffffffffu : 0u;
+          for (int l0 = 2; l0 < LW; l0 += 32) {
+            const int li = l0 + lane;
+            const bool in = li < LW && base + li < OL;
+            const uint32_t x = in ? rowp[base + li] : stop;
+            const unsigned hit = __ballot_sync(0xffffffffu, in && x != stop);
+            const int z = hit ? __ffs(hit) - 1 : 32;
+            if (in && lane <= z) rowp[base + li] = lane == z ? (hi == 1 ? x + 1u : x - 1u) : ~stop;
+            if (hit) break;
+          }
+          if (hi == 1)
+            zero = false;
+          else
+            ones = false;
         }
       }
     }
+    // limbs >= OL are part of the two's complement chain but not of the record
+    nonzero |= (low != 0 || !zero) ? 1 : 0;
+    cin = co;
   }
   const int neg = cin < 0 ? 1 : 0;  // |V| < M / 2 fits the record: the final carry is 0 or -1
   __syncwarp();
