@@ -367,7 +367,11 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks, c
     plan.upload(sh)
 
     send = torch.zeros((B, Pb, N), dtype=torch.int32, device=dev)
-    full = torch.zeros((G, B, Pb, N), dtype=torch.int32, device=dev) if G > 1 else None
+    # G > 1: the column-block exchange -- K4 writes each coefficient by destination rank
+    # (ctg_plan_interp_cols: [G][B][Pb][Jc]), one all-to-all, K5 on this rank's columns
+    Jc = (D + G - 1) // G
+    xsend = torch.zeros((G, B, Pb, Jc), dtype=torch.int32, device=dev) if G > 1 else None
+    xrecv = torch.zeros((G, B, Pb, Jc), dtype=torch.int32, device=dev) if G > 1 else None
     out = torch.zeros((B * Jb * W,), dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
@@ -378,8 +382,8 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks, c
 
     def crt():
         if G > 1:
-            plan.crt_batch(full.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N, row_block=Pb,
-                           block_stride=B * Pb * N)
+            if j1 > j0:
+                plan.crt_cols(xrecv.data_ptr(), G, rank, Pb, out.data_ptr(), sh)
         else:
             plan.crt_batch(send.data_ptr(), j0, j1, out.data_ptr(), sh, curve_stride=Pb * N)
 
@@ -387,13 +391,19 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks, c
         if timed:
             evs[0].record(stream)
         for i, s_ in enumerate((1, 4, 5, 3)):  # K1, K2, K3 (+ exact fallback), K4
-            plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
+            if s_ == 3 and G > 1:
+                plan.interp_cols(k0, k1, send.data_ptr(), G, Pb, xsend.data_ptr(), sh, curve_stride=Pb * N)
+            else:
+                plan.stage(s_, k0, k1, send.data_ptr(), sh, curve_stride=Pb * N)
             if timed:
                 evs[i + 1].record(stream)
-        if comm:  # ctg_comm_all_gather: libctg's NCCL communicator, on the launch stream
-            comm.all_gather(send.data_ptr(), full.data_ptr(), send.numel(), sh)
-        elif G > 1:  # CTG_BENCH_SIM_GLOO: functional multi-rank test on one GPU
-            dist.all_gather_into_tensor(full.view(-1, Pb, N), send)
+        if comm:  # ctg_comm_all_to_all: libctg's NCCL communicator (grouped send / recv), launch stream
+            comm.all_to_all(xsend.data_ptr(), xrecv.data_ptr(), xsend[0].numel(), sh)
+        elif G > 1:  # CTG_BENCH_SIM_GLOO: functional multi-rank test on one GPU (the all-to-all
+            # emulated by an all-gather of the send blocks, this rank's column blocks kept)
+            gathered = torch.empty((G,) + tuple(xsend.shape), dtype=xsend.dtype, device=dev)
+            dist.all_gather_into_tensor(gathered.view(-1, Pb, Jc), xsend.view(-1, Pb, Jc))
+            xrecv.copy_(gathered[:, rank])
         if timed:
             evs[5].record(stream)
         crt()
@@ -490,7 +500,7 @@ def measure(args, workload, B, P, curves, torch, dist, stream, rank, G, peaks, c
                 "stage2_frac": imad_launch / ((sm["eval"] + sm["modres"]) * 1e-3) / 1e12 / peak,
                 "stage_ms_per_step": sm}
     plan.close()
-    del send, full, out, flush
+    del send, xsend, xrecv, out, flush
     return {
         "value": value, "ms_per_step": ms_per_step, "units_per_curve": units_step / B,
         "sample": {"curves_per_step": B, "seeds": f"1..{B}", "primes": Pn, "points": N, "coeffs": D,

@@ -232,6 +232,23 @@ ctg_status ctg_comm_unique_id(uint8_t* id /* CTG_COMM_ID_BYTES */);
 ctg_status ctg_comm_init_rank(int32_t nranks, int32_t rank, const uint8_t* id, int32_t device, ctg_comm** comm);
 void ctg_comm_destroy(ctg_comm* comm);
 ctg_status ctg_comm_all_gather(ctg_comm* comm, const void* d_send, void* d_recv, size_t words, void* stream);
+/* All-to-all (grouped ncclSend / ncclRecv): block r of d_send (words u32 each) goes to rank r,
+ * block s of d_recv arrives from rank s. */
+ctg_status ctg_comm_all_to_all(ctg_comm* comm, const void* d_send, void* d_recv, size_t words, void* stream);
+
+/* Column-block exchange of a prime-sharded plan: instead of all-gathering whole
+ * residue rows, the interpolation (stage 3) of primes [k0, k1) writes each coefficient j straight
+ * into the block of the rank that reconstructs it, r = j / Jb with Jb = ceil(D / nranks):
+ * d_send = [nranks][B][row_block][Jb] (prime k at row k - k0; row_block >= k1 - k0), point values
+ * read from d_rows as for ctg_plan_stage_batch(stage 3).  After ctg_comm_all_to_all (or any
+ * exchange giving rank r the blocks [s][B][row_block][Jb] of every rank s), ctg_plan_crt_cols
+ * reconstructs coefficients [r Jb, min(D, (r + 1) Jb)) of every curve from d_recv (prime k in
+ * block k / row_block) into d_out [B][J][out_limbs + 1].  Each rank then receives 1/nranks of
+ * the bytes of a row all-gather. */
+ctg_status ctg_plan_interp_cols(ctg_plan* plan, int32_t k0, int32_t k1, uint32_t* d_rows, int64_t curve_stride,
+                                int32_t nranks, int32_t row_block, uint32_t* d_send, void* stream);
+ctg_status ctg_plan_crt_cols(ctg_plan* plan, const uint32_t* d_recv, int32_t nranks, int32_t rank, int32_t row_block,
+                             uint32_t* d_out, void* stream);
 
 /* Integer-pipe peak microbenchmarks on `device` (-1 = current): 32-bit IMAD
  * (a*b+c) and IMAD.WIDE (u32*u32+u64) results per second over all SMs, and

@@ -114,7 +114,8 @@ EXPORTS = (
     "ctg_microbench_int", "ctg_plan_crt_sharded", "ctg_resultant_batch", "ctg_plan_create_batch",
     "ctg_plan_stage_batch", "ctg_plan_crt_batch", "ctg_upoly_free_batch", "ctg_gcd_bivariate", "ctg_bipoly_free",
     "ctg_comm_unique_id", "ctg_comm_init_rank", "ctg_comm_destroy", "ctg_comm_all_gather",
-    "ctg_yun_squarefree_batch", "ctg_modp_gcd_degree",
+    "ctg_yun_squarefree_batch", "ctg_modp_gcd_degree", "ctg_comm_all_to_all", "ctg_plan_interp_cols",
+    "ctg_plan_crt_cols",
 )
 
 _lib = None
@@ -178,6 +179,11 @@ def lib():
         L.ctg_comm_init_rank.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
         L.ctg_comm_destroy.argtypes = [C.c_void_p]
         L.ctg_comm_all_gather.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.ctg_comm_all_to_all.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.ctg_plan_interp_cols.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int32,
+                                           C.c_int32, C.c_void_p, C.c_void_p]
+        L.ctg_plan_crt_cols.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                        C.c_void_p]
         _lib = L
         return L
 
@@ -320,6 +326,11 @@ class Comm:
     def all_gather(self, send_ptr, recv_ptr, words, stream=0):
         _check(lib().ctg_comm_all_gather(self.handle, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), words,
                                          C.c_void_p(stream)), "comm_all_gather")
+
+    def all_to_all(self, send_ptr, recv_ptr, words, stream=0):
+        """Block r of send (words u32) to rank r; block s of recv from rank s."""
+        _check(lib().ctg_comm_all_to_all(self.handle, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), words,
+                                         C.c_void_p(stream)), "comm_all_to_all")
 
     def close(self):
         if self.handle:
@@ -604,6 +615,16 @@ class Plan:
     def crt_batch(self, all_ptr, j0, j1, out_ptr, stream=0, curve_stride=0, row_block=0, block_stride=0):
         _check(lib().ctg_plan_crt_batch(self._h, C.c_void_p(all_ptr), curve_stride, row_block, block_stride, j0, j1,
                                         C.c_void_p(out_ptr), C.c_void_p(stream)), "plan_crt_batch")
+
+    def interp_cols(self, k0, k1, rows_ptr, nranks, row_block, send_ptr, stream=0, curve_stride=0):
+        """Stage 3 of primes [k0, k1) written by destination rank: send = [nranks][B][row_block][Jb]."""
+        _check(lib().ctg_plan_interp_cols(self._h, k0, k1, C.c_void_p(rows_ptr), curve_stride, nranks, row_block,
+                                          C.c_void_p(send_ptr), C.c_void_p(stream)), "plan_interp_cols")
+
+    def crt_cols(self, recv_ptr, nranks, rank, row_block, out_ptr, stream=0):
+        """K5 of this rank's coefficient columns from recv = [nranks][B][row_block][Jb]."""
+        _check(lib().ctg_plan_crt_cols(self._h, C.c_void_p(recv_ptr), nranks, rank, row_block, C.c_void_p(out_ptr),
+                                       C.c_void_p(stream)), "plan_crt_cols")
 
     def crt(self, all_ptr, j0, j1, out_ptr, stream=0):
         _check(lib().ctg_plan_crt(self._h, C.c_void_p(all_ptr), j0, j1, C.c_void_p(out_ptr), C.c_void_p(stream)),

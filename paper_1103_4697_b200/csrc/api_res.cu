@@ -1405,6 +1405,39 @@ ctg_status ctg_plan_stage_batch(ctg_plan* pl, int32_t stage, int32_t k0, int32_t
   });
 }
 
+ctg_status ctg_plan_interp_cols(ctg_plan* pl, int32_t k0, int32_t k1, uint32_t* d_rows, int64_t curve_stride,
+                                int32_t nranks, int32_t row_block, uint32_t* d_send, void* stream) {
+  return guarded([&] {
+    if (!pl || !d_send || curve_stride < 0) throw ApiError(CTG_INVALID, "plan: null or negative stride");
+    if (nranks < 1 || nranks > kMaxScatter) throw ApiError(CTG_INVALID, "plan: interp_cols supports 1..8 ranks");
+    if (row_block < k1 - k0 || row_block < 1) throw ApiError(CTG_INVALID, "plan: row_block < k1 - k0");
+    PlanDeviceGuard g(pl->device);
+    const int D = static_cast<int>(pl->D), Jb = (D + nranks - 1) / nranks;
+    RowScatter sc{};
+    sc.G = nranks;
+    sc.Jb = Jb;
+    for (int r = 0; r < nranks; ++r) sc.dst[r] = d_send + static_cast<size_t>(r) * pl->B * row_block * Jb;
+    sc.shard_off = 0;
+    sc.curve_stride = static_cast<long long>(row_block) * Jb;
+    plan_stage(pl, 3, k0, k1, d_rows, curve_stride, resolve_stream(pl->device, stream), &sc);
+  });
+}
+
+ctg_status ctg_plan_crt_cols(ctg_plan* pl, const uint32_t* d_recv, int32_t nranks, int32_t rank, int32_t row_block,
+                             uint32_t* d_out, void* stream) {
+  return guarded([&] {
+    if (!pl || !d_recv) throw ApiError(CTG_INVALID, "plan: null");
+    if (nranks < 1 || rank < 0 || rank >= nranks || row_block < 1)
+      throw ApiError(CTG_INVALID, "plan: bad nranks / rank / row_block");
+    PlanDeviceGuard g(pl->device);
+    const int D = static_cast<int>(pl->D), Jb = (D + nranks - 1) / nranks;
+    const int j0 = std::min(rank * Jb, D), j1 = std::min((rank + 1) * Jb, D);
+    plan_crt(pl, d_recv, static_cast<long long>(row_block) * Jb, row_block,
+             static_cast<long long>(pl->B) * row_block * Jb, j0, j1, d_out, 0, resolve_stream(pl->device, stream),
+             /*pitch=*/Jb, /*col0=*/j0);
+  });
+}
+
 ctg_status ctg_plan_crt(ctg_plan* pl, const uint32_t* d_all, int32_t j0, int32_t j1, uint32_t* d_out, void* stream) {
   return guarded([&] {
     if (!pl) throw ApiError(CTG_INVALID, "plan: null");

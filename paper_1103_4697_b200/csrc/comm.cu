@@ -115,4 +115,20 @@ ctg_status ctg_comm_all_gather(ctg_comm* comm, const void* d_send, void* d_recv,
   });
 }
 
+ctg_status ctg_comm_all_to_all(ctg_comm* comm, const void* d_send, void* d_recv, size_t words, void* stream) {
+  return guarded([&] {
+    if (!comm || !comm->nc) throw ApiError(CTG_INVALID, "comm: null communicator");
+    PlanDeviceGuard g(comm->device);
+    const cudaStream_t st = resolve_stream(comm->device, stream);
+    const auto* s = static_cast<const uint32_t*>(d_send);
+    auto* r = static_cast<uint32_t*>(d_recv);
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    for (int q = 0; q < comm->nranks; ++q) {
+      nccl_check(nccl().Send(s + q * words, words, ncclUint32, q, comm->nc, st), "ncclSend");
+      nccl_check(nccl().Recv(r + q * words, words, ncclUint32, q, comm->nc, st), "ncclRecv");
+    }
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  });
+}
+
 }  // extern "C"

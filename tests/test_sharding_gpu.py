@@ -109,3 +109,52 @@ def test_c_abi_comm_single_rank():
         assert P.resultant_batch(pairs, comm=comm) == P.resultant_batch(pairs)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("G,kind,a,b", [(2, "dense", 12, 40), (3, "dense", 20, 64), (8, "sheared", 2, 0)])
+def test_sharded_column_exchange_matches_one_shot(G, kind, a, b):
+    """The column-block exchange of the staged API (bench.py --gpus G): each rank's K4 writes by
+    destination (ctg_plan_interp_cols: send = [G][B][Pb][Jb]), the all-to-all is emulated by
+    taking block r of every rank's send for rank r, and ctg_plan_crt_cols reconstructs rank r's
+    columns.  Reassembled, the limbs must decode to exactly the one-shot resultants."""
+    import torch
+
+    B = 4
+    fs = [curves.make(kind, a, b, s) for s in range(1, B + 1)]
+    pairs = [(f, curves.derive_y(f)) for f in fs]
+    want = [P.resultant(*pq) for pq in pairs]
+    plan = P.Plan(pairs)
+    info = plan.info
+    Pn, N, D, W = info["n_primes"], info["n_points"], info["n_coeffs"], info["out_limbs"] + 1
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sh = stream.cuda_stream
+    plan.upload(sh)
+    Pb = sharding.prime_block(Pn, G, 0)[2]
+    Jb = (D + G - 1) // G
+    sends = []
+    for r in range(G):
+        k0, k1, _ = sharding.prime_block(Pn, G, r)
+        rows = torch.zeros((B, Pb, N), dtype=torch.int32, device="cuda")
+        send = torch.zeros((G, B, Pb, Jb), dtype=torch.int32, device="cuda")
+        if k1 > k0:
+            for s_ in (1, 2):
+                plan.stage(s_, k0, k1, rows.data_ptr(), sh, curve_stride=Pb * N)
+            plan.interp_cols(k0, k1, rows.data_ptr(), G, Pb, send.data_ptr(), sh, curve_stride=Pb * N)
+        sends.append(send)
+    outs = []
+    for r in range(G):
+        recv = torch.stack([sends[s_][r] for s_ in range(G)]).contiguous()  # the all-to-all
+        j0, j1 = min(r * Jb, D), min((r + 1) * Jb, D)
+        out = torch.zeros((B * max(j1 - j0, 1) * W,), dtype=torch.int32, device="cuda")
+        if j1 > j0:
+            plan.crt_cols(recv.data_ptr(), G, r, Pb, out.data_ptr(), sh)
+        outs.append((j0, j1, out))
+    torch.cuda.synchronize()
+    plan.check(sh)
+    dense = np.zeros((B, D, W), dtype=np.uint32)
+    for j0, j1, out in outs:
+        if j1 > j0:
+            dense[:, j0:j1, :] = out.cpu().numpy().view("uint32").reshape(B, j1 - j0, W)
+    for bi in range(B):
+        assert plan.decode(np.ascontiguousarray(dense[bi])) == want[bi], (G, kind, bi)
