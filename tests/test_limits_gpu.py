@@ -253,3 +253,16 @@ def test_multi_unit_warp_kernel_staged_plan():
     plan.check(sh)
     host = out.cpu().numpy().view("uint32").reshape(B, D, W)
     assert [plan.decode(host[b]) for b in range(B)] == want
+
+
+def test_yun_probe_beyond_small_primes():
+    """Degree 33,000 (> 2^15): the square-freeness probe cannot use the primes below 2^15 and
+    runs the blocked remainder sequence modulo the 31-bit primes, its buffers in global memory
+    (four of 33,002 words); a random square-free input comes back as (sgn, [(P sgn, 1)])."""
+    import random
+    rng = random.Random(33)
+    n = 33000
+    poly = [rng.randrange(-1000, 1001) for _ in range(n)] + [rng.choice([-7, 7])]
+    poly[0] = 1  # content 1
+    sgn = -1 if poly[-1] < 0 else 1
+    assert P.yun_squarefree(poly) == (sgn, [([sgn * c for c in poly], 1)])
