@@ -21,6 +21,7 @@ void* __gmpz_export(void*, size_t*, int, size_t, int, size_t, const ctg_mpz_stru
 void __gmpz_gcd(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_divexact(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_set(ctg_mpz_struct*, const ctg_mpz_struct*);
+int __gmpz_divisible_p(const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_tdiv_r(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 void __gmpz_mul(ctg_mpz_struct*, const ctg_mpz_struct*, const ctg_mpz_struct*);
 size_t __gmpz_sizeinbase(const ctg_mpz_struct*, int);

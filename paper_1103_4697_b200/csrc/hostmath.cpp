@@ -333,6 +333,7 @@ bool big_gcd_update(Big& g, const uint32_t* c, int n) {
   d[nl - 1] = 0;
   std::memcpy(d, c, 4 * static_cast<size_t>(n));
   __gmpz_limbs_finish(&x.z, static_cast<long>(nl));
+  if (__gmpz_divisible_p(&x.z, &y.z)) return false;  // the common case once g is the content
   __gmpz_gcd(&r.z, &y.z, &x.z);
   if (r.z._mp_size == y.z._mp_size &&
       std::memcmp(r.z._mp_d, y.z._mp_d, 8 * static_cast<size_t>(r.z._mp_size < 0 ? -r.z._mp_size : r.z._mp_size)) == 0)
