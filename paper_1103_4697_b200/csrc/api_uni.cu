@@ -414,6 +414,42 @@ uint32_t* reduce_slots(DevArena& ar, const std::vector<Slot>& slot, const CrtTab
   return d_tab;
 }
 
+// The staging half of reduce_slots without the K1 launch (kernels that reduce their own inputs):
+// coefficient-major limbs [S][Lw] followed by the S signs, ONE H2D copy.
+struct StagedSlots {
+  const uint32_t* limbs = nullptr;
+  const int8_t* sign = nullptr;
+  int Lw = 0;
+};
+template <class List>
+StagedSlots stage_polys(DevArena& ar, const List& ps) {
+  int S = 0, Lw = 1;
+  for (const ZPoly* p : ps)
+    for (const auto& c : *p) {
+      ++S;
+      Lw = std::max(Lw, static_cast<int>(c.mag.size()));
+    }
+  const size_t nl = static_cast<size_t>(Lw) * S, bytes = 4 * nl + S;
+  uint8_t* stage = tls_stage.get(bytes);
+  uint32_t* limbs = reinterpret_cast<uint32_t*>(stage);
+  int8_t* sign = reinterpret_cast<int8_t*>(stage + 4 * nl);
+  int s = 0;
+  for (const ZPoly* p : ps)
+    for (const auto& c : *p) {
+      sign[s] = static_cast<int8_t>(c.sign);
+      uint32_t* row = limbs + static_cast<size_t>(s) * Lw;
+      const int n = static_cast<int>(c.mag.size());
+      if (n) std::memcpy(row, c.mag.data(), 4 * static_cast<size_t>(n));
+      if (n < Lw) std::memset(row + n, 0, 4 * static_cast<size_t>(Lw - n));
+      ++s;
+    }
+  uint8_t* d = ar.alloc<uint8_t>(bytes);
+  CTG_CUDA_CHECK(cudaMemcpyAsync(d, stage, bytes, cudaMemcpyHostToDevice, ar.st));
+  tls_stage.mark(ar.st);
+  stats_tls().h2d_bytes += static_cast<int64_t>(bytes);
+  return StagedSlots{reinterpret_cast<const uint32_t*>(d), reinterpret_cast<const int8_t*>(d + 4 * nl), Lw};
+}
+
 // Several polynomials as consecutive slots of one table (row k = p_0 | p_1 | ...).
 template <class List>
 uint32_t* reduce_polys(DevArena& ar, const List& ps, const CrtTables& tabs, Launches& L) {
@@ -756,16 +792,27 @@ ZPoly gcd_modular(const ZPoly& A, const ZPoly& B, int device, cudaStream_t st, L
     std::vector<uint32_t> primes = select_uni_primes(need + extra);
     const int nk = static_cast<int>(primes.size());
     auto T = get_tables(device, 1, primes);
-    // one staging copy, one K1 launch for both operands (tiny gcds are latency-bound)
-    const int pitch_ab = na + nb + 2;
-    uint32_t* tA = reduce_polys(ar, std::initializer_list<const ZPoly*>{&A, &B}, *T, L);
-    uint32_t* tB = tA + (na + 1);
     const int pitch = na + nb + 3;
     int32_t* d_deg = ar.alloc<int32_t>(nk);
     uint32_t* d_out = ar.alloc<uint32_t>(static_cast<size_t>(nk) * pitch);
     const size_t gb = uni_gbuf_bytes(modgcd_smem(na, nb), nk);
     uint32_t* gbuf = gb ? ar.alloc<uint32_t>(gb / 4) : nullptr;
-    L.n += launched(launch_modgcd(tA, na, tB, nb, pitch_ab, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st));
+    int maxl = 1;
+    for (const ZPoly* p : {&A, &B})
+      for (const auto& c : *p) maxl = std::max(maxl, static_cast<int>(c.mag.size()));
+    if (maxl <= kRedL && na + nb + 2 <= 4096) {
+      // small inputs (the realroots / multiplicity_at calls): one staging copy and ONE launch --
+      // the gcd kernel reduces the coefficients itself (a GPU round trip is the whole cost)
+      const StagedSlots sg = stage_polys(ar, std::initializer_list<const ZPoly*>{&A, &B});
+      L.n += launched(launch_modgcd(nullptr, na, nullptr, nb, 0, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st,
+                                    sg.limbs, sg.sign, sg.Lw, T->d_rpow));
+    } else {
+      // one staging copy, one K1 launch for both operands
+      const int pitch_ab = na + nb + 2;
+      uint32_t* tA = reduce_polys(ar, std::initializer_list<const ZPoly*>{&A, &B}, *T, L);
+      uint32_t* tB = tA + (na + 1);
+      L.n += launched(launch_modgcd(tA, na, tB, nb, pitch_ab, T->d_pc, nk, d_deg, d_out, pitch, gbuf, ar.st));
+    }
     CTG_CUDA_CHECK(cudaGetLastError());
     std::vector<int32_t> deg(nk);
     CTG_CUDA_CHECK(cudaMemcpyAsync(deg.data(), d_deg, 4 * nk, cudaMemcpyDeviceToHost, ar.st));

@@ -318,11 +318,21 @@ __global__ void __launch_bounds__(256) k_gcd_degree(const uint32_t* __restrict__
 // Row layout (plain residues): g (dg+1) | u (na-dg+1) | w (nb-dg+1).  deg[k] = dg,
 // or -2 if lc(A) or lc(B) vanishes mod p.
 // ---------------------------------------------------------------------------
+// Inputs either as K1 residue rows (tabA / tabB) or, for small gcds (one launch instead of two),
+// as the staged coefficients themselves: `limbs` [na + nb + 2][Lw] (coefficient-major, A then B)
+// and `sign`, reduced here with the K1 weights rpow (Lw <= kRedL).
+struct GcdStaged {
+  const uint32_t* limbs = nullptr;
+  const int8_t* sign = nullptr;
+  int Lw = 0;
+  const uint32_t* rpow = nullptr;
+};
+
 template <bool GB>
 __global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tabA, int na,
                                                 const uint32_t* __restrict__ tabB, int nb, int tab_pitch,
                                                 const PrimeConst* __restrict__ pc, int32_t* deg, uint32_t* out,
-                                                int pitch, uint32_t* gbuf) {
+                                                int pitch, uint32_t* gbuf, GcdStaged sg) {
   extern __shared__ uint32_t sm[];
   __shared__ __align__(16) uint32_t Ms[2 * 128];  // lehmer::blk_gcd_core's matrices and control
   __shared__ int ctl[4];
@@ -332,10 +342,24 @@ __global__ void __launch_bounds__(512) k_modgcd(const uint32_t* __restrict__ tab
   uint32_t* base = cta_buffers<GB>(sm, gbuf, 6 * static_cast<size_t>(cap));
   uint32_t *A = base, *B = base + cap, *X = base + 2 * cap, *Y = base + 3 * cap, *Q = base + 4 * cap,
            *Z = base + 5 * cap;
-  const uint32_t* ra = tabA + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : na + 1);
-  const uint32_t* rb = tabB + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : nb + 1);
-  for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
-  for (int i = threadIdx.x; i <= nb; i += blockDim.x) B[i] = Y[i] = rb[i];
+  if (sg.limbs) {  // fused K1: coefficient s of A (s <= na) or B (s - na - 1), Montgomery form
+    const uint32_t* w = sg.rpow + static_cast<size_t>(kl) * kRedL;
+    for (int s = threadIdx.x; s <= na + nb + 1; s += blockDim.x) {
+      const uint32_t* lb = sg.limbs + static_cast<size_t>(s) * sg.Lw;
+      uint32_t acc = 0;
+      for (int l = 0; l < sg.Lw; ++l) acc = madd(acc, mmul(lb[l], __ldg(&w[l]), M), M.p);
+      if (sg.sign[s] < 0) acc = mneg(acc, M.p);
+      if (s <= na)
+        A[s] = X[s] = acc;
+      else
+        B[s - na - 1] = Y[s - na - 1] = acc;
+    }
+  } else {
+    const uint32_t* ra = tabA + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : na + 1);
+    const uint32_t* rb = tabB + static_cast<size_t>(kl) * (tab_pitch ? tab_pitch : nb + 1);
+    for (int i = threadIdx.x; i <= na; i += blockDim.x) A[i] = X[i] = ra[i];
+    for (int i = threadIdx.x; i <= nb; i += blockDim.x) B[i] = Y[i] = rb[i];
+  }
   __syncthreads();
   if (A[na] == 0u || B[nb] == 0u) {
     if (threadIdx.x == 0) deg[kl] = -2;
@@ -602,14 +626,24 @@ int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int3
 }
 
 int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, int tab_pitch, const PrimeConst* pc,
-                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st) {
+                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st,
+                  const uint32_t* staged_limbs, const int8_t* staged_sign, int Lw, const uint32_t* rpow) {
   const size_t smem = smem_or_global(k_modgcd<false>, modgcd_smem(na, nb), gbuf);
   if (smem == SIZE_MAX) return -1;
+  GcdStaged sg;
+  if (staged_limbs) {
+    if (Lw < 1 || Lw > kRedL || !staged_sign || !rpow) return -1;
+    sg.limbs = staged_limbs;
+    sg.sign = staged_sign;
+    sg.Lw = Lw;
+    sg.rpow = rpow;
+  }
   if (smem)
     k_modgcd<false><<<nk, uni_threads(std::max(na, nb)), smem, st>>>(tabA, na, tabB, nb, tab_pitch, pc, deg, out, pitch,
-                                                                     nullptr);
+                                                                     nullptr, sg);
   else
-    k_modgcd<true><<<nk, uni_threads(std::max(na, nb)), 0, st>>>(tabA, na, tabB, nb, tab_pitch, pc, deg, out, pitch, gbuf);
+    k_modgcd<true><<<nk, uni_threads(std::max(na, nb)), 0, st>>>(tabA, na, tabB, nb, tab_pitch, pc, deg, out, pitch, gbuf,
+                                                                 sg);
   return 1;
 }
 

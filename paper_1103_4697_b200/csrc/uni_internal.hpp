@@ -35,8 +35,12 @@ int launch_gcd_degree(const uint32_t* a, int na, const uint32_t* b, int nb, cons
 int launch_modyun(const uint32_t* tab, int n, const PrimeConst* pc, int nk, int32_t* deg, uint32_t* fac,
                   uint32_t* sqf, uint32_t* gbuf, cudaStream_t st);
 // tab_pitch: words between the rows of consecutive primes for both operands (0: na + 1 / nb + 1)
+// staged_limbs / staged_sign / Lw / rpow: the inputs as staged coefficients ([na + nb + 2][Lw],
+// A then B, Lw <= kRedL) reduced inside the kernel (no K1 launch); tabA / tabB are then unused.
 int launch_modgcd(const uint32_t* tabA, int na, const uint32_t* tabB, int nb, int tab_pitch, const PrimeConst* pc,
-                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st);
+                  int nk, int32_t* deg, uint32_t* out, int pitch, uint32_t* gbuf, cudaStream_t st,
+                  const uint32_t* staged_limbs = nullptr, const int8_t* staged_sign = nullptr, int Lw = 0,
+                  const uint32_t* rpow = nullptr);
 // Bivariate gcd probe: deg[k * npts + j] = deg gcd(f(a_j, y), g(a_j, y)) mod p_k, or -1.
 // dir = offf[nf+1], lenf[nf+1], offg[ng+1], leng[ng+1] (slot runs in tab, x ascending).
 int launch_bigcd_probe(const uint32_t* tab, int S, const int32_t* dir, int nf, int ng, const PrimeConst* pc,
